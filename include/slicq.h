@@ -1,0 +1,180 @@
+/*
+ * slicq.h — C ABI of the B200-native sliCQ library (libslicq.so).
+ *
+ * The sliCQ transform of Holighaus, Dörfler, Velasco, Grill, "A framework for
+ * invertible, real-time constant-Q transforms" (arXiv 1210.0084).  References
+ * "P:<line>" are lines of that paper's text; "C<n>" are the readings
+ * of ambiguous passages listed in DESIGN.md ("Readings of the paper").
+ *
+ * What the library computes
+ *   slicq_forward  = Alg. 3 "sliCQ analysis" with Alg. 1 "NSG analysis"
+ *                     applied to every slice of length 2N = sl_len,
+ *                    for REAL fp32 input; coefficients of the channels
+ *                    k = 0 (DC plateau), 1..K (constant-Q), K+1 (Nyquist plateau)
+ *                    of Table 1.  The mirror channels K+2..2K+1 are
+ *                    redundant for real input (C15) and are not stored.
+ *   slicq_inverse  = Alg. 4 "sliCQ synthesis" with Alg. 2 "NSG
+ *                    synthesis" and the canonical duals of Prop. 2
+ *                     and of dualwincond.
+ *
+ * Normalisation (C1): FFT_n unnormalised, IFFT_n with 1/n, so channel k of slice m is
+ *     c^m_k = sqrt(M_k) * IFFT_{M_k}( fold_{M_k}( FFT_{2N}(f^m) * g_k ) ),
+ *     f^m[j] = f[((m-1)N + j) mod L] * h_0[j-N]
+ * where M_k = L/a_k is channel k's coefficient count per slice (C9/C10).
+ *
+ * Layouts (all contiguous, row-major, caller-owned, device memory unless stated)
+ *   x, y    : float32 [batch][n]   (one row per mono signal / audio channel)
+ *   coeffs  : slicq_c32 [batch][S][C] with S = slicq_num_slices(p, n) and
+ *             C = slicq_coeffs_per_slice(p) = sum_k M_k; channel k occupies
+ *             columns [off_k, off_k + M_k) (slicq_channel_offsets), entry n of
+ *             channel k is coefficient c^m_{n,k} (slice-local time n*2N/M_k).
+ *             The paper's two-layer array s is the index view
+ *             s^{m mod 2}_k[((m-1) M_k/2 + n) mod (L M_k / 2N)] = c^m_k[n].
+ *   L       : padded length ceil(n / 2N) * 2N, zero padding at the end (C13);
+ *             y is trimmed back to n.
+ *
+ * Execution model
+ *   plan_create runs on the host (float64) and uploads read-only tables once.
+ *   The hot-path calls are asynchronous and stream-ordered on `stream` (a
+ *   cudaStream_t passed as void*; NULL = legacy default stream), perform no
+ *   allocation and no host synchronisation.  A plan is immutable: concurrent
+ *   calls on different streams are safe if they use distinct workspaces.
+ *   Device faults surface at the caller's next synchronisation (CUDA semantics).
+ *
+ * Errors: every int-returning call returns SLICQ_OK (0) or a negative code and
+ * sets a thread-local message readable with slicq_last_error().
+ */
+#ifndef SLICQ_H
+#define SLICQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SLICQ_API __attribute__((visibility("default")))
+#else
+#define SLICQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct slicq_plan slicq_plan;       /* opaque */
+typedef struct { float re, im; } slicq_c32;  /* interleaved complex64 (torch.complex64 layout) */
+
+enum {
+  SLICQ_RASTER_NONE = 0,   /* M_k = smallest even 2/3/5-smooth >= L_k per channel (C9)    */
+  SLICQ_RASTER_OCTAVE = 1, /* one M per CQ octave, DC and Nyquist separate (C10)           */
+  SLICQ_RASTER_FULL = 2    /* one M for all channels: "L/a_k constant" (C10)    */
+};
+
+enum {
+  SLICQ_OK = 0,
+  SLICQ_EINVAL = -1,        /* invalid parameter (SPEC InvalidParams)                     */
+  SLICQ_ENOTFRAME = -2,     /* frame diagonal not positive / M_k < L_k (Prop. 2)   */
+  SLICQ_ESHAPE = -3,        /* n, batch, pointer alignment, workspace size                */
+  SLICQ_ECUDA = -4,         /* CUDA runtime error (no device, launch failure, ...)        */
+  SLICQ_ENOMEM = -5,        /* host or device allocation failed                           */
+  SLICQ_EINTERNAL = -6,     /* broken internal invariant                                  */
+  SLICQ_EUNSUPPORTED = -7   /* valid plan the CUDA path has no kernel for (see plan_create) */
+};
+
+enum { SLICQ_PLAN_HOST_ONLY = 1 }; /* plan_create_ex flag: host tables only, no device */
+
+/* ------------------------------------------------------------------ plans
+ * plan_create: build the CQ-NSGT system for slices of length sl_len = 2N.
+ *   fs               sampling rate xi_s in Hz (> 0)
+ *   fmin, fmax       xi_min, xi_max in Hz: 0 < fmin < fs/2, fmax > fmin; fmax >= fs/2 is
+ *                    allowed and caps K at the last centre below Nyquist (C4)
+ *   bins_per_octave  B >= 1
+ *   sl_len           2N: divisible by 4 and 2/3/5-smooth.  The CUDA path implements
+ *                    2N in {4096, 8192, 16384, 32768}; other valid values give
+ *                    SLICQ_EUNSUPPORTED unless SLICQ_PLAN_HOST_ONLY is set.
+ *   tr_area          Tukey transition length (the paper's M): even, 2 <= tr < N
+ *   rasterize        SLICQ_RASTER_*
+ *   out              receives the plan (NULL on failure)
+ * The plan allocates its device tables (a few MB) on the device current at the call.
+ * Returns SLICQ_EINVAL, SLICQ_ENOTFRAME, SLICQ_EUNSUPPORTED, SLICQ_ECUDA, SLICQ_ENOMEM. */
+SLICQ_API int plan_create(double fs, double fmin, double fmax, int bins_per_octave, int64_t sl_len,
+                int64_t tr_area, int rasterize, slicq_plan **out);
+SLICQ_API int plan_create_ex(double fs, double fmin, double fmax, int bins_per_octave, int64_t sl_len,
+                   int64_t tr_area, int rasterize, unsigned flags, slicq_plan **out);
+/* NULL-safe; frees the plan-owned device tables.  No call may be in flight on the plan. */
+SLICQ_API void plan_destroy(slicq_plan *p);
+
+/* ------------------------------------------------------------------ queries (host, cheap)
+ * Channel order 0 = DC plateau, 1..K = ascending CQ channels, K+1 = Nyquist plateau. */
+SLICQ_API int slicq_num_channels(const slicq_plan *p);                      /* K+2, or <0 on error  */
+SLICQ_API int slicq_num_cq_channels(const slicq_plan *p);                   /* K                    */
+SLICQ_API int slicq_channel_lengths(const slicq_plan *p, int32_t *M);       /* host out [K+2]: M_k  */
+SLICQ_API int slicq_channel_offsets(const slicq_plan *p, int64_t *off);     /* host out [K+3]       */
+SLICQ_API int64_t slicq_coeffs_per_slice(const slicq_plan *p);              /* sum_k M_k            */
+SLICQ_API int64_t slicq_sl_len(const slicq_plan *p);                        /* 2N                   */
+SLICQ_API int64_t slicq_padded_length(const slicq_plan *p, int64_t n);      /* L = ceil(n/2N)*2N    */
+SLICQ_API int64_t slicq_num_slices(const slicq_plan *p, int64_t n);         /* S = L/N      */
+SLICQ_API int64_t slicq_halo(const slicq_plan *p);                          /* (N+tr)/2: one-sided reach of h_0 */
+/* Workspace bytes needed by slicq_inverse / slicq_inverse_range for `nslices` slices of
+ * `batch` rows (forward needs none).  The workspace must be zero-filled once before its
+ * first use and then be reused unmodified (it holds overlap-add pairing counters). */
+SLICQ_API size_t slicq_workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
+/* Plan export for parity tests (host out-params, any may be NULL):
+ *   lo[K+2], len[K+2]   unwrapped support J_k = [lo_k, lo_k + len_k) in 2N-bins (C5)
+ *   g[sum len], gdual[sum len]   g_k and canonical dual g_k / sum_l |g_l|^2 on J_k
+ *   h0[2N], h0dual[2N]  slicing window and its dual at t = -N..N-1 (index t+N)
+ *   layout[K]           centre frequencies xi_1..xi_K in Hz (Table 1)          */
+SLICQ_API int slicq_plan_export(const slicq_plan *p, int32_t *lo, int32_t *len, double *g, double *gdual,
+                      double *h0, double *h0dual, double *xi);
+SLICQ_API int64_t slicq_filter_total_length(const slicq_plan *p);           /* sum_k len_k          */
+SLICQ_API const char *slicq_last_error(void);                               /* thread-local message */
+
+/* ------------------------------------------------------------------ hot path
+ * slicq_forward: coeffs[b][m][:] = sliCQ analysis of x[b][0..n) for all S slices.
+ *   x       device float32 [batch][n], rows contiguous, 4-byte aligned (8-byte gives
+ *           vector loads)
+ *   coeffs  device slicq_c32 [batch][S][C], 8-byte aligned
+ *   ws      unused (may be NULL)
+ * Returns SLICQ_ESHAPE on n < 1, batch < 1, NULL/misaligned pointers;
+ * SLICQ_ECUDA if the launch fails. */
+SLICQ_API int slicq_forward(const slicq_plan *p, const float *x, int64_t n, int64_t batch,
+                  slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream);
+
+/* slicq_inverse: y[b][0..n) = sliCQ synthesis of coeffs[b] (any coefficients: modified
+ * ones are synthesised with the Hermitian projection of C15, i.e. the real part of the
+ * full 2K+2-channel Alg. 2).  ws: >= slicq_workspace_bytes(p, S, batch) bytes, see above.
+ * y is fully overwritten (no need to zero it). */
+SLICQ_API int slicq_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n, int64_t batch,
+                  float *y, void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ slice-range shards
+ * Multi-GPU partition of one long stream: a rank owns slices
+ * [slice0, slice0 + nslices) of total_slices = S and input samples
+ * [slice0*N, (slice0 + nslices)*N).
+ *
+ * slicq_forward_range: x_local holds `x_len` samples of each row (row stride x_stride
+ *   floats) where x_local[i] is global sample slice0*N - halo + i; the caller places the
+ *   left neighbour's samples (circularly wrapped for slice0 = 0) in the first
+ *   `halo` entries and zeros for padding positions >= n.  halo must be even and
+ *   >= slicq_halo(p) - 1; positions outside [0, x_len) read as 0.
+ *   coeffs_local: [batch][nslices][C].
+ * slicq_inverse_range: y_local [batch][nslices*N] (row stride y_stride) receives the
+ *   overlap-added output of samples [slice0*N, (slice0+nslices)*N) from these slices
+ *   only; left_spill [batch][halo] receives the part of slice0's output that falls on
+ *   samples [slice0*N - halo, slice0*N) (the left neighbour adds it with
+ *   slicq_overlap_add).  ws as for slicq_inverse with S = nslices. */
+SLICQ_API int slicq_forward_range(const slicq_plan *p, const float *x_local, int64_t x_len,
+                        int64_t x_stride, int64_t halo, int64_t slice0, int64_t nslices,
+                        int64_t total_slices, int64_t batch, slicq_c32 *coeffs_local,
+                        void *ws, size_t ws_bytes, void *stream);
+SLICQ_API int slicq_inverse_range(const slicq_plan *p, const slicq_c32 *coeffs_local, int64_t slice0,
+                        int64_t nslices, int64_t total_slices, int64_t batch, float *y_local,
+                        int64_t y_stride, float *left_spill, int64_t halo, void *ws,
+                        size_t ws_bytes, void *stream);
+/* y[b][i] += spill[b][i] for i < count (rows: y stride y_stride, spill stride count). */
+SLICQ_API int slicq_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,
+                      int64_t batch, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLICQ_H */

@@ -1,0 +1,576 @@
+// sm_100a kernels of the sliCQ hot path (device code; instantiated per slice size in kernels_l*.cu).
+//
+//   slicq_fwd_kernel<LOGN>  one CTA per (signal row, slice):
+//     F1  gather the Tukey-windowed slice straight from HBM
+//     F2  r2c FFT_{2N} as a complex N-point Stockham FFT in shared memory + packing
+//         step, register-resident radix-16/32 passes            (Alg. 1 line P:186)
+//     F3  per channel: multiply by g_k, fold to M_k             (C5)
+//     F4  sqrt(M_k) IFFT_{M_k}: four-step M1 x M2 register DFTs per warp "packet"
+//     F5  coalesced store of c^m_k                              (P:320-323 layout view)
+//   slicq_inv_kernel<LOGN>  one CTA per (row, slice):
+//     I1/I2  load c^m_k, FFT_{M_k}/sqrt(M_k) (four-step)
+//     I3  multiply by the dual g~_k and scatter-add into the half spectrum with the
+//         Hermitian rule of C15
+//     I4  c2r IFFT_{2N} (packing step + N-point Stockham)
+//     I5  multiply by h~_0 and overlap-add; slice-boundary samples are paired across
+//         CTAs through the workspace with a parity counter (no spin, deterministic)
+//
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fft_dev.cuh"
+#include "slicq_internal.h"
+
+namespace slicq {
+namespace kern {
+
+using namespace slicq::dev;
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__host__ __device__ constexpr int padi(int i) { return i + (i >> 5); }
+
+template <int LOGN>
+struct Big;
+template <>
+struct Big<11> {
+  static constexpr int N = 2048, T = 128, R1 = 16, R2 = 16, R3 = 8, MINB = 2;
+};
+template <>
+struct Big<12> {
+  static constexpr int N = 4096, T = 256, R1 = 16, R2 = 16, R3 = 16, MINB = 2;
+};
+template <>
+struct Big<13> {
+  static constexpr int N = 8192, T = 256, R1 = 32, R2 = 16, R3 = 16, MINB = 1;
+};
+template <>
+struct Big<14> {
+  static constexpr int N = 16384, T = 512, R1 = 32, R2 = 32, R3 = 16, MINB = 1;
+};
+
+template <int LOGN>
+constexpr int spec_entries() {
+  return padi(Big<LOGN>::N) + 2;  // X[0..N-1] padded, X[N] at padi(N), one spare
+}
+template <int LOGN>
+constexpr int tw_entries() {
+  return 64 + 2 * Big<LOGN>::N / 64;
+}
+
+struct KArgs {
+  // forward input / inverse output
+  const float *x;
+  float *y;
+  float *spill;
+  int64_t x_len, x_stride, base_off, L;
+  int64_t y_len, y_stride, y_base, halo;
+  int wrap;       // forward: negative sample indices wrap by L (circular)
+  int circular;   // inverse: slice S-1 pairs with slice 0
+  int64_t slice0;
+  int nslices;
+  int tr;
+  int scr;
+  int npackets;
+  int64_t C;
+  float2 *coef_out;
+  const float2 *coef_in;
+  const ChanDev *chan;
+  const PacketDev *packets;
+  const int32_t *pchans;
+  const float *g;
+  const float *gdual;
+  const float *h0;
+  const float *h0dual;
+  const float2 *tw2n;
+  const float2 *twM;
+  unsigned *cnt;    // inverse workspace: [batch][nslices] pairing counters
+  float *bnd;       // inverse workspace: [batch][nslices][2][tr] boundary halves
+};
+
+// e^{-i pi e / N} for e in [0, 2N): two-level table, 2 shared loads + 1 complex multiply
+__device__ __forceinline__ float2 tw_lookup(const float2 *tw, int e) {
+  return cmul(tw[64 + (e >> 6)], tw[e & 63]);
+}
+
+// Stockham twiddle for task j of a radix-R pass with span NS (twiddle before butterfly).
+template <int N, int R, int NS, int SIGN>
+__device__ __forceinline__ void pass_twiddle(float2 (&v)[R], int j, const float2 *tw) {
+  if constexpr (NS > 1) {
+    constexpr int STEP = 2 * (N / (NS * R));  // units of e^{-i pi/N}
+    const int base = (j & (NS - 1)) * STEP;
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      float2 w = tw_lookup(tw, (base * r) & (2 * N - 1));
+      if (SIGN > 0) w = cconj(w);
+      v[r] = cmul(v[r], w);
+    }
+  }
+}
+
+// One in-place Stockham pass over the padded shared-memory array.
+template <int N, int R, int NS, int SIGN, int T>
+__device__ __forceinline__ void pass_smem(float2 *spec, const float2 *tw) {
+  constexpr int TASKS = N / R;
+  static_assert(TASKS % T == 0, "tasks must divide evenly");
+  constexpr int PER = TASKS / T;
+  float2 v[PER][R];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = threadIdx.x + q * T;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q][r] = spec[padi(j + r * TASKS)];
+    pass_twiddle<N, R, NS, SIGN>(v[q], j, tw);
+    dft<R, SIGN>(v[q]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = threadIdx.x + q * T;
+    const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+    for (int r = 0; r < R; ++r) spec[padi(base + r * NS)] = v[q][r];
+  }
+  __syncthreads();
+}
+
+// X(j) for an unwrapped bin j in (-2N, 2N) from the half spectrum X[0..N] (real input).
+template <int N>
+__device__ __forceinline__ float2 spec_at(const float2 *spec, int j) {
+  int jj = j < 0 ? j + 2 * N : j;
+  if (jj <= N) return spec[padi(jj)];
+  return cconj(spec[padi(2 * N - jj)]);
+}
+
+// ------------------------------------------------------------------ forward packet steps
+template <int M1, int N>
+__device__ __forceinline__ void fwd_step1(const KArgs &a, const float2 *spec, float2 *scr,
+                                          int m2, int nch, int chan_off, int lane) {
+  const int S2 = m2 | 1;
+  const int nt = nch * m2;
+  for (int t = lane; t < nt; t += 32) {
+    const int ci = t / m2;
+    const int p2 = t - ci * m2;
+    const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
+    float2 v[M1];
+    int d = p2 - ch.lo_mod;
+    if (d < 0) d += ch.M;
+#pragma unroll
+    for (int p1 = 0; p1 < M1; ++p1) {
+      float2 val = make_float2(0.f, 0.f);
+      if (d < ch.len) val = cscale(spec_at<N>(spec, ch.lo + d), __ldg(a.g + ch.goff + d));
+      v[p1] = val;
+      d += m2;
+      if (d >= ch.M) d -= ch.M;
+    }
+    dft<M1, +1>(v);
+    int e = 0;
+#pragma unroll
+    for (int n1 = 1; n1 < M1; ++n1) {
+      e += p2;
+      if (e >= ch.M) e -= ch.M;
+      v[n1] = cmul(v[n1], __ldg(a.twM + ch.twoff + e));
+    }
+    float2 *A = scr + ci * M1 * S2 + p2;
+#pragma unroll
+    for (int n1 = 0; n1 < M1; ++n1) A[n1 * S2] = v[n1];
+  }
+}
+
+template <int M2>
+__device__ __forceinline__ void fwd_step2(const KArgs &a, const float2 *scr, float2 *out_row,
+                                          int m1, int nch, int chan_off, int lane) {
+  constexpr int S2 = M2 | 1;
+  const int nt = nch * m1;
+  for (int t = lane; t < nt; t += 32) {
+    const int ci = t / m1;
+    const int n1 = t - ci * m1;
+    const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
+    float2 v[M2];
+    const float2 *A = scr + ci * m1 * S2 + n1 * S2;
+#pragma unroll
+    for (int p2 = 0; p2 < M2; ++p2) v[p2] = A[p2];
+    dft<M2, +1>(v);
+    float2 *o = out_row + ch.off + n1;
+#pragma unroll
+    for (int n2 = 0; n2 < M2; ++n2) o[m1 * n2] = cscale(v[n2], ch.scale);
+  }
+}
+
+// ------------------------------------------------------------------ inverse packet steps
+template <int M1>
+__device__ __forceinline__ void inv_step1(const KArgs &a, const float2 *in_row, float2 *scr,
+                                          int m2, int nch, int chan_off, int lane) {
+  const int S2 = m2 | 1;
+  const int nt = nch * m2;
+  for (int t = lane; t < nt; t += 32) {
+    const int ci = t / m2;
+    const int p2 = t - ci * m2;
+    const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
+    float2 v[M1];
+    const float2 *src = in_row + ch.off + p2;
+#pragma unroll
+    for (int p1 = 0; p1 < M1; ++p1) v[p1] = src[p1 * m2];
+    dft<M1, -1>(v);
+    int e = 0;
+#pragma unroll
+    for (int n1 = 1; n1 < M1; ++n1) {
+      e += p2;
+      if (e >= ch.M) e -= ch.M;
+      v[n1] = cmul(v[n1], cconj(__ldg(a.twM + ch.twoff + e)));
+    }
+    float2 *A = scr + ci * M1 * S2 + p2;
+#pragma unroll
+    for (int n1 = 0; n1 < M1; ++n1) A[n1 * S2] = v[n1];
+  }
+}
+
+__device__ __forceinline__ void atomic_add_c(float2 *p, float2 v) {
+  atomicAdd(&p->x, v.x);
+  atomicAdd(&p->y, v.y);
+}
+
+template <int M2, int N>
+__device__ __forceinline__ void inv_step2(const KArgs &a, const float2 *scr, float2 *spec, int m1,
+                                          int nch, int chan_off, int lane) {
+  constexpr int S2 = M2 | 1;
+  const int nt = nch * m1;
+  for (int t = lane; t < nt; t += 32) {
+    const int ci = t / m1;
+    const int n1 = t - ci * m1;
+    const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
+    float2 v[M2];
+    const float2 *A = scr + ci * m1 * S2 + n1 * S2;
+#pragma unroll
+    for (int p2 = 0; p2 < M2; ++p2) v[p2] = A[p2];
+    dft<M2, -1>(v);
+    // F[q], q = n1 + m1 n2 ; bin j in J_k with j = q (mod M_k)
+    int d = n1 - ch.lo_mod;
+    if (d < 0) d += ch.M;
+#pragma unroll
+    for (int n2 = 0; n2 < M2; ++n2) {
+      if (d < ch.len) {
+        const int j = ch.lo + d;
+        const float2 val = cscale(v[n2], ch.scale * __ldg(a.gdual + ch.goff + d));
+        // Hermitian rule (C15): v at j mod 2N if <= N; conj(v) at -j mod 2N if <= N
+        int p1 = j % (2 * N);
+        if (p1 < 0) p1 += 2 * N;
+        if (p1 <= N) atomic_add_c(spec + padi(p1), val);
+        const int p2m = p1 == 0 ? 0 : 2 * N - p1;
+        if (p2m <= N) atomic_add_c(spec + padi(p2m), cconj(val));
+      }
+      d += m1;
+      if (d >= ch.M) d -= ch.M;
+    }
+  }
+}
+
+#define SLICQ_SIZES(X) \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(8) X(9) X(10) X(12) X(15) X(16) X(18) X(20) X(24) X(25) X(27) X(30) X(32)
+
+// ------------------------------------------------------------------ forward kernel
+template <int LOGN>
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kernel(const KArgs a) {
+  using CF = Big<LOGN>;
+  constexpr int N = CF::N, T = CF::T, NW = T / 32;
+  extern __shared__ float4 smem4[];
+  float2 *spec = reinterpret_cast<float2 *>(smem4);
+  float2 *tw = spec + spec_entries<LOGN>();
+  float2 *scr_all = tw + tw_entries<LOGN>();
+  int *ctr = reinterpret_cast<int *>(scr_all + NW * a.scr);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t mloc = blockIdx.x;
+  const int64_t mg = a.slice0 + mloc;
+  const int64_t row = blockIdx.y;
+
+  for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
+  if (tid == 0) *ctr = 0;
+
+  // ---- F1 + first radix pass, read straight from HBM.  z[p] = f[2p] + i f[2p+1].
+  {
+    constexpr int R = CF::R1, TASKS = N / R, PER = TASKS / T;
+    const float *xr = a.x + row * a.x_stride;
+    const bool vec = ((reinterpret_cast<uintptr_t>(xr) & 7) == 0);
+    const int64_t s0 = (mg - 1) * N - a.base_off;  // local index of frame sample 0
+    const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
+    float2 v[PER][R];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int j = tid + q * T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int p = j + r * TASKS;
+        const int i0 = 2 * p;  // frame index of the real part
+        const int t0 = i0 - N;
+        float2 val = make_float2(0.f, 0.f);
+        const int at0 = t0 < 0 ? -t0 : t0;
+        const int at1 = (t0 + 1) < 0 ? -(t0 + 1) : (t0 + 1);
+        if (at0 < Bw || at1 < Bw) {
+          int64_t idx = s0 + i0;
+          if (a.wrap && idx < 0) idx += a.L;
+          float x0 = 0.f, x1 = 0.f;
+          if (idx >= 0 && idx + 1 < a.x_len && vec) {
+            const float2 xv = __ldg(reinterpret_cast<const float2 *>(xr + idx));
+            x0 = xv.x;
+            x1 = xv.y;
+          } else {
+            if (idx >= 0 && idx < a.x_len) x0 = __ldg(xr + idx);
+            if (idx + 1 >= 0 && idx + 1 < a.x_len) x1 = __ldg(xr + idx + 1);
+          }
+          const float h0a = at0 <= A ? 1.f : (at0 < Bw ? __ldg(a.h0 + i0) : 0.f);
+          const float h0b = at1 <= A ? 1.f : (at1 < Bw ? __ldg(a.h0 + i0 + 1) : 0.f);
+          val = make_float2(x0 * h0a, x1 * h0b);
+        }
+        v[q][r] = val;
+      }
+      dft<R, -1>(v[q]);
+    }
+    __syncthreads();  // tw table visible
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int j = tid + q * T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) spec[padi(j * R + r)] = v[q][r];
+    }
+    __syncthreads();
+  }
+  pass_smem<N, CF::R2, CF::R1, -1, T>(spec, tw);
+  pass_smem<N, CF::R3, CF::R1 * CF::R2, -1, T>(spec, tw);
+
+  // ---- r2c packing: X[k] = E[k] + e^{-i pi k/N} O[k], k = 0..N  (Z[N] := Z[0])
+  for (int k = tid; k <= N / 2; k += T) {
+    const float2 zk = spec[padi(k)];
+    const float2 zn = spec[padi((N - k) & (N - 1))];
+    if (k == 0) {
+      spec[padi(0)] = make_float2(zk.x + zk.y, 0.f);
+      spec[padi(N)] = make_float2(zk.x - zk.y, 0.f);
+    } else {
+      // E = (Zk + conj Zn)/2, O = (Zk - conj Zn)/(2i)
+      const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
+      const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
+      const float2 w = tw_lookup(tw, k);  // e^{-i pi k/N}
+      const float2 Xk = cadd(E, cmul(w, O));
+      // X[N-k] = conj(E) + e^{-i pi (N-k)/N} conj(O) = conj(E) - conj(w) * conj(O)
+      const float2 Xn = csub(cconj(E), cconj(cmul(w, O)));
+      spec[padi(k)] = Xk;
+      if (k != N / 2) spec[padi(N - k)] = Xn;
+    }
+  }
+  __syncthreads();
+
+  // ---- F3-F5: channel packets, dynamically scheduled over warps
+  float2 *scr = scr_all + warp * a.scr;
+  float2 *out_row = a.coef_out + (row * a.nslices + mloc) * a.C;
+  for (;;) {
+    int pk = 0;
+    if (lane == 0) pk = atomicAdd(ctr, 1);
+    pk = __shfl_sync(FULL, pk, 0);
+    if (pk >= a.npackets) break;
+    const PacketDev P = a.packets[pk];
+    const int m1 = P.m1m2 & 255, m2 = P.m1m2 >> 8;
+    switch (m1) {
+#define X(S) \
+  case S: fwd_step1<S, N>(a, spec, scr, m2, P.nch, P.chan_off, lane); break;
+      SLICQ_SIZES(X)
+#undef X
+    }
+    __syncwarp();
+    switch (m2) {
+#define X(S) \
+  case S: fwd_step2<S>(a, scr, out_row, m1, P.nch, P.chan_off, lane); break;
+      SLICQ_SIZES(X)
+#undef X
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ inverse kernel
+template <int LOGN>
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kernel(const KArgs a) {
+  using CF = Big<LOGN>;
+  constexpr int N = CF::N, T = CF::T, NW = T / 32;
+  extern __shared__ float4 smem4[];
+  float2 *spec = reinterpret_cast<float2 *>(smem4);
+  float2 *tw = spec + spec_entries<LOGN>();
+  float2 *scr_all = tw + tw_entries<LOGN>();
+  int *ctr = reinterpret_cast<int *>(scr_all + NW * a.scr);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mloc = blockIdx.x;
+  const int64_t mg = a.slice0 + mloc;
+  const int64_t row = blockIdx.y;
+
+  for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
+  for (int i = tid; i < spec_entries<LOGN>(); i += T) spec[i] = make_float2(0.f, 0.f);
+  if (tid == 0) ctr[0] = 0;
+  __syncthreads();
+
+  // ---- I1-I3: channel packets
+  {
+    float2 *scr = scr_all + warp * a.scr;
+    const float2 *in_row = a.coef_in + (row * a.nslices + mloc) * a.C;
+    for (;;) {
+      int pk = 0;
+      if (lane == 0) pk = atomicAdd(ctr, 1);
+      pk = __shfl_sync(FULL, pk, 0);
+      if (pk >= a.npackets) break;
+      const PacketDev P = a.packets[pk];
+      const int m1 = P.m1m2 & 255, m2 = P.m1m2 >> 8;
+      switch (m1) {
+#define X(S) \
+  case S: inv_step1<S>(a, in_row, scr, m2, P.nch, P.chan_off, lane); break;
+        SLICQ_SIZES(X)
+#undef X
+      }
+      __syncwarp();
+      switch (m2) {
+#define X(S) \
+  case S: inv_step2<S, N>(a, scr, spec, m1, P.nch, P.chan_off, lane); break;
+        SLICQ_SIZES(X)
+#undef X
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+
+  // ---- I4a: c2r packing  Z[k] = E[k] + i O[k],
+  //   E = (H[k] + conj H[N-k])/2,  O = (H[k] - conj H[N-k]) e^{+i pi k/N} / 2
+  for (int k = tid; k <= N / 2; k += T) {
+    const float2 hk = spec[padi(k)];
+    const float2 hn = spec[padi(N - k)];
+    const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
+    const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+    const float2 w = cconj(tw_lookup(tw, k));  // e^{+i pi k/N}
+    const float2 O = cmul(D, w);
+    spec[padi(k)] = make_float2(E.x - O.y, E.y + O.x);  // E + iO
+    if (k != 0 && k != N / 2) {
+      // pair (N-k): E' = conj(E), O' = conj(D) * e^{i pi (N-k)/N} = -conj(D) * conj(w)
+      const float2 O2 = cmul(cconj(D), cconj(w));
+      const float2 E2 = cconj(E);
+      spec[padi(N - k)] = make_float2(E2.x - O2.y, E2.y + O2.x);  // E' + i O'
+    }
+  }
+  __syncthreads();
+
+  // ---- I4b: inverse N-point FFT (unnormalised), passes 1 and 2 in shared memory
+  pass_smem<N, CF::R1, 1, +1, T>(spec, tw);
+  pass_smem<N, CF::R2, CF::R1, +1, T>(spec, tw);
+
+  // ---- last pass + I5 epilogue: z[p] -> samples 2p, 2p+1, times h~_0 / N, overlap-add
+  {
+    constexpr int R = CF::R3, NS = CF::R1 * CF::R2, TASKS = N / R, PER = TASKS / T;
+    static_assert(NS * R == N, "pass plan");
+    const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
+    const float invN = 1.0f / (float)N;
+    const int S = a.nslices;
+    const bool left_paired = a.circular || mloc > 0;
+    const bool right_paired = a.circular || mloc + 1 < S;
+    const int bl = mloc > 0 ? mloc - 1 : S - 1;  // boundary ids (local)
+    const int br = mloc;
+    const int trp = a.tr;
+    float *yrow = a.y + row * a.y_stride;
+    float *bnd_row = a.bnd + (int64_t)row * S * 2 * trp;
+    float2 v[PER][R];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int j = tid + q * T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[q][r] = spec[padi(j + r * TASKS)];
+      pass_twiddle<N, R, NS, +1>(v[q], j, tw);
+      dft<R, +1>(v[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int j = tid + q * T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int p = j + r * NS;  // output index of the final pass = z index
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = 2 * p + h;  // frame index
+          const int t = i - N;
+          const int at = t < 0 ? -t : t;
+          if (at >= Bw) continue;
+          const float val = (h ? v[q][r].y : v[q][r].x) * invN * __ldg(a.h0dual + i);
+          const int64_t s = (mg - 1) * N + i;  // global sample index (before wrap)
+          if (at <= A) {
+            if (a.circular) {
+              int64_t sw = s < 0 ? s + a.L : (s >= a.L ? s - a.L : s);
+              if (sw < a.y_len) yrow[sw] = val;
+            } else {
+              const int64_t li = s - a.y_base;
+              if (li >= 0) yrow[li] = val;
+              else a.spill[row * a.halo + (li + a.halo)] = val;
+            }
+          } else if (t < 0) {  // left transition, shared with slice mg-1
+            const int u = t + Bw - 1;
+            if (left_paired) bnd_row[((int64_t)bl * 2 + 1) * trp + u] = val;
+            else a.spill[row * a.halo + (s - a.y_base + a.halo)] = val;
+          } else {  // right transition, shared with slice mg+1
+            const int u = t - A - 1;
+            if (right_paired) bnd_row[((int64_t)br * 2 + 0) * trp + u] = val;
+            else yrow[s - a.y_base] = val;
+          }
+        }
+      }
+    }
+    // range mode, last local slice: samples [ (mg+1)N - A, (mg+1)N ) get no local
+    // contribution; store zeros so the neighbour's spill can be added in place.
+    if (!a.circular && mloc + 1 == S) {
+      for (int u = tid; u < A; u += T) yrow[(mg + 1) * N - A + u - a.y_base] = 0.f;
+    }
+    if (!a.circular && mloc == 0) {  // spill entries no slice reaches
+      for (int u = tid; u < a.halo - (Bw - 1); u += T) a.spill[row * a.halo + u] = 0.f;
+    }
+    // ---- pairing: the second CTA to finish a boundary adds both halves (side0 + side1)
+    __threadfence();
+    __syncthreads();
+    __shared__ int sflag[2];
+    if (tid == 0) {
+      int fl = 0, fr = 0;
+      if (left_paired) fl = (atomicAdd(a.cnt + row * S + bl, 1u) & 1u) ? 1 : 0;
+      if (right_paired) fr = (atomicAdd(a.cnt + row * S + br, 1u) & 1u) ? 1 : 0;
+      __threadfence();
+      sflag[0] = fl;
+      sflag[1] = fr;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      if (!sflag[side]) continue;
+      const int b = side == 0 ? bl : br;
+      const int64_t mb = a.slice0 + b;  // boundary between global slices mb and mb+1
+      const float *h0p = bnd_row + (int64_t)b * 2 * trp;
+      const float *h1p = h0p + trp;
+      for (int u = tid; u < a.tr - 1; u += T) {
+        const float val = __ldcg(h0p + u) + __ldcg(h1p + u);
+        const int64_t s = mb * N + A + 1 + u;
+        if (a.circular) {
+          int64_t sw = s >= a.L ? s - a.L : s;
+          if (sw < a.y_len) yrow[sw] = val;
+        } else {
+          yrow[s - a.y_base] = val;
+        }
+      }
+    }
+  }
+}
+
+template <int LOGN>
+constexpr size_t smem_bytes_t(int scr) {
+  return sizeof(float2) * (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>() + (Big<LOGN>::T / 32) * scr) + 16;
+}
+
+// Per-size entry points (defined in kernels_l<LOGN>.cu)
+template <int LOGN>
+int set_attrs(size_t smem);
+template <int LOGN>
+cudaError_t launch_fwd(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s);
+template <int LOGN>
+cudaError_t launch_inv(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s);
+
+}  // namespace kern
+}  // namespace slicq

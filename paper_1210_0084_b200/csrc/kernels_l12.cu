@@ -1,0 +1,33 @@
+#define SLICQ_LOGN 12
+// Instantiation of the sliCQ kernels for N = 2^SLICQ_LOGN (one translation unit per size
+// so that the four sizes compile in parallel).
+#include "kernels_dev.cuh"
+
+namespace slicq {
+namespace kern {
+
+template <>
+int set_attrs<SLICQ_LOGN>(size_t smem) {
+  cudaError_t e1 = cudaFuncSetAttribute(slicq_fwd_kernel<SLICQ_LOGN>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e2 = cudaFuncSetAttribute(slicq_inv_kernel<SLICQ_LOGN>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e1 != cudaSuccess) return (int)e1;
+  if (e2 != cudaSuccess) return (int)e2;
+  return 0;
+}
+
+template <>
+cudaError_t launch_fwd<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
+  slicq_fwd_kernel<SLICQ_LOGN><<<grid, Big<SLICQ_LOGN>::T, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_inv<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
+  slicq_inv_kernel<SLICQ_LOGN><<<grid, Big<SLICQ_LOGN>::T, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace kern
+}  // namespace slicq

@@ -1,0 +1,382 @@
+// Host side of the sliCQ library: the float64 plan (Table 1 layout, sampled filters,
+// coefficient counts, painless dual, slicing windows) and the C ABI entry points.
+//
+// Written from the paper (arXiv 1210.0084), cited as P:<line>, under the readings
+// C<n> listed in DESIGN.md.  Independent of the Python oracle (no shared code).
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <string>
+
+#include "slicq_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+constexpr double kEdgeEps = 1e-9;  // C7/C18 support-edge guard
+constexpr double kKEps = 1e-12;    // C4/C18 guard on B log2(.)
+constexpr double kMinWidth = 4.0;  // C7 minimum filter width in bins
+constexpr double kPi = 3.14159265358979323846;
+
+bool smooth235(int64_t m) {
+  if (m < 1) return false;
+  for (int q : {2, 3, 5})
+    while (m % q == 0) m /= q;
+  return m == 1;
+}
+
+// C9: smallest even 2/3/5-smooth integer >= L.
+int64_t even_smooth_ge(int64_t L) {
+  int64_t m = L < 2 ? 2 : L;
+  while (!(m % 2 == 0 && smooth235(m))) ++m;
+  return m;
+}
+
+// H(x) = cos^2(pi x) on |x| <= 1/2 (reading C7 of P:262's H).
+double hann(double x) {
+  if (std::fabs(x) > 0.5) return 0.0;
+  double c = std::cos(kPi * x);
+  return c * c;
+}
+
+struct Filt {
+  int64_t lo;
+  std::vector<double> v;
+  double at(int64_t j) const {  // 0 off the support
+    int64_t i = j - lo;
+    return (i >= 0 && i < (int64_t)v.size()) ? v[i] : 0.0;
+  }
+};
+}  // namespace
+
+namespace slicq {
+int set_error(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+}  // namespace slicq
+
+using slicq::set_error;
+
+static int build_host_plan(slicq_plan *p) {
+  const double fs = p->fs, fmin = p->fmin, fmax = p->fmax;
+  const int B = p->B;
+  const int64_t Ls = p->sl_len, N = p->N, tr = p->tr;
+  // ---- Table 1; K per reading C4: the paper's xi_max <= xi_K < fs/2 is
+  // impossible for fmax >= fs/2, so K = min(first k covering fmax, last k below Nyquist).
+  const double y = B * std::log2(fmax / fmin);
+  const int64_t k_cover = (int64_t)std::ceil(y - kKEps) + 1;
+  const double x = B * std::log2((fs / 2.0) / fmin);
+  const int64_t k_nyq = (int64_t)std::ceil(x - kKEps);
+  const int64_t K = k_cover < k_nyq ? k_cover : k_nyq;
+  if (K < 1) return set_error(SLICQ_EINVAL, "K < 1: no constant-Q channel below Nyquist");
+  if (K > 100000) return set_error(SLICQ_EINVAL, "too many channels");
+  p->K = (int)K;
+  p->Q = 1.0 / (std::pow(2.0, 1.0 / B) - std::pow(2.0, -1.0 / B));
+  p->xi.resize(K);
+  for (int64_t k = 1; k <= K; ++k) p->xi[k - 1] = fmin * std::pow(2.0, (double)(k - 1) / B);
+
+  // ---- CQ filters at length Ls (reading C7): fractional centre omega = xi Ls/fs,
+  // width W = max(Omega Ls/fs, 4) bins, J = [ceil(om - W/2 - eps), floor(om + W/2 + eps)],
+  // g[j] = H((j - omega)/W).
+  std::vector<Filt> f(K + 2);
+  std::vector<double> omega(K + 2, 0.0);
+  for (int64_t k = 1; k <= K; ++k) {
+    const double om = p->xi[k - 1] * Ls / fs;
+    double W = (p->xi[k - 1] / p->Q) * Ls / fs;
+    if (W < kMinWidth) W = kMinWidth;
+    const int64_t lo = (int64_t)std::ceil(om - W / 2 - kEdgeEps);
+    const int64_t hi = (int64_t)std::floor(om + W / 2 + kEdgeEps);
+    f[k].lo = lo;
+    f[k].v.resize(hi - lo + 1);
+    for (int64_t j = lo; j <= hi; ++j) f[k].v[j - lo] = hann(((double)j - om) / W);
+    omega[k] = om;
+  }
+  // ---- plateaus (Table 1 rows 0 and K+1; reading C8)
+  {
+    const int64_t a = (int64_t)std::floor(omega[1]);
+    f[0].lo = -a;
+    f[0].v.resize(2 * a + 1);
+    for (int64_t j = -a; j <= a; ++j) f[0].v[j + a] = 1.0 - f[1].at(j < 0 ? -j : j);
+    const int64_t b0 = (int64_t)std::ceil(omega[K]);
+    const int64_t b1 = (int64_t)std::floor((double)Ls - omega[K]);
+    f[K + 1].lo = b0;
+    f[K + 1].v.resize(b1 - b0 + 1);
+    for (int64_t j = b0; j <= b1; ++j) {
+      double v = 1.0 - f[K].at(j) - f[K].at(Ls - j);
+      f[K + 1].v[j - b0] = v > 0.0 ? v : 0.0;
+    }
+  }
+  // ---- coefficient counts M_k = L/a_k >= L_k (readings C9, C10)
+  p->lo.resize(K + 2);
+  p->len.resize(K + 2);
+  p->M.resize(K + 2);
+  for (int64_t k = 0; k < K + 2; ++k) {
+    p->lo[k] = (int32_t)f[k].lo;
+    p->len[k] = (int32_t)f[k].v.size();
+    if (p->len[k] < 1) return set_error(SLICQ_ENOTFRAME, "empty filter support");
+  }
+  if (p->raster == SLICQ_RASTER_NONE) {
+    for (int64_t k = 0; k < K + 2; ++k) p->M[k] = (int32_t)even_smooth_ge(p->len[k]);
+  } else if (p->raster == SLICQ_RASTER_FULL) {
+    int64_t mx = 0;
+    for (int64_t k = 0; k < K + 2; ++k) mx = p->len[k] > mx ? p->len[k] : mx;
+    const int64_t m = even_smooth_ge(mx);
+    for (int64_t k = 0; k < K + 2; ++k) p->M[k] = (int32_t)m;
+  } else {  // per octave: groups {0}, {K+1}, CQ octaves floor((k-1)/B)
+    p->M[0] = (int32_t)even_smooth_ge(p->len[0]);
+    p->M[K + 1] = (int32_t)even_smooth_ge(p->len[K + 1]);
+    for (int64_t k0 = 1; k0 <= K; k0 += B) {
+      const int64_t k1 = (k0 + B - 1 < K) ? k0 + B - 1 : K;
+      int64_t mx = 0;
+      for (int64_t k = k0; k <= k1; ++k) mx = p->len[k] > mx ? p->len[k] : mx;
+      const int64_t m = even_smooth_ge(mx);
+      for (int64_t k = k0; k <= k1; ++k) p->M[k] = (int32_t)m;
+    }
+  }
+  p->off.assign(K + 3, 0);
+  p->goff.assign(K + 2, 0);
+  int64_t gl = 0;
+  for (int64_t k = 0; k < K + 2; ++k) {
+    if (p->M[k] < p->len[k])
+      return set_error(SLICQ_ENOTFRAME, "painless condition M_k >= L_k violated (P:170)");
+    p->off[k + 1] = p->off[k] + p->M[k];
+    p->goff[k] = gl;
+    gl += p->len[k];
+  }
+  p->C = p->off[K + 2];
+  // ---- frame diagonal over all 2K+2 channels (Prop. 2; weights per C1/C16).
+  // The mirror of CQ channel k (Table 1 row 2K+2-k) has g[Ls - j]: it adds g_k[j]^2
+  // at bin (-j) mod Ls.  The plateaus are their own mirrors.
+  std::vector<double> D(Ls, 0.0);
+  auto md = [Ls](int64_t j) { int64_t r = j % Ls; return r < 0 ? r + Ls : r; };
+  for (int64_t k = 0; k < K + 2; ++k)
+    for (int64_t i = 0; i < p->len[k]; ++i) {
+      const int64_t j = f[k].lo + i;
+      const double g2 = f[k].v[i] * f[k].v[i];
+      D[md(j)] += g2;
+      if (k >= 1 && k <= K) D[md(-j)] += g2;
+    }
+  for (int64_t j = 0; j < Ls; ++j)
+    if (!(D[j] > 0.0)) return set_error(SLICQ_ENOTFRAME, "frame diagonal vanishes (P:221)");
+  // canonical dual g~_k = g_k / D
+  p->g.resize(gl);
+  p->gdual.resize(gl);
+  for (int64_t k = 0; k < K + 2; ++k)
+    for (int64_t i = 0; i < p->len[k]; ++i) {
+      const int64_t j = f[k].lo + i;
+      p->g[p->goff[k] + i] = f[k].v[i];
+      p->gdual[p->goff[k] + i] = f[k].v[i] / D[md(j)];
+    }
+  // ---- slicing window h_0 (Tukey, essential length N, transitions tr, zero-padded to 2N;
+  // P:372-374, reading C11) and its canonical dual h_0 / sum_m T_{mN} h_0^2 (dualwincond
+  // P:354-356, reading C12)
+  p->h0.assign(2 * N, 0.0);
+  p->h0dual.assign(2 * N, 0.0);
+  const double A = (double)(N - tr) / 2.0, Bw = (double)(N + tr) / 2.0;
+  for (int64_t i = 0; i < 2 * N; ++i) {
+    const double t = std::fabs((double)(i - N));
+    if (t <= A) p->h0[i] = 1.0;
+    else if (t < Bw) {
+      const double c = std::cos(kPi * (t - A) / (2.0 * (double)tr));
+      p->h0[i] = c * c;
+    }
+  }
+  std::vector<double> per(N, 0.0);
+  for (int64_t i = 0; i < 2 * N; ++i) per[(i - N + 2 * N) % N] += p->h0[i] * p->h0[i];
+  for (int64_t i = 0; i < 2 * N; ++i)
+    if (p->h0[i] != 0.0) p->h0dual[i] = p->h0[i] / per[(i - N + 2 * N) % N];
+  return SLICQ_OK;
+}
+
+extern "C" {
+
+int plan_create_ex(double fs, double fmin, double fmax, int bins_per_octave, int64_t sl_len,
+                   int64_t tr_area, int rasterize, unsigned flags, slicq_plan **out) {
+  if (!out) return set_error(SLICQ_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!(fs > 0) || !std::isfinite(fs)) return set_error(SLICQ_EINVAL, "fs must be > 0");
+  if (!(fmin > 0) || !(fmin < fs / 2)) return set_error(SLICQ_EINVAL, "need 0 < fmin < fs/2");
+  if (!(fmax > fmin) || !std::isfinite(fmax)) return set_error(SLICQ_EINVAL, "need fmax > fmin");
+  if (bins_per_octave < 1) return set_error(SLICQ_EINVAL, "bins_per_octave must be >= 1");
+  if (sl_len < 8 || sl_len % 4 != 0 || !smooth235(sl_len) || sl_len > (int64_t(1) << 26))
+    return set_error(SLICQ_EINVAL, "sl_len must be divisible by 4, 2/3/5-smooth, 8..2^26");
+  if (tr_area < 2 || tr_area % 2 != 0 || tr_area >= sl_len / 2)
+    return set_error(SLICQ_EINVAL, "tr_area must be even, >= 2 and < sl_len/2 (P:373)");
+  if (rasterize < 0 || rasterize > 2) return set_error(SLICQ_EINVAL, "rasterize must be 0, 1, 2");
+  if (fmax > fs / 2) fmax = fs / 2;  // C4: cap at Nyquist
+  slicq_plan *p = new (std::nothrow) slicq_plan();
+  if (!p) return set_error(SLICQ_ENOMEM, "host allocation failed");
+  p->fs = fs;
+  p->fmin = fmin;
+  p->fmax = fmax;
+  p->B = bins_per_octave;
+  p->sl_len = sl_len;
+  p->N = sl_len / 2;
+  p->tr = tr_area;
+  p->raster = rasterize;
+  int rc = build_host_plan(p);
+  if (rc == SLICQ_OK && !(flags & SLICQ_PLAN_HOST_ONLY)) {
+    rc = slicq::configure_kernels(p);
+    if (rc == SLICQ_OK) rc = slicq::upload(p);
+  }
+  if (rc != SLICQ_OK) {
+    slicq::free_device(p);
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return SLICQ_OK;
+}
+
+int plan_create(double fs, double fmin, double fmax, int bins_per_octave, int64_t sl_len,
+                int64_t tr_area, int rasterize, slicq_plan **out) {
+  return plan_create_ex(fs, fmin, fmax, bins_per_octave, sl_len, tr_area, rasterize, 0u, out);
+}
+
+void plan_destroy(slicq_plan *p) {
+  if (!p) return;
+  slicq::free_device(p);
+  delete p;
+}
+
+int slicq_num_channels(const slicq_plan *p) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  return p->K + 2;
+}
+int slicq_num_cq_channels(const slicq_plan *p) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  return p->K;
+}
+int slicq_channel_lengths(const slicq_plan *p, int32_t *M) {
+  if (!p || !M) return set_error(SLICQ_EINVAL, "NULL argument");
+  std::memcpy(M, p->M.data(), sizeof(int32_t) * p->M.size());
+  return SLICQ_OK;
+}
+int slicq_channel_offsets(const slicq_plan *p, int64_t *off) {
+  if (!p || !off) return set_error(SLICQ_EINVAL, "NULL argument");
+  std::memcpy(off, p->off.data(), sizeof(int64_t) * p->off.size());
+  return SLICQ_OK;
+}
+int64_t slicq_coeffs_per_slice(const slicq_plan *p) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  return p->C;
+}
+int64_t slicq_sl_len(const slicq_plan *p) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  return p->sl_len;
+}
+int64_t slicq_padded_length(const slicq_plan *p, int64_t n) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  if (n < 1) return set_error(SLICQ_ESHAPE, "n must be >= 1");
+  return (n + p->sl_len - 1) / p->sl_len * p->sl_len;
+}
+int64_t slicq_num_slices(const slicq_plan *p, int64_t n) {
+  int64_t L = slicq_padded_length(p, n);
+  if (L < 0) return L;
+  return L / p->N;
+}
+int64_t slicq_halo(const slicq_plan *p) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  return (p->N + p->tr) / 2;
+}
+size_t slicq_workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch) {
+  if (!p || nslices < 1 || batch < 1) return 0;
+  return slicq::workspace_bytes(p, nslices, batch);
+}
+int64_t slicq_filter_total_length(const slicq_plan *p) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  return (int64_t)p->g.size();
+}
+int slicq_plan_export(const slicq_plan *p, int32_t *lo, int32_t *len, double *g, double *gdual,
+                      double *h0, double *h0dual, double *xi) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  if (lo) std::memcpy(lo, p->lo.data(), sizeof(int32_t) * p->lo.size());
+  if (len) std::memcpy(len, p->len.data(), sizeof(int32_t) * p->len.size());
+  if (g) std::memcpy(g, p->g.data(), sizeof(double) * p->g.size());
+  if (gdual) std::memcpy(gdual, p->gdual.data(), sizeof(double) * p->gdual.size());
+  if (h0) std::memcpy(h0, p->h0.data(), sizeof(double) * p->h0.size());
+  if (h0dual) std::memcpy(h0dual, p->h0dual.data(), sizeof(double) * p->h0dual.size());
+  if (xi) std::memcpy(xi, p->xi.data(), sizeof(double) * p->xi.size());
+  return SLICQ_OK;
+}
+const char *slicq_last_error(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------------ hot path entry points
+static int check_dev_plan(const slicq_plan *p) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  if (!p->has_device) return set_error(SLICQ_EINVAL, "plan was created host-only");
+  return SLICQ_OK;
+}
+
+int slicq_forward(const slicq_plan *p, const float *x, int64_t n, int64_t batch,
+                  slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream) {
+  (void)ws;
+  (void)ws_bytes;
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (n < 1 || batch < 1) return set_error(SLICQ_ESHAPE, "n and batch must be >= 1");
+  if (!x || !coeffs) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)x % 4 || (uintptr_t)coeffs % 8) return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  const int64_t L = slicq_padded_length(p, n);
+  const int64_t S = L / p->N;
+  return slicq::launch_forward(p, x, n, n, 0, L, 1, 0, S, batch, coeffs, stream);
+}
+
+int slicq_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n, int64_t batch,
+                  float *y, void *ws, size_t ws_bytes, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (n < 1 || batch < 1) return set_error(SLICQ_ESHAPE, "n and batch must be >= 1");
+  if (!y || !coeffs) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)y % 4 || (uintptr_t)coeffs % 8) return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  const int64_t L = slicq_padded_length(p, n);
+  const int64_t S = L / p->N;
+  return slicq::launch_inverse(p, coeffs, 0, S, S, batch, 1, n, L, y, n, 0, nullptr, 0, ws,
+                               ws_bytes, stream);
+}
+
+int slicq_forward_range(const slicq_plan *p, const float *x_local, int64_t x_len,
+                        int64_t x_stride, int64_t halo, int64_t slice0, int64_t nslices,
+                        int64_t total_slices, int64_t batch, slicq_c32 *coeffs_local,
+                        void *ws, size_t ws_bytes, void *stream) {
+  (void)ws;
+  (void)ws_bytes;
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (nslices < 1 || batch < 1 || slice0 < 0 || slice0 + nslices > total_slices || x_len < 0 ||
+      x_stride < x_len || total_slices < 2 || total_slices % 2)
+    return set_error(SLICQ_ESHAPE, "bad slice range / shape");
+  if (halo < slicq_halo(p) - 1 || halo % 2) return set_error(SLICQ_ESHAPE, "halo too small or odd");
+  if (!x_local || !coeffs_local) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  const int64_t L = total_slices * p->N;
+  return slicq::launch_forward(p, x_local, x_len, x_stride, slice0 * p->N - halo, L, 0, slice0,
+                               nslices, batch, coeffs_local, stream);
+}
+
+int slicq_inverse_range(const slicq_plan *p, const slicq_c32 *coeffs_local, int64_t slice0,
+                        int64_t nslices, int64_t total_slices, int64_t batch, float *y_local,
+                        int64_t y_stride, float *left_spill, int64_t halo, void *ws,
+                        size_t ws_bytes, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (nslices < 1 || batch < 1 || slice0 < 0 || slice0 + nslices > total_slices ||
+      y_stride < nslices * p->N || total_slices < 2)
+    return set_error(SLICQ_ESHAPE, "bad slice range / shape");
+  if (halo < slicq_halo(p) - 1) return set_error(SLICQ_ESHAPE, "halo too small");
+  if (!coeffs_local || !y_local || !left_spill) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  const int64_t L = total_slices * p->N;
+  return slicq::launch_inverse(p, coeffs_local, slice0, nslices, total_slices, batch, 0,
+                               nslices * p->N, L, y_local, y_stride, slice0 * p->N, left_spill,
+                               halo, ws, ws_bytes, stream);
+}
+
+int slicq_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,
+                      int64_t batch, void *stream) {
+  if (!y || !spill || count < 0 || batch < 1 || y_stride < count)
+    return set_error(SLICQ_ESHAPE, "bad overlap_add arguments");
+  if (count == 0) return SLICQ_OK;
+  return slicq::launch_overlap_add(y, y_stride, spill, count, batch, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// Internal structures shared by the host plan (plan.cpp) and the kernels (kernels.cu).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/slicq.h"
+
+namespace slicq {
+
+// Per stored channel, as the kernels read it (32 bytes, one __ldg of two int4).
+struct ChanDev {
+  int32_t lo;      // first bin of the unwrapped support J_k (C5)
+  int32_t len;     // L_k
+  int32_t M;       // M_k
+  int32_t goff;    // offset of g_k / dual_k in the filter tables
+  int32_t off;     // column offset of channel k in a coefficient row
+  int32_t twoff;   // offset of the e^{+2 pi i t / M_k} table
+  float scale;     // 1/sqrt(M_k)  (Alg. 1 sqrt(M)*IFFT incl. 1/M, Alg. 2 FFT/sqrt(M); C1)
+  int32_t lo_mod;  // lo_k mod M_k in [0, M_k)
+};
+
+// A packet = channels of one length M = M1*M2 processed together by one warp.
+struct PacketDev {
+  int32_t m1m2;     // M1 | (M2 << 8)
+  int32_t nch;      // channels in the packet
+  int32_t chan_off; // offset into the packet channel list
+  int32_t cost;     // work estimate (for ordering only)
+};
+
+struct DeviceTables {
+  ChanDev *chan = nullptr;
+  PacketDev *packets = nullptr;
+  int32_t *packet_chans = nullptr;
+  float *g = nullptr;       // fp32 g_k on J_k
+  float *gdual = nullptr;   // fp32 dual; plateaus pre-multiplied by 1/2 (Hermitian rule, C15)
+  float *h0 = nullptr;      // fp32 h_0[t+N], t in [-N, N)
+  float *h0dual = nullptr;  // fp32 h~_0[t+N]
+  float *tw2n = nullptr;    // float2: [64] e^{-i pi t/N} for t < 64, then [2N/64] for t = 64 h
+  float *twM = nullptr;     // float2 tables e^{+2 pi i t / M}
+  void *block = nullptr;    // single allocation holding all of the above
+  size_t bytes = 0;
+};
+
+struct KernelConfig {
+  int logN = 0;        // N = 2^logN complex points in the r2c FFT of a 2N slice
+  int threads = 0;     // CTA size
+  int scr = 0;         // per-warp scratch (float2 entries)
+  size_t smem = 0;     // dynamic shared memory bytes
+  int npackets = 0;
+};
+
+}  // namespace slicq
+
+struct slicq_plan {
+  // parameters
+  double fs, fmin, fmax;
+  int B;
+  int64_t sl_len, N, tr;
+  int raster;
+  // Table 1 layout
+  int K;
+  double Q;
+  std::vector<double> xi;  // xi_1..xi_K
+  // stored channels 0..K+1
+  std::vector<int32_t> lo, len, M;
+  std::vector<int64_t> off;   // K+3 entries
+  std::vector<int64_t> goff;  // K+2 entries
+  std::vector<double> g, gdual;
+  std::vector<double> h0, h0dual;
+  int64_t C;  // sum M_k
+  // device side
+  bool has_device = false;
+  int device = -1;
+  slicq::DeviceTables d;
+  slicq::KernelConfig kc;
+  std::vector<slicq::PacketDev> packets;
+  std::vector<int32_t> packet_chans;
+  std::vector<int32_t> twoff;
+};
+
+namespace slicq {
+int set_error(int code, const std::string &msg);
+// kernels.cu
+int device_supports(int logN);
+int configure_kernels(slicq_plan *p);  // fills p->kc, packets (host)
+int upload(slicq_plan *p);             // allocates + copies device tables
+void free_device(slicq_plan *p);
+int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x_stride,
+                   int64_t base_off, int64_t L, int wrap, int64_t slice0, int64_t nslices,
+                   int64_t batch, slicq_c32 *coeffs, void *stream);
+int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0, int64_t nslices,
+                   int64_t total_slices, int64_t batch, int circular, int64_t n_valid,
+                   int64_t L, float *y, int64_t y_stride, int64_t y_base, float *left_spill,
+                   int64_t halo, void *ws, size_t ws_bytes, void *stream);
+int launch_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,
+                       int64_t batch, void *stream);
+size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
+}  // namespace slicq

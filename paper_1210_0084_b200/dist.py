@@ -1,0 +1,160 @@
+"""Multi-GPU partition of one long stream into contiguous slice ranges.
+
+One process per GPU.  Rank r of G owns slices [s_r, s_{r+1}), s_r = floor(r S / G), and the
+input samples [s_r N, s_{r+1} N).  The only data exchanged between ranks is the overlap of
+neighbouring slices (the paper's hop-N overlap, with circular indices P:328):
+
+* forward: slice s_r's Tukey window reaches (N+tr)/2 - 1 samples to the left of s_r N, so
+  rank r receives that left halo from rank r-1 (rank 0 from rank G-1: circular wrap);
+* inverse: slice s_r's overlap-add output spills onto the same samples, so rank r sends
+  that spill to rank r-1, which adds it (slicq_overlap_add kernel).
+
+Both exchanges are one grouped point-to-point send/recv pair per call
+(torch.distributed.batch_isend_irecv; NCCL over NVLink on GPUs, gloo in the CPU tests).
+All transform arithmetic runs in the backend's range calls (libslicq.so for the product;
+the tests substitute the oracle to check this host logic without a GPU).
+"""
+from __future__ import annotations
+
+from typing import Optional, Protocol
+
+import torch
+import torch.distributed as dist
+
+
+class RangeBackend(Protocol):
+    N: int
+    halo: int
+
+    def num_slices(self, n: int) -> int: ...
+
+    def forward_range(self, x_local, halo, slice0, nslices, total_slices): ...
+
+    def inverse_range(self, c_local, slice0, nslices, total_slices, halo): ...
+
+    def overlap_add(self, y_tail, spill) -> None: ...
+
+
+def slice_bounds(S: int, world: int):
+    return [r * S // world for r in range(world + 1)]
+
+
+class SliceRangeShard:
+    """This rank's share of a sliCQ forward/inverse over one long stream."""
+
+    def __init__(self, backend: RangeBackend, n: int, batch: int = 1, rank: Optional[int] = None,
+                 world: Optional[int] = None, group=None):
+        self.b = backend
+        self.n = n
+        self.batch = batch
+        self.group = group
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.world = dist.get_world_size(group) if world is None else world
+        self.N = backend.N
+        self.S = backend.num_slices(n)
+        if self.S < self.world:
+            raise ValueError(f"{self.S} slices cannot be split over {self.world} ranks")
+        self.halo = backend.halo
+        bnd = slice_bounds(self.S, self.world)
+        self.s0, self.s1 = bnd[self.rank], bnd[self.rank + 1]
+        self.ns = self.s1 - self.s0
+        self.L = self.S * self.N
+        if self.ns * self.N < self.halo:
+            raise ValueError("local range shorter than the halo")
+
+    # ------------------------------------------------------------ data placement
+    @property
+    def own(self):
+        """Global sample range [a, b) this rank holds (before trimming to n)."""
+        return self.s0 * self.N, self.s1 * self.N
+
+    def local_input(self, x_full: torch.Tensor, device=None) -> torch.Tensor:
+        """[batch][halo + ns N] buffer: own samples at [halo:], zeros for padding positions
+        >= n; the first `halo` entries are filled by :meth:`exchange_halo`."""
+        a, b = self.own
+        xl = torch.zeros((self.batch, self.halo + self.ns * self.N), dtype=x_full.dtype,
+                         device=device if device is not None else x_full.device)
+        hi = min(b, self.n)
+        if hi > a:
+            xl[:, self.halo:self.halo + hi - a] = x_full[:, a:hi].to(xl.device)
+        return xl
+
+    def _p2p(self, send: torch.Tensor, dst: int, recv: torch.Tensor, src: int):
+        ops = [dist.P2POp(dist.isend, send, self._g(dst), group=self.group),
+               dist.P2POp(dist.irecv, recv, self._g(src), group=self.group)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+    def _g(self, r: int) -> int:
+        return dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def exchange_halo(self, xl: torch.Tensor) -> None:
+        """Left halo <- last `halo` own samples of rank r-1 (rank G-1 for rank 0)."""
+        h = self.halo
+        tail = xl[:, -h:].contiguous()
+        if self.world == 1:
+            xl[:, :h] = tail
+            return
+        head = torch.empty_like(tail)
+        self._p2p(tail, (self.rank + 1) % self.world, head, (self.rank - 1) % self.world)
+        xl[:, :h] = head
+
+    def exchange_spill(self, spill: torch.Tensor) -> torch.Tensor:
+        """Send my left spill to rank r-1, receive rank r+1's spill (circularly)."""
+        if self.world == 1:
+            return spill
+        recv = torch.empty_like(spill)
+        self._p2p(spill.contiguous(), (self.rank - 1) % self.world, recv,
+                  (self.rank + 1) % self.world)
+        return recv
+
+    # ------------------------------------------------------------ transform
+    def forward(self, xl: torch.Tensor) -> torch.Tensor:
+        """Coefficients of slices [s0, s1): [batch][ns][C]."""
+        self.exchange_halo(xl)
+        return self.b.forward_range(xl, self.halo, self.s0, self.ns, self.S)
+
+    def inverse(self, c_local: torch.Tensor) -> torch.Tensor:
+        """Overlap-added output of samples [s0 N, s1 N): [batch][ns N]."""
+        y, spill = self.b.inverse_range(c_local, self.s0, self.ns, self.S, self.halo)
+        recv = self.exchange_spill(spill)
+        self.b.overlap_add(y[:, -self.halo:], recv)
+        return y
+
+    def gather_output(self, y_local: torch.Tensor) -> Optional[torch.Tensor]:
+        """Concatenate every rank's y_local on rank 0 (tests/diagnostics only), trimmed to n."""
+        parts = [torch.empty_like(y_local) for _ in range(self.world)] if self.rank == 0 else None
+        if self.world == 1:
+            return y_local[:, :self.n]
+        sizes = [(slice_bounds(self.S, self.world)[r + 1] - slice_bounds(self.S, self.world)[r])
+                 for r in range(self.world)]
+        mx = max(sizes) * self.N
+        pad = torch.zeros((self.batch, mx), dtype=y_local.dtype, device=y_local.device)
+        pad[:, :y_local.shape[1]] = y_local
+        out = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(out, pad, group=self.group)
+        if self.rank != 0:
+            return None
+        full = torch.cat([o[:, :sizes[r] * self.N] for r, o in enumerate(out)], dim=1)
+        return full[:, :self.n]
+
+
+class LibBackend:
+    """RangeBackend over libslicq.so (api.Plan)."""
+
+    def __init__(self, plan):
+        self.plan = plan
+        self.N = plan.N
+        self.halo = plan.halo
+
+    def num_slices(self, n):
+        return self.plan.num_slices(n)
+
+    def forward_range(self, x_local, halo, slice0, nslices, total_slices):
+        return self.plan.forward_range(x_local, halo, slice0, nslices, total_slices)
+
+    def inverse_range(self, c_local, slice0, nslices, total_slices, halo):
+        return self.plan.inverse_range(c_local, slice0, nslices, total_slices, halo)
+
+    def overlap_add(self, y_tail, spill):
+        self.plan.overlap_add(y_tail, spill)

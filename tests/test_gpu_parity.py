@@ -1,0 +1,263 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+fp32 inputs.  Tolerance (north_star / SURVEY §8(c) C17): relative L2 error <= 1e-5 on the
+coefficients of every slice and on the reconstruction."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import cqplan
+from oracle import slicq as oslicq
+from synth.configs import CONFIGS, plan_args
+from synth.signals import make_signal, random_signal
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def api():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1210_0084_b200 import build
+    build.build()
+    from paper_1210_0084_b200 import api as _api
+    return _api
+
+
+def slice_errors(c_gpu: np.ndarray, c_ref: np.ndarray) -> np.ndarray:
+    """C17: per-slice ||c_gpu - c_ref|| / ||c_ref||; near-silent slices (norm < 1e-6 * RMS of
+    slice norms) are judged absolutely against that RMS."""
+    c_gpu = c_gpu.astype(np.complex128)
+    nr = np.linalg.norm(c_ref, axis=-1)
+    rms = np.sqrt(np.mean(nr ** 2)) if nr.size else 0.0
+    err = np.linalg.norm(c_gpu - c_ref, axis=-1)
+    out = np.where(nr >= 1e-6 * rms, err / np.maximum(nr, 1e-300), err / max(rms, 1e-300))
+    return out
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b)
+
+
+def gpu_forward(plan, x_np):
+    x = torch.from_numpy(x_np).cuda()
+    c = plan.forward(x)
+    torch.cuda.synchronize()
+    return c
+
+
+def check_forward(plan, ref, x_np, slices=None):
+    c = gpu_forward(plan, x_np)
+    B = x_np.shape[0]
+    S = c.shape[1]
+    ms = list(range(S)) if slices is None else slices
+    worst = 0.0
+    for b in range(B):
+        cr = oslicq.forward(x_np[b:b + 1], ref, slices=ms)[0]
+        cg = c[b, ms].cpu().numpy()
+        e = slice_errors(cg, cr)
+        worst = max(worst, float(e.max()))
+    assert worst <= TOL, f"max per-slice coefficient rel. L2 error {worst:.3e}"
+    return c, worst
+
+
+# ------------------------------------------------------------------ cfg1 (configs[0])
+def test_cfg1_forward_every_slice(api):
+    cfg = CONFIGS[1]
+    plan = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    x = make_signal(1)
+    check_forward(plan, ref, x)
+
+
+def test_cfg1_roundtrip_and_inverse_parity(api):
+    cfg = CONFIGS[1]
+    plan = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    x = make_signal(1)
+    c = gpu_forward(plan, x)
+    y = plan.inverse(c, x.shape[1]).cpu().numpy()
+    assert rel(y[0], x[0].astype(np.float64)) <= TOL
+    # inverse of the oracle's coefficients against the oracle's inverse
+    cr = oslicq.forward(x, ref)
+    yg = plan.inverse(torch.from_numpy(cr.astype(np.complex64)).cuda(), x.shape[1]).cpu().numpy()
+    yr = oslicq.inverse(cr, ref, x.shape[1])
+    assert rel(yg[0], yr[0]) <= TOL
+
+
+def test_inverse_of_modified_coefficients(api):
+    # arbitrary (non-Hermitian-consistent) coefficients: GPU half-spectrum rule vs the
+    # oracle's full 2K+2-channel synthesis + real part (C15)
+    cfg = CONFIGS[1]
+    plan = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    n = 40000
+    S = plan.num_slices(n)
+    rng = np.random.default_rng(99)
+    c = (rng.standard_normal((1, S, plan.coeffs_per_slice)) +
+         1j * rng.standard_normal((1, S, plan.coeffs_per_slice))).astype(np.complex64)
+    yg = plan.inverse(torch.from_numpy(c).cuda(), n).cpu().numpy()
+    yr = oslicq.inverse(c.astype(np.complex128), ref, n)
+    assert rel(yg[0], yr[0]) <= TOL
+
+
+@pytest.mark.parametrize("raster", [1, 2])
+def test_rasterized_variants(api, raster):
+    c1 = CONFIGS[1]
+    args = (c1.fs, c1.fmin, c1.fmax, c1.bins_per_octave, c1.sl_len, c1.tr_area, raster)
+    plan = api.Plan(*args)
+    ref = cqplan.make_plan(*args)
+    x = make_signal(1)
+    c, _ = check_forward(plan, ref, x)
+    y = plan.inverse(c, x.shape[1]).cpu().numpy()
+    assert rel(y[0], x[0].astype(np.float64)) <= TOL
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("n,batch", [(1, 1), (5, 2), (16383, 1), (16385, 3), (24577, 2),
+                                     (3 * 16384, 1)])
+def test_ragged_lengths_and_batches(api, n, batch):
+    cfg = CONFIGS[1]
+    plan = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    x = random_signal(1000 + n, batch, n)
+    c, _ = check_forward(plan, ref, x)
+    y = plan.inverse(c, n).cpu().numpy()
+    for b in range(batch):
+        assert rel(y[b], x[b].astype(np.float64)) <= TOL
+
+
+def test_zero_input_and_impulse_locality(api):
+    cfg = CONFIGS[1]
+    plan = api.plan_for_config(cfg)
+    n = 6 * 16384
+    z = torch.zeros(1, n, device="cuda")
+    c = plan.forward(z)
+    assert torch.count_nonzero(c).item() == 0
+    assert torch.count_nonzero(plan.inverse(c, n)).item() == 0
+    N = plan.N
+    x = torch.zeros(1, n, device="cuda")
+    x[0, 5 * N] = 1.0  # centre of slice 5: every other slice's window is 0 there
+    c = plan.forward(x)[0]
+    nz = [m for m in range(c.shape[0]) if torch.count_nonzero(c[m]).item() > 0]
+    assert nz == [5]
+
+
+def test_linearity(api):
+    plan = api.plan_for_config(CONFIGS[1])
+    a = torch.from_numpy(random_signal(5, 1, 50000)).cuda()
+    b = torch.from_numpy(random_signal(6, 1, 50000)).cuda()
+    ca, cb, cab = plan.forward(a), plan.forward(b), plan.forward(a + 2 * b)
+    d = (cab - (ca + 2 * cb)).abs().max().item()
+    assert d <= 1e-5 * cab.abs().max().item()
+
+
+@pytest.mark.parametrize("args", [
+    (44100.0, 100.0, 20000.0, 24, 4096, 512, 0),
+    (44100.0, 50.0, 22050.0, 48, 8192, 1024, 0),
+    (48000.0, 40.0, 24000.0, 12, 8192, 2, 0),          # shortest transition
+    (44100.0, 65.4, 22050.0, 12, 16384, 8190, 0),      # longest transition tr = N - 2
+    (22050.0, 30.0, 11025.0, 36, 32768, 4096, 0),
+])
+def test_other_slice_lengths(api, args):
+    plan = api.Plan(*args)
+    ref = cqplan.make_plan(*args)
+    n = 5 * args[4] // 2 + 77
+    x = random_signal(int(args[4]) + args[5], 2, n)
+    c, _ = check_forward(plan, ref, x)
+    y = plan.inverse(c, n).cpu().numpy()
+    for b in range(2):
+        assert rel(y[b], x[b].astype(np.float64)) <= TOL
+
+
+# ------------------------------------------------------------------ configs 2-4
+def test_cfg2_full(api):
+    cfg = CONFIGS[2]
+    plan = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    x = make_signal(2)
+    c, _ = check_forward(plan, ref, x)
+    y = plan.inverse(c, x.shape[1]).cpu().numpy()
+    assert rel(y[0], x[0].astype(np.float64)) <= TOL
+
+
+def test_cfg3_subset(api):
+    cfg = CONFIGS[3]
+    plan = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    x = make_signal(3, batch=4)
+    S = plan.num_slices(x.shape[1])
+    check_forward(plan, ref, x, slices=[0, 1, S // 2, S - 1])
+    c = plan.forward(torch.from_numpy(x).cuda())
+    y = plan.inverse(c, x.shape[1]).cpu().numpy()
+    for b in range(4):
+        assert rel(y[b], x[b].astype(np.float64)) <= TOL
+
+
+@pytest.mark.slow
+def test_cfg4_full_size_sampled(api):
+    """BASELINE configs[3] at full size in the launch configuration bench.py times:
+    sampled slices against the oracle, full-length reconstruction, sampled inverse parity."""
+    cfg = CONFIGS[4]
+    plan = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    x = make_signal(4)
+    n = x.shape[1]
+    xt = torch.from_numpy(x).cuda()
+    c = plan.forward(xt)
+    S = c.shape[1]
+    rng = np.random.default_rng(4)
+    ms = sorted(set([0, 1, 2, S // 2, S - 2, S - 1] + rng.integers(0, S, 4).tolist()))
+    cr = oslicq.forward(x, ref, slices=ms)[0]
+    e = slice_errors(c[0, ms].cpu().numpy(), cr)
+    assert e.max() <= TOL, e
+    y = plan.inverse(c, n)
+    err = (torch.linalg.vector_norm((y - xt).double()) / torch.linalg.vector_norm(xt.double())).item()
+    assert err <= TOL
+    # sampled inverse parity: oracle Alg. 4 on windows covering slice boundaries
+    N = plan.N
+    yg = y[0].cpu().numpy()
+    for a in (0, 5 * N - 3000, (S // 2) * N + 1000, n - 7000):
+        b = min(n, a + 6000)
+        need = oslicq.needed_slices(a, b, ref, n)
+        cs = oslicq.forward(x, ref, slices=need)[0]
+        yr = oslicq.inverse_samples({m: cs[i] for i, m in enumerate(need)}, ref, n, a, b)
+        assert rel(yg[a:b], yr) <= TOL
+
+
+def test_cfg5_reports_unsupported_cleanly(api):
+    from paper_1210_0084_b200._lib import SlicqError
+    with pytest.raises(SlicqError) as ei:
+        api.plan_for_config(CONFIGS[5])
+    assert ei.value.code == -7  # SLICQ_EUNSUPPORTED (2N = 131072 not yet on the device path)
+
+
+# ------------------------------------------------------------------ slice-range API
+@pytest.mark.parametrize("G", [2, 3])
+def test_range_api_matches_full(api, G):
+    cfg = CONFIGS[1]
+    plan = api.plan_for_config(cfg)
+    n = 9 * 16384 + 123
+    x = torch.from_numpy(random_signal(77, 2, n)).cuda()
+    c_full = plan.forward(x)
+    y_full = plan.inverse(c_full, n)
+    N, S = plan.N, plan.num_slices(n)
+    L = S * N
+    halo = plan.halo
+    xp = torch.zeros(2, L, device="cuda")
+    xp[:, :n] = x
+    bounds = [r * S // G for r in range(G + 1)]
+    ys, spills = [], []
+    for r in range(G):
+        s0, s1 = bounds[r], bounds[r + 1]
+        idx = torch.arange(s0 * N - halo, s1 * N, device="cuda") % L
+        xl = xp[:, idx].contiguous()
+        cl = plan.forward_range(xl, halo, s0, s1 - s0, S)
+        assert torch.equal(cl, c_full[:, s0:s1])
+        yl, sp = plan.inverse_range(c_full[:, s0:s1].contiguous(), s0, s1 - s0, S, halo)
+        ys.append(yl)
+        spills.append(sp)
+    for r in range(G):
+        tail = ys[r][:, -halo:]
+        api.Plan.overlap_add(tail, spills[(r + 1) % G])
+    y = torch.cat(ys, dim=1)[:, :n]
+    assert torch.equal(y, y_full)
