@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""sliCQ forward+inverse throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl reference]
+
+A *step* is one pass of the whole hot path — slicq_forward then slicq_inverse (every row
+of SURVEY.md §8(a)) — over the config's whole synthetic workload.  Default workload:
+BASELINE configs[3] ("cfg4": one hour of 48 kHz mono, 172.8 M samples, 21 094 slices of
+2N = 16384), the config the north_star's multi-GPU target is stated on; configs[0..1]
+are microsecond-scale (8 / 28 slices) and serve as parity cases.
+
+N = 1: one process, slicq_forward + slicq_inverse on the whole stream (circular slices).
+N > 1 (torchrun): contiguous slice ranges per rank with the NCCL halo / spill exchange
+(paper_1210_0084_b200/dist.py), total work fixed => "scaling": "strong".
+
+Timing: W warm-up steps; barrier + synchronize; CUDA events on the launching stream around
+exactly K steps; barrier + synchronize; max over ranks.  Inputs (691 MB) and coefficients
+(3 GB) are far larger than the 126 MB L2, so no flush is needed between steps.
+`--impl reference` times the fp64 oracle (oracle/, the test oracle) on the host cores
+instead — a deliberately slow reference, reported, not a target.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "sliCQ fwd+inv input samples/s"
+UNIT = "samples/s"
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region."""
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.ok = False
+        self.samples, self.reasons = [], set()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "nvml unavailable"}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def oracle_sample_rate(cfg, nsl: int = 12, budget_s: float = 20.0):
+    """The fp64 oracle as it stands (single process; numpy's pocketfft is single-threaded),
+    forward + inverse of `nsl` consecutive slices of the config via its slice-range functions.
+    Returns (samples/s, seconds, description)."""
+    from oracle import cqplan
+    from oracle import slicq as oslicq
+    from synth.configs import plan_args
+    from synth.signals import random_signal
+    ref = cqplan.make_plan(*plan_args(cfg))
+    N = ref.N
+    halo = (N + ref.tr) // 2
+    x = random_signal(cfg.seed, 1, halo + nsl * N)[0].astype(np.float64)
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        c = oslicq.forward_range(x, halo, 1000, nsl, ref)
+        oslicq.inverse_range(c, 1000, nsl, ref, halo)
+        done += 1
+        if time.perf_counter() - t0 > budget_s * 0.5 or done >= 3:
+            break
+    dt = (time.perf_counter() - t0) / done
+    return nsl * N / dt, dt, (f"{nsl} consecutive slices of {cfg.name} ({nsl * N} input samples), "
+                              f"oracle.slicq.forward_range + inverse_range, fp64 NumPy, 1 process")
+
+
+def run_reference(args, cfg):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return  # rank 0 alone runs and prints the reference arm
+    per = []
+    desc = None
+    for _ in range(args.warmup):
+        oracle_sample_rate(cfg, budget_s=5.0)
+    for _ in range(args.steps):
+        v, dt, desc = oracle_sample_rate(cfg, budget_s=5.0)
+        per.append(dt)
+    nsamp = 12 * (cfg.sl_len // 2)
+    value = nsamp / (sum(per) / len(per))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(per) / len(per), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(cfg, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, world):
+    return {"workload": f"BASELINE configs[{cfg.cfg - 1}] ({cfg.name})", "batch": cfg.batch,
+            "samples_per_row": cfg.n, "fs": cfg.fs, "fmin": cfg.fmin, "fmax": cfg.fmax_eff,
+            "bins_per_octave": cfg.bins_per_octave, "sl_len": cfg.sl_len, "tr_area": cfg.tr_area,
+            "rasterize": cfg.rasterize,
+            "parallelism": "single GPU" if world == 1 else f"slice ranges x{world} (NCCL halo)",
+            "l2": "no flush: inputs and coefficients exceed the 126 MB L2"}
+
+
+def run_gpu(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1210_0084_b200 import api
+    from paper_1210_0084_b200.dist import LibBackend, SliceRangeShard
+    from synth.signals import make_signal
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    plan = api.plan_for_config(cfg)
+    x_np = make_signal(cfg.cfg)
+    B, n = x_np.shape
+    C = plan.coeffs_per_slice
+    stream = torch.cuda.current_stream()
+
+    if world == 1:
+        x = torch.from_numpy(x_np).to(dev)
+        c = torch.empty((B, plan.num_slices(n), C), dtype=torch.complex64, device=dev)
+        y = torch.empty((B, n), dtype=torch.float32, device=dev)
+        S_local = c.shape[1]
+        L_local = plan.padded_length(n)
+        launches_per_step = 2
+
+        def fwd():
+            plan.forward(x, out=c)
+
+        def inv():
+            plan.inverse(c, n, out=y)
+    else:
+        shard = SliceRangeShard(LibBackend(plan), n, B, rank, world)
+        xl = shard.local_input(torch.from_numpy(x_np), device=dev)
+        S_local = shard.ns
+        L_local = shard.ns * plan.N
+        state = {}
+        launches_per_step = 3  # forward_range, inverse_range, overlap_add
+
+        def fwd():
+            state["c"] = shard.forward(xl)
+
+        def inv():
+            state["y"] = shard.inverse(state["c"])
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for _ in range(args.warmup):
+        fwd()
+        inv()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e_f0, e_f1, e_i1 = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)], \
+        [ev() for _ in range(args.steps)]
+    t_start, t_end = ev(), ev()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for k in range(args.steps):
+            e_f0[k].record(stream)
+            fwd()
+            e_f1[k].record(stream)
+            inv()
+            e_i1[k].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_total = t_start.elapsed_time(t_end)
+    ms_f = sum(e_f0[k].elapsed_time(e_f1[k]) for k in range(args.steps)) / args.steps
+    ms_i = sum(e_f1[k].elapsed_time(e_i1[k]) for k in range(args.steps)) / args.steps
+    t = torch.tensor([ms_total, ms_f, ms_i], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, ms_f, ms_i = t.tolist()
+    ms_step = ms_total / args.steps
+    samples = B * n
+    value = samples / (ms_step / 1e3)
+
+    # parity spot-check of this run's output (reconstruction, C17)
+    if world == 1:
+        rec = (torch.linalg.vector_norm((y - x).double()) / torch.linalg.vector_norm(x.double())).item()
+    else:
+        yl = state["y"]
+        a, b = shard.own
+        hi = min(b, n) - a
+        xs = torch.from_numpy(x_np[:, a:a + hi]).to(dev) if hi > 0 else None
+        num = torch.tensor([0.0, 0.0], dtype=torch.float64, device=dev)
+        if hi > 0:
+            num[0] = torch.sum((yl[:, :hi] - xs).double() ** 2)
+            num[1] = torch.sum(xs.double() ** 2)
+        dist.all_reduce(num)
+        rec = float((num[0] / num[1]).sqrt())
+
+    # roofline for the dominant kernel (algorithmic bytes)
+    peak, peak_src = peaks()
+    bytes_fwd = B * (4 * L_local + 8 * S_local * C)  # read x once, write complex64 coefficients
+    bytes_inv = bytes_fwd                             # read coefficients, write y
+    dom = "slicq_inv_kernel" if ms_i >= ms_f else "slicq_fwd_kernel"
+    ms_dom = max(ms_i, ms_f)
+    achieved = (bytes_inv if dom == "slicq_inv_kernel" else bytes_fwd) / (ms_dom / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"cfg{cfg.cfg}", {}).get(dom)
+        except Exception:
+            traffic = None
+
+    # end to end through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        xh = torch.from_numpy(x_np).pin_memory()
+        yh = torch.empty((B, n), dtype=torch.float32).pin_memory()
+        xd = torch.empty_like(x)
+        ke = max(2, min(args.steps, 5))
+        for _ in range(1):
+            xd.copy_(xh, non_blocking=True)
+            plan.forward(xd, out=c)
+            plan.inverse(c, n, out=y)
+            yh.copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+        a0, a1 = ev(), ev()
+        a0.record(stream)
+        for _ in range(ke):
+            xd.copy_(xh, non_blocking=True)
+            plan.forward(xd, out=c)
+            plan.inverse(c, n, out=y)
+            yh.copy_(y, non_blocking=True)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = a0.elapsed_time(a1) / ke
+        e2e = {"value": samples / (ms_e2e / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * B * n, "d2h_bytes_per_step": 4 * B * n,
+               "ms_per_step": ms_e2e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, dt, desc = oracle_sample_rate(cfg)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, world),
+            "forward_samples_per_s": samples / (ms_f / 1e3),
+            "inverse_samples_per_s": samples / (ms_i / 1e3),
+            "ms_forward": ms_f, "ms_inverse": ms_i,
+            "recon_rel_l2": rec,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic,
+                         "algorithmic_bytes_per_launch": bytes_inv if dom == "slicq_inv_kernel" else bytes_fwd},
+            "roofline_step_frac": (bytes_fwd + bytes_inv) / (ms_step / 1e3) / 1e9 / peak,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "cuda" else args.warmup
+    from synth.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,19 +1,23 @@
-// sm_100a kernels of the sliCQ hot path (device code; instantiated per slice size in kernels_l*.cu).
+// sm_100a kernels of the sliCQ hot path (device code, instantiated per slice size in
+// kernels_l<LOGN>.cu).  DESIGN.md "Kernels" describes the design; step names follow
+// SURVEY.md §8(a).
 //
 //   slicq_fwd_kernel<LOGN>  one CTA per (signal row, slice):
 //     F1  gather the Tukey-windowed slice straight from HBM
-//     F2  r2c FFT_{2N} as a complex N-point Stockham FFT in shared memory + packing
-//         step, register-resident radix-16/32 passes            (Alg. 1 line P:186)
+//     F2  r2c FFT_{2N}: complex N-point Stockham FFT in shared memory (register radix
+//         16/32 passes) + packing step                          (Alg. 1 line P:186)
 //     F3  per channel: multiply by g_k, fold to M_k             (C5)
-//     F4  sqrt(M_k) IFFT_{M_k}: four-step M1 x M2 register DFTs per warp "packet"
-//     F5  coalesced store of c^m_k                              (P:320-323 layout view)
+//     F4  sqrt(M_k) IFFT_{M_k} as a four-step M1 x M2 register DFT; channels of one length
+//         form a warp "packet" (<= 32 tasks per step, one per lane)
+//     F5  store c^m_k                                           (P:320-323 layout view)
 //   slicq_inv_kernel<LOGN>  one CTA per (row, slice):
-//     I1/I2  load c^m_k, FFT_{M_k}/sqrt(M_k) (four-step)
-//     I3  multiply by the dual g~_k and scatter-add into the half spectrum with the
-//         Hermitian rule of C15
-//     I4  c2r IFFT_{2N} (packing step + N-point Stockham)         (P:203)
-//     I5  multiply by h~_0 and overlap-add; slice-boundary samples are paired across
-//         CTAs through the workspace with a parity counter (no spin, deterministic)
+//     I1/I2  load c^m_k, FFT_{M_k} (four-step, in place in the chunk scratch)
+//     I3  dual multiply + overlap sum as a per-bin GATHER: every half-spectrum bin is
+//         summed by one thread from plan-time (F position, dual weight, conj) lists, with the
+//         Hermitian rule of C15 folded in -- deterministic, no atomics
+//     I4  c2r IFFT_{2N} (packing step + N-point Stockham)        (P:203)
+//     I5  multiply by h~_0 and overlap-add; slice-boundary samples are paired across CTAs
+//         through the workspace with a parity counter (no spinning, deterministic a+b)
 //
 #pragma once
 #include <cuda_runtime.h>
@@ -32,23 +36,32 @@ constexpr unsigned FULL = 0xffffffffu;
 
 __host__ __device__ constexpr int padi(int i) { return i + (i >> 5); }
 
+// Big-FFT plans: N = 2^LOGN complex points, T threads, radix sequences per direction.
 template <int LOGN>
 struct Big;
 template <>
 struct Big<11> {
-  static constexpr int N = 2048, T = 128, R1 = 16, R2 = 16, R3 = 8, MINB = 2;
+  static constexpr int N = 2048, T = 128;
+  static constexpr int F1 = 16, F2 = 16, F3 = 8;   // forward pass radices
+  static constexpr int I1 = 8, I2 = 16, I3 = 16;   // inverse pass radices
 };
 template <>
 struct Big<12> {
-  static constexpr int N = 4096, T = 256, R1 = 16, R2 = 16, R3 = 16, MINB = 2;
+  static constexpr int N = 4096, T = 256;
+  static constexpr int F1 = 16, F2 = 16, F3 = 16;
+  static constexpr int I1 = 16, I2 = 16, I3 = 16;
 };
 template <>
 struct Big<13> {
-  static constexpr int N = 8192, T = 256, R1 = 32, R2 = 16, R3 = 16, MINB = 1;
+  static constexpr int N = 8192, T = 512;
+  static constexpr int F1 = 16, F2 = 16, F3 = 32;
+  static constexpr int I1 = 32, I2 = 16, I3 = 16;
 };
 template <>
 struct Big<14> {
-  static constexpr int N = 16384, T = 512, R1 = 32, R2 = 32, R3 = 16, MINB = 1;
+  static constexpr int N = 16384, T = 512;
+  static constexpr int F1 = 32, F2 = 32, F3 = 16;
+  static constexpr int I1 = 16, I2 = 32, I3 = 32;
 };
 
 template <int LOGN>
@@ -61,7 +74,6 @@ constexpr int tw_entries() {
 }
 
 struct KArgs {
-  // forward input / inverse output
   const float *x;
   float *y;
   float *spill;
@@ -72,22 +84,25 @@ struct KArgs {
   int64_t slice0;
   int nslices;
   int tr;
-  int scr;
-  int npackets;
+  int scr;        // forward: per-warp scratch entries; inverse: chunk scratch entries
+  int npackets;   // forward packets
+  int nchunks;    // inverse chunks
   int64_t C;
   float2 *coef_out;
   const float2 *coef_in;
   const ChanDev *chan;
   const PacketDev *packets;
   const int32_t *pchans;
+  const ChunkDev *chunks;
+  const int32_t *bin_off;
+  const GatherEnt *gents;
   const float *g;
-  const float *gdual;
   const float *h0;
   const float *h0dual;
   const float2 *tw2n;
   const float2 *twM;
-  unsigned *cnt;    // inverse workspace: [batch][nslices] pairing counters
-  float *bnd;       // inverse workspace: [batch][nslices][2][tr] boundary halves
+  unsigned *cnt;  // inverse workspace: [batch][nslices] pairing counters
+  float *bnd;     // inverse workspace: [batch][nslices][2][tr] boundary halves
 };
 
 // e^{-i pi e / N} for e in [0, 2N): two-level table, 2 shared loads + 1 complex multiply
@@ -95,16 +110,29 @@ __device__ __forceinline__ float2 tw_lookup(const float2 *tw, int e) {
   return cmul(tw[64 + (e >> 6)], tw[e & 63]);
 }
 
-// Stockham twiddle for task j of a radix-R pass with span NS (twiddle before butterfly).
+// Stockham twiddles for task j of a radix-R pass with span NS (applied before the
+// butterfly): w^r for r = 1..R-1, w = e^{SIGN 2 pi i (j mod NS)/(NS R)}.  w^{4q} comes
+// from the table, w^{4q+s} = w^{4q} * w^s (s = 1..3): at most two roundings deep.
 template <int N, int R, int NS, int SIGN>
 __device__ __forceinline__ void pass_twiddle(float2 (&v)[R], int j, const float2 *tw) {
   if constexpr (NS > 1) {
+    static_assert(R % 4 == 0, "big-FFT radices are multiples of 4");
     constexpr int STEP = 2 * (N / (NS * R));  // units of e^{-i pi/N}
     const int base = (j & (NS - 1)) * STEP;
+    float2 w1 = tw_lookup(tw, base);
+    if (SIGN > 0) w1 = cconj(w1);
+    const float2 w2 = cmul(w1, w1);
+    const float2 w3 = cmul(w2, w1);
+    float2 w4q = make_float2(1.f, 0.f);
 #pragma unroll
     for (int r = 1; r < R; ++r) {
-      float2 w = tw_lookup(tw, (base * r) & (2 * N - 1));
-      if (SIGN > 0) w = cconj(w);
+      const int s = r & 3;
+      if (s == 0) {
+        w4q = tw_lookup(tw, (base * r) & (2 * N - 1));
+        if (SIGN > 0) w4q = cconj(w4q);
+      }
+      const float2 ws = s == 1 ? w1 : (s == 2 ? w2 : w3);
+      const float2 w = s == 0 ? w4q : (r < 4 ? ws : cmul(w4q, ws));
       v[r] = cmul(v[r], w);
     }
   }
@@ -114,24 +142,27 @@ __device__ __forceinline__ void pass_twiddle(float2 (&v)[R], int j, const float2
 template <int N, int R, int NS, int SIGN, int T>
 __device__ __forceinline__ void pass_smem(float2 *spec, const float2 *tw) {
   constexpr int TASKS = N / R;
-  static_assert(TASKS % T == 0, "tasks must divide evenly");
-  constexpr int PER = TASKS / T;
+  constexpr int PER = (TASKS + T - 1) / T;
   float2 v[PER][R];
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int j = threadIdx.x + q * T;
+    if (TASKS % T == 0 || j < TASKS) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[q][r] = spec[padi(j + r * TASKS)];
-    pass_twiddle<N, R, NS, SIGN>(v[q], j, tw);
-    dft<R, SIGN>(v[q]);
+      for (int r = 0; r < R; ++r) v[q][r] = spec[padi(j + r * TASKS)];
+      pass_twiddle<N, R, NS, SIGN>(v[q], j, tw);
+      dft<R, SIGN>(v[q]);
+    }
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int j = threadIdx.x + q * T;
-    const int base = (j / NS) * NS * R + (j & (NS - 1));
+    if (TASKS % T == 0 || j < TASKS) {
+      const int base = (j / NS) * NS * R + (j & (NS - 1));
 #pragma unroll
-    for (int r = 0; r < R; ++r) spec[padi(base + r * NS)] = v[q][r];
+      for (int r = 0; r < R; ++r) spec[padi(base + r * NS)] = v[q][r];
+    }
   }
   __syncthreads();
 }
@@ -139,131 +170,131 @@ __device__ __forceinline__ void pass_smem(float2 *spec, const float2 *tw) {
 // X(j) for an unwrapped bin j in (-2N, 2N) from the half spectrum X[0..N] (real input).
 template <int N>
 __device__ __forceinline__ float2 spec_at(const float2 *spec, int j) {
-  int jj = j < 0 ? j + 2 * N : j;
-  if (jj <= N) return spec[padi(jj)];
-  return cconj(spec[padi(2 * N - jj)]);
+  const int jj = j < 0 ? j + 2 * N : j;
+  const bool up = jj > N;
+  const float2 v = spec[padi(up ? 2 * N - jj : jj)];
+  return make_float2(v.x, up ? -v.y : v.y);
+}
+
+// v[n1] *= e^{SIGN 2 pi i p2 n1 / M}, n1 = 1..M1-1, from the per-M table e^{+2 pi i t/M}:
+// table loads at n1 = 1 and n1 = 4q, products for the rest.
+template <int M1, int SIGN>
+__device__ __forceinline__ void chan_twiddle(float2 (&v)[M1], int p2, int M, const float2 *tab) {
+  if constexpr (M1 > 1) {
+    float2 w1 = __ldg(tab + p2);
+    if (SIGN < 0) w1 = cconj(w1);
+    const float2 w2 = cmul(w1, w1);
+    const float2 w3 = cmul(w2, w1);
+    float2 w4q = make_float2(1.f, 0.f);
+    int step4 = 4 * p2;
+    while (step4 >= M) step4 -= M;
+    int e4 = 0;
+#pragma unroll
+    for (int n1 = 1; n1 < M1; ++n1) {
+      const int s = n1 & 3;
+      if (s == 0) {
+        e4 += step4;
+        if (e4 >= M) e4 -= M;
+        w4q = __ldg(tab + e4);
+        if (SIGN < 0) w4q = cconj(w4q);
+      }
+      const float2 ws = s == 1 ? w1 : (s == 2 ? w2 : w3);
+      const float2 w = s == 0 ? w4q : (n1 < 4 ? ws : cmul(w4q, ws));
+      v[n1] = cmul(v[n1], w);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ forward packet steps
+// Step 1, task (ci, p2): inputs buf[M2 p1 + p2] = X(j) g_k[j]/sqrt(M) for the bin j of J_k
+// congruent to M2 p1 + p2 (mod M), else 0 (fold / zero-pad, C5); DFT_{M1}; twiddle.
 template <int M1, int N>
 __device__ __forceinline__ void fwd_step1(const KArgs &a, const float2 *spec, float2 *scr,
                                           int m2, int nch, int chan_off, int lane) {
-  const int S2 = m2 | 1;
   const int nt = nch * m2;
-  for (int t = lane; t < nt; t += 32) {
-    const int ci = t / m2;
-    const int p2 = t - ci * m2;
-    const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
-    float2 v[M1];
-    int d = p2 - ch.lo_mod;
-    if (d < 0) d += ch.M;
+  if (lane >= nt) return;
+  const int ci = lane / m2;
+  const int p2 = lane - ci * m2;
+  const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
+  float2 v[M1];
+  int d = p2 - ch.lo_mod;
+  if (d < 0) d += ch.M;
 #pragma unroll
-    for (int p1 = 0; p1 < M1; ++p1) {
-      float2 val = make_float2(0.f, 0.f);
-      if (d < ch.len) val = cscale(spec_at<N>(spec, ch.lo + d), __ldg(a.g + ch.goff + d));
-      v[p1] = val;
-      d += m2;
-      if (d >= ch.M) d -= ch.M;
-    }
-    dft<M1, +1>(v);
-    int e = 0;
-#pragma unroll
-    for (int n1 = 1; n1 < M1; ++n1) {
-      e += p2;
-      if (e >= ch.M) e -= ch.M;
-      v[n1] = cmul(v[n1], __ldg(a.twM + ch.twoff + e));
-    }
-    float2 *A = scr + ci * M1 * S2 + p2;
-#pragma unroll
-    for (int n1 = 0; n1 < M1; ++n1) A[n1 * S2] = v[n1];
+  for (int p1 = 0; p1 < M1; ++p1) {
+    float2 val = make_float2(0.f, 0.f);
+    if (d < ch.len) val = cscale(spec_at<N>(spec, ch.lo + d), __ldg(a.g + ch.goff + d));
+    v[p1] = val;
+    d += m2;
+    if (d >= ch.M) d -= ch.M;
   }
+  dft<M1, +1>(v);
+  chan_twiddle<M1, +1>(v, p2, ch.M, a.twM + ch.twoff);
+  const int S2 = m2 | 1;
+  float2 *A = scr + ci * M1 * S2 + p2;
+#pragma unroll
+  for (int n1 = 0; n1 < M1; ++n1) A[n1 * S2] = v[n1];
 }
 
+// Step 2, task (ci, n1): DFT_{M2} over p2 -> c[n1 + M1 n2].
 template <int M2>
 __device__ __forceinline__ void fwd_step2(const KArgs &a, const float2 *scr, float2 *out_row,
                                           int m1, int nch, int chan_off, int lane) {
-  constexpr int S2 = M2 | 1;
   const int nt = nch * m1;
-  for (int t = lane; t < nt; t += 32) {
-    const int ci = t / m1;
-    const int n1 = t - ci * m1;
-    const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
-    float2 v[M2];
-    const float2 *A = scr + ci * m1 * S2 + n1 * S2;
+  if (lane >= nt) return;
+  constexpr int S2 = M2 | 1;
+  const int ci = lane / m1;
+  const int n1 = lane - ci * m1;
+  const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
+  float2 v[M2];
+  const float2 *A = scr + ci * m1 * S2 + n1 * S2;
 #pragma unroll
-    for (int p2 = 0; p2 < M2; ++p2) v[p2] = A[p2];
-    dft<M2, +1>(v);
-    float2 *o = out_row + ch.off + n1;
+  for (int p2 = 0; p2 < M2; ++p2) v[p2] = A[p2];
+  dft<M2, +1>(v);
+  float2 *o = out_row + ch.off + n1;
 #pragma unroll
-    for (int n2 = 0; n2 < M2; ++n2) o[m1 * n2] = cscale(v[n2], ch.scale);
-  }
+  for (int n2 = 0; n2 < M2; ++n2) o[m1 * n2] = v[n2];
 }
 
 // ------------------------------------------------------------------ inverse packet steps
 template <int M1>
-__device__ __forceinline__ void inv_step1(const KArgs &a, const float2 *in_row, float2 *scr,
+__device__ __forceinline__ void inv_step1(const KArgs &a, const float2 *in_row, float2 *reg,
                                           int m2, int nch, int chan_off, int lane) {
-  const int S2 = m2 | 1;
   const int nt = nch * m2;
-  for (int t = lane; t < nt; t += 32) {
-    const int ci = t / m2;
-    const int p2 = t - ci * m2;
-    const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
-    float2 v[M1];
-    const float2 *src = in_row + ch.off + p2;
+  if (lane >= nt) return;
+  const int ci = lane / m2;
+  const int p2 = lane - ci * m2;
+  const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
+  float2 v[M1];
+  const float2 *src = in_row + ch.off + p2;
 #pragma unroll
-    for (int p1 = 0; p1 < M1; ++p1) v[p1] = src[p1 * m2];
-    dft<M1, -1>(v);
-    int e = 0;
+  for (int p1 = 0; p1 < M1; ++p1) v[p1] = __ldcs(src + p1 * m2);
+  dft<M1, -1>(v);
+  chan_twiddle<M1, -1>(v, p2, ch.M, a.twM + ch.twoff);
+  const int S2 = m2 | 1;
+  float2 *A = reg + ci * M1 * S2 + p2;
 #pragma unroll
-    for (int n1 = 1; n1 < M1; ++n1) {
-      e += p2;
-      if (e >= ch.M) e -= ch.M;
-      v[n1] = cmul(v[n1], cconj(__ldg(a.twM + ch.twoff + e)));
-    }
-    float2 *A = scr + ci * M1 * S2 + p2;
-#pragma unroll
-    for (int n1 = 0; n1 < M1; ++n1) A[n1 * S2] = v[n1];
-  }
+  for (int n1 = 0; n1 < M1; ++n1) A[n1 * S2] = v[n1];
 }
 
-__device__ __forceinline__ void atomic_add_c(float2 *p, float2 v) {
-  atomicAdd(&p->x, v.x);
-  atomicAdd(&p->y, v.y);
-}
-
-template <int M2, int N>
-__device__ __forceinline__ void inv_step2(const KArgs &a, const float2 *scr, float2 *spec, int m1,
-                                          int nch, int chan_off, int lane) {
-  constexpr int S2 = M2 | 1;
+// Step 2 in place: every lane loads its row, the warp syncs, then F[n1 + M1 n2] (the
+// unnormalised FFT_{M} of c) overwrites the channel's region.
+template <int M2>
+__device__ __forceinline__ void inv_step2(float2 *reg, int m1, int nch, int lane) {
   const int nt = nch * m1;
-  for (int t = lane; t < nt; t += 32) {
-    const int ci = t / m1;
-    const int n1 = t - ci * m1;
-    const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
-    float2 v[M2];
-    const float2 *A = scr + ci * m1 * S2 + n1 * S2;
+  constexpr int S2 = M2 | 1;
+  const bool act = lane < nt;
+  const int ci = act ? lane / m1 : 0;
+  const int n1 = act ? lane - ci * m1 : 0;
+  float2 v[M2];
+  float2 *base = reg + ci * m1 * S2;
+  // idle lanes read row 0 too (valid memory) so that v is defined on every path
 #pragma unroll
-    for (int p2 = 0; p2 < M2; ++p2) v[p2] = A[p2];
-    dft<M2, -1>(v);
-    // F[q], q = n1 + m1 n2 ; bin j in J_k with j = q (mod M_k)
-    int d = n1 - ch.lo_mod;
-    if (d < 0) d += ch.M;
+  for (int p2 = 0; p2 < M2; ++p2) v[p2] = base[n1 * S2 + p2];
+  dft<M2, -1>(v);
+  __syncwarp();
+  if (act) {
 #pragma unroll
-    for (int n2 = 0; n2 < M2; ++n2) {
-      if (d < ch.len) {
-        const int j = ch.lo + d;
-        const float2 val = cscale(v[n2], ch.scale * __ldg(a.gdual + ch.goff + d));
-        // Hermitian rule (C15): v at j mod 2N if <= N; conj(v) at -j mod 2N if <= N
-        int p1 = j % (2 * N);
-        if (p1 < 0) p1 += 2 * N;
-        if (p1 <= N) atomic_add_c(spec + padi(p1), val);
-        const int p2m = p1 == 0 ? 0 : 2 * N - p1;
-        if (p2m <= N) atomic_add_c(spec + padi(p2m), cconj(val));
-      }
-      d += m1;
-      if (d >= ch.M) d -= ch.M;
-    }
+    for (int n2 = 0; n2 < M2; ++n2) base[n1 + m1 * n2] = v[n2];
   }
 }
 
@@ -272,7 +303,7 @@ __device__ __forceinline__ void inv_step2(const KArgs &a, const float2 *scr, flo
 
 // ------------------------------------------------------------------ forward kernel
 template <int LOGN>
-__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kernel(const KArgs a) {
+__global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_fwd_kernel(const KArgs a) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T, NW = T / 32;
   extern __shared__ float4 smem4[];
@@ -290,7 +321,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kerne
 
   // ---- F1 + first radix pass, read straight from HBM.  z[p] = f[2p] + i f[2p+1].
   {
-    constexpr int R = CF::R1, TASKS = N / R, PER = TASKS / T;
+    constexpr int R = CF::F1, TASKS = N / R, PER = (TASKS + T - 1) / T;
     const float *xr = a.x + row * a.x_stride;
     const bool vec = ((reinterpret_cast<uintptr_t>(xr) & 7) == 0);
     const int64_t s0 = (mg - 1) * N - a.base_off;  // local index of frame sample 0
@@ -299,45 +330,49 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kerne
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = tid + q * T;
+      if (TASKS % T == 0 || j < TASKS) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int p = j + r * TASKS;
-        const int i0 = 2 * p;  // frame index of the real part
-        const int t0 = i0 - N;
-        float2 val = make_float2(0.f, 0.f);
-        const int at0 = t0 < 0 ? -t0 : t0;
-        const int at1 = (t0 + 1) < 0 ? -(t0 + 1) : (t0 + 1);
-        if (at0 < Bw || at1 < Bw) {
-          int64_t idx = s0 + i0;
-          if (a.wrap && idx < 0) idx += a.L;
-          float x0 = 0.f, x1 = 0.f;
-          if (idx >= 0 && idx + 1 < a.x_len && vec) {
-            const float2 xv = __ldg(reinterpret_cast<const float2 *>(xr + idx));
-            x0 = xv.x;
-            x1 = xv.y;
-          } else {
-            if (idx >= 0 && idx < a.x_len) x0 = __ldg(xr + idx);
-            if (idx + 1 >= 0 && idx + 1 < a.x_len) x1 = __ldg(xr + idx + 1);
+        for (int r = 0; r < R; ++r) {
+          const int p = j + r * TASKS;
+          const int i0 = 2 * p;  // frame index of the real part
+          const int t0 = i0 - N;
+          const int at0 = t0 < 0 ? -t0 : t0;
+          const int at1 = (t0 + 1) < 0 ? -(t0 + 1) : (t0 + 1);
+          float2 val = make_float2(0.f, 0.f);
+          if (at0 < Bw || at1 < Bw) {
+            int64_t idx = s0 + i0;
+            if (a.wrap && idx < 0) idx += a.L;
+            float x0 = 0.f, x1 = 0.f;
+            if (vec && idx >= 0 && idx + 1 < a.x_len) {
+              const float2 xv = __ldcs(reinterpret_cast<const float2 *>(xr + idx));
+              x0 = xv.x;
+              x1 = xv.y;
+            } else {
+              if (idx >= 0 && idx < a.x_len) x0 = __ldg(xr + idx);
+              if (idx + 1 >= 0 && idx + 1 < a.x_len) x1 = __ldg(xr + idx + 1);
+            }
+            const float h0a = at0 <= A ? 1.f : (at0 < Bw ? __ldg(a.h0 + i0) : 0.f);
+            const float h0b = at1 <= A ? 1.f : (at1 < Bw ? __ldg(a.h0 + i0 + 1) : 0.f);
+            val = make_float2(x0 * h0a, x1 * h0b);
           }
-          const float h0a = at0 <= A ? 1.f : (at0 < Bw ? __ldg(a.h0 + i0) : 0.f);
-          const float h0b = at1 <= A ? 1.f : (at1 < Bw ? __ldg(a.h0 + i0 + 1) : 0.f);
-          val = make_float2(x0 * h0a, x1 * h0b);
+          v[q][r] = val;
         }
-        v[q][r] = val;
+        dft<R, -1>(v[q]);
       }
-      dft<R, -1>(v[q]);
     }
-    __syncthreads();  // tw table visible
+    __syncthreads();  // twiddle table and counter visible; nothing read spec yet
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = tid + q * T;
+      if (TASKS % T == 0 || j < TASKS) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) spec[padi(j * R + r)] = v[q][r];
+        for (int r = 0; r < R; ++r) spec[padi(j * R + r)] = v[q][r];
+      }
     }
     __syncthreads();
   }
-  pass_smem<N, CF::R2, CF::R1, -1, T>(spec, tw);
-  pass_smem<N, CF::R3, CF::R1 * CF::R2, -1, T>(spec, tw);
+  pass_smem<N, CF::F2, CF::F1, -1, T>(spec, tw);
+  pass_smem<N, CF::F3, CF::F1 * CF::F2, -1, T>(spec, tw);
 
   // ---- r2c packing: X[k] = E[k] + e^{-i pi k/N} O[k], k = 0..N  (Z[N] := Z[0])
   for (int k = tid; k <= N / 2; k += T) {
@@ -350,17 +385,15 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kerne
       // E = (Zk + conj Zn)/2, O = (Zk - conj Zn)/(2i)
       const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
       const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
-      const float2 w = tw_lookup(tw, k);  // e^{-i pi k/N}
-      const float2 Xk = cadd(E, cmul(w, O));
-      // X[N-k] = conj(E) + e^{-i pi (N-k)/N} conj(O) = conj(E) - conj(w) * conj(O)
-      const float2 Xn = csub(cconj(E), cconj(cmul(w, O)));
-      spec[padi(k)] = Xk;
-      if (k != N / 2) spec[padi(N - k)] = Xn;
+      const float2 wO = cmul(tw_lookup(tw, k), O);  // e^{-i pi k/N} O
+      spec[padi(k)] = cadd(E, wO);
+      // X[N-k] = conj(E) + e^{-i pi (N-k)/N} conj(O) = conj(E) - conj(wO)
+      if (k != N / 2) spec[padi(N - k)] = csub(cconj(E), cconj(wO));
     }
   }
   __syncthreads();
 
-  // ---- F3-F5: channel packets, dynamically scheduled over warps
+  // ---- F3-F5: channel packets (shape-sorted), dynamically scheduled over warps
   float2 *scr = scr_all + warp * a.scr;
   float2 *out_row = a.coef_out + (row * a.nslices + mloc) * a.C;
   for (;;) {
@@ -389,14 +422,13 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kerne
 
 // ------------------------------------------------------------------ inverse kernel
 template <int LOGN>
-__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kernel(const KArgs a) {
+__global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_inv_kernel(const KArgs a) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T, NW = T / 32;
   extern __shared__ float4 smem4[];
   float2 *spec = reinterpret_cast<float2 *>(smem4);
   float2 *tw = spec + spec_entries<LOGN>();
-  float2 *scr_all = tw + tw_entries<LOGN>();
-  int *ctr = reinterpret_cast<int *>(scr_all + NW * a.scr);
+  float2 *chs = tw + tw_entries<LOGN>();  // chunk scratch
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int mloc = blockIdx.x;
   const int64_t mg = a.slice0 + mloc;
@@ -404,37 +436,47 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kerne
 
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
   for (int i = tid; i < spec_entries<LOGN>(); i += T) spec[i] = make_float2(0.f, 0.f);
-  if (tid == 0) ctr[0] = 0;
-  __syncthreads();
 
-  // ---- I1-I3: channel packets
-  {
-    float2 *scr = scr_all + warp * a.scr;
-    const float2 *in_row = a.coef_in + (row * a.nslices + mloc) * a.C;
-    for (;;) {
-      int pk = 0;
-      if (lane == 0) pk = atomicAdd(ctr, 1);
-      pk = __shfl_sync(FULL, pk, 0);
-      if (pk >= a.npackets) break;
+  // ---- I1-I3 per chunk: channel FFTs into the chunk scratch, then the per-bin gather
+  const float2 *in_row = a.coef_in + (row * a.nslices + mloc) * a.C;
+  for (int c = 0; c < a.nchunks; ++c) {
+    const ChunkDev ck = a.chunks[c];
+    for (int pk = ck.pk0 + warp; pk < ck.pk1; pk += NW) {
       const PacketDev P = a.packets[pk];
       const int m1 = P.m1m2 & 255, m2 = P.m1m2 >> 8;
+      float2 *reg = chs + P.region;
       switch (m1) {
 #define X(S) \
-  case S: inv_step1<S>(a, in_row, scr, m2, P.nch, P.chan_off, lane); break;
+  case S: inv_step1<S>(a, in_row, reg, m2, P.nch, P.chan_off, lane); break;
         SLICQ_SIZES(X)
 #undef X
       }
       __syncwarp();
       switch (m2) {
 #define X(S) \
-  case S: inv_step2<S, N>(a, scr, spec, m1, P.nch, P.chan_off, lane); break;
+  case S: inv_step2<S>(reg, m1, P.nch, lane); break;
         SLICQ_SIZES(X)
 #undef X
       }
-      __syncwarp();
     }
+    __syncthreads();
+    const int32_t *bo = a.bin_off + ck.bin_base;
+    for (int b = ck.blo + tid; b <= ck.bhi; b += T) {
+      const int e0 = __ldg(bo + (b - ck.blo)), e1 = __ldg(bo + (b - ck.blo) + 1);
+      float2 acc = make_float2(0.f, 0.f);
+      for (int e = e0; e < e1; ++e) {
+        const uint2 ge = __ldg(reinterpret_cast<const uint2 *>(a.gents) + e);
+        const float2 f = chs[ge.x & 0x7fffffffu];
+        const float gv = __uint_as_float(ge.y);
+        const float im = (ge.x >> 31) ? -f.y : f.y;
+        acc.x = fmaf(f.x, gv, acc.x);
+        acc.y = fmaf(im, gv, acc.y);
+      }
+      float2 &sp = spec[padi(b)];
+      sp = cadd(sp, acc);
+    }
+    __syncthreads();
   }
-  __syncthreads();
 
   // ---- I4a: c2r packing  Z[k] = E[k] + i O[k],
   //   E = (H[k] + conj H[N-k])/2,  O = (H[k] - conj H[N-k]) e^{+i pi k/N} / 2
@@ -447,21 +489,21 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kerne
     const float2 O = cmul(D, w);
     spec[padi(k)] = make_float2(E.x - O.y, E.y + O.x);  // E + iO
     if (k != 0 && k != N / 2) {
-      // pair (N-k): E' = conj(E), O' = conj(D) * e^{i pi (N-k)/N} = -conj(D) * conj(w)
+      // pair N-k: E' = conj(E), O' = conj(D) e^{-i pi k/N}
       const float2 O2 = cmul(cconj(D), cconj(w));
-      const float2 E2 = cconj(E);
-      spec[padi(N - k)] = make_float2(E2.x - O2.y, E2.y + O2.x);  // E' + i O'
+      spec[padi(N - k)] = make_float2(E.x - O2.y, -E.y + O2.x);  // conj(E) + i O'
     }
   }
   __syncthreads();
 
-  // ---- I4b: inverse N-point FFT (unnormalised), passes 1 and 2 in shared memory
-  pass_smem<N, CF::R1, 1, +1, T>(spec, tw);
-  pass_smem<N, CF::R2, CF::R1, +1, T>(spec, tw);
+  // ---- I4b: inverse N-point FFT (unnormalised), first passes in shared memory
+  pass_smem<N, CF::I1, 1, +1, T>(spec, tw);
+  pass_smem<N, CF::I2, CF::I1, +1, T>(spec, tw);
 
   // ---- last pass + I5 epilogue: z[p] -> samples 2p, 2p+1, times h~_0 / N, overlap-add
   {
-    constexpr int R = CF::R3, NS = CF::R1 * CF::R2, TASKS = N / R, PER = TASKS / T;
+    constexpr int R = CF::I3, NS = CF::I1 * CF::I2, TASKS = N / R;
+    constexpr int PER = (TASKS + T - 1) / T;
     static_assert(NS * R == N, "pass plan");
     const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
     const float invN = 1.0f / (float)N;
@@ -477,14 +519,17 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kerne
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = tid + q * T;
+      if (TASKS % T == 0 || j < TASKS) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = spec[padi(j + r * TASKS)];
-      pass_twiddle<N, R, NS, +1>(v[q], j, tw);
-      dft<R, +1>(v[q]);
+        for (int r = 0; r < R; ++r) v[q][r] = spec[padi(j + r * TASKS)];
+        pass_twiddle<N, R, NS, +1>(v[q], j, tw);
+        dft<R, +1>(v[q]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = tid + q * T;
+      if (!(TASKS % T == 0 || j < TASKS)) continue;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int p = j + r * NS;  // output index of the final pass = z index
@@ -498,7 +543,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kerne
           const int64_t s = (mg - 1) * N + i;  // global sample index (before wrap)
           if (at <= A) {
             if (a.circular) {
-              int64_t sw = s < 0 ? s + a.L : (s >= a.L ? s - a.L : s);
+              const int64_t sw = s < 0 ? s + a.L : (s >= a.L ? s - a.L : s);
               if (sw < a.y_len) yrow[sw] = val;
             } else {
               const int64_t li = s - a.y_base;
@@ -517,7 +562,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kerne
         }
       }
     }
-    // range mode, last local slice: samples [ (mg+1)N - A, (mg+1)N ) get no local
+    // range mode, last local slice: samples [(mg+1)N - A, (mg+1)N) get no local
     // contribution; store zeros so the neighbour's spill can be added in place.
     if (!a.circular && mloc + 1 == S) {
       for (int u = tid; u < A; u += T) yrow[(mg + 1) * N - A + u - a.y_base] = 0.f;
@@ -549,7 +594,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kerne
         const float val = __ldcg(h0p + u) + __ldcg(h1p + u);
         const int64_t s = mb * N + A + 1 + u;
         if (a.circular) {
-          int64_t sw = s >= a.L ? s - a.L : s;
+          const int64_t sw = s >= a.L ? s - a.L : s;
           if (sw < a.y_len) yrow[sw] = val;
         } else {
           yrow[s - a.y_base] = val;
@@ -560,13 +605,19 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kerne
 }
 
 template <int LOGN>
-constexpr size_t smem_bytes_t(int scr) {
-  return sizeof(float2) * (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>() + (Big<LOGN>::T / 32) * scr) + 16;
+constexpr size_t fwd_smem_bytes(int scr) {
+  return sizeof(float2) *
+             (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>() + (Big<LOGN>::T / 32) * scr) +
+         16;
+}
+template <int LOGN>
+constexpr size_t inv_smem_bytes(int scr) {
+  return sizeof(float2) * (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>() + scr) + 16;
 }
 
 // Per-size entry points (defined in kernels_l<LOGN>.cu)
 template <int LOGN>
-int set_attrs(size_t smem);
+int set_attrs(size_t fwd_smem, size_t inv_smem);
 template <int LOGN>
 cudaError_t launch_fwd(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s);
 template <int LOGN>

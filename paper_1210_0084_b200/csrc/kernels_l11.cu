@@ -7,11 +7,11 @@ namespace slicq {
 namespace kern {
 
 template <>
-int set_attrs<SLICQ_LOGN>(size_t smem) {
+int set_attrs<SLICQ_LOGN>(size_t fwd_smem, size_t inv_smem) {
   cudaError_t e1 = cudaFuncSetAttribute(slicq_fwd_kernel<SLICQ_LOGN>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem);
   cudaError_t e2 = cudaFuncSetAttribute(slicq_inv_kernel<SLICQ_LOGN>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inv_smem);
   if (e1 != cudaSuccess) return (int)e1;
   if (e2 != cudaSuccess) return (int)e2;
   return 0;

@@ -20,20 +20,42 @@ struct ChanDev {
   int32_t lo_mod;  // lo_k mod M_k in [0, M_k)
 };
 
-// A packet = channels of one length M = M1*M2 processed together by one warp.
+// A packet = channels of one length M = M1*M2 processed together by one warp, with at most
+// 32 tasks per DFT step (nch*M2 <= 32 and nch*M1 <= 32): one task per lane.
 struct PacketDev {
   int32_t m1m2;     // M1 | (M2 << 8)
   int32_t nch;      // channels in the packet
   int32_t chan_off; // offset into the packet channel list
-  int32_t cost;     // work estimate (for ordering only)
+  int32_t region;   // inverse: float2 offset of the packet's region in the chunk scratch
+};
+
+// Inverse: channels are processed in chunks whose F_k fit in shared memory; after each
+// chunk, every target bin b in [blo, bhi] is gathered by exactly one thread (no atomics).
+struct ChunkDev {
+  int32_t pk0, pk1;   // packets [pk0, pk1) of the inverse packet list
+  int32_t blo, bhi;   // target half-spectrum bins touched by the chunk
+  int32_t bin_base;   // this chunk's (bhi - blo + 2) entries in bin_off
+  int32_t pad0, pad1, pad2;
+};
+
+// One term of the per-bin gather: F value at chunk-scratch position (fidx & 0x7fffffff),
+// conjugated if bit 31 is set (Hermitian rule, C15), times gval = dual (x 1/2 on the
+// self-mirrored plateaus) / sqrt(M_k).
+struct GatherEnt {
+  uint32_t fidx;
+  float gval;
 };
 
 struct DeviceTables {
   ChanDev *chan = nullptr;
-  PacketDev *packets = nullptr;
-  int32_t *packet_chans = nullptr;
-  float *g = nullptr;       // fp32 g_k on J_k
-  float *gdual = nullptr;   // fp32 dual; plateaus pre-multiplied by 1/2 (Hermitian rule, C15)
+  PacketDev *fwd_packets = nullptr;
+  int32_t *fwd_pchans = nullptr;
+  PacketDev *inv_packets = nullptr;
+  int32_t *inv_pchans = nullptr;
+  ChunkDev *chunks = nullptr;
+  int32_t *bin_off = nullptr;
+  GatherEnt *gents = nullptr;
+  float *g = nullptr;       // fp32 g_k / sqrt(M_k) on J_k (forward)
   float *h0 = nullptr;      // fp32 h_0[t+N], t in [-N, N)
   float *h0dual = nullptr;  // fp32 h~_0[t+N]
   float *tw2n = nullptr;    // float2: [64] e^{-i pi t/N} for t < 64, then [2N/64] for t = 64 h
@@ -43,11 +65,14 @@ struct DeviceTables {
 };
 
 struct KernelConfig {
-  int logN = 0;        // N = 2^logN complex points in the r2c FFT of a 2N slice
-  int threads = 0;     // CTA size
-  int scr = 0;         // per-warp scratch (float2 entries)
-  size_t smem = 0;     // dynamic shared memory bytes
-  int npackets = 0;
+  int logN = 0;          // N = 2^logN complex points in the r2c FFT of a 2N slice
+  int threads = 0;       // CTA size
+  int fwd_scr = 0;       // forward: per-warp scratch (float2 entries)
+  int inv_scr = 0;       // inverse: chunk scratch (float2 entries)
+  size_t fwd_smem = 0;   // dynamic shared memory bytes
+  size_t inv_smem = 0;
+  int fwd_npackets = 0;
+  int nchunks = 0;
 };
 
 }  // namespace slicq
@@ -74,9 +99,11 @@ struct slicq_plan {
   int device = -1;
   slicq::DeviceTables d;
   slicq::KernelConfig kc;
-  std::vector<slicq::PacketDev> packets;
-  std::vector<int32_t> packet_chans;
-  std::vector<int32_t> twoff;
+  std::vector<slicq::PacketDev> fwd_packets, inv_packets;
+  std::vector<int32_t> fwd_pchans, inv_pchans;
+  std::vector<slicq::ChunkDev> chunks;
+  std::vector<int32_t> bin_off;
+  std::vector<slicq::GatherEnt> gents;
 };
 
 namespace slicq {

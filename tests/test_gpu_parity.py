@@ -260,4 +260,9 @@ def test_range_api_matches_full(api, G):
         tail = ys[r][:, -halo:]
         api.Plan.overlap_add(tail, spills[(r + 1) % G])
     y = torch.cat(ys, dim=1)[:, :n]
-    assert torch.equal(y, y_full)
+    d = (y - y_full).abs()
+    if not torch.equal(y, y_full):
+        bad = torch.nonzero(d > 0)
+        raise AssertionError(f"range/full mismatch: max {d.max().item():.3e} at {bad[:8].tolist()} "
+                             f"(N={N}, S={S}, halo={halo}, bounds={bounds}, n={n}); "
+                             f"y={y[bad[0,0], bad[0,1]].item()} full={y_full[bad[0,0], bad[0,1]].item()}")
