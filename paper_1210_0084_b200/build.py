@@ -33,44 +33,50 @@ def nvcc() -> str:
     return p
 
 
-def _compile(src: str) -> tuple[str, str]:
-    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
-    cmd = [nvcc(), *ARCH, *FLAGS, "-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src: str, objdir: str = OBJ, extra=()) -> tuple[str, str]:
+    obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+    cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     return obj, r.stderr
 
 
-def _stale() -> bool:
-    if not os.path.exists(OUT):
+def _stale(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(PKG, "..", "include", "slicq.h"))
     deps.append(__file__)
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return OUT
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, debug_timing: bool = False) -> str:
+    """Build libslicq.so (or, with debug_timing, libslicq_dbg.so with per-phase clock64
+    instrumentation for tools/phase_timing.py; never used by the product path)."""
+    out = OUT if not debug_timing else os.path.join(PKG, "libslicq_dbg.so")
+    if not force and not _stale(out):
+        return out
+    objdir = OBJ if not debug_timing else OBJ + "_dbg"
+    os.makedirs(objdir, exist_ok=True)
+    extra = ["-DSLICQ_PHASE_TIMING"] if debug_timing else []
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        results = list(ex.map(_compile, SOURCES))
+        results = list(ex.map(lambda s: _compile(s, objdir, extra), SOURCES))
     log = "\n".join(r[1] for r in results)
-    with open(os.path.join(OBJ, "ptxas.log"), "w") as f:
+    with open(os.path.join(objdir, "ptxas.log"), "w") as f:
         f.write(log)
     if verbose:
         print(log)
-    tmp = OUT + ".tmp"
+    tmp = out + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *[r[0] for r in results]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                debug_timing="--debug-timing" in sys.argv))

@@ -34,33 +34,64 @@ using namespace slicq::dev;
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__host__ __device__ constexpr int padi(int i) { return i + (i >> 5); }
+// Opt-in phase timing (debug library only: -DSLICQ_PHASE_TIMING).  Thread 0 of every CTA
+// accumulates clock64 deltas between phase marks; read with slicq_debug_phase_times().
+#ifdef SLICQ_PHASE_TIMING
+static __device__ unsigned long long g_phase_cycles[2][16];
+#define PHASE_INIT() long long _t_prev = clock64()
+#define PHASE_MARK(dir, i)                                             \
+  do {                                                                 \
+    __syncthreads();                                                   \
+    if (threadIdx.x == 0) {                                            \
+      const long long _t = clock64();                                  \
+      atomicAdd(&g_phase_cycles[dir][i], (unsigned long long)(_t - _t_prev)); \
+      _t_prev = _t;                                                    \
+    }                                                                  \
+  } while (0)
+#else
+#define PHASE_INIT() \
+  do {               \
+  } while (0)
+#define PHASE_MARK(dir, i) \
+  do {                     \
+  } while (0)
+#endif
+
+// one pad entry per 16 complex: radix-16 strided stores and contiguous loads are
+// bank-conflict free for 8-byte accesses
+__host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
 
 // Big-FFT plans: N = 2^LOGN complex points, T threads, radix sequences per direction.
 template <int LOGN>
 struct Big;
+#ifndef SLICQ_T13
+#define SLICQ_T13 256
+#define SLICQ_MINB13 2
+#endif
+// MINB = CTAs per SM the shared-memory budget is sized for (two slices in flight per SM
+// overlap one CTA's HBM loads / barriers with the other's arithmetic).
 template <>
 struct Big<11> {
-  static constexpr int N = 2048, T = 128;
+  static constexpr int N = 2048, T = 128, MINB = 2;
   static constexpr int F1 = 16, F2 = 16, F3 = 8;   // forward pass radices
-  static constexpr int I1 = 8, I2 = 16, I3 = 16;   // inverse pass radices
+  static constexpr int I1 = 16, I2 = 8, I3 = 16;   // inverse pass radices
 };
 template <>
 struct Big<12> {
-  static constexpr int N = 4096, T = 256;
+  static constexpr int N = 4096, T = 256, MINB = 2;
   static constexpr int F1 = 16, F2 = 16, F3 = 16;
   static constexpr int I1 = 16, I2 = 16, I3 = 16;
 };
 template <>
 struct Big<13> {
-  static constexpr int N = 8192, T = 512;
+  static constexpr int N = 8192, T = SLICQ_T13, MINB = SLICQ_MINB13;
   static constexpr int F1 = 16, F2 = 16, F3 = 32;
-  static constexpr int I1 = 32, I2 = 16, I3 = 16;
+  static constexpr int I1 = 16, I2 = 32, I3 = 16;
 };
 template <>
 struct Big<14> {
-  static constexpr int N = 16384, T = 512;
-  static constexpr int F1 = 32, F2 = 32, F3 = 16;
+  static constexpr int N = 16384, T = 512, MINB = 1;
+  static constexpr int F1 = 16, F2 = 32, F3 = 32;
   static constexpr int I1 = 16, I2 = 32, I3 = 32;
 };
 
@@ -86,17 +117,16 @@ struct KArgs {
   int tr;
   int scr;        // forward: per-warp scratch entries; inverse: chunk scratch entries
   int npackets;   // forward packets
-  int nchunks;    // inverse chunks
+  int nchunks;    // inverse phases
   int64_t C;
   float2 *coef_out;
   const float2 *coef_in;
   const ChanDev *chan;
   const PacketDev *packets;
   const int32_t *pchans;
-  const ChunkDev *chunks;
-  const int32_t *bin_off;
-  const GatherEnt *gents;
-  const float *g;
+  const ChunkDev *chunks;   // inverse: packet ranges of the phases
+  const float *g;           // g_k / sqrt(M_k) on J_k
+  const float *gdual;       // dual / sqrt(M_k) on J_k (plateaus x 1/2, C15)
   const float *h0;
   const float *h0dual;
   const float2 *tw2n;
@@ -205,85 +235,130 @@ __device__ __forceinline__ void chan_twiddle(float2 (&v)[M1], int p2, int M, con
   }
 }
 
-// ------------------------------------------------------------------ forward packet steps
-// Step 1, task (ci, p2): inputs buf[M2 p1 + p2] = X(j) g_k[j]/sqrt(M) for the bin j of J_k
-// congruent to M2 p1 + p2 (mod M), else 0 (fold / zero-pad, C5); DFT_{M1}; twiddle.
-template <int M1, int N>
-__device__ __forceinline__ void fwd_step1(const KArgs &a, const float2 *spec, float2 *scr,
-                                          int m2, int nch, int chan_off, int lane) {
-  const int nt = nch * m2;
-  if (lane >= nt) return;
-  const int ci = lane / m2;
-  const int p2 = lane - ci * m2;
-  const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
-  float2 v[M1];
-  int d = p2 - ch.lo_mod;
-  if (d < 0) d += ch.M;
-#pragma unroll
-  for (int p1 = 0; p1 < M1; ++p1) {
-    float2 val = make_float2(0.f, 0.f);
-    if (d < ch.len) val = cscale(spec_at<N>(spec, ch.lo + d), __ldg(a.g + ch.goff + d));
-    v[p1] = val;
-    d += m2;
-    if (d >= ch.M) d -= ch.M;
+// ------------------------------------------------------------------ channel packets
+// A packet's channel ci owns the region reg + ci*M1*S2 (S2 = M2 | 1) of the warp scratch:
+// first the length-M vector of the fold (forward) / of F (inverse), in between the
+// M1 x S2 four-step intermediate A[n1][p2].  One task per lane and step (nch*M1, nch*M2
+// <= 32), so the in-place steps only need a warp barrier between their loads and stores.
+
+// Packet channel descriptors live in registers: lane c holds channel c's ChanDev (one
+// parallel load per packet); fields are broadcast with shuffles.
+struct PDesc {
+  ChanDev c;
+};
+__device__ __forceinline__ PDesc load_desc(const KArgs &a, int chan_off, int nch, int lane) {
+  const int k = __ldg(a.pchans + chan_off + (lane < nch ? lane : 0));
+  return PDesc{a.chan[k]};
+}
+__device__ __forceinline__ int shf(int v, int src) { return __shfl_sync(FULL, v, src); }
+
+// F3 (forward fold, C5): buf[p] = X(j) g_k[j]/sqrt(M_k) for the j in J_k with
+// j = p (mod M_k), 0 where there is none (zero padding).  Flattened over the packet's
+// channels (all of length M): element e -> channel e / M, d = e mod M; consecutive lanes
+// write consecutive p (conflict-free).  SIMPLE: every J_k lies in [0, N].
+template <int N, bool SIMPLE>
+__device__ __forceinline__ void fwd_fold(const KArgs &a, const float2 *spec, float2 *reg,
+                                         const PDesc &pd, int M, int m1, int S2, int nch,
+                                         unsigned mag, int lane) {
+  const int tot = nch * M;
+#pragma unroll 4
+  for (int base = 0; base < tot; base += 32) {
+    const int e = base + lane;
+    const int ci = min((int)__umulhi((unsigned)e, mag), nch - 1);
+    const int d = e - ci * M;
+    const int lo = shf(pd.c.lo, ci), len = shf(pd.c.len, ci);
+    const int lo_mod = shf(pd.c.lo_mod, ci), goff = shf(pd.c.goff, ci);
+    if (e < tot) {
+      int p = lo_mod + d;
+      if (p >= M) p -= M;
+      float2 val = make_float2(0.f, 0.f);
+      if (d < len) {
+        const float gv = __ldg(a.g + goff + d);
+        const float2 xv = SIMPLE ? spec[padi(lo + d)] : spec_at<N>(spec, lo + d);
+        val = cscale(xv, gv);
+      }
+      reg[ci * m1 * S2 + p] = val;
+    }
   }
-  dft<M1, +1>(v);
-  chan_twiddle<M1, +1>(v, p2, ch.M, a.twM + ch.twoff);
-  const int S2 = m2 | 1;
-  float2 *A = scr + ci * M1 * S2 + p2;
-#pragma unroll
-  for (int n1 = 0; n1 < M1; ++n1) A[n1 * S2] = v[n1];
 }
 
-// Step 2, task (ci, n1): DFT_{M2} over p2 -> c[n1 + M1 n2].
+// F4 step 1, in place: task (ci, p2) takes buf[M2 p1 + p2], p1 < M1; DFT_{M1} (sign +);
+// twiddle e^{+2 pi i p2 n1 / M}; stores A[n1 S2 + p2].
+__device__ __forceinline__ int div_small(int q, unsigned mag16) { return (q * (int)mag16) >> 16; }
+
+template <int M1>
+__device__ __forceinline__ void fwd_step1(const KArgs &a, float2 *reg, const PDesc &pd, int m2,
+                                          int nch, unsigned mag2, int lane) {
+  const int nt = nch * m2;
+  const bool act = lane < nt;
+  const int ci = act ? div_small(lane, mag2) : 0;
+  const int p2 = act ? lane - ci * m2 : 0;
+  const int S2 = m2 | 1;
+  float2 *base = reg + ci * M1 * S2;
+  float2 v[M1];
+#pragma unroll
+  for (int p1 = 0; p1 < M1; ++p1) v[p1] = base[m2 * p1 + p2];
+  const int twoff = shf(pd.c.twoff, ci);
+  const int M = M1 * m2;
+  __syncwarp();
+  if (act) {
+    dft<M1, +1>(v);
+    chan_twiddle<M1, +1>(v, p2, M, a.twM + twoff);
+#pragma unroll
+    for (int n1 = 0; n1 < M1; ++n1) base[n1 * S2 + p2] = v[n1];
+  }
+}
+
+// F4 step 2 + F5: task (ci, n1): DFT_{M2} over p2 -> c[n1 + M1 n2] (coalesced over n1).
 template <int M2>
-__device__ __forceinline__ void fwd_step2(const KArgs &a, const float2 *scr, float2 *out_row,
-                                          int m1, int nch, int chan_off, int lane) {
+__device__ __forceinline__ void fwd_step2(const KArgs &a, const float2 *reg, float2 *out_row,
+                                          const PDesc &pd, int m1, int nch, unsigned mag1,
+                                          int lane) {
   const int nt = nch * m1;
-  if (lane >= nt) return;
   constexpr int S2 = M2 | 1;
-  const int ci = lane / m1;
+  const int ci = lane < nt ? div_small(lane, mag1) : 0;
   const int n1 = lane - ci * m1;
-  const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
+  const int off = shf(pd.c.off, ci);
+  if (lane >= nt) return;
   float2 v[M2];
-  const float2 *A = scr + ci * m1 * S2 + n1 * S2;
+  const float2 *A = reg + ci * m1 * S2 + n1 * S2;
 #pragma unroll
   for (int p2 = 0; p2 < M2; ++p2) v[p2] = A[p2];
   dft<M2, +1>(v);
-  float2 *o = out_row + ch.off + n1;
+  float2 *o = out_row + off + n1;
 #pragma unroll
-  for (int n2 = 0; n2 < M2; ++n2) o[m1 * n2] = v[n2];
+  for (int n2 = 0; n2 < M2; ++n2) __stcs(o + m1 * n2, v[n2]);
 }
 
-// ------------------------------------------------------------------ inverse packet steps
+// I2 step 1: task (ci, p2) loads c[M2 p1 + p2] from HBM; DFT_{M1} (sign -); twiddle.
 template <int M1>
 __device__ __forceinline__ void inv_step1(const KArgs &a, const float2 *in_row, float2 *reg,
-                                          int m2, int nch, int chan_off, int lane) {
+                                          const PDesc &pd, int m2, int nch, unsigned mag2,
+                                          int lane) {
   const int nt = nch * m2;
-  if (lane >= nt) return;
-  const int ci = lane / m2;
+  const int ci = lane < nt ? div_small(lane, mag2) : 0;
   const int p2 = lane - ci * m2;
-  const ChanDev ch = a.chan[__ldg(a.pchans + chan_off + ci)];
+  const int off = shf(pd.c.off, ci), twoff = shf(pd.c.twoff, ci);
+  if (lane >= nt) return;
   float2 v[M1];
-  const float2 *src = in_row + ch.off + p2;
+  const float2 *src = in_row + off + p2;
 #pragma unroll
   for (int p1 = 0; p1 < M1; ++p1) v[p1] = __ldcs(src + p1 * m2);
   dft<M1, -1>(v);
-  chan_twiddle<M1, -1>(v, p2, ch.M, a.twM + ch.twoff);
+  chan_twiddle<M1, -1>(v, p2, M1 * m2, a.twM + twoff);
   const int S2 = m2 | 1;
   float2 *A = reg + ci * M1 * S2 + p2;
 #pragma unroll
   for (int n1 = 0; n1 < M1; ++n1) A[n1 * S2] = v[n1];
 }
 
-// Step 2 in place: every lane loads its row, the warp syncs, then F[n1 + M1 n2] (the
-// unnormalised FFT_{M} of c) overwrites the channel's region.
+// I2 step 2, in place: F[n1 + M1 n2] = (unnormalised FFT_M of c) overwrites the region.
 template <int M2>
-__device__ __forceinline__ void inv_step2(float2 *reg, int m1, int nch, int lane) {
+__device__ __forceinline__ void inv_step2(float2 *reg, int m1, int nch, unsigned mag1, int lane) {
   const int nt = nch * m1;
   constexpr int S2 = M2 | 1;
   const bool act = lane < nt;
-  const int ci = act ? lane / m1 : 0;
+  const int ci = act ? div_small(lane, mag1) : 0;
   const int n1 = act ? lane - ci * m1 : 0;
   float2 v[M2];
   float2 *base = reg + ci * m1 * S2;
@@ -298,34 +373,150 @@ __device__ __forceinline__ void inv_step2(float2 *reg, int m1, int nch, int lane
   }
 }
 
+// I3: spectrum[j] += F[j mod M] g~_k[j]/sqrt(M) over j in J_k, channel after
+// channel (channels of a packet may overlap), lanes over j (distinct bins).  Non-SIMPLE
+// channels apply the Hermitian rule of C15: the term goes to j mod 2N if <= N and its
+// conjugate to -j mod 2N if <= N (plateau weights carry the 1/2).  Packets that run
+// concurrently never share a bin (plan-time phase colouring), so plain read-modify-write.
+template <int N, bool SIMPLE>
+__device__ __forceinline__ void inv_unfold(const KArgs &a, float2 *spec, const float2 *reg,
+                                           const PDesc &pd, int M, int m1, int S2, int nch,
+                                           int lane) {
+  for (int ci = 0; ci < nch; ++ci) {
+    const int lo = shf(pd.c.lo, ci), len = shf(pd.c.len, ci);
+    const int lo_mod = shf(pd.c.lo_mod, ci), goff = shf(pd.c.goff, ci);
+    const float2 *F = reg + ci * m1 * S2;
+    const float *gd = a.gdual + goff;
+#pragma unroll 4
+    for (int d = lane; d < len; d += 32) {
+      int p = lo_mod + d;
+      if (p >= M) p -= M;
+      const float2 v = cscale(F[p], __ldg(gd + d));
+      const int j = lo + d;
+      if (SIMPLE) {
+        float2 &sp = spec[padi(j)];
+        sp = cadd(sp, v);
+      } else {
+        int p1 = j < 0 ? j + 2 * N : j;
+        if (p1 <= N) {
+          float2 &sp = spec[padi(p1)];
+          sp = cadd(sp, v);
+        }
+        const int p2 = p1 == 0 ? 0 : 2 * N - p1;
+        if (p2 <= N) {
+          float2 &sp = spec[padi(p2)];
+          sp = cadd(sp, cconj(v));
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- small channels (M <= 32): lane c owns channel c of the packet, DFT_M in registers
+// F3-F5 for one channel per lane: fold into registers, DFT_M (sign +), store c^m_k.
+template <int M, int N>
+__device__ __forceinline__ void fwd_small(const KArgs &a, const float2 *spec, float2 *out_row,
+                                          const PDesc &pd, int nch, bool simple, int lane) {
+  if (lane >= nch) return;
+  const ChanDev &ch = pd.c;
+  float2 v[M];
+#pragma unroll
+  for (int p = 0; p < M; ++p) {
+    int d = p - ch.lo_mod;
+    if (d < 0) d += M;
+    float2 val = make_float2(0.f, 0.f);
+    if (d < ch.len) {
+      const float gv = __ldg(a.g + ch.goff + d);
+      const float2 xv = simple ? spec[padi(ch.lo + d)] : spec_at<N>(spec, ch.lo + d);
+      val = cscale(xv, gv);
+    }
+    v[p] = val;
+  }
+  dft<M, +1>(v);
+  float2 *o = out_row + ch.off;
+#pragma unroll
+  for (int n = 0; n < M; ++n) __stcs(o + n, v[n]);
+}
+
+// I1-I3 for one channel per lane: load c, DFT_M (sign -) into scratch F[q][lane], then the
+// channels scatter one after another (they may overlap), lanes over bins.
+template <int M, int N>
+__device__ __forceinline__ void inv_small(const KArgs &a, const float2 *in_row, float2 *spec,
+                                          float2 *scr, const PDesc &pd, int nch, bool simple,
+                                          int lane) {
+  if (lane < nch) {
+    const float2 *src = in_row + pd.c.off;
+    float2 v[M];
+#pragma unroll
+    for (int n = 0; n < M; ++n) v[n] = __ldcs(src + n);
+    dft<M, -1>(v);
+#pragma unroll
+    for (int q = 0; q < M; ++q) scr[q * nch + lane] = v[q];
+  }
+  __syncwarp();
+  for (int ci = 0; ci < nch; ++ci) {
+    const int lo = shf(pd.c.lo, ci), len = shf(pd.c.len, ci);
+    const int lo_mod = shf(pd.c.lo_mod, ci), goff = shf(pd.c.goff, ci);
+    if (lane < len) {
+      const int d = lane;
+      int q = lo_mod + d;
+      if (q >= M) q -= M;
+      const float2 v = cscale(scr[q * nch + ci], __ldg(a.gdual + goff + d));
+      const int j = lo + d;
+      if (simple) {
+        float2 &sp = spec[padi(j)];
+        sp = cadd(sp, v);
+      } else {
+        int p1 = j < 0 ? j + 2 * N : j;
+        if (p1 <= N) {
+          float2 &sp = spec[padi(p1)];
+          sp = cadd(sp, v);
+        }
+        const int p2 = p1 == 0 ? 0 : 2 * N - p1;
+        if (p2 <= N) {
+          float2 &sp = spec[padi(p2)];
+          sp = cadd(sp, cconj(v));
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+#define SLICQ_SMALL(X) X(4) X(6) X(8) X(10) X(12) X(16) X(18) X(20) X(24) X(30) X(32)
+
 #define SLICQ_SIZES(X) \
   X(1) X(2) X(3) X(4) X(5) X(6) X(8) X(9) X(10) X(12) X(15) X(16) X(18) X(20) X(24) X(25) X(27) X(30) X(32)
 
 // ------------------------------------------------------------------ forward kernel
 template <int LOGN>
-__global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_fwd_kernel(const KArgs a) {
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kernel(const KArgs a) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T, NW = T / 32;
   extern __shared__ float4 smem4[];
   float2 *spec = reinterpret_cast<float2 *>(smem4);
   float2 *tw = spec + spec_entries<LOGN>();
   float2 *scr_all = tw + tw_entries<LOGN>();
-  int *ctr = reinterpret_cast<int *>(scr_all + NW * a.scr);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t mloc = blockIdx.x;
   const int64_t mg = a.slice0 + mloc;
   const int64_t row = blockIdx.y;
 
+  PHASE_INIT();
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
-  if (tid == 0) *ctr = 0;
 
   // ---- F1 + first radix pass, read straight from HBM.  z[p] = f[2p] + i f[2p+1].
+  // The window's transition values h_0(|t|), |t| = A+1 .. Bw-1 (h_0 is even), are staged
+  // in the (still unused) packet scratch while the HBM loads are in flight.
   {
     constexpr int R = CF::F1, TASKS = N / R, PER = (TASKS + T - 1) / T;
     const float *xr = a.x + row * a.x_stride;
     const bool vec = ((reinterpret_cast<uintptr_t>(xr) & 7) == 0);
     const int64_t s0 = (mg - 1) * N - a.base_off;  // local index of frame sample 0
     const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
+    float *htab = reinterpret_cast<float *>(scr_all);
+    const bool hsm = a.tr - 1 <= NW * a.scr * 2;
     float2 v[PER][R];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
@@ -333,16 +524,14 @@ __global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_fwd_kernel(const KArgs 
       if (TASKS % T == 0 || j < TASKS) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int p = j + r * TASKS;
-          const int i0 = 2 * p;  // frame index of the real part
+          const int i0 = 2 * (j + r * TASKS);  // frame index of the real part
           const int t0 = i0 - N;
           const int at0 = t0 < 0 ? -t0 : t0;
           const int at1 = (t0 + 1) < 0 ? -(t0 + 1) : (t0 + 1);
-          float2 val = make_float2(0.f, 0.f);
+          float x0 = 0.f, x1 = 0.f;
           if (at0 < Bw || at1 < Bw) {
             int64_t idx = s0 + i0;
             if (a.wrap && idx < 0) idx += a.L;
-            float x0 = 0.f, x1 = 0.f;
             if (vec && idx >= 0 && idx + 1 < a.x_len) {
               const float2 xv = __ldcs(reinterpret_cast<const float2 *>(xr + idx));
               x0 = xv.x;
@@ -351,28 +540,42 @@ __global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_fwd_kernel(const KArgs 
               if (idx >= 0 && idx < a.x_len) x0 = __ldg(xr + idx);
               if (idx + 1 >= 0 && idx + 1 < a.x_len) x1 = __ldg(xr + idx + 1);
             }
-            const float h0a = at0 <= A ? 1.f : (at0 < Bw ? __ldg(a.h0 + i0) : 0.f);
-            const float h0b = at1 <= A ? 1.f : (at1 < Bw ? __ldg(a.h0 + i0 + 1) : 0.f);
-            val = make_float2(x0 * h0a, x1 * h0b);
           }
-          v[q][r] = val;
+          v[q][r] = make_float2(x0, x1);
         }
-        dft<R, -1>(v[q]);
       }
     }
-    __syncthreads();  // twiddle table and counter visible; nothing read spec yet
+    if (hsm)
+      for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0 + N + A + 1 + u);
+    __syncthreads();  // twiddles and window staged; nothing has read spec yet
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = tid + q * T;
       if (TASKS % T == 0 || j < TASKS) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i0 = 2 * (j + r * TASKS);
+          const int t0 = i0 - N;
+          const int at0 = t0 < 0 ? -t0 : t0;
+          const int at1 = (t0 + 1) < 0 ? -(t0 + 1) : (t0 + 1);
+          const float h0a = at0 <= A ? 1.f
+                            : (at0 < Bw ? (hsm ? htab[at0 - A - 1] : __ldg(a.h0 + i0)) : 0.f);
+          const float h0b = at1 <= A ? 1.f
+                            : (at1 < Bw ? (hsm ? htab[at1 - A - 1] : __ldg(a.h0 + i0 + 1)) : 0.f);
+          v[q][r] = make_float2(v[q][r].x * h0a, v[q][r].y * h0b);
+        }
+        dft<R, -1>(v[q]);
 #pragma unroll
         for (int r = 0; r < R; ++r) spec[padi(j * R + r)] = v[q][r];
       }
     }
     __syncthreads();
   }
+  PHASE_MARK(0, 0);
   pass_smem<N, CF::F2, CF::F1, -1, T>(spec, tw);
+  PHASE_MARK(0, 1);
   pass_smem<N, CF::F3, CF::F1 * CF::F2, -1, T>(spec, tw);
+  PHASE_MARK(0, 2);
 
   // ---- r2c packing: X[k] = E[k] + e^{-i pi k/N} O[k], k = 0..N  (Z[N] := Z[0])
   for (int k = tid; k <= N / 2; k += T) {
@@ -392,91 +595,115 @@ __global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_fwd_kernel(const KArgs 
     }
   }
   __syncthreads();
+  PHASE_MARK(0, 3);
 
-  // ---- F3-F5: channel packets (shape-sorted), dynamically scheduled over warps
+  // ---- F3-F5: channel packets, shape-sorted; warp w takes packets w, w + NW, ...
   float2 *scr = scr_all + warp * a.scr;
   float2 *out_row = a.coef_out + (row * a.nslices + mloc) * a.C;
-  for (;;) {
-    int pk = 0;
-    if (lane == 0) pk = atomicAdd(ctr, 1);
-    pk = __shfl_sync(FULL, pk, 0);
-    if (pk >= a.npackets) break;
+  for (int pk = warp; pk < a.npackets; pk += NW) {
     const PacketDev P = a.packets[pk];
-    const int m1 = P.m1m2 & 255, m2 = P.m1m2 >> 8;
+    const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
+    const bool simple = (P.m1m2 >> 16) & 1;
+    const PDesc pd = load_desc(a, P.chan_off, P.nch, lane);
+    if ((P.m1m2 >> 17) & 1) {
+      switch (m1) {
+#define X(S) \
+  case S: fwd_small<S, N>(a, spec, out_row, pd, P.nch, simple, lane); break;
+        SLICQ_SMALL(X)
+#undef X
+      }
+      continue;
+    }
+    if (simple) fwd_fold<N, true>(a, spec, scr, pd, m1 * m2, m1, m2 | 1, P.nch, P.magM, lane);
+    else fwd_fold<N, false>(a, spec, scr, pd, m1 * m2, m1, m2 | 1, P.nch, P.magM, lane);
+    __syncwarp();
     switch (m1) {
 #define X(S) \
-  case S: fwd_step1<S, N>(a, spec, scr, m2, P.nch, P.chan_off, lane); break;
+  case S: fwd_step1<S>(a, scr, pd, m2, P.nch, P.mag2, lane); break;
       SLICQ_SIZES(X)
 #undef X
     }
     __syncwarp();
     switch (m2) {
 #define X(S) \
-  case S: fwd_step2<S>(a, scr, out_row, m1, P.nch, P.chan_off, lane); break;
+  case S: fwd_step2<S>(a, scr, out_row, pd, m1, P.nch, P.mag1, lane); break;
       SLICQ_SIZES(X)
 #undef X
     }
     __syncwarp();
   }
+  PHASE_MARK(0, 4);
 }
 
 // ------------------------------------------------------------------ inverse kernel
 template <int LOGN>
-__global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_inv_kernel(const KArgs a) {
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kernel(const KArgs a) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T, NW = T / 32;
   extern __shared__ float4 smem4[];
   float2 *spec = reinterpret_cast<float2 *>(smem4);
   float2 *tw = spec + spec_entries<LOGN>();
-  float2 *chs = tw + tw_entries<LOGN>();  // chunk scratch
+  float2 *chs = tw + tw_entries<LOGN>();  // per-warp scratch
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int mloc = blockIdx.x;
   const int64_t mg = a.slice0 + mloc;
   const int64_t row = blockIdx.y;
 
+  PHASE_INIT();
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
   for (int i = tid; i < spec_entries<LOGN>(); i += T) spec[i] = make_float2(0.f, 0.f);
 
-  // ---- I1-I3 per chunk: channel FFTs into the chunk scratch, then the per-bin gather
-  const float2 *in_row = a.coef_in + (row * a.nslices + mloc) * a.C;
-  for (int c = 0; c < a.nchunks; ++c) {
-    const ChunkDev ck = a.chunks[c];
-    for (int pk = ck.pk0 + warp; pk < ck.pk1; pk += NW) {
-      const PacketDev P = a.packets[pk];
-      const int m1 = P.m1m2 & 255, m2 = P.m1m2 >> 8;
-      float2 *reg = chs + P.region;
-      switch (m1) {
+  // ---- I1-I3: channel packets by phase (packets of one phase touch disjoint bins)
+  {
+    float2 *scr = chs + warp * a.scr;
+    const float2 *in_row = a.coef_in + (row * a.nslices + mloc) * a.C;
+    __syncthreads();  // spectrum zeroed
+    for (int ph = 0; ph < a.nchunks; ++ph) {
+      const ChunkDev pr = a.chunks[ph];
+      for (int pk = pr.pk0 + warp; pk < pr.pk1; pk += NW) {
+        const PacketDev P = a.packets[pk];
+        const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
+        const bool simple = (P.m1m2 >> 16) & 1;
+        const PDesc pd = load_desc(a, P.chan_off, P.nch, lane);
+        if ((P.m1m2 >> 17) & 1) {
+          switch (m1) {
 #define X(S) \
-  case S: inv_step1<S>(a, in_row, reg, m2, P.nch, P.chan_off, lane); break;
-        SLICQ_SIZES(X)
+  case S: inv_small<S, N>(a, in_row, spec, scr, pd, P.nch, simple, lane); break;
+            SLICQ_SMALL(X)
 #undef X
-      }
-      __syncwarp();
-      switch (m2) {
+          }
+          continue;
+        }
+        switch (m1) {
 #define X(S) \
-  case S: inv_step2<S>(reg, m1, P.nch, lane); break;
-        SLICQ_SIZES(X)
+  case S: inv_step1<S>(a, in_row, scr, pd, m2, P.nch, P.mag2, lane); break;
+          SLICQ_SIZES(X)
 #undef X
+        }
+        __syncwarp();
+        switch (m2) {
+#define X(S) \
+  case S: inv_step2<S>(scr, m1, P.nch, P.mag1, lane); break;
+          SLICQ_SIZES(X)
+#undef X
+        }
+        __syncwarp();
+        if (simple)
+          inv_unfold<N, true>(a, spec, scr, pd, m1 * m2, m1, m2 | 1, P.nch, lane);
+        else
+          inv_unfold<N, false>(a, spec, scr, pd, m1 * m2, m1, m2 | 1, P.nch, lane);
       }
+      __syncthreads();
     }
-    __syncthreads();
-    const int32_t *bo = a.bin_off + ck.bin_base;
-    for (int b = ck.blo + tid; b <= ck.bhi; b += T) {
-      const int e0 = __ldg(bo + (b - ck.blo)), e1 = __ldg(bo + (b - ck.blo) + 1);
-      float2 acc = make_float2(0.f, 0.f);
-      for (int e = e0; e < e1; ++e) {
-        const uint2 ge = __ldg(reinterpret_cast<const uint2 *>(a.gents) + e);
-        const float2 f = chs[ge.x & 0x7fffffffu];
-        const float gv = __uint_as_float(ge.y);
-        const float im = (ge.x >> 31) ? -f.y : f.y;
-        acc.x = fmaf(f.x, gv, acc.x);
-        acc.y = fmaf(im, gv, acc.y);
-      }
-      float2 &sp = spec[padi(b)];
-      sp = cadd(sp, acc);
-    }
-    __syncthreads();
   }
+  // stage h~_0(|t|), |t| = A+1 .. Bw-1 (even window) into the now free scratch
+  const bool hsm = a.tr - 1 <= NW * a.scr * 2;
+  {
+    float *htab = reinterpret_cast<float *>(chs);
+    if (hsm)
+      for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u);
+  }
+  PHASE_MARK(1, 0);
 
   // ---- I4a: c2r packing  Z[k] = E[k] + i O[k],
   //   E = (H[k] + conj H[N-k])/2,  O = (H[k] - conj H[N-k]) e^{+i pi k/N} / 2
@@ -496,9 +723,12 @@ __global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_inv_kernel(const KArgs 
   }
   __syncthreads();
 
+  PHASE_MARK(1, 1);
   // ---- I4b: inverse N-point FFT (unnormalised), first passes in shared memory
   pass_smem<N, CF::I1, 1, +1, T>(spec, tw);
+  PHASE_MARK(1, 2);
   pass_smem<N, CF::I2, CF::I1, +1, T>(spec, tw);
+  PHASE_MARK(1, 3);
 
   // ---- last pass + I5 epilogue: z[p] -> samples 2p, 2p+1, times h~_0 / N, overlap-add
   {
@@ -539,7 +769,9 @@ __global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_inv_kernel(const KArgs 
           const int t = i - N;
           const int at = t < 0 ? -t : t;
           if (at >= Bw) continue;
-          const float val = (h ? v[q][r].y : v[q][r].x) * invN * __ldg(a.h0dual + i);
+          const float hd = at <= A ? 1.f  // h~_0 = 1 on the flat top
+                           : (hsm ? reinterpret_cast<const float *>(chs)[at - A - 1] : __ldg(a.h0dual + i));
+          const float val = (h ? v[q][r].y : v[q][r].x) * invN * hd;
           const int64_t s = (mg - 1) * N + i;  // global sample index (before wrap)
           if (at <= A) {
             if (a.circular) {
@@ -570,11 +802,14 @@ __global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_inv_kernel(const KArgs 
     if (!a.circular && mloc == 0) {  // spill entries no slice reaches
       for (int u = tid; u < a.halo - (Bw - 1); u += T) a.spill[row * a.halo + u] = 0.f;
     }
-    // ---- pairing: the second CTA to finish a boundary adds both halves (side0 + side1)
-    __threadfence();
+    PHASE_MARK(1, 4);
+    // ---- pairing: the second CTA to finish a boundary adds both halves (side0 + side1).
+    // Release: barrier, then one thread fences (cumulative, gpu scope) and counts; acquire:
+    // that thread fences after the count, then the barrier (the cooperative-groups pattern).
     __syncthreads();
     __shared__ int sflag[2];
     if (tid == 0) {
+      __threadfence();
       int fl = 0, fr = 0;
       if (left_paired) fl = (atomicAdd(a.cnt + row * S + bl, 1u) & 1u) ? 1 : 0;
       if (right_paired) fr = (atomicAdd(a.cnt + row * S + br, 1u) & 1u) ? 1 : 0;
@@ -590,6 +825,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_inv_kernel(const KArgs 
       const int64_t mb = a.slice0 + b;  // boundary between global slices mb and mb+1
       const float *h0p = bnd_row + (int64_t)b * 2 * trp;
       const float *h1p = h0p + trp;
+#pragma unroll 4
       for (int u = tid; u < a.tr - 1; u += T) {
         const float val = __ldcg(h0p + u) + __ldcg(h1p + u);
         const int64_t s = mb * N + A + 1 + u;
@@ -602,20 +838,22 @@ __global__ void __launch_bounds__(Big<LOGN>::T, 1) slicq_inv_kernel(const KArgs 
       }
     }
   }
+  PHASE_MARK(1, 5);
 }
 
 template <int LOGN>
 constexpr size_t fwd_smem_bytes(int scr) {
   return sizeof(float2) *
-             (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>() + (Big<LOGN>::T / 32) * scr) +
-         16;
+         (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>() + (Big<LOGN>::T / 32) * scr);
 }
 template <int LOGN>
 constexpr size_t inv_smem_bytes(int scr) {
-  return sizeof(float2) * (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>() + scr) + 16;
+  return fwd_smem_bytes<LOGN>(scr);
 }
 
 // Per-size entry points (defined in kernels_l<LOGN>.cu)
+template <int LOGN>
+int phase_times(unsigned long long *out32, int reset);
 template <int LOGN>
 int set_attrs(size_t fwd_smem, size_t inv_smem);
 template <int LOGN>

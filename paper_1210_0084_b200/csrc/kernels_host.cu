@@ -83,13 +83,24 @@ size_t inv_smem_for(int logN, int scr) {
   return 0;
 }
 
-constexpr size_t kSmemCap = 227 * 1024;
+constexpr size_t kSmemCap = 227 * 1024;  // per CTA
+constexpr int kSmallScratch = 640;        // float2 entries a small inverse packet may use
+constexpr size_t kSmemSM = 228 * 1024;   // per SM, 1 KB of it reserved per resident CTA
+
+int minb_for(int logN) {
+  switch (logN) {
+    case 11: return Big<11>::MINB;
+    case 12: return Big<12>::MINB;
+    case 13: return Big<13>::MINB;
+    case 14: return Big<14>::MINB;
+  }
+  return 1;
+}
+
+// shared-memory bytes a CTA may use if `ctas` CTAs are to be resident per SM
+size_t smem_budget(int ctas) { return std::min(kSmemCap, kSmemSM / ctas - 1024); }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
-
-struct ChanSlot {  // where a channel's F_k lives in its chunk's scratch (inverse)
-  int chunk = -1, region = 0, ci = 0, m1 = 1, s2 = 1;
-};
 
 }  // namespace
 
@@ -118,140 +129,123 @@ int configure_kernels(slicq_plan *p) {
   }
   auto nch_for = [](int m1, int m2) { return std::max(1, 32 / std::max(m1, m2)); };
 
-  // ---------------- forward: packets grouped by length, shape-sorted (I-cache locality),
-  // larger packets first (dynamic scheduling tail)
-  {
-    std::map<int, std::vector<int>> groups;
-    for (int k = 0; k < K2; ++k) groups[p->M[k]].push_back(k);
-    struct G { int M, cost; };
-    std::vector<G> order;
-    for (auto &kv : groups) {
-      const int m1 = fac[kv.first].first, m2 = fac[kv.first].second;
-      order.push_back({kv.first, nch_for(m1, m2) * kv.first * (m1 + m2)});
+  // ---------------- packets: runs of consecutive channels with the same length M and the
+  // same SIMPLE flag (J_k inside [0, N]), at most 32 / max(M1, M2) channels each
+  struct Pk {
+    PacketDev d;
+    std::vector<int> ks;
+    int size;
+    std::vector<std::pair<int, int>> bins;  // touched half-spectrum bins (closed intervals)
+  };
+  std::vector<Pk> pks;
+  auto is_simple = [&](int k) { return p->lo[k] >= 0 && p->lo[k] + p->len[k] - 1 <= N; };
+  for (int k = 0; k < K2;) {
+    const int M = p->M[k];
+    const bool simple = is_simple(k);
+    const bool small = M <= 32;  // one lane per channel, DFT_M in registers
+    const int m1 = small ? M : fac[M].first, m2 = small ? 1 : fac[M].second;
+    const int nch = small ? std::min(32, kSmallScratch / M) : nch_for(m1, m2);
+    Pk pk;
+    pk.d = PacketDev{};
+    pk.d.m1m2 = m1 | (m2 << 8) | ((simple ? 1 : 0) << 16) | ((small ? 1 : 0) << 17);
+    pk.d.magM = (uint32_t)(((uint64_t(1) << 32) + M - 1) / M);
+    pk.d.mag1 = (uint32_t)((65536 + m1 - 1) / m1);
+    pk.d.mag2 = (uint32_t)((65536 + m2 - 1) / m2);
+    while (k < K2 && p->M[k] == M && is_simple(k) == simple && (int)pk.ks.size() < nch)
+      pk.ks.push_back(k++);
+    pk.d.nch = (int)pk.ks.size();
+    pk.size = small ? pk.d.nch * M : pk.d.nch * m1 * (m2 | 1);
+    for (int kk : pk.ks) {  // bins the Hermitian rule of C15 touches
+      const int lo = p->lo[kk], hi = p->lo[kk] + p->len[kk] - 1;
+      auto clip = [&](int a0, int b0) {
+        a0 = std::max(a0, 0);
+        b0 = std::min(b0, N);
+        if (a0 <= b0) pk.bins.push_back({a0, b0});
+      };
+      clip(lo, hi);                  // direct bins j in [0, N]
+      clip(-hi, -lo);                // mirror of j <= 0 (DC side)
+      clip(N2 - hi, N2 - lo);        // mirror of j >= N (Nyquist side)
+      if (lo < 0) clip(lo + N2, hi + N2);  // j mod 2N for negative j (never <= N here)
     }
-    std::stable_sort(order.begin(), order.end(), [](const G &x, const G &y) { return x.cost > y.cost; });
+    pks.push_back(std::move(pk));
+  }
+  int need = 8;
+  for (const Pk &pk : pks) need = std::max(need, pk.size);
+  const int NW = kc.threads / 32;
+  const size_t budget2 = smem_budget(minb_for(logN));
+  const int cap2 = (int)((budget2 - fwd_smem_for(logN, 0)) / sizeof(float2) / NW) & ~7;
+  const int cap1 = (int)((kSmemCap - fwd_smem_for(logN, 0)) / sizeof(float2) / NW) & ~7;
+  if (need > cap1)
+    return set_error(SLICQ_EUNSUPPORTED, "channel scratch does not fit in shared memory");
+  (void)cap2;  // need <= cap2 keeps Big<LOGN>::MINB CTAs per SM
+  const int scr = need;
+  kc.fwd_scr = kc.inv_scr = (scr + 7) & ~7;
+  kc.fwd_smem = fwd_smem_for(logN, kc.fwd_scr);
+  kc.inv_smem = inv_smem_for(logN, kc.inv_scr);
+
+  // ---------------- forward order: shape-sorted (warps of a CTA walk the list together:
+  // I-cache locality), larger lengths first
+  {
+    std::vector<int> ord(pks.size());
+    for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+      const int Mx = (pks[x].d.m1m2 & 255) * ((pks[x].d.m1m2 >> 8) & 255);
+      const int My = (pks[y].d.m1m2 & 255) * ((pks[y].d.m1m2 >> 8) & 255);
+      if (Mx != My) return Mx > My;
+      return (pks[x].d.m1m2 >> 16) < (pks[y].d.m1m2 >> 16);
+    });
     p->fwd_packets.clear();
     p->fwd_pchans.clear();
-    int need = 8;
-    for (const G &g : order) {
-      const int m1 = fac[g.M].first, m2 = fac[g.M].second, nch = nch_for(m1, m2);
-      const std::vector<int> &ks = groups[g.M];
-      for (size_t i = 0; i < ks.size(); i += nch) {
-        PacketDev pk{};
-        pk.nch = (int)std::min<size_t>(nch, ks.size() - i);
-        pk.m1m2 = m1 | (m2 << 8);
-        pk.chan_off = (int)p->fwd_pchans.size();
-        for (int c = 0; c < pk.nch; ++c) p->fwd_pchans.push_back(ks[i + c]);
-        p->fwd_packets.push_back(pk);
-        need = std::max(need, pk.nch * m1 * (m2 | 1));
-      }
+    for (int i : ord) {
+      PacketDev d = pks[i].d;
+      d.chan_off = (int)p->fwd_pchans.size();
+      for (int k : pks[i].ks) p->fwd_pchans.push_back(k);
+      p->fwd_packets.push_back(d);
     }
-    kc.fwd_scr = (need + 7) & ~7;
-    kc.fwd_smem = fwd_smem_for(logN, kc.fwd_scr);
     kc.fwd_npackets = (int)p->fwd_packets.size();
-    if (kc.fwd_smem > kSmemCap)
-      return set_error(SLICQ_EUNSUPPORTED, "forward scratch does not fit in shared memory");
   }
 
-  // ---------------- inverse: packets of consecutive equal-length channels, cut into chunks
-  // whose F_k fit in shared memory; per chunk a per-bin gather list (CSR).
+  // ---------------- inverse: greedy colouring of the packet conflict graph (packets that
+  // share a touched bin get different phases), shape-sorted inside a phase
   {
-    const int cap = (int)((kSmemCap - inv_smem_for(logN, 0)) / sizeof(float2)) & ~7;
-    struct Pk { PacketDev d; std::vector<int> ks; int size; };
-    std::vector<Pk> pks;
-    for (int k = 0; k < K2;) {
-      const int M = p->M[k];
-      const int m1 = fac[M].first, m2 = fac[M].second, nch = nch_for(m1, m2);
-      Pk pk;
-      pk.d.m1m2 = m1 | (m2 << 8);
-      while (k < K2 && p->M[k] == M && (int)pk.ks.size() < nch) pk.ks.push_back(k++);
-      pk.d.nch = (int)pk.ks.size();
-      pk.size = pk.d.nch * m1 * (m2 | 1);
-      pks.push_back(pk);
+    auto overlap = [](const Pk &x, const Pk &y) {
+      for (auto &a0 : x.bins)
+        for (auto &b0 : y.bins)
+          if (a0.first <= b0.second && b0.first <= a0.second) return true;
+      return false;
+    };
+    std::vector<int> phase(pks.size(), -1);
+    int nph = 0;
+    for (size_t i = 0; i < pks.size(); ++i) {
+      std::vector<char> used(nph + 1, 0);
+      for (size_t j = 0; j < i; ++j)
+        if (phase[j] >= 0 && overlap(pks[i], pks[j])) used[phase[j]] = 1;
+      int ph = 0;
+      while (ph < nph && used[ph]) ++ph;
+      phase[i] = ph;
+      nph = std::max(nph, ph + 1);
     }
-    // chunks of consecutive packets
-    std::vector<std::vector<int>> chunk_pk(1);
-    int used = 0;
-    for (int i = 0; i < (int)pks.size(); ++i) {
-      if (pks[i].size > cap)
-        return set_error(SLICQ_EUNSUPPORTED, "inverse channel scratch does not fit in shared memory");
-      if (used + pks[i].size > cap) {
-        chunk_pk.emplace_back();
-        used = 0;
-      }
-      chunk_pk.back().push_back(i);
-      used += pks[i].size;
-    }
-    std::vector<ChanSlot> slot(K2);
     p->inv_packets.clear();
     p->inv_pchans.clear();
     p->chunks.clear();
-    p->bin_off.clear();
-    p->gents.clear();
-    int maxscr = 8;
-    for (int c = 0; c < (int)chunk_pk.size(); ++c) {
-      std::vector<int> &ids = chunk_pk[c];
-      // shape-sort inside the chunk (warps walk packets pk0 + warp, pk0 + warp + NW, ...)
+    for (int ph = 0; ph < nph; ++ph) {
+      std::vector<int> ids;
+      for (size_t i = 0; i < pks.size(); ++i)
+        if (phase[i] == ph) ids.push_back((int)i);
       std::stable_sort(ids.begin(), ids.end(),
-                       [&](int x, int y) { return pks[x].d.m1m2 < pks[y].d.m1m2; });
-      ChunkDev ck{};
-      ck.pk0 = (int)p->inv_packets.size();
-      int region = 0;
+                       [&](int x, int y) { return (pks[x].d.m1m2 & 0xffff) < (pks[y].d.m1m2 & 0xffff); });
+      ChunkDev pr{};
+      pr.pk0 = (int)p->inv_packets.size();
       for (int i : ids) {
-        Pk &pk = pks[i];
-        pk.d.region = region;
-        pk.d.chan_off = (int)p->inv_pchans.size();
-        const int m1 = pk.d.m1m2 & 255, m2 = pk.d.m1m2 >> 8;
-        for (int ci = 0; ci < pk.d.nch; ++ci) {
-          const int k = pk.ks[ci];
-          p->inv_pchans.push_back(k);
-          slot[k] = {c, region, ci, m1, m2 | 1};
-        }
-        p->inv_packets.push_back(pk.d);
-        region += pk.size;
+        PacketDev d = pks[i].d;
+        d.chan_off = (int)p->inv_pchans.size();
+        for (int k : pks[i].ks) p->inv_pchans.push_back(k);
+        p->inv_packets.push_back(d);
       }
-      ck.pk1 = (int)p->inv_packets.size();
-      maxscr = std::max(maxscr, region);
-      // gather terms of the chunk's channels
-      struct Term { int bin; int k; GatherEnt e; };
-      std::vector<Term> terms;
-      for (int i : ids)
-        for (int k : pks[i].ks) {
-          const ChanSlot &sl = slot[k];
-          const int M = p->M[k];
-          const int lo_mod = ((p->lo[k] % M) + M) % M;
-          const double half = (k == 0 || k == K2 - 1) ? 0.5 : 1.0;  // self-mirrored plateaus
-          const double sc = half / std::sqrt((double)M);
-          for (int d = 0; d < p->len[k]; ++d) {
-            const int j = p->lo[k] + d;
-            int q = lo_mod + d;
-            if (q >= M) q -= M;
-            const uint32_t fidx = (uint32_t)(sl.region + sl.ci * sl.m1 * sl.s2 + q);
-            const float gv = (float)(p->gdual[p->goff[k] + d] * sc);
-            int p1 = j % N2;
-            if (p1 < 0) p1 += N2;
-            if (p1 <= N) terms.push_back({p1, k, {fidx, gv}});
-            const int p2 = p1 == 0 ? 0 : N2 - p1;
-            if (p2 <= N) terms.push_back({p2, k, {fidx | 0x80000000u, gv}});
-          }
-        }
-      std::stable_sort(terms.begin(), terms.end(), [](const Term &x, const Term &y) {
-        return x.bin != y.bin ? x.bin < y.bin : x.k < y.k;
-      });
-      ck.blo = terms.empty() ? 0 : terms.front().bin;
-      ck.bhi = terms.empty() ? -1 : terms.back().bin;
-      ck.bin_base = (int)p->bin_off.size();
-      size_t t = 0;
-      for (int b = ck.blo; b <= ck.bhi + 1; ++b) {
-        while (t < terms.size() && terms[t].bin < b) ++t;
-        p->bin_off.push_back((int32_t)(p->gents.size() + t));
-      }
-      for (const Term &tm : terms) p->gents.push_back(tm.e);
-      p->chunks.push_back(ck);
+      pr.pk1 = (int)p->inv_packets.size();
+      p->chunks.push_back(pr);
     }
-    kc.inv_scr = (maxscr + 7) & ~7;
-    kc.inv_smem = inv_smem_for(logN, kc.inv_scr);
-    kc.nchunks = (int)p->chunks.size();
+    kc.nchunks = nph;
   }
   return SLICQ_OK;
 }
@@ -290,10 +284,14 @@ int upload(slicq_plan *p) {
     c.lo_mod = ((c.lo % c.M) + c.M) % c.M;
   }
   const size_t nG = p->g.size();
-  std::vector<float> g(nG);
+  std::vector<float> g(nG), gd(nG);
   for (int k = 0; k < K2; ++k) {
     const double sc = 1.0 / std::sqrt((double)p->M[k]);  // Alg. 1: sqrt(M) * IFFT (1/M)
-    for (int i = 0; i < p->len[k]; ++i) g[p->goff[k] + i] = (float)(p->g[p->goff[k] + i] * sc);
+    const double half = (k == 0 || k == K2 - 1) ? 0.5 : 1.0;  // self-mirrored plateaus (C15)
+    for (int i = 0; i < p->len[k]; ++i) {
+      g[p->goff[k] + i] = (float)(p->g[p->goff[k] + i] * sc);
+      gd[p->goff[k] + i] = (float)(p->gdual[p->goff[k] + i] * sc * half);
+    }
   }
   std::vector<float> h0(N2), h0d(N2);
   for (int64_t i = 0; i < N2; ++i) {
@@ -320,8 +318,7 @@ int upload(slicq_plan *p) {
       {p->inv_packets.data(), sizeof(PacketDev) * p->inv_packets.size(), 0},
       {p->inv_pchans.data(), sizeof(int32_t) * p->inv_pchans.size(), 0},
       {p->chunks.data(), sizeof(ChunkDev) * p->chunks.size(), 0},
-      {p->bin_off.data(), sizeof(int32_t) * p->bin_off.size(), 0},
-      {p->gents.data(), sizeof(GatherEnt) * p->gents.size(), 0},
+      {gd.data(), sizeof(float) * gd.size(), 0},
       {g.data(), sizeof(float) * g.size(), 0},
       {h0.data(), sizeof(float) * h0.size(), 0},
       {h0d.data(), sizeof(float) * h0d.size(), 0},
@@ -349,13 +346,12 @@ int upload(slicq_plan *p) {
   p->d.inv_packets = reinterpret_cast<PacketDev *>(b + parts[3].off);
   p->d.inv_pchans = reinterpret_cast<int32_t *>(b + parts[4].off);
   p->d.chunks = reinterpret_cast<ChunkDev *>(b + parts[5].off);
-  p->d.bin_off = reinterpret_cast<int32_t *>(b + parts[6].off);
-  p->d.gents = reinterpret_cast<GatherEnt *>(b + parts[7].off);
-  p->d.g = reinterpret_cast<float *>(b + parts[8].off);
-  p->d.h0 = reinterpret_cast<float *>(b + parts[9].off);
-  p->d.h0dual = reinterpret_cast<float *>(b + parts[10].off);
-  p->d.tw2n = reinterpret_cast<float *>(b + parts[11].off);
-  p->d.twM = reinterpret_cast<float *>(b + parts[12].off);
+  p->d.gdual = reinterpret_cast<float *>(b + parts[6].off);
+  p->d.g = reinterpret_cast<float *>(b + parts[7].off);
+  p->d.h0 = reinterpret_cast<float *>(b + parts[8].off);
+  p->d.h0dual = reinterpret_cast<float *>(b + parts[9].off);
+  p->d.tw2n = reinterpret_cast<float *>(b + parts[10].off);
+  p->d.twM = reinterpret_cast<float *>(b + parts[11].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
@@ -392,10 +388,9 @@ static KArgs base_args(const slicq_plan *p) {
   a.C = p->C;
   a.chan = p->d.chan;
   a.chunks = p->d.chunks;
-  a.bin_off = p->d.bin_off;
-  a.gents = p->d.gents;
   a.nchunks = p->kc.nchunks;
   a.g = p->d.g;
+  a.gdual = p->d.gdual;
   a.h0 = p->d.h0;
   a.h0dual = p->d.h0dual;
   a.tw2n = reinterpret_cast<const float2 *>(p->d.tw2n);
@@ -503,3 +498,17 @@ int launch_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t c
 }
 
 }  // namespace slicq
+
+// Debug only (not part of include/slicq.h): accumulated per-phase clock64 cycles of the
+// forward [0..15] and inverse [16..31] kernels, in a library built with
+// -DSLICQ_PHASE_TIMING (tools/phase_timing.py).  Returns -1 in the product build.
+extern "C" __attribute__((visibility("default"))) int slicq_debug_phase_times(
+    int logN, unsigned long long *out32, int reset) {
+  switch (logN) {
+    case 11: return slicq::kern::phase_times<11>(out32, reset);
+    case 12: return slicq::kern::phase_times<12>(out32, reset);
+    case 13: return slicq::kern::phase_times<13>(out32, reset);
+    case 14: return slicq::kern::phase_times<14>(out32, reset);
+  }
+  return -1;
+}

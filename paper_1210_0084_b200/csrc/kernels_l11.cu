@@ -29,5 +29,21 @@ cudaError_t launch_inv<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaS
   return cudaGetLastError();
 }
 
+template <>
+int phase_times<SLICQ_LOGN>(unsigned long long *out32, int reset) {
+#ifdef SLICQ_PHASE_TIMING
+  if (cudaMemcpyFromSymbol(out32, g_phase_cycles, sizeof(g_phase_cycles)) != cudaSuccess) return -1;
+  if (reset) {
+    static const unsigned long long zero[2][16] = {};
+    if (cudaMemcpyToSymbol(g_phase_cycles, zero, sizeof(zero)) != cudaSuccess) return -1;
+  }
+  return 0;
+#else
+  (void)out32;
+  (void)reset;
+  return -1;
+#endif
+}
+
 }  // namespace kern
 }  // namespace slicq

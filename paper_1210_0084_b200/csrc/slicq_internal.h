@@ -22,28 +22,22 @@ struct ChanDev {
 
 // A packet = channels of one length M = M1*M2 processed together by one warp, with at most
 // 32 tasks per DFT step (nch*M2 <= 32 and nch*M1 <= 32): one task per lane.
+// Small packets (M <= 32, flag bit 17): one lane per channel, whole DFT_M in registers.
 struct PacketDev {
-  int32_t m1m2;     // M1 | (M2 << 8)
+  int32_t m1m2;     // M1 | (M2 << 8) | SIMPLE << 16 | SMALL << 17  (small: M1 = M, M2 = 1)
   int32_t nch;      // channels in the packet
   int32_t chan_off; // offset into the packet channel list
-  int32_t region;   // inverse: float2 offset of the packet's region in the chunk scratch
+  uint32_t magM;    // ceil(2^32 / M): e / M = umulhi(e, magM) for e < 2^16
+  uint32_t mag1;    // ceil(2^16 / M1): q / M1 = (q * mag1) >> 16 for q < 64
+  uint32_t mag2;    // ceil(2^16 / M2)
+  int32_t pad0, pad1;
 };
 
-// Inverse: channels are processed in chunks whose F_k fit in shared memory; after each
-// chunk, every target bin b in [blo, bhi] is gathered by exactly one thread (no atomics).
+// Inverse: a phase is a range of packets that touch pairwise disjoint half-spectrum bins
+// (plan-time colouring), so they scatter concurrently without atomics.
 struct ChunkDev {
   int32_t pk0, pk1;   // packets [pk0, pk1) of the inverse packet list
-  int32_t blo, bhi;   // target half-spectrum bins touched by the chunk
-  int32_t bin_base;   // this chunk's (bhi - blo + 2) entries in bin_off
-  int32_t pad0, pad1, pad2;
-};
-
-// One term of the per-bin gather: F value at chunk-scratch position (fidx & 0x7fffffff),
-// conjugated if bit 31 is set (Hermitian rule, C15), times gval = dual (x 1/2 on the
-// self-mirrored plateaus) / sqrt(M_k).
-struct GatherEnt {
-  uint32_t fidx;
-  float gval;
+  int32_t pad0, pad1;
 };
 
 struct DeviceTables {
@@ -53,9 +47,8 @@ struct DeviceTables {
   PacketDev *inv_packets = nullptr;
   int32_t *inv_pchans = nullptr;
   ChunkDev *chunks = nullptr;
-  int32_t *bin_off = nullptr;
-  GatherEnt *gents = nullptr;
   float *g = nullptr;       // fp32 g_k / sqrt(M_k) on J_k (forward)
+  float *gdual = nullptr;   // fp32 dual / sqrt(M_k) on J_k, plateaus x 1/2 (inverse)
   float *h0 = nullptr;      // fp32 h_0[t+N], t in [-N, N)
   float *h0dual = nullptr;  // fp32 h~_0[t+N]
   float *tw2n = nullptr;    // float2: [64] e^{-i pi t/N} for t < 64, then [2N/64] for t = 64 h
@@ -68,11 +61,11 @@ struct KernelConfig {
   int logN = 0;          // N = 2^logN complex points in the r2c FFT of a 2N slice
   int threads = 0;       // CTA size
   int fwd_scr = 0;       // forward: per-warp scratch (float2 entries)
-  int inv_scr = 0;       // inverse: chunk scratch (float2 entries)
+  int inv_scr = 0;       // inverse: per-warp scratch (float2 entries)
   size_t fwd_smem = 0;   // dynamic shared memory bytes
   size_t inv_smem = 0;
   int fwd_npackets = 0;
-  int nchunks = 0;
+  int nchunks = 0;       // inverse phases
 };
 
 }  // namespace slicq
@@ -102,8 +95,6 @@ struct slicq_plan {
   std::vector<slicq::PacketDev> fwd_packets, inv_packets;
   std::vector<int32_t> fwd_pchans, inv_pchans;
   std::vector<slicq::ChunkDev> chunks;
-  std::vector<int32_t> bin_off;
-  std::vector<slicq::GatherEnt> gents;
 };
 
 namespace slicq {
