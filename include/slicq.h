@@ -114,9 +114,11 @@ SLICQ_API int64_t slicq_sl_len(const slicq_plan *p);                        /* 2
 SLICQ_API int64_t slicq_padded_length(const slicq_plan *p, int64_t n);      /* L = ceil(n/2N)*2N    */
 SLICQ_API int64_t slicq_num_slices(const slicq_plan *p, int64_t n);         /* S = L/N      */
 SLICQ_API int64_t slicq_halo(const slicq_plan *p);                          /* (N+tr)/2: one-sided reach of h_0 */
-/* Workspace bytes needed by slicq_inverse / slicq_inverse_range for `nslices` slices of
- * `batch` rows (forward needs none).  The workspace must be zero-filled once before its
- * first use and then be reused unmodified (it holds overlap-add pairing counters). */
+/* Workspace bytes needed by the hot-path calls for `nslices` slices of `batch` rows (0 for
+ * host-only plans).  One workspace serves both directions: it holds the inverse's overlap-add
+ * pairing counters and boundary halves, and a staging area for the spectra / channel
+ * contributions of one chunk of slices.  Zero-fill it once before its first use and then
+ * reuse it unmodified, one workspace per concurrently running call. */
 SLICQ_API size_t slicq_workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
 /* Plan export for parity tests (host out-params, any may be NULL):
  *   lo[K+2], len[K+2]   unwrapped support J_k = [lo_k, lo_k + len_k) in 2N-bins (C5)
@@ -133,9 +135,9 @@ SLICQ_API const char *slicq_last_error(void);                               /* t
  *   x       device float32 [batch][n], rows contiguous, 4-byte aligned (8-byte gives
  *           vector loads)
  *   coeffs  device slicq_c32 [batch][S][C], 8-byte aligned
- *   ws      unused (may be NULL)
- * Returns SLICQ_ESHAPE on n < 1, batch < 1, NULL/misaligned pointers;
- * SLICQ_ECUDA if the launch fails. */
+ *   ws      >= slicq_workspace_bytes(p, S, batch) bytes, 16-byte aligned (see above)
+ * Returns SLICQ_ESHAPE on n < 1, batch < 1, NULL/misaligned pointers, small workspace;
+ * SLICQ_ECUDA if a launch fails. */
 SLICQ_API int slicq_forward(const slicq_plan *p, const float *x, int64_t n, int64_t batch,
                   slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream);
 
@@ -156,7 +158,7 @@ SLICQ_API int slicq_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_
  *   left neighbour's samples (circularly wrapped for slice0 = 0) in the first
  *   `halo` entries and zeros for padding positions >= n.  halo must be even and
  *   >= slicq_halo(p) - 1; positions outside [0, x_len) read as 0.
- *   coeffs_local: [batch][nslices][C].
+ *   coeffs_local: [batch][nslices][C]; ws as for slicq_forward with S = nslices.
  * slicq_inverse_range: y_local [batch][nslices*N] (row stride y_stride) receives the
  *   overlap-added output of samples [slice0*N, (slice0+nslices)*N) from these slices
  *   only; left_spill [batch][halo] receives the part of slice0's output that falls on

@@ -145,8 +145,9 @@ class Plan:
             out = torch.empty((B, S, self.coeffs_per_slice), dtype=torch.complex64, device=x.device)
         else:
             _check_tensor(out, torch.complex64, "out", (B, S, self.coeffs_per_slice))
-        check(lib().slicq_forward(self._h, x.data_ptr(), n, B, out.data_ptr(), None, 0,
-                                  _stream_ptr(stream)), "slicq_forward")
+        ws = self.workspace(S, B, x.device)
+        check(lib().slicq_forward(self._h, x.data_ptr(), n, B, out.data_ptr(), ws.data_ptr(),
+                                  ws.numel() * 4, _stream_ptr(stream)), "slicq_forward")
         return out
 
     def inverse(self, c: torch.Tensor, n: int, out: Optional[torch.Tensor] = None,
@@ -180,9 +181,11 @@ class Plan:
         if out is None:
             out = torch.empty((B, nslices, self.coeffs_per_slice), dtype=torch.complex64,
                               device=x_local.device)
+        ws = self.workspace(nslices, B, x_local.device)
         check(lib().slicq_forward_range(self._h, x_local.data_ptr(), xl, x_local.stride(0), halo,
-                                        slice0, nslices, total_slices, B, out.data_ptr(), None, 0,
-                                        _stream_ptr(stream)), "slicq_forward_range")
+                                        slice0, nslices, total_slices, B, out.data_ptr(),
+                                        ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)),
+              "slicq_forward_range")
         return out
 
     def inverse_range(self, c_local: torch.Tensor, slice0: int, nslices: int, total_slices: int,

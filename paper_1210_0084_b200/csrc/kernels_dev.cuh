@@ -1,24 +1,32 @@
-// sm_100a kernels of the sliCQ hot path (device code, instantiated per slice size in
-// kernels_l<LOGN>.cu).  DESIGN.md "Kernels" describes the design; step names follow
-// SURVEY.md §8(a).
+// sm_100a kernels of the sliCQ hot path (device code).  DESIGN.md "Kernels" describes the
+// design; step names follow SURVEY.md §8(a).  Two kernels per direction, run over chunks of
+// (row, slice) units whose intermediate stays in a workspace staging buffer (sized to stay
+// L2-resident):
 //
-//   slicq_fwd_kernel<LOGN>  one CTA per (signal row, slice):
-//     F1  gather the Tukey-windowed slice straight from HBM
-//     F2  r2c FFT_{2N}: complex N-point Stockham FFT in shared memory (register radix
-//         16/32 passes) + packing step                          (Alg. 1 line P:186)
-//     F3  per channel: multiply by g_k, fold to M_k             (C5)
-//     F4  sqrt(M_k) IFFT_{M_k} as a four-step M1 x M2 register DFT; channels of one length
-//         form a warp "packet" (<= 32 tasks per step, one per lane)
-//     F5  store c^m_k                                           (P:320-323 layout view)
-//   slicq_inv_kernel<LOGN>  one CTA per (row, slice):
-//     I1/I2  load c^m_k, FFT_{M_k} (four-step, in place in the chunk scratch)
-//     I3  dual multiply + overlap sum as a per-bin GATHER: every half-spectrum bin is
-//         summed by one thread from plan-time (F position, dual weight, conj) lists, with the
-//         Hermitian rule of C15 folded in -- deterministic, no atomics
-//     I4  c2r IFFT_{2N} (packing step + N-point Stockham)
-//     I5  multiply by h~_0 and overlap-add; slice-boundary samples are paired across CTAs
-//         through the workspace with a parity counter (no spinning, deterministic a+b)
-//                                                                 (P:342-345)
+//   forward
+//     slicq_fwd_spec_kernel<LOGN>   one CTA per unit:
+//       F1  gather the Tukey-windowed slice straight from HBM
+//       F2  r2c FFT_{2N}: complex N-point Stockham FFT in shared memory (register radix
+//           16/32 passes) + packing step -> X[0..N] into the staging buffer
+//     slicq_fwd_chan_kernel         one warp per (packet, tile of units):
+//       F3  fold: buf[p] = X(j) g_k[j]/sqrt(M_k), j = p mod M_k, from a plan-time element
+//           table (bin, conj flag, scratch position, weight)       (C5)
+//       F4  IFFT_{M_k} as a four-step M1 x M2 register DFT (M_k > 32) or a whole DFT_M per
+//           lane (M_k <= 32), compile-time twiddles
+//       F5  store c^m_k                                            (P:320-323 layout view)
+//   inverse
+//     slicq_inv_chan_kernel         one warp per (packet, tile of units):
+//       I1/I2  load c^m_k, FFT_{M_k} (four-step / per lane)
+//       I3a    contribution Z[k][d] = F_k[j mod M_k] g~_k[j]/sqrt(M_k), j = lo_k + d
+//     slicq_inv_spec_kernel<LOGN>   one CTA per unit:
+//       I3b per-bin gather of the contributions with the Hermitian rule of C15 folded into
+//           a plan-time CSR list -- deterministic, no atomics
+//       I4  c2r IFFT_{2N} (packing step + N-point Stockham)
+//       I5  multiply by h~_0 and overlap-add; slice-boundary samples are paired across CTAs
+//           through the workspace with a parity counter (no spinning, deterministic a+b)
+//                                                                  (P:342-345)
+// The channel kernels amortise their per-shape code (I-cache) and plan tables over a tile of
+// slices: the plan is identical for every slice.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -105,6 +113,7 @@ constexpr int tw_entries() {
 }
 
 struct KArgs {
+  // signal side
   const float *x;
   float *y;
   float *spill;
@@ -112,21 +121,30 @@ struct KArgs {
   int64_t y_len, y_stride, y_base, halo;
   int wrap;       // forward: negative sample indices wrap by L (circular)
   int circular;   // inverse: slice S-1 pairs with slice 0
-  int64_t slice0;
-  int nslices;
+  int64_t slice0; // global index of local slice 0
+  int nslices;    // slices per row (S, or the local range)
   int tr;
-  int scr;        // forward: per-warp scratch entries; inverse: chunk scratch entries
-  int npackets;   // forward packets
-  int nchunks;    // inverse phases
+  // chunk of units (unit u = row * nslices + local slice)
+  int64_t unit0;
+  int nunits;
+  int tile;       // units per channel-kernel tile
+  // coefficients
   int64_t C;
   float2 *coef_out;
   const float2 *coef_in;
+  // staging (workspace): X spectra [unit][xs], contributions [unit][zs]
+  float2 *stage;
+  int64_t xs, zs;
+  // plan tables
   const ChanDev *chan;
   const PacketDev *packets;
   const int32_t *pchans;
-  const ChunkDev *chunks;   // inverse: packet ranges of the phases
-  const float *g;           // g_k / sqrt(M_k) on J_k
-  const float *gdual;       // dual / sqrt(M_k) on J_k (plateaus x 1/2, C15)
+  int npackets;
+  int scr;                  // channel kernels: per-warp scratch entries
+  const uint2 *fent;        // forward element table (enc, weight bits)
+  const uint2 *ient;        // inverse element table (scratch pos, weight bits)
+  const int32_t *bin_off;   // inverse gather CSR: [N+2]
+  const uint32_t *gents;    // contribution index | conj << 31
   const float *h0;
   const float *h0dual;
   const float2 *tw2n;
@@ -134,6 +152,7 @@ struct KArgs {
   unsigned *cnt;  // inverse workspace: [batch][nslices] pairing counters
   float *bnd;     // inverse workspace: [batch][nslices][2][tr] boundary halves
 };
+
 
 // e^{-i pi e / N} for e in [0, 2N): two-level table, 2 shared loads + 1 complex multiply
 __device__ __forceinline__ float2 tw_lookup(const float2 *tw, int e) {
@@ -235,75 +254,40 @@ __device__ __forceinline__ void chan_twiddle(float2 (&v)[M1], int p2, int M, con
   }
 }
 
+// ------------------------------------------------------------------ PDL helpers
+// Programmatic dependent launch: kernels of a call are launched back to back; each waits for
+// its predecessor's memory before touching shared buffers and lets the next one launch
+// when its CTA is done (hides launch gaps, keeps stream order).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ channel packets
-// A packet's channel ci owns the region reg + ci*M1*S2 (S2 = M2 | 1) of the warp scratch:
-// first the length-M vector of the fold (forward) / of F (inverse), in between the
-// M1 x S2 four-step intermediate A[n1][p2].  One task per lane and step (nch*M1, nch*M2
-// <= 32), so the in-place steps only need a warp barrier between their loads and stores.
-
-// Packet channel descriptors live in registers: lane c holds channel c's ChanDev (one
-// parallel load per packet); fields are broadcast with shuffles.
-struct PDesc {
-  ChanDev c;
-};
-__device__ __forceinline__ PDesc load_desc(const KArgs &a, int chan_off, int nch, int lane) {
-  const int k = __ldg(a.pchans + chan_off + (lane < nch ? lane : 0));
-  return PDesc{a.chan[k]};
-}
-__device__ __forceinline__ int shf(int v, int src) { return __shfl_sync(FULL, v, src); }
-
-// F3 (forward fold, C5): buf[p] = X(j) g_k[j]/sqrt(M_k) for the j in J_k with
-// j = p (mod M_k), 0 where there is none (zero padding).  Flattened over the packet's
-// channels (all of length M): element e -> channel e / M, d = e mod M; consecutive lanes
-// write consecutive p (conflict-free).  SIMPLE: every J_k lies in [0, N].
-template <int N, bool SIMPLE>
-__device__ __forceinline__ void fwd_fold(const KArgs &a, const float2 *spec, float2 *reg,
-                                         const PDesc &pd, int M, int m1, int S2, int nch,
-                                         unsigned mag, int lane) {
-  const int tot = nch * M;
-#pragma unroll 4
-  for (int base = 0; base < tot; base += 32) {
-    const int e = base + lane;
-    const int ci = min((int)__umulhi((unsigned)e, mag), nch - 1);
-    const int d = e - ci * M;
-    const int lo = shf(pd.c.lo, ci), len = shf(pd.c.len, ci);
-    const int lo_mod = shf(pd.c.lo_mod, ci), goff = shf(pd.c.goff, ci);
-    if (e < tot) {
-      int p = lo_mod + d;
-      if (p >= M) p -= M;
-      float2 val = make_float2(0.f, 0.f);
-      if (d < len) {
-        const float gv = __ldg(a.g + goff + d);
-        const float2 xv = SIMPLE ? spec[padi(lo + d)] : spec_at<N>(spec, lo + d);
-        val = cscale(xv, gv);
-      }
-      reg[ci * m1 * S2 + p] = val;
-    }
-  }
-}
+// A packet = channels of one length M.  Big packets (M > 32) are a four-step M1 x M2 DFT
+// with one task per lane and step; channel ci owns the region ci*M1*S2 (S2 = M2 | 1) of the
+// warp scratch: first the length-M vector (fold / F), in between A[n1][p2].  Small packets
+// (M <= 32) give each lane a whole channel.
 
 // F4 step 1, in place: task (ci, p2) takes buf[M2 p1 + p2], p1 < M1; DFT_{M1} (sign +);
 // twiddle e^{+2 pi i p2 n1 / M}; stores A[n1 S2 + p2].
-__device__ __forceinline__ int div_small(int q, unsigned mag16) { return (q * (int)mag16) >> 16; }
-
 template <int M1>
-__device__ __forceinline__ void fwd_step1(const KArgs &a, float2 *reg, const PDesc &pd, int m2,
-                                          int nch, unsigned mag2, int lane) {
+__device__ __noinline__ void fwd_step1(const float2 *twM, float2 *reg, int m2, int nch,
+                                          unsigned mag2, int twoff_lane, int lane) {
   const int nt = nch * m2;
   const bool act = lane < nt;
-  const int ci = act ? div_small(lane, mag2) : 0;
+  const int ci = act ? (lane * (int)mag2) >> 16 : 0;
   const int p2 = act ? lane - ci * m2 : 0;
   const int S2 = m2 | 1;
   float2 *base = reg + ci * M1 * S2;
   float2 v[M1];
 #pragma unroll
   for (int p1 = 0; p1 < M1; ++p1) v[p1] = base[m2 * p1 + p2];
-  const int twoff = shf(pd.c.twoff, ci);
-  const int M = M1 * m2;
+  const int twoff = __shfl_sync(FULL, twoff_lane, ci);
   __syncwarp();
   if (act) {
     dft<M1, +1>(v);
-    chan_twiddle<M1, +1>(v, p2, M, a.twM + twoff);
+    chan_twiddle<M1, +1>(v, p2, M1 * m2, twM + twoff);
 #pragma unroll
     for (int n1 = 0; n1 < M1; ++n1) base[n1 * S2 + p2] = v[n1];
   }
@@ -311,14 +295,13 @@ __device__ __forceinline__ void fwd_step1(const KArgs &a, float2 *reg, const PDe
 
 // F4 step 2 + F5: task (ci, n1): DFT_{M2} over p2 -> c[n1 + M1 n2] (coalesced over n1).
 template <int M2>
-__device__ __forceinline__ void fwd_step2(const KArgs &a, const float2 *reg, float2 *out_row,
-                                          const PDesc &pd, int m1, int nch, unsigned mag1,
-                                          int lane) {
+__device__ __noinline__ void fwd_step2(const float2 *reg, float2 *out_row, int m1, int nch,
+                                          unsigned mag1, int off_lane, int lane) {
   const int nt = nch * m1;
   constexpr int S2 = M2 | 1;
-  const int ci = lane < nt ? div_small(lane, mag1) : 0;
+  const int ci = lane < nt ? (lane * (int)mag1) >> 16 : 0;
   const int n1 = lane - ci * m1;
-  const int off = shf(pd.c.off, ci);
+  const int off = __shfl_sync(FULL, off_lane, ci);
   if (lane >= nt) return;
   float2 v[M2];
   const float2 *A = reg + ci * m1 * S2 + n1 * S2;
@@ -330,22 +313,42 @@ __device__ __forceinline__ void fwd_step2(const KArgs &a, const float2 *reg, flo
   for (int n2 = 0; n2 < M2; ++n2) __stcs(o + m1 * n2, v[n2]);
 }
 
-// I2 step 1: task (ci, p2) loads c[M2 p1 + p2] from HBM; DFT_{M1} (sign -); twiddle.
+// Small forward packet: lane c < nch owns channel c; element p of its fold comes from the
+// table entry p*32 + c (bin | conj << 15, weight; weight 0 for zero padding).
+template <int M>
+__device__ __noinline__ void fwd_small(const uint2 *ent, const float2 *X, float2 *out_row,
+                                          int nch, int off_lane, int lane) {
+  if (lane >= nch) return;
+  float2 v[M];
+#pragma unroll
+  for (int p = 0; p < M; ++p) {
+    const uint2 e = __ldg(ent + p * 32 + lane);
+    const float2 xv = X[e.x & 0x7fff];
+    const float gv = __uint_as_float(e.y);
+    v[p] = make_float2(xv.x * gv, ((e.x >> 15) & 1) ? -xv.y * gv : xv.y * gv);
+  }
+  dft<M, +1>(v);
+  float2 *o = out_row + off_lane;
+#pragma unroll
+  for (int n = 0; n < M; ++n) __stcs(o + n, v[n]);
+}
+
+// I2 step 1: task (ci, p2) loads c[M2 p1 + p2]; DFT_{M1} (sign -); twiddle.
 template <int M1>
-__device__ __forceinline__ void inv_step1(const KArgs &a, const float2 *in_row, float2 *reg,
-                                          const PDesc &pd, int m2, int nch, unsigned mag2,
-                                          int lane) {
+__device__ __noinline__ void inv_step1(const float2 *twM, const float2 *in_row, float2 *reg,
+                                          int m2, int nch, unsigned mag2, int off_lane,
+                                          int twoff_lane, int lane) {
   const int nt = nch * m2;
-  const int ci = lane < nt ? div_small(lane, mag2) : 0;
+  const int ci = lane < nt ? (lane * (int)mag2) >> 16 : 0;
   const int p2 = lane - ci * m2;
-  const int off = shf(pd.c.off, ci), twoff = shf(pd.c.twoff, ci);
+  const int off = __shfl_sync(FULL, off_lane, ci), twoff = __shfl_sync(FULL, twoff_lane, ci);
   if (lane >= nt) return;
   float2 v[M1];
   const float2 *src = in_row + off + p2;
 #pragma unroll
   for (int p1 = 0; p1 < M1; ++p1) v[p1] = __ldcs(src + p1 * m2);
   dft<M1, -1>(v);
-  chan_twiddle<M1, -1>(v, p2, M1 * m2, a.twM + twoff);
+  chan_twiddle<M1, -1>(v, p2, M1 * m2, twM + twoff);
   const int S2 = m2 | 1;
   float2 *A = reg + ci * M1 * S2 + p2;
 #pragma unroll
@@ -354,11 +357,11 @@ __device__ __forceinline__ void inv_step1(const KArgs &a, const float2 *in_row, 
 
 // I2 step 2, in place: F[n1 + M1 n2] = (unnormalised FFT_M of c) overwrites the region.
 template <int M2>
-__device__ __forceinline__ void inv_step2(float2 *reg, int m1, int nch, unsigned mag1, int lane) {
+__device__ __noinline__ void inv_step2(float2 *reg, int m1, int nch, unsigned mag1, int lane) {
   const int nt = nch * m1;
   constexpr int S2 = M2 | 1;
   const bool act = lane < nt;
-  const int ci = act ? div_small(lane, mag1) : 0;
+  const int ci = act ? (lane * (int)mag1) >> 16 : 0;
   const int n1 = act ? lane - ci * m1 : 0;
   float2 v[M2];
   float2 *base = reg + ci * m1 * S2;
@@ -373,138 +376,177 @@ __device__ __forceinline__ void inv_step2(float2 *reg, int m1, int nch, unsigned
   }
 }
 
-// I3: spectrum[j] += F[j mod M] g~_k[j]/sqrt(M) over j in J_k, channel after
-// channel (channels of a packet may overlap), lanes over j (distinct bins).  Non-SIMPLE
-// channels apply the Hermitian rule of C15: the term goes to j mod 2N if <= N and its
-// conjugate to -j mod 2N if <= N (plateau weights carry the 1/2).  Packets that run
-// concurrently never share a bin (plan-time phase colouring), so plain read-modify-write.
-template <int N, bool SIMPLE>
-__device__ __forceinline__ void inv_unfold(const KArgs &a, float2 *spec, const float2 *reg,
-                                           const PDesc &pd, int M, int m1, int S2, int nch,
-                                           int lane) {
-  for (int ci = 0; ci < nch; ++ci) {
-    const int lo = shf(pd.c.lo, ci), len = shf(pd.c.len, ci);
-    const int lo_mod = shf(pd.c.lo_mod, ci), goff = shf(pd.c.goff, ci);
-    const float2 *F = reg + ci * m1 * S2;
-    const float *gd = a.gdual + goff;
-#pragma unroll 4
-    for (int d = lane; d < len; d += 32) {
-      int p = lo_mod + d;
-      if (p >= M) p -= M;
-      const float2 v = cscale(F[p], __ldg(gd + d));
-      const int j = lo + d;
-      if (SIMPLE) {
-        float2 &sp = spec[padi(j)];
-        sp = cadd(sp, v);
-      } else {
-        int p1 = j < 0 ? j + 2 * N : j;
-        if (p1 <= N) {
-          float2 &sp = spec[padi(p1)];
-          sp = cadd(sp, v);
-        }
-        const int p2 = p1 == 0 ? 0 : 2 * N - p1;
-        if (p2 <= N) {
-          float2 &sp = spec[padi(p2)];
-          sp = cadd(sp, cconj(v));
-        }
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// ---- small channels (M <= 32): lane c owns channel c of the packet, DFT_M in registers
-// F3-F5 for one channel per lane: fold into registers, DFT_M (sign +), store c^m_k.
-template <int M, int N>
-__device__ __forceinline__ void fwd_small(const KArgs &a, const float2 *spec, float2 *out_row,
-                                          const PDesc &pd, int nch, bool simple, int lane) {
+// Small inverse packet: lane c loads channel c, FFT_M, F[q] -> scratch q*nch + c.
+template <int M>
+__device__ __noinline__ void inv_small(const float2 *in_row, float2 *reg, int nch,
+                                          int off_lane, int lane) {
   if (lane >= nch) return;
-  const ChanDev &ch = pd.c;
+  const float2 *src = in_row + off_lane;
   float2 v[M];
 #pragma unroll
-  for (int p = 0; p < M; ++p) {
-    int d = p - ch.lo_mod;
-    if (d < 0) d += M;
-    float2 val = make_float2(0.f, 0.f);
-    if (d < ch.len) {
-      const float gv = __ldg(a.g + ch.goff + d);
-      const float2 xv = simple ? spec[padi(ch.lo + d)] : spec_at<N>(spec, ch.lo + d);
-      val = cscale(xv, gv);
-    }
-    v[p] = val;
-  }
-  dft<M, +1>(v);
-  float2 *o = out_row + ch.off;
+  for (int n = 0; n < M; ++n) v[n] = __ldcs(src + n);
+  dft<M, -1>(v);
 #pragma unroll
-  for (int n = 0; n < M; ++n) __stcs(o + n, v[n]);
-}
-
-// I1-I3 for one channel per lane: load c, DFT_M (sign -) into scratch F[q][lane], then the
-// channels scatter one after another (they may overlap), lanes over bins.
-template <int M, int N>
-__device__ __forceinline__ void inv_small(const KArgs &a, const float2 *in_row, float2 *spec,
-                                          float2 *scr, const PDesc &pd, int nch, bool simple,
-                                          int lane) {
-  if (lane < nch) {
-    const float2 *src = in_row + pd.c.off;
-    float2 v[M];
-#pragma unroll
-    for (int n = 0; n < M; ++n) v[n] = __ldcs(src + n);
-    dft<M, -1>(v);
-#pragma unroll
-    for (int q = 0; q < M; ++q) scr[q * nch + lane] = v[q];
-  }
-  __syncwarp();
-  for (int ci = 0; ci < nch; ++ci) {
-    const int lo = shf(pd.c.lo, ci), len = shf(pd.c.len, ci);
-    const int lo_mod = shf(pd.c.lo_mod, ci), goff = shf(pd.c.goff, ci);
-    if (lane < len) {
-      const int d = lane;
-      int q = lo_mod + d;
-      if (q >= M) q -= M;
-      const float2 v = cscale(scr[q * nch + ci], __ldg(a.gdual + goff + d));
-      const int j = lo + d;
-      if (simple) {
-        float2 &sp = spec[padi(j)];
-        sp = cadd(sp, v);
-      } else {
-        int p1 = j < 0 ? j + 2 * N : j;
-        if (p1 <= N) {
-          float2 &sp = spec[padi(p1)];
-          sp = cadd(sp, v);
-        }
-        const int p2 = p1 == 0 ? 0 : 2 * N - p1;
-        if (p2 <= N) {
-          float2 &sp = spec[padi(p2)];
-          sp = cadd(sp, cconj(v));
-        }
-      }
-    }
-    __syncwarp();
-  }
+  for (int q = 0; q < M; ++q) reg[q * nch + lane] = v[q];
 }
 
 #define SLICQ_SMALL(X) X(4) X(6) X(8) X(10) X(12) X(16) X(18) X(20) X(24) X(30) X(32)
-
 #define SLICQ_SIZES(X) \
   X(1) X(2) X(3) X(4) X(5) X(6) X(8) X(9) X(10) X(12) X(15) X(16) X(18) X(20) X(24) X(25) X(27) X(30) X(32)
 
-// ------------------------------------------------------------------ forward kernel
+// ------------------------------------------------------------------ channel kernels
+// Persistent grid; a work item is (packet group c, tile t): warp w owns packet c*NW + w for
+// the units of tile t.  Defined in one translation unit only (kernels_host.cu).
+constexpr int CHAN_T = 256;
+#ifdef SLICQ_DEFINE_CHAN_KERNELS
+
+__global__ void __launch_bounds__(CHAN_T, 2) slicq_fwd_chan_kernel(const KArgs a) {
+  extern __shared__ float4 smem4[];
+  constexpr int NW = CHAN_T / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_wait();
+  // persistent: work items (packet group, tile) in packet-group-major order, so that all
+  // SMs run the same packet shapes (code) at the same time
+  const int ntiles = (a.nunits + a.tile - 1) / a.tile;
+  const int nitems = ((a.npackets + NW - 1) / NW) * ntiles;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int pk = (item / ntiles) * NW + warp;
+    if (pk >= a.npackets) continue;
+    float2 *scr = reinterpret_cast<float2 *>(smem4) + warp * a.scr;
+    const PacketDev P = a.packets[pk];
+    const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
+    const bool small = (P.m1m2 >> 17) & 1;
+    const int nch = P.nch;
+    const int ck = __ldg(a.pchans + P.chan_off + (lane < nch ? lane : 0));
+    const int c_off = __ldg(&a.chan[ck].off), c_twoff = __ldg(&a.chan[ck].twoff);
+    const uint2 *ent = a.fent + P.fent_off;
+    const int ne = small ? 0 : nch * m1 * m2;
+    const int u_lo = (item % ntiles) * a.tile;
+    const int u_hi = min(a.nunits, u_lo + a.tile);
+    for (int ul = u_lo; ul < u_hi; ++ul) {
+      const float2 *X = a.stage + (int64_t)ul * a.xs;
+      float2 *out_row = a.coef_out + (a.unit0 + ul) * a.C;
+      if (small) {
+        switch (m1) {
+#define X_(S) \
+  case S: fwd_small<S>(ent, X, out_row, nch, c_off, lane); break;
+          SLICQ_SMALL(X_)
+#undef X_
+        }
+        continue;
+      }
+      // F3 fold from the element table (coalesced over e; positions conflict-free)
+#pragma unroll 4
+      for (int e = lane; e < ne; e += 32) {
+        const uint2 en = __ldg(ent + e);
+        const float2 xv = X[en.x & 0x7fff];
+        const float gv = __uint_as_float(en.y);
+        scr[en.x >> 16] = make_float2(xv.x * gv, ((en.x >> 15) & 1) ? -xv.y * gv : xv.y * gv);
+      }
+      __syncwarp();
+      switch (m1) {
+#define X_(S) \
+  case S: fwd_step1<S>(a.twM, scr, m2, nch, P.mag2, c_twoff, lane); break;
+        SLICQ_SIZES(X_)
+#undef X_
+      }
+      __syncwarp();
+      switch (m2) {
+#define X_(S) \
+  case S: fwd_step2<S>(scr, out_row, m1, nch, P.mag1, c_off, lane); break;
+        SLICQ_SIZES(X_)
+#undef X_
+      }
+      __syncwarp();
+    }
+  }
+  pdl_trigger();
+}
+
+__global__ void __launch_bounds__(CHAN_T, 2) slicq_inv_chan_kernel(const KArgs a) {
+  extern __shared__ float4 smem4[];
+  constexpr int NW = CHAN_T / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_wait();
+  // persistent: work items (packet group, tile) in packet-group-major order, so that all
+  // SMs run the same packet shapes (code) at the same time
+  const int ntiles = (a.nunits + a.tile - 1) / a.tile;
+  const int nitems = ((a.npackets + NW - 1) / NW) * ntiles;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int pk = (item / ntiles) * NW + warp;
+    if (pk >= a.npackets) continue;
+    float2 *scr = reinterpret_cast<float2 *>(smem4) + warp * a.scr;
+    const PacketDev P = a.packets[pk];
+    const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
+    const bool small = (P.m1m2 >> 17) & 1;
+    const int nch = P.nch;
+    const int ck = __ldg(a.pchans + P.chan_off + (lane < nch ? lane : 0));
+    const int c_off = __ldg(&a.chan[ck].off), c_twoff = __ldg(&a.chan[ck].twoff);
+    const uint2 *ent = a.ient + P.ient_off;
+    const int ne = P.nz;  // contributions of the packet = sum of its L_k
+    const int zb = __shfl_sync(FULL, __ldg(&a.chan[ck].goff), 0);  // packet's range in Z
+    const int u_lo = (item % ntiles) * a.tile;
+    const int u_hi = min(a.nunits, u_lo + a.tile);
+    for (int ul = u_lo; ul < u_hi; ++ul) {
+      const float2 *in_row = a.coef_in + (a.unit0 + ul) * a.C;
+      float2 *Zb = a.stage + (int64_t)ul * a.zs + zb;
+      if (small) {
+        switch (m1) {
+#define X_(S) \
+  case S: inv_small<S>(in_row, scr, nch, c_off, lane); break;
+          SLICQ_SMALL(X_)
+#undef X_
+        }
+      } else {
+        switch (m1) {
+#define X_(S) \
+  case S: inv_step1<S>(a.twM, in_row, scr, m2, nch, P.mag2, c_off, c_twoff, lane); break;
+          SLICQ_SIZES(X_)
+#undef X_
+        }
+        __syncwarp();
+        switch (m2) {
+#define X_(S) \
+  case S: inv_step2<S>(scr, m1, nch, P.mag1, lane); break;
+          SLICQ_SIZES(X_)
+#undef X_
+        }
+      }
+      __syncwarp();
+      // I3a contributions Z[goff_k + d] = F[q] * g~_k[j]/sqrt(M_k), (k, d) contiguous
+#pragma unroll 4
+      for (int e = lane; e < ne; e += 32) {
+        const uint2 en = __ldg(ent + e);
+        const float2 f = scr[en.x];
+        __stcg(Zb + e, cscale(f, __uint_as_float(en.y)));
+      }
+      __syncwarp();
+    }
+  }
+  pdl_trigger();
+}
+
+#endif  // SLICQ_DEFINE_CHAN_KERNELS
+
+// ------------------------------------------------------------------ forward spectrum kernel
 template <int LOGN>
-__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kernel(const KArgs a) {
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_kernel(const KArgs a) {
   using CF = Big<LOGN>;
-  constexpr int N = CF::N, T = CF::T, NW = T / 32;
+  constexpr int N = CF::N, T = CF::T;
   extern __shared__ float4 smem4[];
   float2 *spec = reinterpret_cast<float2 *>(smem4);
   float2 *tw = spec + spec_entries<LOGN>();
-  float2 *scr_all = tw + tw_entries<LOGN>();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t mloc = blockIdx.x;
+  float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());  // window transitions
+  const int tid = threadIdx.x;
+  const int64_t ul = blockIdx.x;             // unit within the chunk
+  const int64_t u = a.unit0 + ul;
+  const int64_t row = u / a.nslices;
+  const int64_t mloc = u - row * a.nslices;
   const int64_t mg = a.slice0 + mloc;
-  const int64_t row = blockIdx.y;
 
   PHASE_INIT();
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
+  pdl_wait();  // the staging buffer may still be read by the previous chunk's kernel
 
   // ---- F1 + first radix pass, read straight from HBM.  z[p] = f[2p] + i f[2p+1].
   // The window's transition values h_0(|t|), |t| = A+1 .. Bw-1 (h_0 is even), are staged
@@ -515,8 +557,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kerne
     const bool vec = ((reinterpret_cast<uintptr_t>(xr) & 7) == 0);
     const int64_t s0 = (mg - 1) * N - a.base_off;  // local index of frame sample 0
     const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
-    float *htab = reinterpret_cast<float *>(scr_all);
-    const bool hsm = a.tr - 1 <= NW * a.scr * 2;
+    constexpr bool hsm = true;  // the transition table always has its own smem
     float2 v[PER][R];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
@@ -597,112 +638,81 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_kerne
   __syncthreads();
   PHASE_MARK(0, 3);
 
-  // ---- F3-F5: channel packets, shape-sorted; warp w takes packets w, w + NW, ...
-  float2 *scr = scr_all + warp * a.scr;
-  float2 *out_row = a.coef_out + (row * a.nslices + mloc) * a.C;
-  for (int pk = warp; pk < a.npackets; pk += NW) {
-    const PacketDev P = a.packets[pk];
-    const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
-    const bool simple = (P.m1m2 >> 16) & 1;
-    const PDesc pd = load_desc(a, P.chan_off, P.nch, lane);
-    if ((P.m1m2 >> 17) & 1) {
-      switch (m1) {
-#define X(S) \
-  case S: fwd_small<S, N>(a, spec, out_row, pd, P.nch, simple, lane); break;
-        SLICQ_SMALL(X)
-#undef X
-      }
-      continue;
-    }
-    if (simple) fwd_fold<N, true>(a, spec, scr, pd, m1 * m2, m1, m2 | 1, P.nch, P.magM, lane);
-    else fwd_fold<N, false>(a, spec, scr, pd, m1 * m2, m1, m2 | 1, P.nch, P.magM, lane);
-    __syncwarp();
-    switch (m1) {
-#define X(S) \
-  case S: fwd_step1<S>(a, scr, pd, m2, P.nch, P.mag2, lane); break;
-      SLICQ_SIZES(X)
-#undef X
-    }
-    __syncwarp();
-    switch (m2) {
-#define X(S) \
-  case S: fwd_step2<S>(a, scr, out_row, pd, m1, P.nch, P.mag1, lane); break;
-      SLICQ_SIZES(X)
-#undef X
-    }
-    __syncwarp();
+  // ---- X[0..N] -> staging (coalesced)
+  {
+    float2 *Xo = a.stage + ul * a.xs;
+    for (int k = tid; k <= N; k += T) Xo[k] = spec[padi(k)];
   }
   PHASE_MARK(0, 4);
+  pdl_trigger();
 }
 
-// ------------------------------------------------------------------ inverse kernel
+// ------------------------------------------------------------------ inverse spectrum kernel
 template <int LOGN>
-__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kernel(const KArgs a) {
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_kernel(const KArgs a) {
   using CF = Big<LOGN>;
-  constexpr int N = CF::N, T = CF::T, NW = T / 32;
+  constexpr int N = CF::N, T = CF::T;
   extern __shared__ float4 smem4[];
   float2 *spec = reinterpret_cast<float2 *>(smem4);
   float2 *tw = spec + spec_entries<LOGN>();
-  float2 *chs = tw + tw_entries<LOGN>();  // per-warp scratch
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int mloc = blockIdx.x;
+  float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());
+  const int tid = threadIdx.x;
+  const int64_t ul = blockIdx.x;
+  const int64_t u = a.unit0 + ul;
+  const int64_t row = u / a.nslices;
+  const int mloc = (int)(u - row * a.nslices);
   const int64_t mg = a.slice0 + mloc;
-  const int64_t row = blockIdx.y;
 
   PHASE_INIT();
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
-  for (int i = tid; i < spec_entries<LOGN>(); i += T) spec[i] = make_float2(0.f, 0.f);
+  for (int u2 = tid; u2 < a.tr - 1; u2 += T) htab[u2] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u2);
+  constexpr bool hsm = true;
+  pdl_wait();  // contributions of this chunk come from the channel kernel
 
-  // ---- I1-I3: channel packets by phase (packets of one phase touch disjoint bins)
+  // ---- I3b: per-bin gather of the contributions (Hermitian rule folded into the list)
   {
-    float2 *scr = chs + warp * a.scr;
-    const float2 *in_row = a.coef_in + (row * a.nslices + mloc) * a.C;
-    __syncthreads();  // spectrum zeroed
-    for (int ph = 0; ph < a.nchunks; ++ph) {
-      const ChunkDev pr = a.chunks[ph];
-      for (int pk = pr.pk0 + warp; pk < pr.pk1; pk += NW) {
-        const PacketDev P = a.packets[pk];
-        const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
-        const bool simple = (P.m1m2 >> 16) & 1;
-        const PDesc pd = load_desc(a, P.chan_off, P.nch, lane);
-        if ((P.m1m2 >> 17) & 1) {
-          switch (m1) {
-#define X(S) \
-  case S: inv_small<S, N>(a, in_row, spec, scr, pd, P.nch, simple, lane); break;
-            SLICQ_SMALL(X)
-#undef X
-          }
-          continue;
-        }
-        switch (m1) {
-#define X(S) \
-  case S: inv_step1<S>(a, in_row, scr, pd, m2, P.nch, P.mag2, lane); break;
-          SLICQ_SIZES(X)
-#undef X
-        }
-        __syncwarp();
-        switch (m2) {
-#define X(S) \
-  case S: inv_step2<S>(scr, m1, P.nch, P.mag1, lane); break;
-          SLICQ_SIZES(X)
-#undef X
-        }
-        __syncwarp();
-        if (simple)
-          inv_unfold<N, true>(a, spec, scr, pd, m1 * m2, m1, m2 | 1, P.nch, lane);
-        else
-          inv_unfold<N, false>(a, spec, scr, pd, m1 * m2, m1, m2 | 1, P.nch, lane);
+    const float2 *Z = a.stage + ul * a.zs;
+    // most bins have <= 2 terms: those loads are issued unconditionally (predicated) for
+    // 4 bins at a time so that ~8 staging loads are in flight per thread
+    constexpr int G = 4;
+    for (int b0 = tid; b0 <= N; b0 += G * T) {
+      int e0[G], e1[G];
+      uint32_t g0[G], g1[G];
+      float2 z0[G], z1[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        const int b = b0 + q * T;
+        e0[q] = b <= N ? __ldg(a.bin_off + b) : 0;
+        e1[q] = b <= N ? __ldg(a.bin_off + b + 1) : 0;
       }
-      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        g0[q] = e0[q] < e1[q] ? __ldg(a.gents + e0[q]) : 0u;
+        g1[q] = e0[q] + 1 < e1[q] ? __ldg(a.gents + e0[q] + 1) : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        z0[q] = e0[q] < e1[q] ? __ldcg(Z + (g0[q] & 0x7fffffffu)) : make_float2(0.f, 0.f);
+        z1[q] = e0[q] + 1 < e1[q] ? __ldcg(Z + (g1[q] & 0x7fffffffu)) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        const int b = b0 + q * T;
+        if (b > N) continue;
+        float2 acc = make_float2(z0[q].x, (g0[q] >> 31) ? -z0[q].y : z0[q].y);
+        acc.x += z1[q].x;
+        acc.y += (g1[q] >> 31) ? -z1[q].y : z1[q].y;
+        for (int e = e0[q] + 2; e < e1[q]; ++e) {  // deep-overlap bins
+          const uint32_t ge = __ldg(a.gents + e);
+          const float2 z = __ldcg(Z + (ge & 0x7fffffffu));
+          acc.x += z.x;
+          acc.y += (ge >> 31) ? -z.y : z.y;
+        }
+        spec[padi(b)] = acc;
+      }
     }
   }
-  // stage h~_0(|t|), |t| = A+1 .. Bw-1 (even window) into the now free scratch
-  const bool hsm = a.tr - 1 <= NW * a.scr * 2;
-  {
-    float *htab = reinterpret_cast<float *>(chs);
-    if (hsm)
-      for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u);
-  }
+  __syncthreads();
   PHASE_MARK(1, 0);
 
   // ---- I4a: c2r packing  Z[k] = E[k] + i O[k],
@@ -770,7 +780,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kerne
           const int at = t < 0 ? -t : t;
           if (at >= Bw) continue;
           const float hd = at <= A ? 1.f  // h~_0 = 1 on the flat top
-                           : (hsm ? reinterpret_cast<const float *>(chs)[at - A - 1] : __ldg(a.h0dual + i));
+                           : (hsm ? htab[at - A - 1] : __ldg(a.h0dual + i));
           const float val = (h ? v[q][r].y : v[q][r].x) * invN * hd;
           const int64_t s = (mg - 1) * N + i;  // global sample index (before wrap)
           if (at <= A) {
@@ -839,27 +849,24 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_kerne
     }
   }
   PHASE_MARK(1, 5);
+  pdl_trigger();
 }
 
 template <int LOGN>
-constexpr size_t fwd_smem_bytes(int scr) {
-  return sizeof(float2) *
-         (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>() + (Big<LOGN>::T / 32) * scr);
-}
-template <int LOGN>
-constexpr size_t inv_smem_bytes(int scr) {
-  return fwd_smem_bytes<LOGN>(scr);
+constexpr size_t spec_smem_bytes(int tr) {
+  return sizeof(float2) * (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>()) +
+         sizeof(float) * (size_t)((tr + 3) & ~3);
 }
 
 // Per-size entry points (defined in kernels_l<LOGN>.cu)
 template <int LOGN>
 int phase_times(unsigned long long *out32, int reset);
 template <int LOGN>
-int set_attrs(size_t fwd_smem, size_t inv_smem);
+int set_attrs(size_t smem);
 template <int LOGN>
-cudaError_t launch_fwd(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s);
+cudaError_t launch_fwd_spec(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s, bool pdl);
 template <int LOGN>
-cudaError_t launch_inv(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s);
+cudaError_t launch_inv_spec(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s, bool pdl);
 
 }  // namespace kern
 }  // namespace slicq

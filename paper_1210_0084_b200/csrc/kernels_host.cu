@@ -1,21 +1,24 @@
-// Host side of the kernels: kernel configuration (channel packets, shared-memory
-// budget), device-table upload and launch dispatch.  Device code: kernels_dev.cuh.
+// Host side of the kernels: plan-time kernel configuration (packets, element tables, the
+// inverse gather list, shared-memory budgets, staging chunking), device-table upload and the
+// launch sequences.  Device code: kernels_dev.cuh.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <vector>
 
+#define SLICQ_DEFINE_CHAN_KERNELS
 #include "kernels_dev.cuh"
 
 namespace slicq {
 namespace {
 using namespace slicq::kern;
 
-// y += spill (the left neighbour's overlap-add spill, multi-GPU slice ranges)
+// y += spill (the right neighbour's overlap-add spill, multi-GPU slice ranges)
 __global__ void overlap_add_kernel(float *y, int64_t y_stride, const float *spill, int64_t count) {
   const int64_t row = blockIdx.y;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
@@ -23,14 +26,16 @@ __global__ void overlap_add_kernel(float *y, int64_t y_stride, const float *spil
     y[row * y_stride + i] += spill[row * count + i];
 }
 
-
 const int kSizes[] = {1, 2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16, 18, 20, 24, 25, 27, 30, 32};
+const int kSmall[] = {4, 6, 8, 10, 12, 16, 18, 20, 24, 30, 32};
 
-bool in_sizes(int v) {
-  for (int s : kSizes)
-    if (s == v) return true;
+bool in_list(const int *l, int n, int v) {
+  for (int i = 0; i < n; ++i)
+    if (l[i] == v) return true;
   return false;
 }
+bool in_sizes(int v) { return in_list(kSizes, sizeof(kSizes) / sizeof(int), v); }
+bool in_small(int v) { return in_list(kSmall, sizeof(kSmall) / sizeof(int), v); }
 
 // M = M1 * M2 with both register-DFT sizes, minimising max(M1, M2) then padding.
 bool factor_m(int M, int &M1, int &M2) {
@@ -63,44 +68,26 @@ int threads_for(int logN) {
   return 0;
 }
 
-size_t fwd_smem_for(int logN, int scr) {
+size_t spec_smem_for(int logN, int tr) {
   switch (logN) {
-    case 11: return fwd_smem_bytes<11>(scr);
-    case 12: return fwd_smem_bytes<12>(scr);
-    case 13: return fwd_smem_bytes<13>(scr);
-    case 14: return fwd_smem_bytes<14>(scr);
-  }
-  return 0;
-}
-
-size_t inv_smem_for(int logN, int scr) {
-  switch (logN) {
-    case 11: return inv_smem_bytes<11>(scr);
-    case 12: return inv_smem_bytes<12>(scr);
-    case 13: return inv_smem_bytes<13>(scr);
-    case 14: return inv_smem_bytes<14>(scr);
+    case 11: return spec_smem_bytes<11>(tr);
+    case 12: return spec_smem_bytes<12>(tr);
+    case 13: return spec_smem_bytes<13>(tr);
+    case 14: return spec_smem_bytes<14>(tr);
   }
   return 0;
 }
 
 constexpr size_t kSmemCap = 227 * 1024;  // per CTA
-constexpr int kSmallScratch = 640;        // float2 entries a small inverse packet may use
-constexpr size_t kSmemSM = 228 * 1024;   // per SM, 1 KB of it reserved per resident CTA
-
-int minb_for(int logN) {
-  switch (logN) {
-    case 11: return Big<11>::MINB;
-    case 12: return Big<12>::MINB;
-    case 13: return Big<13>::MINB;
-    case 14: return Big<14>::MINB;
-  }
-  return 1;
-}
-
-// shared-memory bytes a CTA may use if `ctas` CTAs are to be resident per SM
-size_t smem_budget(int ctas) { return std::min(kSmemCap, kSmemSM / ctas - 1024); }
+constexpr int kSmallCap = 640;           // float2 scratch entries a small packet may use
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+int64_t env_int(const char *name, int64_t dflt) {
+  const char *v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atoll(v);
+}
 
 }  // namespace
 
@@ -115,6 +102,9 @@ int configure_kernels(slicq_plan *p) {
   KernelConfig &kc = p->kc;
   kc.logN = logN;
   kc.threads = threads_for(logN);
+  kc.spec_smem = spec_smem_for(logN, (int)p->tr);
+  if (kc.spec_smem > kSmemCap)
+    return set_error(SLICQ_EUNSUPPORTED, "spectrum kernel shared memory exceeds 227 KB");
   const int K2 = p->K + 2;
   const int N = (int)p->N, N2 = 2 * N;
   std::map<int, std::pair<int, int>> fac;
@@ -122,131 +112,163 @@ int configure_kernels(slicq_plan *p) {
     const int M = p->M[k];
     if (fac.count(M)) continue;
     int m1 = 0, m2 = 0;
+    if (M <= 32 && in_small(M)) {
+      fac[M] = {M, 1};
+      continue;
+    }
     if (M > 1024 || !factor_m(M, m1, m2))
       return set_error(SLICQ_EUNSUPPORTED, "channel length M_k = " + std::to_string(M) +
                                                " is not a product of two DFT sizes <= 32");
     fac[M] = {m1, m2};
   }
-  auto nch_for = [](int m1, int m2) { return std::max(1, 32 / std::max(m1, m2)); };
 
-  // ---------------- packets: runs of consecutive channels with the same length M and the
-  // same SIMPLE flag (J_k inside [0, N]), at most 32 / max(M1, M2) channels each
+  // ---------------- packets: runs of consecutive channels of one length
   struct Pk {
     PacketDev d;
     std::vector<int> ks;
-    int size;
-    std::vector<std::pair<int, int>> bins;  // touched half-spectrum bins (closed intervals)
+    int M, scr;
   };
   std::vector<Pk> pks;
-  auto is_simple = [&](int k) { return p->lo[k] >= 0 && p->lo[k] + p->len[k] - 1 <= N; };
   for (int k = 0; k < K2;) {
     const int M = p->M[k];
-    const bool simple = is_simple(k);
-    const bool small = M <= 32;  // one lane per channel, DFT_M in registers
-    const int m1 = small ? M : fac[M].first, m2 = small ? 1 : fac[M].second;
-    const int nch = small ? std::min(32, kSmallScratch / M) : nch_for(m1, m2);
+    const bool small = M <= 32 && in_small(M);
+    const int m1 = fac[M].first, m2 = fac[M].second;
+    const int nch = small ? std::min(32, kSmallCap / M) : std::max(1, 32 / std::max(m1, m2));
     Pk pk;
     pk.d = PacketDev{};
-    pk.d.m1m2 = m1 | (m2 << 8) | ((simple ? 1 : 0) << 16) | ((small ? 1 : 0) << 17);
-    pk.d.magM = (uint32_t)(((uint64_t(1) << 32) + M - 1) / M);
+    pk.M = M;
+    pk.d.m1m2 = m1 | (m2 << 8) | ((small ? 1 : 0) << 17);
     pk.d.mag1 = (uint32_t)((65536 + m1 - 1) / m1);
     pk.d.mag2 = (uint32_t)((65536 + m2 - 1) / m2);
-    while (k < K2 && p->M[k] == M && is_simple(k) == simple && (int)pk.ks.size() < nch)
-      pk.ks.push_back(k++);
+    while (k < K2 && p->M[k] == M && (int)pk.ks.size() < nch) pk.ks.push_back(k++);
     pk.d.nch = (int)pk.ks.size();
-    pk.size = small ? pk.d.nch * M : pk.d.nch * m1 * (m2 | 1);
-    for (int kk : pk.ks) {  // bins the Hermitian rule of C15 touches
-      const int lo = p->lo[kk], hi = p->lo[kk] + p->len[kk] - 1;
-      auto clip = [&](int a0, int b0) {
-        a0 = std::max(a0, 0);
-        b0 = std::min(b0, N);
-        if (a0 <= b0) pk.bins.push_back({a0, b0});
-      };
-      clip(lo, hi);                  // direct bins j in [0, N]
-      clip(-hi, -lo);                // mirror of j <= 0 (DC side)
-      clip(N2 - hi, N2 - lo);        // mirror of j >= N (Nyquist side)
-      if (lo < 0) clip(lo + N2, hi + N2);  // j mod 2N for negative j (never <= N here)
-    }
+    pk.scr = small ? pk.d.nch * M : pk.d.nch * m1 * (m2 | 1);
     pks.push_back(std::move(pk));
   }
+  // shape-sorted (the warps of a channel-kernel CTA run the same code), longer first
+  std::stable_sort(pks.begin(), pks.end(), [](const Pk &x, const Pk &y) { return x.M > y.M; });
+
+  // ---------------- element tables
+  auto bin_of = [&](int j, int &conj) {  // X(j) = X[b] or conj(X[b]) for real input
+    int jj = j % N2;
+    if (jj < 0) jj += N2;
+    conj = jj > N;
+    return jj > N ? N2 - jj : jj;
+  };
+  auto fbits = [](double v) {
+    const float f = (float)v;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return u;
+  };
+  p->packets.clear();
+  p->pchans.clear();
+  p->fent.clear();
+  p->ient.clear();
   int need = 8;
-  for (const Pk &pk : pks) need = std::max(need, pk.size);
-  const int NW = kc.threads / 32;
-  const size_t budget2 = smem_budget(minb_for(logN));
-  const int cap2 = (int)((budget2 - fwd_smem_for(logN, 0)) / sizeof(float2) / NW) & ~7;
-  const int cap1 = (int)((kSmemCap - fwd_smem_for(logN, 0)) / sizeof(float2) / NW) & ~7;
-  if (need > cap1)
-    return set_error(SLICQ_EUNSUPPORTED, "channel scratch does not fit in shared memory");
-  (void)cap2;  // need <= cap2 keeps Big<LOGN>::MINB CTAs per SM
-  const int scr = need;
-  kc.fwd_scr = kc.inv_scr = (scr + 7) & ~7;
-  kc.fwd_smem = fwd_smem_for(logN, kc.fwd_scr);
-  kc.inv_smem = inv_smem_for(logN, kc.inv_scr);
-
-  // ---------------- forward order: shape-sorted (warps of a CTA walk the list together:
-  // I-cache locality), larger lengths first
-  {
-    std::vector<int> ord(pks.size());
-    for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
-    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
-      const int Mx = (pks[x].d.m1m2 & 255) * ((pks[x].d.m1m2 >> 8) & 255);
-      const int My = (pks[y].d.m1m2 & 255) * ((pks[y].d.m1m2 >> 8) & 255);
-      if (Mx != My) return Mx > My;
-      return (pks[x].d.m1m2 >> 16) < (pks[y].d.m1m2 >> 16);
-    });
-    p->fwd_packets.clear();
-    p->fwd_pchans.clear();
-    for (int i : ord) {
-      PacketDev d = pks[i].d;
-      d.chan_off = (int)p->fwd_pchans.size();
-      for (int k : pks[i].ks) p->fwd_pchans.push_back(k);
-      p->fwd_packets.push_back(d);
-    }
-    kc.fwd_npackets = (int)p->fwd_packets.size();
-  }
-
-  // ---------------- inverse: greedy colouring of the packet conflict graph (packets that
-  // share a touched bin get different phases), shape-sorted inside a phase
-  {
-    auto overlap = [](const Pk &x, const Pk &y) {
-      for (auto &a0 : x.bins)
-        for (auto &b0 : y.bins)
-          if (a0.first <= b0.second && b0.first <= a0.second) return true;
-      return false;
-    };
-    std::vector<int> phase(pks.size(), -1);
-    int nph = 0;
-    for (size_t i = 0; i < pks.size(); ++i) {
-      std::vector<char> used(nph + 1, 0);
-      for (size_t j = 0; j < i; ++j)
-        if (phase[j] >= 0 && overlap(pks[i], pks[j])) used[phase[j]] = 1;
-      int ph = 0;
-      while (ph < nph && used[ph]) ++ph;
-      phase[i] = ph;
-      nph = std::max(nph, ph + 1);
-    }
-    p->inv_packets.clear();
-    p->inv_pchans.clear();
-    p->chunks.clear();
-    for (int ph = 0; ph < nph; ++ph) {
-      std::vector<int> ids;
-      for (size_t i = 0; i < pks.size(); ++i)
-        if (phase[i] == ph) ids.push_back((int)i);
-      std::stable_sort(ids.begin(), ids.end(),
-                       [&](int x, int y) { return (pks[x].d.m1m2 & 0xffff) < (pks[y].d.m1m2 & 0xffff); });
-      ChunkDev pr{};
-      pr.pk0 = (int)p->inv_packets.size();
-      for (int i : ids) {
-        PacketDev d = pks[i].d;
-        d.chan_off = (int)p->inv_pchans.size();
-        for (int k : pks[i].ks) p->inv_pchans.push_back(k);
-        p->inv_packets.push_back(d);
+  for (Pk &pk : pks) {
+    PacketDev &d = pk.d;
+    const int M = pk.M;
+    const bool small = (d.m1m2 >> 17) & 1;
+    const int m1 = d.m1m2 & 255, S2 = ((d.m1m2 >> 8) & 255) | 1;
+    d.chan_off = (int)p->pchans.size();
+    d.fent_off = (int)p->fent.size();
+    d.ient_off = (int)p->ient.size();
+    const double sc = 1.0 / std::sqrt((double)M);  // Alg. 1 sqrt(M) IFFT (1/M); Alg. 2 FFT/sqrt(M)
+    // forward fold table (weight 0 and bin 0 for the zero padding)
+    if (small) {
+      std::vector<uint2> t(32 * M, make_uint2(0u, 0u));
+      for (int c = 0; c < d.nch; ++c) {
+        const int k = pk.ks[c];
+        const int lo_mod = ((p->lo[k] % M) + M) % M;
+        for (int q = 0; q < M; ++q) {
+          int dd = q - lo_mod;
+          if (dd < 0) dd += M;
+          if (dd >= p->len[k]) continue;
+          int conj = 0;
+          const int b = bin_of(p->lo[k] + dd, conj);
+          t[q * 32 + c] = make_uint2((uint32_t)b | ((uint32_t)conj << 15),
+                                     fbits(p->g[p->goff[k] + dd] * sc));
+        }
       }
-      pr.pk1 = (int)p->inv_packets.size();
-      p->chunks.push_back(pr);
+      p->fent.insert(p->fent.end(), t.begin(), t.end());
+    } else {
+      for (int c = 0; c < d.nch; ++c) {
+        const int k = pk.ks[c];
+        const int lo_mod = ((p->lo[k] % M) + M) % M;
+        for (int q = 0; q < M; ++q) {
+          int dd = q - lo_mod;
+          if (dd < 0) dd += M;
+          const uint32_t pos = (uint32_t)(c * m1 * S2 + q);
+          uint2 e = make_uint2(pos << 16, 0u);
+          if (dd < p->len[k]) {
+            int conj = 0;
+            const int b = bin_of(p->lo[k] + dd, conj);
+            e = make_uint2((uint32_t)b | ((uint32_t)conj << 15) | (pos << 16),
+                           fbits(p->g[p->goff[k] + dd] * sc));
+          }
+          p->fent.push_back(e);
+        }
+      }
     }
-    kc.nchunks = nph;
+    // inverse contribution table: e over (channel, d), Z index goff_first + e
+    int nz = 0;
+    for (int c = 0; c < d.nch; ++c) {
+      const int k = pk.ks[c];
+      const int lo_mod = ((p->lo[k] % M) + M) % M;
+      const double half = (k == 0 || k == K2 - 1) ? 0.5 : 1.0;  // self-mirrored plateaus (C15)
+      for (int dd = 0; dd < p->len[k]; ++dd) {
+        int q = lo_mod + dd;
+        if (q >= M) q -= M;
+        const uint32_t pos = small ? (uint32_t)(q * d.nch + c) : (uint32_t)(c * m1 * S2 + q);
+        p->ient.push_back(make_uint2(pos, fbits(p->gdual[p->goff[k] + dd] * sc * half)));
+        ++nz;
+      }
+    }
+    d.nz = nz;
+    for (int k : pk.ks) p->pchans.push_back(k);
+    p->packets.push_back(d);
+    need = std::max(need, pk.scr);
   }
+  kc.npackets = (int)p->packets.size();
+  kc.scr = (need + 7) & ~7;
+  kc.chan_smem = sizeof(float2) * (size_t)kc.scr * (CHAN_T / 32);
+  if (kc.chan_smem > kSmemCap)
+    return set_error(SLICQ_EUNSUPPORTED, "channel scratch does not fit in shared memory");
+
+  // ---------------- inverse gather CSR: half-spectrum bin b <- contributions Z[goff_k + d]
+  // with the Hermitian rule of C15 (term at j mod 2N if <= N, conjugate at -j mod 2N if <= N)
+  {
+    std::vector<std::vector<uint32_t>> per(N + 1);
+    for (int k = 0; k < K2; ++k)
+      for (int dd = 0; dd < p->len[k]; ++dd) {
+        const uint32_t zi = (uint32_t)(p->goff[k] + dd);
+        const int j = p->lo[k] + dd;
+        int p1 = j % N2;
+        if (p1 < 0) p1 += N2;
+        if (p1 <= N) per[p1].push_back(zi);
+        const int p2 = p1 == 0 ? 0 : N2 - p1;
+        if (p2 <= N) per[p2].push_back(zi | 0x80000000u);
+      }
+    p->bin_off.assign(N + 2, 0);
+    p->gents.clear();
+    for (int b = 0; b <= N; ++b) {
+      p->bin_off[b] = (int32_t)p->gents.size();
+      p->gents.insert(p->gents.end(), per[b].begin(), per[b].end());
+    }
+    p->bin_off[N + 1] = (int32_t)p->gents.size();
+  }
+
+  // ---------------- staging: X spectra (N+1) and contributions (sum L_k) per unit
+  kc.xs = (p->N + 2) & ~int64_t(1);
+  kc.zs = ((int64_t)p->g.size() + 1) & ~int64_t(1);
+  kc.tile = (int)std::max<int64_t>(1, env_int("SLICQ_TILE", 16));
+  const int64_t per_unit = sizeof(float2) * std::max(kc.xs, kc.zs);
+  const int64_t budget = env_int("SLICQ_STAGE_MB", 48) << 20;
+  int64_t cu = env_int("SLICQ_CHUNK_UNITS", int64_t(1) << 40);  // default: no chunking
+  (void)budget;
+  cu = std::max<int64_t>(kc.tile, cu / kc.tile * kc.tile);
+  kc.chunk_units = cu;
   return SLICQ_OK;
 }
 
@@ -283,16 +305,6 @@ int upload(slicq_plan *p) {
     c.scale = (float)(1.0 / std::sqrt((double)c.M));
     c.lo_mod = ((c.lo % c.M) + c.M) % c.M;
   }
-  const size_t nG = p->g.size();
-  std::vector<float> g(nG), gd(nG);
-  for (int k = 0; k < K2; ++k) {
-    const double sc = 1.0 / std::sqrt((double)p->M[k]);  // Alg. 1: sqrt(M) * IFFT (1/M)
-    const double half = (k == 0 || k == K2 - 1) ? 0.5 : 1.0;  // self-mirrored plateaus (C15)
-    for (int i = 0; i < p->len[k]; ++i) {
-      g[p->goff[k] + i] = (float)(p->g[p->goff[k] + i] * sc);
-      gd[p->goff[k] + i] = (float)(p->gdual[p->goff[k] + i] * sc * half);
-    }
-  }
   std::vector<float> h0(N2), h0d(N2);
   for (int64_t i = 0; i < N2; ++i) {
     h0[i] = (float)p->h0[i];
@@ -310,16 +322,19 @@ int upload(slicq_plan *p) {
     tw.push_back((float)std::cos(a));
     tw.push_back((float)std::sin(a));
   }
-  struct Part { const void *src; size_t bytes; size_t off; };
+  struct Part {
+    const void *src;
+    size_t bytes;
+    size_t off;
+  };
   std::vector<Part> parts = {
       {ch.data(), sizeof(ChanDev) * ch.size(), 0},
-      {p->fwd_packets.data(), sizeof(PacketDev) * p->fwd_packets.size(), 0},
-      {p->fwd_pchans.data(), sizeof(int32_t) * p->fwd_pchans.size(), 0},
-      {p->inv_packets.data(), sizeof(PacketDev) * p->inv_packets.size(), 0},
-      {p->inv_pchans.data(), sizeof(int32_t) * p->inv_pchans.size(), 0},
-      {p->chunks.data(), sizeof(ChunkDev) * p->chunks.size(), 0},
-      {gd.data(), sizeof(float) * gd.size(), 0},
-      {g.data(), sizeof(float) * g.size(), 0},
+      {p->packets.data(), sizeof(PacketDev) * p->packets.size(), 0},
+      {p->pchans.data(), sizeof(int32_t) * p->pchans.size(), 0},
+      {p->fent.data(), sizeof(uint2) * p->fent.size(), 0},
+      {p->ient.data(), sizeof(uint2) * p->ient.size(), 0},
+      {p->bin_off.data(), sizeof(int32_t) * p->bin_off.size(), 0},
+      {p->gents.data(), sizeof(uint32_t) * p->gents.size(), 0},
       {h0.data(), sizeof(float) * h0.size(), 0},
       {h0d.data(), sizeof(float) * h0d.size(), 0},
       {tw.data(), sizeof(float) * tw.size(), 0},
@@ -341,26 +356,34 @@ int upload(slicq_plan *p) {
     if (pt.bytes) std::memcpy(host.data() + pt.off, pt.src, pt.bytes);
   char *b = static_cast<char *>(blk);
   p->d.chan = reinterpret_cast<ChanDev *>(b + parts[0].off);
-  p->d.fwd_packets = reinterpret_cast<PacketDev *>(b + parts[1].off);
-  p->d.fwd_pchans = reinterpret_cast<int32_t *>(b + parts[2].off);
-  p->d.inv_packets = reinterpret_cast<PacketDev *>(b + parts[3].off);
-  p->d.inv_pchans = reinterpret_cast<int32_t *>(b + parts[4].off);
-  p->d.chunks = reinterpret_cast<ChunkDev *>(b + parts[5].off);
-  p->d.gdual = reinterpret_cast<float *>(b + parts[6].off);
-  p->d.g = reinterpret_cast<float *>(b + parts[7].off);
-  p->d.h0 = reinterpret_cast<float *>(b + parts[8].off);
-  p->d.h0dual = reinterpret_cast<float *>(b + parts[9].off);
-  p->d.tw2n = reinterpret_cast<float *>(b + parts[10].off);
-  p->d.twM = reinterpret_cast<float *>(b + parts[11].off);
+  p->d.packets = reinterpret_cast<PacketDev *>(b + parts[1].off);
+  p->d.pchans = reinterpret_cast<int32_t *>(b + parts[2].off);
+  p->d.fent = reinterpret_cast<uint2 *>(b + parts[3].off);
+  p->d.ient = reinterpret_cast<uint2 *>(b + parts[4].off);
+  p->d.bin_off = reinterpret_cast<int32_t *>(b + parts[5].off);
+  p->d.gents = reinterpret_cast<uint32_t *>(b + parts[6].off);
+  p->d.h0 = reinterpret_cast<float *>(b + parts[7].off);
+  p->d.h0dual = reinterpret_cast<float *>(b + parts[8].off);
+  p->d.tw2n = reinterpret_cast<float *>(b + parts[9].off);
+  p->d.twM = reinterpret_cast<float *>(b + parts[10].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
   int rc = 0;
   switch (p->kc.logN) {
-    case 11: rc = set_attrs<11>(p->kc.fwd_smem, p->kc.inv_smem); break;
-    case 12: rc = set_attrs<12>(p->kc.fwd_smem, p->kc.inv_smem); break;
-    case 13: rc = set_attrs<13>(p->kc.fwd_smem, p->kc.inv_smem); break;
-    case 14: rc = set_attrs<14>(p->kc.fwd_smem, p->kc.inv_smem); break;
+    case 11: rc = set_attrs<11>(p->kc.spec_smem); break;
+    case 12: rc = set_attrs<12>(p->kc.spec_smem); break;
+    case 13: rc = set_attrs<13>(p->kc.spec_smem); break;
+    case 14: rc = set_attrs<14>(p->kc.spec_smem); break;
+  }
+  if (rc == 0) {
+    cudaError_t e1 = cudaFuncSetAttribute(slicq_fwd_chan_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)p->kc.chan_smem);
+    cudaError_t e2 = cudaFuncSetAttribute(slicq_inv_chan_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)p->kc.chan_smem);
+    rc = e1 != cudaSuccess ? (int)e1 : (int)e2;
   }
   if (rc != 0)
     return set_error(SLICQ_ECUDA, std::string("cudaFuncSetAttribute: ") +
@@ -377,9 +400,27 @@ void free_device(slicq_plan *p) {
   if (p) p->has_device = false;
 }
 
+namespace {
+// workspace layout: [pairing counters][boundary halves][staging for one chunk of units]
+struct WsLayout {
+  size_t cnt, bnd, stage, total;
+  int64_t chunk;
+};
+WsLayout ws_layout(const slicq_plan *p, int64_t nslices, int64_t batch) {
+  WsLayout w{};
+  const int64_t units = nslices * batch;
+  w.chunk = std::min<int64_t>(units, p->kc.chunk_units);
+  w.cnt = 0;
+  w.bnd = align_up(sizeof(unsigned) * (size_t)units);
+  w.stage = align_up(w.bnd + sizeof(float) * (size_t)(units * 2 * p->tr));
+  w.total = w.stage + sizeof(float2) * (size_t)(w.chunk * std::max(p->kc.xs, p->kc.zs));
+  return w;
+}
+}  // namespace
+
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch) {
-  const size_t cnt = align_up(sizeof(unsigned) * (size_t)(batch * nslices));
-  return cnt + sizeof(float) * (size_t)(batch * nslices * 2 * p->tr);
+  if (!p->has_device) return 0;  // the layout depends on the device configuration
+  return ws_layout(p, nslices, batch).total;
 }
 
 static KArgs base_args(const slicq_plan *p) {
@@ -387,14 +428,21 @@ static KArgs base_args(const slicq_plan *p) {
   a.tr = (int)p->tr;
   a.C = p->C;
   a.chan = p->d.chan;
-  a.chunks = p->d.chunks;
-  a.nchunks = p->kc.nchunks;
-  a.g = p->d.g;
-  a.gdual = p->d.gdual;
+  a.packets = p->d.packets;
+  a.pchans = p->d.pchans;
+  a.npackets = p->kc.npackets;
+  a.scr = p->kc.scr;
+  a.fent = p->d.fent;
+  a.ient = p->d.ient;
+  a.bin_off = p->d.bin_off;
+  a.gents = p->d.gents;
   a.h0 = p->d.h0;
   a.h0dual = p->d.h0dual;
   a.tw2n = reinterpret_cast<const float2 *>(p->d.tw2n);
   a.twM = reinterpret_cast<const float2 *>(p->d.twM);
+  a.xs = p->kc.xs;
+  a.zs = p->kc.zs;
+  a.tile = p->kc.tile;
   return a;
 }
 
@@ -405,12 +453,60 @@ static int check_device(const slicq_plan *p) {
   return SLICQ_OK;
 }
 
+// persistent channel-kernel grid: resident CTAs (2 per SM), capped by the work items
+static unsigned chan_grid(const slicq_plan *p, const KArgs &a) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int64_t items = (int64_t)((p->kc.npackets + CHAN_T / 32 - 1) / (CHAN_T / 32)) *
+                        ((a.nunits + a.tile - 1) / a.tile);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, 2 * (int64_t)nsm));
+}
+
+static cudaError_t launch_chan(bool fwd, const KArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(CHAN_T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return fwd ? cudaLaunchKernelEx(&cfg, slicq_fwd_chan_kernel, a)
+             : cudaLaunchKernelEx(&cfg, slicq_inv_chan_kernel, a);
+}
+
+static cudaError_t launch_spec(bool fwd, const slicq_plan *p, const KArgs &a, dim3 grid,
+                               cudaStream_t s) {
+  const size_t sm = p->kc.spec_smem;
+  switch (p->kc.logN) {
+    case 11:
+      return fwd ? launch_fwd_spec<11>(a, grid, sm, s, true) : launch_inv_spec<11>(a, grid, sm, s, true);
+    case 12:
+      return fwd ? launch_fwd_spec<12>(a, grid, sm, s, true) : launch_inv_spec<12>(a, grid, sm, s, true);
+    case 13:
+      return fwd ? launch_fwd_spec<13>(a, grid, sm, s, true) : launch_inv_spec<13>(a, grid, sm, s, true);
+    case 14:
+      return fwd ? launch_fwd_spec<14>(a, grid, sm, s, true) : launch_inv_spec<14>(a, grid, sm, s, true);
+  }
+  return cudaErrorInvalidValue;
+}
+
 int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x_stride,
                    int64_t base_off, int64_t L, int wrap, int64_t slice0, int64_t nslices,
-                   int64_t batch, slicq_c32 *coeffs, void *stream) {
+                   int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream) {
   int rc = check_device(p);
   if (rc) return rc;
-  if (nslices > 0x7fffffff || batch > 65535) return set_error(SLICQ_ESHAPE, "grid too large");
+  if (nslices > 0x7fffffff) return set_error(SLICQ_ESHAPE, "too many slices");
+  const WsLayout w = ws_layout(p, nslices, batch);
+  if (!ws || ws_bytes < w.total) return set_error(SLICQ_ESHAPE, "workspace too small");
+  if ((uintptr_t)ws % 16) return set_error(SLICQ_ESHAPE, "workspace must be 16-byte aligned");
   KArgs a = base_args(p);
   a.x = x;
   a.x_len = x_len;
@@ -421,22 +517,17 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
   a.slice0 = slice0;
   a.nslices = (int)nslices;
   a.coef_out = reinterpret_cast<float2 *>(coeffs);
-  a.packets = p->d.fwd_packets;
-  a.pchans = p->d.fwd_pchans;
-  a.npackets = p->kc.fwd_npackets;
-  a.scr = p->kc.fwd_scr;
-  dim3 grid((unsigned)nslices, (unsigned)batch);
+  a.stage = reinterpret_cast<float2 *>(static_cast<char *>(ws) + w.stage);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e;
-  switch (p->kc.logN) {
-    case 11: e = launch_fwd<11>(a, grid, p->kc.fwd_smem, s); break;
-    case 12: e = launch_fwd<12>(a, grid, p->kc.fwd_smem, s); break;
-    case 13: e = launch_fwd<13>(a, grid, p->kc.fwd_smem, s); break;
-    case 14: e = launch_fwd<14>(a, grid, p->kc.fwd_smem, s); break;
-    default: return set_error(SLICQ_EINTERNAL, "bad logN");
+  const int64_t units = nslices * batch;
+  for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
+    a.unit0 = u0;
+    a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
+    cudaError_t e = launch_spec(true, p, a, dim3((unsigned)a.nunits), s);
+    if (e == cudaSuccess) e = launch_chan(true, a, dim3(chan_grid(p, a)), p->kc.chan_smem, s);
+    if (e != cudaSuccess)
+      return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
   }
-  if (e != cudaSuccess)
-    return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
   return SLICQ_OK;
 }
 
@@ -447,9 +538,9 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
   (void)total_slices;
   int rc = check_device(p);
   if (rc) return rc;
-  if (nslices > 0x7fffffff || batch > 65535) return set_error(SLICQ_ESHAPE, "grid too large");
-  const size_t need = workspace_bytes(p, nslices, batch);
-  if (!ws || ws_bytes < need) return set_error(SLICQ_ESHAPE, "workspace too small");
+  if (nslices > 0x7fffffff) return set_error(SLICQ_ESHAPE, "too many slices");
+  const WsLayout w = ws_layout(p, nslices, batch);
+  if (!ws || ws_bytes < w.total) return set_error(SLICQ_ESHAPE, "workspace too small");
   if ((uintptr_t)ws % 16) return set_error(SLICQ_ESHAPE, "workspace must be 16-byte aligned");
   KArgs a = base_args(p);
   a.coef_in = reinterpret_cast<const float2 *>(coeffs);
@@ -463,24 +554,20 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
   a.circular = circular;
   a.slice0 = slice0;
   a.nslices = (int)nslices;
-  a.packets = p->d.inv_packets;
-  a.pchans = p->d.inv_pchans;
-  a.scr = p->kc.inv_scr;
-  a.cnt = static_cast<unsigned *>(ws);
-  a.bnd = reinterpret_cast<float *>(static_cast<char *>(ws) +
-                                    align_up(sizeof(unsigned) * (size_t)(batch * nslices)));
-  dim3 grid((unsigned)nslices, (unsigned)batch);
+  char *wb = static_cast<char *>(ws);
+  a.cnt = reinterpret_cast<unsigned *>(wb + w.cnt);
+  a.bnd = reinterpret_cast<float *>(wb + w.bnd);
+  a.stage = reinterpret_cast<float2 *>(wb + w.stage);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e;
-  switch (p->kc.logN) {
-    case 11: e = launch_inv<11>(a, grid, p->kc.inv_smem, s); break;
-    case 12: e = launch_inv<12>(a, grid, p->kc.inv_smem, s); break;
-    case 13: e = launch_inv<13>(a, grid, p->kc.inv_smem, s); break;
-    case 14: e = launch_inv<14>(a, grid, p->kc.inv_smem, s); break;
-    default: return set_error(SLICQ_EINTERNAL, "bad logN");
+  const int64_t units = nslices * batch;
+  for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
+    a.unit0 = u0;
+    a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
+    cudaError_t e = launch_chan(false, a, dim3(chan_grid(p, a)), p->kc.chan_smem, s);
+    if (e == cudaSuccess) e = launch_spec(false, p, a, dim3((unsigned)a.nunits), s);
+    if (e != cudaSuccess)
+      return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
   }
-  if (e != cudaSuccess)
-    return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
   return SLICQ_OK;
 }
 
@@ -500,7 +587,7 @@ int launch_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t c
 }  // namespace slicq
 
 // Debug only (not part of include/slicq.h): accumulated per-phase clock64 cycles of the
-// forward [0..15] and inverse [16..31] kernels, in a library built with
+// forward [0..15] and inverse [16..31] spectrum kernels, in a library built with
 // -DSLICQ_PHASE_TIMING (tools/phase_timing.py).  Returns -1 in the product build.
 extern "C" __attribute__((visibility("default"))) int slicq_debug_phase_times(
     int logN, unsigned long long *out32, int reset) {

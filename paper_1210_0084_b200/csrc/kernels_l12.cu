@@ -1,32 +1,48 @@
 #define SLICQ_LOGN 12
-// Instantiation of the sliCQ kernels for N = 2^SLICQ_LOGN (one translation unit per size
-// so that the four sizes compile in parallel).
+// Instantiation of the per-slice spectrum kernels for N = 2^SLICQ_LOGN (one translation
+// unit per size so that the sizes compile in parallel).
 #include "kernels_dev.cuh"
 
 namespace slicq {
 namespace kern {
 
 template <>
-int set_attrs<SLICQ_LOGN>(size_t fwd_smem, size_t inv_smem) {
-  cudaError_t e1 = cudaFuncSetAttribute(slicq_fwd_kernel<SLICQ_LOGN>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem);
-  cudaError_t e2 = cudaFuncSetAttribute(slicq_inv_kernel<SLICQ_LOGN>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inv_smem);
+int set_attrs<SLICQ_LOGN>(size_t smem) {
+  cudaError_t e1 = cudaFuncSetAttribute(slicq_fwd_spec_kernel<SLICQ_LOGN>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e2 = cudaFuncSetAttribute(slicq_inv_spec_kernel<SLICQ_LOGN>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e1 != cudaSuccess) return (int)e1;
   if (e2 != cudaSuccess) return (int)e2;
   return 0;
 }
 
-template <>
-cudaError_t launch_fwd<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
-  slicq_fwd_kernel<SLICQ_LOGN><<<grid, Big<SLICQ_LOGN>::T, smem, s>>>(a);
-  return cudaGetLastError();
+template <class K>
+static cudaError_t launch_pdl(K kernel, const KArgs &a, dim3 grid, int threads, size_t smem,
+                              cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
 template <>
-cudaError_t launch_inv<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
-  slicq_inv_kernel<SLICQ_LOGN><<<grid, Big<SLICQ_LOGN>::T, smem, s>>>(a);
-  return cudaGetLastError();
+cudaError_t launch_fwd_spec<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s,
+                                        bool pdl) {
+  return launch_pdl(slicq_fwd_spec_kernel<SLICQ_LOGN>, a, grid, Big<SLICQ_LOGN>::T, smem, s, pdl);
+}
+
+template <>
+cudaError_t launch_inv_spec<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s,
+                                        bool pdl) {
+  return launch_pdl(slicq_inv_spec_kernel<SLICQ_LOGN>, a, grid, Big<SLICQ_LOGN>::T, smem, s, pdl);
 }
 
 template <>

@@ -311,8 +311,6 @@ static int check_dev_plan(const slicq_plan *p) {
 
 int slicq_forward(const slicq_plan *p, const float *x, int64_t n, int64_t batch,
                   slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream) {
-  (void)ws;
-  (void)ws_bytes;
   int rc = check_dev_plan(p);
   if (rc) return rc;
   if (n < 1 || batch < 1) return set_error(SLICQ_ESHAPE, "n and batch must be >= 1");
@@ -320,7 +318,7 @@ int slicq_forward(const slicq_plan *p, const float *x, int64_t n, int64_t batch,
   if ((uintptr_t)x % 4 || (uintptr_t)coeffs % 8) return set_error(SLICQ_ESHAPE, "misaligned buffer");
   const int64_t L = slicq_padded_length(p, n);
   const int64_t S = L / p->N;
-  return slicq::launch_forward(p, x, n, n, 0, L, 1, 0, S, batch, coeffs, stream);
+  return slicq::launch_forward(p, x, n, n, 0, L, 1, 0, S, batch, coeffs, ws, ws_bytes, stream);
 }
 
 int slicq_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n, int64_t batch,
@@ -340,8 +338,6 @@ int slicq_forward_range(const slicq_plan *p, const float *x_local, int64_t x_len
                         int64_t x_stride, int64_t halo, int64_t slice0, int64_t nslices,
                         int64_t total_slices, int64_t batch, slicq_c32 *coeffs_local,
                         void *ws, size_t ws_bytes, void *stream) {
-  (void)ws;
-  (void)ws_bytes;
   int rc = check_dev_plan(p);
   if (rc) return rc;
   if (nslices < 1 || batch < 1 || slice0 < 0 || slice0 + nslices > total_slices || x_len < 0 ||
@@ -351,7 +347,7 @@ int slicq_forward_range(const slicq_plan *p, const float *x_local, int64_t x_len
   if (!x_local || !coeffs_local) return set_error(SLICQ_ESHAPE, "NULL buffer");
   const int64_t L = total_slices * p->N;
   return slicq::launch_forward(p, x_local, x_len, x_stride, slice0 * p->N - halo, L, 0, slice0,
-                               nslices, batch, coeffs_local, stream);
+                               nslices, batch, coeffs_local, ws, ws_bytes, stream);
 }
 
 int slicq_inverse_range(const slicq_plan *p, const slicq_c32 *coeffs_local, int64_t slice0,

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <vector_types.h>
 #include <vector>
 
 #include "../../include/slicq.h"
@@ -20,35 +21,28 @@ struct ChanDev {
   int32_t lo_mod;  // lo_k mod M_k in [0, M_k)
 };
 
-// A packet = channels of one length M = M1*M2 processed together by one warp, with at most
-// 32 tasks per DFT step (nch*M2 <= 32 and nch*M1 <= 32): one task per lane.
-// Small packets (M <= 32, flag bit 17): one lane per channel, whole DFT_M in registers.
+// A packet = consecutive channels of one length M.  Big packets (M > 32): four-step
+// M1 x M2 DFT, one task per lane and step (nch*M1, nch*M2 <= 32).  Small packets (M <= 32,
+// flag bit 17): one lane per channel, whole DFT_M in registers.
 struct PacketDev {
-  int32_t m1m2;     // M1 | (M2 << 8) | SIMPLE << 16 | SMALL << 17  (small: M1 = M, M2 = 1)
+  int32_t m1m2;     // M1 | (M2 << 8) | SMALL << 17  (small: M1 = M, M2 = 1)
   int32_t nch;      // channels in the packet
   int32_t chan_off; // offset into the packet channel list
-  uint32_t magM;    // ceil(2^32 / M): e / M = umulhi(e, magM) for e < 2^16
+  int32_t fent_off; // forward element table offset
+  int32_t ient_off; // inverse element table offset
+  int32_t nz;       // inverse contributions (sum of the channels' L_k)
   uint32_t mag1;    // ceil(2^16 / M1): q / M1 = (q * mag1) >> 16 for q < 64
   uint32_t mag2;    // ceil(2^16 / M2)
-  int32_t pad0, pad1;
-};
-
-// Inverse: a phase is a range of packets that touch pairwise disjoint half-spectrum bins
-// (plan-time colouring), so they scatter concurrently without atomics.
-struct ChunkDev {
-  int32_t pk0, pk1;   // packets [pk0, pk1) of the inverse packet list
-  int32_t pad0, pad1;
 };
 
 struct DeviceTables {
   ChanDev *chan = nullptr;
-  PacketDev *fwd_packets = nullptr;
-  int32_t *fwd_pchans = nullptr;
-  PacketDev *inv_packets = nullptr;
-  int32_t *inv_pchans = nullptr;
-  ChunkDev *chunks = nullptr;
-  float *g = nullptr;       // fp32 g_k / sqrt(M_k) on J_k (forward)
-  float *gdual = nullptr;   // fp32 dual / sqrt(M_k) on J_k, plateaus x 1/2 (inverse)
+  PacketDev *packets = nullptr;
+  int32_t *pchans = nullptr;
+  uint2 *fent = nullptr;     // forward element table
+  uint2 *ient = nullptr;     // inverse element table
+  int32_t *bin_off = nullptr;
+  uint32_t *gents = nullptr;
   float *h0 = nullptr;      // fp32 h_0[t+N], t in [-N, N)
   float *h0dual = nullptr;  // fp32 h~_0[t+N]
   float *tw2n = nullptr;    // float2: [64] e^{-i pi t/N} for t < 64, then [2N/64] for t = 64 h
@@ -59,13 +53,14 @@ struct DeviceTables {
 
 struct KernelConfig {
   int logN = 0;          // N = 2^logN complex points in the r2c FFT of a 2N slice
-  int threads = 0;       // CTA size
-  int fwd_scr = 0;       // forward: per-warp scratch (float2 entries)
-  int inv_scr = 0;       // inverse: per-warp scratch (float2 entries)
-  size_t fwd_smem = 0;   // dynamic shared memory bytes
-  size_t inv_smem = 0;
-  int fwd_npackets = 0;
-  int nchunks = 0;       // inverse phases
+  int threads = 0;       // spectrum-kernel CTA size
+  size_t spec_smem = 0;  // spectrum kernels: dynamic shared memory bytes
+  int scr = 0;           // channel kernels: per-warp scratch (float2 entries)
+  size_t chan_smem = 0;
+  int npackets = 0;
+  int64_t xs = 0, zs = 0;     // staging row strides (float2): X spectra, contributions
+  int64_t chunk_units = 0;    // units per chunk (staging is sized for one chunk)
+  int tile = 16;              // units per channel-kernel tile
 };
 
 }  // namespace slicq
@@ -92,9 +87,11 @@ struct slicq_plan {
   int device = -1;
   slicq::DeviceTables d;
   slicq::KernelConfig kc;
-  std::vector<slicq::PacketDev> fwd_packets, inv_packets;
-  std::vector<int32_t> fwd_pchans, inv_pchans;
-  std::vector<slicq::ChunkDev> chunks;
+  std::vector<slicq::PacketDev> packets;
+  std::vector<int32_t> pchans;
+  std::vector<uint2> fent, ient;
+  std::vector<int32_t> bin_off;
+  std::vector<uint32_t> gents;
 };
 
 namespace slicq {
@@ -106,7 +103,7 @@ int upload(slicq_plan *p);             // allocates + copies device tables
 void free_device(slicq_plan *p);
 int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x_stride,
                    int64_t base_off, int64_t L, int wrap, int64_t slice0, int64_t nslices,
-                   int64_t batch, slicq_c32 *coeffs, void *stream);
+                   int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream);
 int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0, int64_t nslices,
                    int64_t total_slices, int64_t batch, int circular, int64_t n_valid,
                    int64_t L, float *y, int64_t y_stride, int64_t y_base, float *left_spill,
