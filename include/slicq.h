@@ -89,8 +89,9 @@ enum { SLICQ_PLAN_HOST_ONLY = 1 }; /* plan_create_ex flag: host tables only, no 
  *                    allowed and caps K at the last centre below Nyquist (C4)
  *   bins_per_octave  B >= 1
  *   sl_len           2N: divisible by 4 and 2/3/5-smooth.  The CUDA path implements
- *                    2N in {4096, 8192, 16384, 32768}; other valid values give
- *                    SLICQ_EUNSUPPORTED unless SLICQ_PLAN_HOST_ONLY is set.
+ *                    2N = 2^12 .. 2^17 (4096 .. 131072; 2N >= 65536 use a four-step FFT
+ *                    through the workspace); other valid values give SLICQ_EUNSUPPORTED
+ *                    unless SLICQ_PLAN_HOST_ONLY is set.
  *   tr_area          Tukey transition length (the paper's M): even, 2 <= tr < N
  *   rasterize        SLICQ_RASTER_*
  *   out              receives the plan (NULL on failure)

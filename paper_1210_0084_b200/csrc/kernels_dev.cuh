@@ -107,9 +107,13 @@ template <int LOGN>
 constexpr int spec_entries() {
   return padi(Big<LOGN>::N) + 2;  // X[0..N-1] padded, X[N] at padi(N), one spare
 }
+template <int N>
+constexpr int tw_entries_n() {
+  return 64 + 2 * N / 64;
+}
 template <int LOGN>
 constexpr int tw_entries() {
-  return 64 + 2 * Big<LOGN>::N / 64;
+  return tw_entries_n<Big<LOGN>::N>();
 }
 
 struct KArgs {
@@ -135,6 +139,7 @@ struct KArgs {
   // staging (workspace): X spectra [unit][xs], contributions [unit][zs]
   float2 *stage;
   int64_t xs, zs;
+  int64_t toff;   // large slices: offset of the four-step intermediate inside a unit's staging
   // plan tables
   const ChanDev *chan;
   const PacketDev *packets;
@@ -314,7 +319,7 @@ __device__ __noinline__ void fwd_step2(const float2 *reg, float2 *out_row, int m
 }
 
 // Small forward packet: lane c < nch owns channel c; element p of its fold comes from the
-// table entry p*32 + c (bin | conj << 15, weight; weight 0 for zero padding).
+// table entry p*32 + c (bin | conj << 17, weight; weight 0 for zero padding).
 template <int M>
 __device__ __noinline__ void fwd_small(const uint2 *ent, const float2 *X, float2 *out_row,
                                           int nch, int off_lane, int lane) {
@@ -323,9 +328,9 @@ __device__ __noinline__ void fwd_small(const uint2 *ent, const float2 *X, float2
 #pragma unroll
   for (int p = 0; p < M; ++p) {
     const uint2 e = __ldg(ent + p * 32 + lane);
-    const float2 xv = X[e.x & 0x7fff];
+    const float2 xv = X[e.x & 0x1ffff];
     const float gv = __uint_as_float(e.y);
-    v[p] = make_float2(xv.x * gv, ((e.x >> 15) & 1) ? -xv.y * gv : xv.y * gv);
+    v[p] = make_float2(xv.x * gv, ((e.x >> 17) & 1) ? -xv.y * gv : xv.y * gv);
   }
   dft<M, +1>(v);
   float2 *o = out_row + off_lane;
@@ -439,9 +444,9 @@ __global__ void __launch_bounds__(CHAN_T, 2) slicq_fwd_chan_kernel(const KArgs a
 #pragma unroll 4
       for (int e = lane; e < ne; e += 32) {
         const uint2 en = __ldg(ent + e);
-        const float2 xv = X[en.x & 0x7fff];
+        const float2 xv = X[en.x & 0x1ffff];
         const float gv = __uint_as_float(en.y);
-        scr[en.x >> 16] = make_float2(xv.x * gv, ((en.x >> 15) & 1) ? -xv.y * gv : xv.y * gv);
+        scr[en.x >> 18] = make_float2(xv.x * gv, ((en.x >> 17) & 1) ? -xv.y * gv : xv.y * gv);
       }
       __syncwarp();
       switch (m1) {

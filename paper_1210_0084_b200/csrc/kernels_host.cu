@@ -13,6 +13,7 @@
 
 #define SLICQ_DEFINE_CHAN_KERNELS
 #include "kernels_dev.cuh"
+#include "kernels_large.cuh"
 
 namespace slicq {
 namespace {
@@ -91,18 +92,20 @@ int64_t env_int(const char *name, int64_t dflt) {
 
 }  // namespace
 
-int device_supports(int logN) { return logN >= 11 && logN <= 14; }
+int device_supports(int logN) { return logN >= 11 && logN <= 16; }
 
 int configure_kernels(slicq_plan *p) {
   int logN = 0;
   while ((int64_t(1) << logN) < p->N) ++logN;
   if ((int64_t(1) << logN) != p->N || !device_supports(logN))
     return set_error(SLICQ_EUNSUPPORTED,
-                     "CUDA path implements sl_len in {4096, 8192, 16384, 32768}");
+                     "CUDA path implements sl_len = 2^12 .. 2^17");
   KernelConfig &kc = p->kc;
   kc.logN = logN;
-  kc.threads = threads_for(logN);
-  kc.spec_smem = spec_smem_for(logN, (int)p->tr);
+  kc.large = logN >= 15;
+  kc.threads = kc.large ? LT : threads_for(logN);
+  kc.spec_smem = kc.large ? (logN == 15 ? large_smem_bytes<15>() : large_smem_bytes<16>())
+                          : spec_smem_for(logN, (int)p->tr);
   if (kc.spec_smem > kSmemCap)
     return set_error(SLICQ_EUNSUPPORTED, "spectrum kernel shared memory exceeds 227 KB");
   const int K2 = p->K + 2;
@@ -187,7 +190,7 @@ int configure_kernels(slicq_plan *p) {
           if (dd >= p->len[k]) continue;
           int conj = 0;
           const int b = bin_of(p->lo[k] + dd, conj);
-          t[q * 32 + c] = make_uint2((uint32_t)b | ((uint32_t)conj << 15),
+          t[q * 32 + c] = make_uint2((uint32_t)b | ((uint32_t)conj << 17),
                                      fbits(p->g[p->goff[k] + dd] * sc));
         }
       }
@@ -200,11 +203,11 @@ int configure_kernels(slicq_plan *p) {
           int dd = q - lo_mod;
           if (dd < 0) dd += M;
           const uint32_t pos = (uint32_t)(c * m1 * S2 + q);
-          uint2 e = make_uint2(pos << 16, 0u);
+          uint2 e = make_uint2(pos << 18, 0u);
           if (dd < p->len[k]) {
             int conj = 0;
             const int b = bin_of(p->lo[k] + dd, conj);
-            e = make_uint2((uint32_t)b | ((uint32_t)conj << 15) | (pos << 16),
+            e = make_uint2((uint32_t)b | ((uint32_t)conj << 17) | (pos << 18),
                            fbits(p->g[p->goff[k] + dd] * sc));
           }
           p->fent.push_back(e);
@@ -233,6 +236,9 @@ int configure_kernels(slicq_plan *p) {
   kc.npackets = (int)p->packets.size();
   kc.scr = (need + 7) & ~7;
   kc.chan_smem = sizeof(float2) * (size_t)kc.scr * (CHAN_T / 32);
+  // element encoding: bin < 2^17, scratch position < 2^14 (fold table, kernels_dev.cuh)
+  if (N > (1 << 17) - 1 || kc.scr > (1 << 14))
+    return set_error(SLICQ_EUNSUPPORTED, "slice or channel too long for the element tables");
   if (kc.chan_smem > kSmemCap)
     return set_error(SLICQ_EUNSUPPORTED, "channel scratch does not fit in shared memory");
 
@@ -262,6 +268,12 @@ int configure_kernels(slicq_plan *p) {
   // ---------------- staging: X spectra (N+1) and contributions (sum L_k) per unit
   kc.xs = (p->N + 2) & ~int64_t(1);
   kc.zs = ((int64_t)p->g.size() + 1) & ~int64_t(1);
+  if (kc.large) {  // the four-step intermediate (N per unit) follows X / the contributions
+    kc.toff_f = kc.xs;
+    kc.toff_i = kc.zs;
+    kc.xs += p->N;
+    kc.zs += p->N;
+  }
   kc.tile = (int)std::max<int64_t>(1, env_int("SLICQ_TILE", 16));
   const int64_t per_unit = sizeof(float2) * std::max(kc.xs, kc.zs);
   const int64_t budget = env_int("SLICQ_STAGE_MB", 48) << 20;
@@ -375,6 +387,8 @@ int upload(slicq_plan *p) {
     case 12: rc = set_attrs<12>(p->kc.spec_smem); break;
     case 13: rc = set_attrs<13>(p->kc.spec_smem); break;
     case 14: rc = set_attrs<14>(p->kc.spec_smem); break;
+    case 15: rc = large_set_attrs<15>(); break;
+    case 16: rc = large_set_attrs<16>(); break;
   }
   if (rc == 0) {
     cudaError_t e1 = cudaFuncSetAttribute(slicq_fwd_chan_kernel,
@@ -520,10 +534,12 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
   a.stage = reinterpret_cast<float2 *>(static_cast<char *>(ws) + w.stage);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t units = nslices * batch;
+  a.toff = p->kc.toff_f;
   for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
     a.unit0 = u0;
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
-    cudaError_t e = launch_spec(true, p, a, dim3((unsigned)a.nunits), s);
+    cudaError_t e = !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), s)
+                    : p->kc.logN == 15 ? large_forward<15>(a, s) : large_forward<16>(a, s);
     if (e == cudaSuccess) e = launch_chan(true, a, dim3(chan_grid(p, a)), p->kc.chan_smem, s);
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
@@ -560,11 +576,14 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
   a.stage = reinterpret_cast<float2 *>(wb + w.stage);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t units = nslices * batch;
+  a.toff = p->kc.toff_i;
   for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
     a.unit0 = u0;
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
     cudaError_t e = launch_chan(false, a, dim3(chan_grid(p, a)), p->kc.chan_smem, s);
-    if (e == cudaSuccess) e = launch_spec(false, p, a, dim3((unsigned)a.nunits), s);
+    if (e == cudaSuccess)
+      e = !p->kc.large ? launch_spec(false, p, a, dim3((unsigned)a.nunits), s)
+          : p->kc.logN == 15 ? large_inverse_spec<15>(a, s) : large_inverse_spec<16>(a, s);
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
   }

@@ -59,6 +59,8 @@ struct KernelConfig {
   size_t chan_smem = 0;
   int npackets = 0;
   int64_t xs = 0, zs = 0;     // staging row strides (float2): X spectra, contributions
+  bool large = false;         // 2N >= 65536: four-step FFT through the staging buffer
+  int64_t toff_f = 0, toff_i = 0;  // offsets of the four-step intermediate in a unit
   int64_t chunk_units = 0;    // units per chunk (staging is sized for one chunk)
   int tile = 16;              // units per channel-kernel tile
 };

@@ -157,6 +157,8 @@ def test_linearity(api):
     (48000.0, 40.0, 24000.0, 12, 8192, 2, 0),          # shortest transition
     (44100.0, 65.4, 22050.0, 12, 16384, 8190, 0),      # longest transition tr = N - 2
     (22050.0, 30.0, 11025.0, 36, 32768, 4096, 0),
+    (44100.0, 50.0, 22050.0, 48, 65536, 4096, 0),      # four-step path, N1 = 128
+    (44100.0, 60.0, 22050.0, 96, 131072, 2000, 0),     # four-step path, N1 = 256
 ])
 def test_other_slice_lengths(api, args):
     plan = api.Plan(*args)
@@ -224,11 +226,25 @@ def test_cfg4_full_size_sampled(api):
         assert rel(yg[a:b], yr) <= TOL
 
 
-def test_cfg5_reports_unsupported_cleanly(api):
-    from paper_1210_0084_b200._lib import SlicqError
-    with pytest.raises(SlicqError) as ei:
-        api.plan_for_config(CONFIGS[5])
-    assert ei.value.code == -7  # SLICQ_EUNSUPPORTED (2N = 131072 not yet on the device path)
+def test_cfg5_sampled(api):
+    """BASELINE configs[4] (2N = 131072, four-step path): 2 of the 16 signals at full
+    length, sampled slices against the oracle, full reconstruction."""
+    cfg = CONFIGS[5]
+    plan = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    x = make_signal(5, batch=2)
+    S = plan.num_slices(x.shape[1])
+    c, _ = check_forward(plan, ref, x, slices=[0, 1, S // 2, S - 1])
+    y = plan.inverse(c, x.shape[1]).cpu().numpy()
+    for b in range(2):
+        assert rel(y[b], x[b].astype(np.float64)) <= TOL
+    # inverse parity on a window straddling a slice boundary
+    N = plan.N
+    a0, b0 = 3 * N - 9000, 3 * N + 9000
+    need = oslicq.needed_slices(a0, b0, ref, x.shape[1])
+    cs = oslicq.forward(x[:1], ref, slices=need)[0]
+    yr = oslicq.inverse_samples({m: cs[i] for i, m in enumerate(need)}, ref, x.shape[1], a0, b0)
+    assert rel(y[0, a0:b0], yr) <= TOL
 
 
 # ------------------------------------------------------------------ slice-range API
