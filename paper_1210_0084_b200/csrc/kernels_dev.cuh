@@ -267,6 +267,12 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// bring [p, p + bytes) into L2 (one prefetch per 128-byte line, spread over the warp)
+__device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes, int idx, int nthr = 32) {
+  const char *c = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(127));
+  const char *end = reinterpret_cast<const char *>(p) + bytes;
+  for (c += 128 * idx; c < end; c += 128 * nthr) asm volatile("prefetch.global.L2 [%0];" ::"l"(c));
+}
 
 // ------------------------------------------------------------------ channel packets
 // A packet = channels of one length M.  Big packets (M > 32) are a four-step M1 x M2 DFT
@@ -403,9 +409,12 @@ __device__ __noinline__ void inv_small(const float2 *in_row, float2 *reg, int nc
 // Persistent grid; a work item is (packet group c, tile t): warp w owns packet c*NW + w for
 // the units of tile t.  Defined in one translation unit only (kernels_host.cu).
 constexpr int CHAN_T = 256;
+#ifndef SLICQ_CHAN_MINB
+#define SLICQ_CHAN_MINB 2
+#endif
 #ifdef SLICQ_DEFINE_CHAN_KERNELS
 
-__global__ void __launch_bounds__(CHAN_T, 2) slicq_fwd_chan_kernel(const KArgs a) {
+__global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_fwd_chan_kernel(const KArgs a) {
   extern __shared__ float4 smem4[];
   constexpr int NW = CHAN_T / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -431,6 +440,8 @@ __global__ void __launch_bounds__(CHAN_T, 2) slicq_fwd_chan_kernel(const KArgs a
     for (int ul = u_lo; ul < u_hi; ++ul) {
       const float2 *X = a.stage + (int64_t)ul * a.xs;
       float2 *out_row = a.coef_out + (a.unit0 + ul) * a.C;
+      if (ul + 1 < u_hi)  // next unit's spectrum bins of this packet -> L2 (staging is in DRAM)
+        prefetch_l2(X + a.xs + P.xlo, (int64_t)(P.xhi - P.xlo + 1) * 8, lane);
       if (small) {
         switch (m1) {
 #define X_(S) \
@@ -468,7 +479,7 @@ __global__ void __launch_bounds__(CHAN_T, 2) slicq_fwd_chan_kernel(const KArgs a
   pdl_trigger();
 }
 
-__global__ void __launch_bounds__(CHAN_T, 2) slicq_inv_chan_kernel(const KArgs a) {
+__global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_inv_chan_kernel(const KArgs a) {
   extern __shared__ float4 smem4[];
   constexpr int NW = CHAN_T / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -492,9 +503,12 @@ __global__ void __launch_bounds__(CHAN_T, 2) slicq_inv_chan_kernel(const KArgs a
     const int zb = __shfl_sync(FULL, __ldg(&a.chan[ck].goff), 0);  // packet's range in Z
     const int u_lo = (item % ntiles) * a.tile;
     const int u_hi = min(a.nunits, u_lo + a.tile);
+    const int cbase = __shfl_sync(FULL, c_off, 0);
+    const int clen = __shfl_sync(FULL, c_off, nch - 1) - cbase + m1 * m2;
     for (int ul = u_lo; ul < u_hi; ++ul) {
       const float2 *in_row = a.coef_in + (a.unit0 + ul) * a.C;
       float2 *Zb = a.stage + (int64_t)ul * a.zs + zb;
+      if (ul + 1 < u_hi) prefetch_l2(in_row + a.C + cbase, (int64_t)clen * 8, lane);
       if (small) {
         switch (m1) {
 #define X_(S) \
@@ -553,66 +567,83 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
   pdl_wait();  // the staging buffer may still be read by the previous chunk's kernel
 
-  // ---- F1 + first radix pass, read straight from HBM.  z[p] = f[2p] + i f[2p+1].
-  // The window's transition values h_0(|t|), |t| = A+1 .. Bw-1 (h_0 is even), are staged
-  // in the (still unused) packet scratch while the HBM loads are in flight.
+  // ---- F1: the Tukey-windowed frame f^m[i], i in [0, 2N), is staged as a plain float
+  // array in the spectrum buffer (z[p] = (f[2p], f[2p+1]) is then its float2 view):
+  // zero-window samples are stored as zeros without loading, the nonzero window
+  // (N - Bw, N + Bw) is read from HBM as aligned float2 pairs, coalesced across threads.
   {
     constexpr int R = CF::F1, TASKS = N / R, PER = (TASKS + T - 1) / T;
+    float *fr = reinterpret_cast<float *>(spec);
     const float *xr = a.x + row * a.x_stride;
     const bool vec = ((reinterpret_cast<uintptr_t>(xr) & 7) == 0);
-    const int64_t s0 = (mg - 1) * N - a.base_off;  // local index of frame sample 0
+    const int64_t s0 = (mg - 1) * N - a.base_off;  // local x index of frame sample 0
     const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
-    constexpr bool hsm = true;  // the transition table always has its own smem
-    float2 v[PER][R];
+    for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0 + N + A + 1 + u);
+    // frame pairs q: samples 2q, 2q+1; window support |2q - N| < Bw for some sample
+    const int q_lo = (N - Bw + 1) >> 1, q_hi = (N + Bw - 1) >> 1;  // inclusive
+    float2 *fz = reinterpret_cast<float2 *>(fr);
+    for (int q = tid; q < N; q += T)
+      if (q < q_lo || q > q_hi) fz[q] = make_float2(0.f, 0.f);
+    // samples with frame index i map to x[s0 + i] (wrapped by L for slice 0); all of
+    // a thread's loads are issued before any is used (HBM latency overlapped)
+    {
+      constexpr int MAXP = (N + T - 1) / T;
+      float2 xv[MAXP];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int j = tid + q * T;
-      if (TASKS % T == 0 || j < TASKS) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int i0 = 2 * (j + r * TASKS);  // frame index of the real part
-          const int t0 = i0 - N;
-          const int at0 = t0 < 0 ? -t0 : t0;
-          const int at1 = (t0 + 1) < 0 ? -(t0 + 1) : (t0 + 1);
-          float x0 = 0.f, x1 = 0.f;
-          if (at0 < Bw || at1 < Bw) {
-            int64_t idx = s0 + i0;
-            if (a.wrap && idx < 0) idx += a.L;
-            if (vec && idx >= 0 && idx + 1 < a.x_len) {
-              const float2 xv = __ldcs(reinterpret_cast<const float2 *>(xr + idx));
-              x0 = xv.x;
-              x1 = xv.y;
-            } else {
-              if (idx >= 0 && idx < a.x_len) x0 = __ldg(xr + idx);
-              if (idx + 1 >= 0 && idx + 1 < a.x_len) x1 = __ldg(xr + idx + 1);
-            }
+      for (int k = 0; k < MAXP; ++k) {
+        const int q = q_lo + tid + k * T;
+        float x0 = 0.f, x1 = 0.f;
+        if (q <= q_hi) {
+          int64_t xi = s0 + 2 * q;
+          if (a.wrap && xi < 0) xi += a.L;
+          if (vec && xi >= 0 && xi + 1 < a.x_len) {
+            const float2 t2 = __ldcs(reinterpret_cast<const float2 *>(xr + xi));
+            x0 = t2.x;
+            x1 = t2.y;
+          } else {
+            if (xi >= 0 && xi < a.x_len) x0 = __ldg(xr + xi);
+            if (xi + 1 >= 0 && xi + 1 < a.x_len) x1 = __ldg(xr + xi + 1);
           }
-          v[q][r] = make_float2(x0, x1);
         }
+        xv[k] = make_float2(x0, x1);
+      }
+#pragma unroll
+      for (int k = 0; k < MAXP; ++k) {
+        const int q = q_lo + tid + k * T;
+        if (q <= q_hi) fz[q] = xv[k];
       }
     }
-    if (hsm)
-      for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0 + N + A + 1 + u);
-    __syncthreads();  // twiddles and window staged; nothing has read spec yet
+    __syncthreads();  // raw samples and window table staged
+    // window: only the transitions need a multiply (h_0 = 1 on the flat top)
+    for (int u = tid; u < 2 * (a.tr - 1); u += T) {
+      const int side = u >= a.tr - 1;
+      const int d = side ? u - (a.tr - 1) : u;  // |t| = A + 1 + d
+      const int i = side ? N + A + 1 + d : N - A - 1 - d;
+      fr[i] *= htab[d];
+    }
+    for (int q = tid; q < 2; q += T) {  // zero-window samples inside the boundary pairs
+      const int i = q == 0 ? N - Bw : N + Bw;
+      if (i >= 0 && i < 2 * N) fr[i] = 0.f;
+    }
+    __syncthreads();
+    // first radix pass from the staged frame (unpadded), written back padded
+    float2 v[PER][R];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int j = tid + q * T;
+    for (int qq = 0; qq < PER; ++qq) {
+      const int j = tid + qq * T;
       if (TASKS % T == 0 || j < TASKS) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int i0 = 2 * (j + r * TASKS);
-          const int t0 = i0 - N;
-          const int at0 = t0 < 0 ? -t0 : t0;
-          const int at1 = (t0 + 1) < 0 ? -(t0 + 1) : (t0 + 1);
-          const float h0a = at0 <= A ? 1.f
-                            : (at0 < Bw ? (hsm ? htab[at0 - A - 1] : __ldg(a.h0 + i0)) : 0.f);
-          const float h0b = at1 <= A ? 1.f
-                            : (at1 < Bw ? (hsm ? htab[at1 - A - 1] : __ldg(a.h0 + i0 + 1)) : 0.f);
-          v[q][r] = make_float2(v[q][r].x * h0a, v[q][r].y * h0b);
-        }
-        dft<R, -1>(v[q]);
+        for (int r = 0; r < R; ++r) v[qq][r] = fz[j + r * TASKS];
+        dft<R, -1>(v[qq]);
+      }
+    }
+    __syncthreads();
 #pragma unroll
-        for (int r = 0; r < R; ++r) spec[padi(j * R + r)] = v[q][r];
+    for (int qq = 0; qq < PER; ++qq) {
+      const int j = tid + qq * T;
+      if (TASKS % T == 0 || j < TASKS) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) spec[padi(j * R + r)] = v[qq][r];
       }
     }
     __syncthreads();
@@ -673,6 +704,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
   for (int u2 = tid; u2 < a.tr - 1; u2 += T) htab[u2] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u2);
   constexpr bool hsm = true;
   pdl_wait();  // contributions of this chunk come from the channel kernel
+  prefetch_l2(a.stage + ul * a.zs, a.zs * 8, tid, T);
 
   // ---- I3b: per-bin gather of the contributions (Hermitian rule folded into the list)
   {
@@ -771,44 +803,47 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
         dft<R, +1>(v[q]);
       }
     }
+    // stage the output frame (unpadded float array in the spectrum buffer), then write the
+    // exclusive part and the two transitions as contiguous, coalesced runs
+    __syncthreads();  // every thread has read its last-pass inputs
+    float2 *fz = reinterpret_cast<float2 *>(spec);
+    const float *fr = reinterpret_cast<const float *>(spec);
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = tid + q * T;
-      if (!(TASKS % T == 0 || j < TASKS)) continue;
+      if (TASKS % T == 0 || j < TASKS) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int p = j + r * NS;  // output index of the final pass = z index
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = 2 * p + h;  // frame index
-          const int t = i - N;
-          const int at = t < 0 ? -t : t;
-          if (at >= Bw) continue;
-          const float hd = at <= A ? 1.f  // h~_0 = 1 on the flat top
-                           : (hsm ? htab[at - A - 1] : __ldg(a.h0dual + i));
-          const float val = (h ? v[q][r].y : v[q][r].x) * invN * hd;
-          const int64_t s = (mg - 1) * N + i;  // global sample index (before wrap)
-          if (at <= A) {
-            if (a.circular) {
-              const int64_t sw = s < 0 ? s + a.L : (s >= a.L ? s - a.L : s);
-              if (sw < a.y_len) yrow[sw] = val;
-            } else {
-              const int64_t li = s - a.y_base;
-              if (li >= 0) yrow[li] = val;
-              else a.spill[row * a.halo + (li + a.halo)] = val;
-            }
-          } else if (t < 0) {  // left transition, shared with slice mg-1
-            const int u = t + Bw - 1;
-            if (left_paired) bnd_row[((int64_t)bl * 2 + 1) * trp + u] = val;
-            else a.spill[row * a.halo + (s - a.y_base + a.halo)] = val;
-          } else {  // right transition, shared with slice mg+1
-            const int u = t - A - 1;
-            if (right_paired) bnd_row[((int64_t)br * 2 + 0) * trp + u] = val;
-            else yrow[s - a.y_base] = val;
-          }
-        }
+        for (int r = 0; r < R; ++r) fz[j + r * NS] = cscale(v[q][r], invN);
       }
     }
+    __syncthreads();
+    const int64_t sbase = (mg - 1) * N;  // global sample of frame index 0
+    // exclusive part |t| <= A: h~_0 = 1
+    for (int i = N - A + tid; i <= N + A; i += T) {
+      const float val = fr[i];
+      const int64_t sg = sbase + i;
+      if (a.circular) {
+        const int64_t sw = sg < 0 ? sg + a.L : (sg >= a.L ? sg - a.L : sg);
+        if (sw < a.y_len) yrow[sw] = val;
+      } else {
+        const int64_t li = sg - a.y_base;
+        if (li >= 0) yrow[li] = val;
+        else a.spill[row * a.halo + (li + a.halo)] = val;
+      }
+    }
+    // transitions, u = 0 .. tr-2 (|t| = A + 1 + u on the right, Bw - 1 - u on the left)
+    for (int u = tid; u < a.tr - 1; u += T) {
+      const int il = N - Bw + 1 + u;  // left: t = u - Bw + 1
+      const float vl = fr[il] * htab[Bw - 2 - u - A];
+      const int64_t sl = sbase + il;
+      if (left_paired) bnd_row[((int64_t)bl * 2 + 1) * trp + u] = vl;
+      else a.spill[row * a.halo + (sl - a.y_base + a.halo)] = vl;
+      const int ir = N + A + 1 + u;   // right: t = A + 1 + u
+      const float vr = fr[ir] * htab[u];
+      if (right_paired) bnd_row[((int64_t)br * 2 + 0) * trp + u] = vr;
+      else yrow[sbase + ir - a.y_base] = vr;
+    }
+    (void)hsm;
     // range mode, last local slice: samples [(mg+1)N - A, (mg+1)N) get no local
     // contribution; store zeros so the neighbour's spill can be added in place.
     if (!a.circular && mloc + 1 == S) {

@@ -229,6 +229,18 @@ int configure_kernels(slicq_plan *p) {
       }
     }
     d.nz = nz;
+    {  // bins the fold reads (X(j) or conj X(2N - j) for real input)
+      int bl = N, bh = 0;
+      for (int k : pk.ks)
+        for (int dd = 0; dd < p->len[k]; ++dd) {
+          int conj = 0;
+          const int b = bin_of(p->lo[k] + dd, conj);
+          bl = std::min(bl, b);
+          bh = std::max(bh, b);
+        }
+      d.xlo = bl;
+      d.xhi = bh;
+    }
     for (int k : pk.ks) p->pchans.push_back(k);
     p->packets.push_back(d);
     need = std::max(need, pk.scr);
@@ -478,7 +490,12 @@ static unsigned chan_grid(const slicq_plan *p, const KArgs &a) {
   }
   const int64_t items = (int64_t)((p->kc.npackets + CHAN_T / 32 - 1) / (CHAN_T / 32)) *
                         ((a.nunits + a.tile - 1) / a.tile);
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, 2 * (int64_t)nsm));
+  int per_sm = SLICQ_CHAN_MINB;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slicq_fwd_chan_kernel, CHAN_T,
+                                                    p->kc.chan_smem) == cudaSuccess && occ > 0)
+    per_sm = occ;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)per_sm * nsm));
 }
 
 static cudaError_t launch_chan(bool fwd, const KArgs &a, dim3 grid, size_t smem, cudaStream_t s) {

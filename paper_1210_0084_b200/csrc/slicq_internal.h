@@ -33,6 +33,7 @@ struct PacketDev {
   int32_t nz;       // inverse contributions (sum of the channels' L_k)
   uint32_t mag1;    // ceil(2^16 / M1): q / M1 = (q * mag1) >> 16 for q < 64
   uint32_t mag2;    // ceil(2^16 / M2)
+  int32_t xlo, xhi; // forward: spectrum bins [xlo, xhi] the fold reads (L2 prefetch)
 };
 
 struct DeviceTables {
