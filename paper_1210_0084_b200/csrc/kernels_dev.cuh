@@ -406,8 +406,8 @@ __device__ __noinline__ void inv_small(const float2 *in_row, float2 *reg, int nc
   X(1) X(2) X(3) X(4) X(5) X(6) X(8) X(9) X(10) X(12) X(15) X(16) X(18) X(20) X(24) X(25) X(27) X(30) X(32)
 
 // ------------------------------------------------------------------ channel kernels
-// Persistent grid; a work item is (packet group c, tile t): warp w owns packet c*NW + w for
-// the units of tile t.  Defined in one translation unit only (kernels_host.cu).
+// Persistent grid; a work item is (packet, tile of units), the CTA's warps split the units.
+// Defined in one translation unit only (kernels_host.cu).
 constexpr int CHAN_T = 256;
 #ifndef SLICQ_CHAN_MINB
 #define SLICQ_CHAN_MINB 2
@@ -419,13 +419,13 @@ __global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_fwd_chan_kernel
   constexpr int NW = CHAN_T / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_wait();
-  // persistent: work items (packet group, tile) in packet-group-major order, so that all
-  // SMs run the same packet shapes (code) at the same time
+  // persistent: a work item is (packet, tile of units), items in packet-major order, the
+  // warps of a CTA split the tile's units: every warp of every SM runs the same packet
+  // code at the same time (instruction-cache locality) and the packet's tables stay hot
   const int ntiles = (a.nunits + a.tile - 1) / a.tile;
-  const int nitems = ((a.npackets + NW - 1) / NW) * ntiles;
+  const int nitems = a.npackets * ntiles;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int pk = (item / ntiles) * NW + warp;
-    if (pk >= a.npackets) continue;
+    const int pk = item / ntiles;
     float2 *scr = reinterpret_cast<float2 *>(smem4) + warp * a.scr;
     const PacketDev P = a.packets[pk];
     const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
@@ -437,11 +437,11 @@ __global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_fwd_chan_kernel
     const int ne = small ? 0 : nch * m1 * m2;
     const int u_lo = (item % ntiles) * a.tile;
     const int u_hi = min(a.nunits, u_lo + a.tile);
-    for (int ul = u_lo; ul < u_hi; ++ul) {
+    for (int ul = u_lo + warp; ul < u_hi; ul += NW) {
       const float2 *X = a.stage + (int64_t)ul * a.xs;
       float2 *out_row = a.coef_out + (a.unit0 + ul) * a.C;
-      if (ul + 1 < u_hi)  // next unit's spectrum bins of this packet -> L2 (staging is in DRAM)
-        prefetch_l2(X + a.xs + P.xlo, (int64_t)(P.xhi - P.xlo + 1) * 8, lane);
+      if (ul + NW < u_hi)  // this warp's next unit: its spectrum bins -> L2 (staging is in DRAM)
+        prefetch_l2(X + NW * a.xs + P.xlo, (int64_t)(P.xhi - P.xlo + 1) * 8, lane);
       if (small) {
         switch (m1) {
 #define X_(S) \
@@ -484,13 +484,13 @@ __global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_inv_chan_kernel
   constexpr int NW = CHAN_T / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_wait();
-  // persistent: work items (packet group, tile) in packet-group-major order, so that all
-  // SMs run the same packet shapes (code) at the same time
+  // persistent: a work item is (packet, tile of units), items in packet-major order, the
+  // warps of a CTA split the tile's units: every warp of every SM runs the same packet
+  // code at the same time (instruction-cache locality) and the packet's tables stay hot
   const int ntiles = (a.nunits + a.tile - 1) / a.tile;
-  const int nitems = ((a.npackets + NW - 1) / NW) * ntiles;
+  const int nitems = a.npackets * ntiles;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int pk = (item / ntiles) * NW + warp;
-    if (pk >= a.npackets) continue;
+    const int pk = item / ntiles;
     float2 *scr = reinterpret_cast<float2 *>(smem4) + warp * a.scr;
     const PacketDev P = a.packets[pk];
     const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
@@ -505,10 +505,10 @@ __global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_inv_chan_kernel
     const int u_hi = min(a.nunits, u_lo + a.tile);
     const int cbase = __shfl_sync(FULL, c_off, 0);
     const int clen = __shfl_sync(FULL, c_off, nch - 1) - cbase + m1 * m2;
-    for (int ul = u_lo; ul < u_hi; ++ul) {
+    for (int ul = u_lo + warp; ul < u_hi; ul += NW) {
       const float2 *in_row = a.coef_in + (a.unit0 + ul) * a.C;
       float2 *Zb = a.stage + (int64_t)ul * a.zs + zb;
-      if (ul + 1 < u_hi) prefetch_l2(in_row + a.C + cbase, (int64_t)clen * 8, lane);
+      if (ul + NW < u_hi) prefetch_l2(in_row + NW * a.C + cbase, (int64_t)clen * 8, lane);
       if (small) {
         switch (m1) {
 #define X_(S) \

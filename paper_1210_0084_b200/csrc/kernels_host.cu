@@ -286,7 +286,7 @@ int configure_kernels(slicq_plan *p) {
     kc.xs += p->N;
     kc.zs += p->N;
   }
-  kc.tile = (int)std::max<int64_t>(1, env_int("SLICQ_TILE", 16));
+  kc.tile = (int)std::max<int64_t>(1, env_int("SLICQ_TILE", 128));
   const int64_t per_unit = sizeof(float2) * std::max(kc.xs, kc.zs);
   const int64_t budget = env_int("SLICQ_STAGE_MB", 48) << 20;
   int64_t cu = env_int("SLICQ_CHUNK_UNITS", int64_t(1) << 40);  // default: no chunking
@@ -488,8 +488,7 @@ static unsigned chan_grid(const slicq_plan *p, const KArgs &a) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  const int64_t items = (int64_t)((p->kc.npackets + CHAN_T / 32 - 1) / (CHAN_T / 32)) *
-                        ((a.nunits + a.tile - 1) / a.tile);
+  const int64_t items = (int64_t)p->kc.npackets * ((a.nunits + a.tile - 1) / a.tile);
   int per_sm = SLICQ_CHAN_MINB;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slicq_fwd_chan_kernel, CHAN_T,
