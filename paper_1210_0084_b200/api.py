@@ -121,10 +121,11 @@ class Plan:
                     M=self.channel_lengths(), off=self.channel_offsets())
 
     # ------------------------------------------------------------ workspace
-    def workspace(self, nslices: int, batch: int, device=None) -> torch.Tensor:
-        """Zero-initialised once, then reused (it carries the overlap-add pairing counters)."""
+    def workspace(self, nslices: int, batch: int, device=None, tag=None) -> torch.Tensor:
+        """Zero-initialised once, then reused (it carries the overlap-add pairing counters).
+        One workspace per (device, shape, tag): calls that may run concurrently use tags."""
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-        key = (str(dev), nslices, batch)
+        key = (str(dev), nslices, batch, tag)
         ws = self._ws.get(key)
         if ws is None:
             nb = self.workspace_bytes(nslices, batch)
@@ -235,3 +236,92 @@ def plan_for_config(cfg) -> Plan:
     """Plan for a synth.configs.SlicqConfig."""
     return Plan(cfg.fs, cfg.fmin, cfg.fmax_eff, cfg.bins_per_octave, cfg.sl_len, cfg.tr_area,
                 cfg.rasterize)
+
+
+def process_host(plan: Plan, x_host: torch.Tensor, y_host: Optional[torch.Tensor] = None,
+                 fn=None, pieces: int = 8, device=None) -> torch.Tensor:
+    """Host-to-host sliCQ round trip of a (long) signal, pipelined over slice ranges.
+
+    x_host: pinned float32 [batch][n] (CPU).  The S slices are cut into `pieces` contiguous
+    ranges; for each range the input (plus its left halo, circular for range 0) is
+    copied host->device on one stream, slicq_forward_range / optional `fn(coeffs_local,
+    slice0)` (in-place coefficient processing on the device) / slicq_inverse_range run on a
+    second stream, and the synthesised samples go device->host on a third stream as soon as
+    the right neighbour's overlap-add spill has been added (slicq_overlap_add).  Copies of
+    range r+1 / r-1 overlap the kernels of range r.  Returns y_host [batch][n].
+    The arithmetic is exactly that of slicq_forward + slicq_inverse (same kernels)."""
+    if x_host.dim() == 1:
+        x_host = x_host[None]
+    if x_host.is_cuda or x_host.dtype != torch.float32:
+        raise ValueError("x_host must be a float32 CPU tensor (pinned for overlap)")
+    B, n = x_host.shape
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    if y_host is None:
+        y_host = torch.empty((B, n), dtype=torch.float32, pin_memory=True)
+    N, halo = plan.N, plan.halo
+    S = plan.num_slices(n)
+    L = S * N
+    P = max(1, min(pieces, S // 2))
+    bounds = [r * S // P for r in range(P + 1)]
+    C = plan.coeffs_per_slice
+    st_in, st_k, st_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    cur = torch.cuda.current_stream(dev)
+    for s_ in (st_in, st_k, st_out):
+        s_.wait_stream(cur)
+    xl, co, yl, sp, ev_in, ev_inv = [], [], [], [], [], []
+    for r in range(P):
+        ns = bounds[r + 1] - bounds[r]
+        xl.append(torch.empty((B, halo + ns * N), dtype=torch.float32, device=dev))
+        co.append(torch.empty((B, ns, C), dtype=torch.complex64, device=dev))
+        yl.append(torch.empty((B, ns * N), dtype=torch.float32, device=dev))
+        sp.append(torch.empty((B, halo), dtype=torch.float32, device=dev))
+        ev_in.append(torch.cuda.Event())
+        ev_inv.append(torch.cuda.Event())
+
+    def copy_in(dst, a, b):  # global samples [a, b) (circular, zero beyond n) -> dst[:, :b-a]
+        pos, o = a, 0
+        while pos < b:
+            g = pos % L
+            seg = min(b - pos, L - g)
+            hi = min(g + seg, n)
+            if hi > g:
+                dst[:, o:o + hi - g].copy_(x_host[:, g:hi], non_blocking=True)
+            if g + seg > max(g, n):
+                dst[:, o + max(hi - g, 0):o + seg].zero_()
+            pos += seg
+            o += seg
+
+    def copy_out(r):
+        a = bounds[r] * N
+        hi = min(bounds[r + 1] * N, n)
+        if hi > a:
+            y_host[:, a:hi].copy_(yl[r][:, :hi - a], non_blocking=True)
+
+    with torch.cuda.stream(st_in):
+        for r in range(P):
+            copy_in(xl[r], bounds[r] * N - halo, bounds[r + 1] * N)
+            ev_in[r].record(st_in)
+    ev_out = [torch.cuda.Event() for _ in range(P)]
+    with torch.cuda.stream(st_k):
+        for r in range(P):
+            s0, ns = bounds[r], bounds[r + 1] - bounds[r]
+            st_k.wait_event(ev_in[r])
+            plan.forward_range(xl[r], halo, s0, ns, S, out=co[r], stream=st_k)
+            if fn is not None:
+                fn(co[r], s0)
+            plan.inverse_range(co[r], s0, ns, S, halo, y_local=yl[r], spill=sp[r], stream=st_k)
+            if r > 0:  # range r's spill completes range r-1's tail
+                Plan.overlap_add(yl[r - 1][:, -halo:], sp[r], stream=st_k)
+                ev_out[r - 1].record(st_k)
+        Plan.overlap_add(yl[P - 1][:, -halo:], sp[0], stream=st_k)  # circular wrap
+        ev_out[P - 1].record(st_k)
+    with torch.cuda.stream(st_out):
+        for r in range(P):
+            st_out.wait_event(ev_out[r])
+            copy_out(r)
+    for s_ in (st_in, st_k, st_out):
+        cur.wait_stream(s_)
+    # keep the buffers alive until the work is done
+    for t in xl + co + yl + sp:
+        t.record_stream(cur)
+    return y_host

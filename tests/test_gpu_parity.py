@@ -282,3 +282,20 @@ def test_range_api_matches_full(api, G):
         raise AssertionError(f"range/full mismatch: max {d.max().item():.3e} at {bad[:8].tolist()} "
                              f"(N={N}, S={S}, halo={halo}, bounds={bounds}, n={n}); "
                              f"y={y[bad[0,0], bad[0,1]].item()} full={y_full[bad[0,0], bad[0,1]].item()}")
+
+
+@pytest.mark.parametrize("pieces,n,batch", [(1, 70000, 1), (3, 9 * 16384 + 5, 2), (8, 200001, 1)])
+def test_process_host_matches_device_path(api, pieces, n, batch):
+    """api.process_host (pipelined host round trip over slice ranges) equals
+    slicq_forward + slicq_inverse bit for bit, and applies fn to every range's coefficients."""
+    plan = api.plan_for_config(CONFIGS[1])
+    x = torch.from_numpy(random_signal(4242 + n, batch, n)).pin_memory()
+    y = api.process_host(plan, x, pieces=pieces)
+    torch.cuda.synchronize()
+    xd = x.cuda()
+    yd = plan.inverse(plan.forward(xd), n).cpu()
+    assert torch.equal(y, yd)
+    # coefficient processing hook: scaling every coefficient by 2 doubles the output
+    y2 = api.process_host(plan, x, pieces=pieces, fn=lambda c, s0: c.mul_(2.0))
+    torch.cuda.synchronize()
+    assert torch.allclose(y2, 2 * yd, rtol=1e-6, atol=1e-6)
