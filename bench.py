@@ -194,7 +194,9 @@ def run_gpu(args, cfg):
         y = torch.empty((B, n), dtype=torch.float32, device=dev)
         S_local = c.shape[1]
         L_local = plan.padded_length(n)
-        launches_per_step = 4  # forward: spectrum + channel kernels; inverse: channel + spectrum
+        # forward: spectrum + channel kernel(s); inverse: channel kernel(s) + spectrum
+        launches_per_step = (plan.kernel_launches("forward", S_local, B)
+                             + plan.kernel_launches("inverse", S_local, B))
 
         def fwd():
             plan.forward(x, out=c)
@@ -207,7 +209,9 @@ def run_gpu(args, cfg):
         S_local = shard.ns
         L_local = shard.ns * plan.N
         state = {}
-        launches_per_step = 5  # forward_range (2 kernels), inverse_range (2), overlap_add
+        # forward_range, inverse_range, overlap_add
+        launches_per_step = (plan.kernel_launches("forward", S_local, B)
+                             + plan.kernel_launches("inverse", S_local, B) + 1)
 
         def fwd():
             state["c"] = shard.forward(xl)

@@ -121,6 +121,11 @@ SLICQ_API int64_t slicq_halo(const slicq_plan *p);                          /* (
  * contributions of one chunk of slices.  Zero-fill it once before its first use and then
  * reuse it unmodified, one workspace per concurrently running call. */
 SLICQ_API size_t slicq_workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
+/* Number of CUDA kernels one slicq_forward (direction 0) or slicq_inverse (direction 1) call
+ * (or the _range variant) launches for nslices x batch slices -- for launch accounting.
+ * Returns 0 for a host-only plan or invalid arguments. */
+SLICQ_API int slicq_kernel_launches(const slicq_plan *p, int direction, int64_t nslices,
+                                    int64_t batch);
 /* Plan export for parity tests (host out-params, any may be NULL):
  *   lo[K+2], len[K+2]   unwrapped support J_k = [lo_k, lo_k + len_k) in 2N-bins (C5)
  *   g[sum len], gdual[sum len]   g_k and canonical dual g_k / sum_l |g_l|^2 on J_k

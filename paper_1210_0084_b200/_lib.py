@@ -28,6 +28,7 @@ SIGNATURES = {
     "slicq_num_slices": (_i64, [_p, _i64]),
     "slicq_halo": (_i64, [_p]),
     "slicq_workspace_bytes": (_sz, [_p, _i64, _i64]),
+    "slicq_kernel_launches": (_i32, [_p, _i32, _i64, _i64]),
     "slicq_plan_export": (_i32, [_p, _p, _p, _p, _p, _p, _p, _p]),
     "slicq_filter_total_length": (_i64, [_p]),
     "slicq_last_error": (C.c_char_p, []),

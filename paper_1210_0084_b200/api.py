@@ -102,6 +102,11 @@ class Plan:
     def workspace_bytes(self, nslices: int, batch: int) -> int:
         return int(lib().slicq_workspace_bytes(self._h, int(nslices), int(batch)))
 
+    def kernel_launches(self, direction: str, nslices: int, batch: int) -> int:
+        """Kernels one forward / inverse call launches (slicq_kernel_launches)."""
+        d = {"forward": 0, "inverse": 1}[direction]
+        return int(lib().slicq_kernel_launches(self._h, d, int(nslices), int(batch)))
+
     def export(self) -> dict:
         """Host copies of the plan tables (slicq_plan_export) for plan-parity tests."""
         K2 = self.num_channels

@@ -52,15 +52,19 @@ def _stale(out: str = OUT) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False, debug_timing: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug_timing: bool = False,
+          variant: str = "", defines=()) -> str:
     """Build libslicq.so (or, with debug_timing, libslicq_dbg.so with per-phase clock64
-    instrumentation for tools/phase_timing.py; never used by the product path)."""
-    out = OUT if not debug_timing else os.path.join(PKG, "libslicq_dbg.so")
+    instrumentation for tools/phase_timing.py; or, with variant, libslicq_<variant>.so with
+    extra -D defines for tuning experiments, selected via SLICQ_LIB; never used by the
+    product path)."""
+    tag = "dbg" if debug_timing else variant
+    out = OUT if not tag else os.path.join(PKG, f"libslicq_{tag}.so")
     if not force and not _stale(out):
         return out
-    objdir = OBJ if not debug_timing else OBJ + "_dbg"
+    objdir = OBJ if not tag else OBJ + "_" + tag
     os.makedirs(objdir, exist_ok=True)
-    extra = ["-DSLICQ_PHASE_TIMING"] if debug_timing else []
+    extra = (["-DSLICQ_PHASE_TIMING"] if debug_timing else []) + [f"-D{d}" for d in defines]
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         results = list(ex.map(lambda s: _compile(s, objdir, extra), SOURCES))
     log = "\n".join(r[1] for r in results)

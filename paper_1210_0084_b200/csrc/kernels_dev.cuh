@@ -282,7 +282,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes, int id
 
 // F4 step 1, in place: task (ci, p2) takes buf[M2 p1 + p2], p1 < M1; DFT_{M1} (sign +);
 // twiddle e^{+2 pi i p2 n1 / M}; stores A[n1 S2 + p2].
-template <int M1>
+template <int M1, int V>  // V: channel-kernel variant (separate register budgets)
 __device__ __noinline__ void fwd_step1(const float2 *twM, float2 *reg, int m2, int nch,
                                           unsigned mag2, int twoff_lane, int lane) {
   const int nt = nch * m2;
@@ -305,7 +305,7 @@ __device__ __noinline__ void fwd_step1(const float2 *twM, float2 *reg, int m2, i
 }
 
 // F4 step 2 + F5: task (ci, n1): DFT_{M2} over p2 -> c[n1 + M1 n2] (coalesced over n1).
-template <int M2>
+template <int M2, int V>  // V: channel-kernel variant (separate register budgets)
 __device__ __noinline__ void fwd_step2(const float2 *reg, float2 *out_row, int m1, int nch,
                                           unsigned mag1, int off_lane, int lane) {
   const int nt = nch * m1;
@@ -324,16 +324,17 @@ __device__ __noinline__ void fwd_step2(const float2 *reg, float2 *out_row, int m
   for (int n2 = 0; n2 < M2; ++n2) __stcs(o + m1 * n2, v[n2]);
 }
 
-// Small forward packet: lane c < nch owns channel c; element p of its fold comes from the
-// table entry p*32 + c (bin | conj << 17, weight; weight 0 for zero padding).
-template <int M>
+// Small forward packet: lane vc = u * nch + c (u < nu) owns channel c of unit u; element p
+// of its fold comes from the table entry p*32 + c (bin | conj << 17, weight; weight 0 for
+// zero padding) -- ent and X arrive offset by c and u.
+template <int M, int V>  // V: channel-kernel variant (separate register budgets)
 __device__ __noinline__ void fwd_small(const uint2 *ent, const float2 *X, float2 *out_row,
-                                          int nch, int off_lane, int lane) {
-  if (lane >= nch) return;
+                                          bool act, int off_lane) {
+  if (!act) return;
   float2 v[M];
 #pragma unroll
   for (int p = 0; p < M; ++p) {
-    const uint2 e = __ldg(ent + p * 32 + lane);
+    const uint2 e = __ldg(ent + p * 32);
     const float2 xv = X[e.x & 0x1ffff];
     const float gv = __uint_as_float(e.y);
     v[p] = make_float2(xv.x * gv, ((e.x >> 17) & 1) ? -xv.y * gv : xv.y * gv);
@@ -345,7 +346,7 @@ __device__ __noinline__ void fwd_small(const uint2 *ent, const float2 *X, float2
 }
 
 // I2 step 1: task (ci, p2) loads c[M2 p1 + p2]; DFT_{M1} (sign -); twiddle.
-template <int M1>
+template <int M1, int V>  // V: channel-kernel variant (separate register budgets)
 __device__ __noinline__ void inv_step1(const float2 *twM, const float2 *in_row, float2 *reg,
                                           int m2, int nch, unsigned mag2, int off_lane,
                                           int twoff_lane, int lane) {
@@ -367,7 +368,7 @@ __device__ __noinline__ void inv_step1(const float2 *twM, const float2 *in_row, 
 }
 
 // I2 step 2, in place: F[n1 + M1 n2] = (unnormalised FFT_M of c) overwrites the region.
-template <int M2>
+template <int M2, int V>  // V: channel-kernel variant (separate register budgets)
 __device__ __noinline__ void inv_step2(float2 *reg, int m1, int nch, unsigned mag1, int lane) {
   const int nt = nch * m1;
   constexpr int S2 = M2 | 1;
@@ -387,18 +388,18 @@ __device__ __noinline__ void inv_step2(float2 *reg, int m1, int nch, unsigned ma
   }
 }
 
-// Small inverse packet: lane c loads channel c, FFT_M, F[q] -> scratch q*nch + c.
-template <int M>
-__device__ __noinline__ void inv_small(const float2 *in_row, float2 *reg, int nch,
+// Small inverse packet: lane vc loads virtual channel vc, FFT_M, F[q] -> scratch q*nv + vc.
+template <int M, int V>  // V: channel-kernel variant (separate register budgets)
+__device__ __noinline__ void inv_small(const float2 *in_row, float2 *reg, int nvc, int nv,
                                           int off_lane, int lane) {
-  if (lane >= nch) return;
+  if (lane >= nvc) return;
   const float2 *src = in_row + off_lane;
   float2 v[M];
 #pragma unroll
   for (int n = 0; n < M; ++n) v[n] = __ldcs(src + n);
   dft<M, -1>(v);
 #pragma unroll
-  for (int q = 0; q < M; ++q) reg[q * nch + lane] = v[q];
+  for (int q = 0; q < M; ++q) reg[q * nv + lane] = v[q];
 }
 
 #define SLICQ_SMALL(X) X(4) X(6) X(8) X(10) X(12) X(16) X(18) X(20) X(24) X(30) X(32)
@@ -414,7 +415,8 @@ constexpr int CHAN_T = 256;
 #endif
 #ifdef SLICQ_DEFINE_CHAN_KERNELS
 
-__global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_fwd_chan_kernel(const KArgs a) {
+template <int MAXS, int MINB>
+__global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArgs a) {
   extern __shared__ float4 smem4[];
   constexpr int NW = CHAN_T / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -430,46 +432,62 @@ __global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_fwd_chan_kernel
     const PacketDev P = a.packets[pk];
     const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
     const bool small = (P.m1m2 >> 17) & 1;
-    const int nch = P.nch;
-    const int ck = __ldg(a.pchans + P.chan_off + (lane < nch ? lane : 0));
-    const int c_off = __ldg(&a.chan[ck].off), c_twoff = __ldg(&a.chan[ck].twoff);
+    const int r = P.nch, nu = P.nu;
+    // this lane's virtual channel vc = u_l * r + c_l (a channel of one of the task's units)
+    const int vcl = lane < nu * r ? lane : 0;
+    const int u_l = (vcl * (int)P.magc) >> 16, c_l = vcl - u_l * r;
+    const int ck = __ldg(a.pchans + P.chan_off + c_l);
+    const int c_off = __ldg(&a.chan[ck].off) + u_l * (int)a.C;
+    const int c_twoff = __ldg(&a.chan[ck].twoff);
     const uint2 *ent = a.fent + P.fent_off;
-    const int ne = small ? 0 : nch * m1 * m2;
+    const int ne = small ? 0 : r * m1 * m2;
     const int u_lo = (item % ntiles) * a.tile;
     const int u_hi = min(a.nunits, u_lo + a.tile);
-    for (int ul = u_lo + warp; ul < u_hi; ul += NW) {
-      const float2 *X = a.stage + (int64_t)ul * a.xs;
-      float2 *out_row = a.coef_out + (a.unit0 + ul) * a.C;
-      if (ul + NW < u_hi)  // this warp's next unit: its spectrum bins -> L2 (staging is in DRAM)
-        prefetch_l2(X + NW * a.xs + P.xlo, (int64_t)(P.xhi - P.xlo + 1) * 8, lane);
+    const int ntask = (u_hi - u_lo + nu - 1) / nu;
+    for (int t = warp; t < ntask; t += NW) {
+      const int g0 = u_lo + t * nu;          // the task's first unit
+      const int nuu = min(nu, u_hi - g0);    // units in this task
+      const int nvc = nuu * r;
+      const float2 *X = a.stage + (int64_t)g0 * a.xs;
+      float2 *out_row = a.coef_out + (a.unit0 + g0) * a.C;
+      if (t + NW < ntask) {  // this warp's next task: its spectrum bins -> L2 (staging in DRAM)
+        const int g1 = g0 + NW * nu, n1u = min(nu, u_hi - g1);
+        for (int u = 0; u < n1u; ++u)
+          prefetch_l2(X + (int64_t)(NW * nu + u) * a.xs + P.xlo, (int64_t)(P.xhi - P.xlo + 1) * 8,
+                      lane);
+      }
       if (small) {
         switch (m1) {
 #define X_(S) \
-  case S: fwd_small<S>(ent, X, out_row, nch, c_off, lane); break;
+  case S: if constexpr (S <= MAXS) fwd_small<S, MAXS>(ent + c_l, X + (int64_t)u_l * a.xs, out_row, lane < nvc, c_off); break;
           SLICQ_SMALL(X_)
 #undef X_
         }
         continue;
       }
       // F3 fold from the element table (coalesced over e; positions conflict-free)
+      for (int u = 0; u < nuu; ++u) {
+        const float2 *Xu = X + (int64_t)u * a.xs;
+        float2 *su = scr + u * P.ustride;
 #pragma unroll 4
-      for (int e = lane; e < ne; e += 32) {
-        const uint2 en = __ldg(ent + e);
-        const float2 xv = X[en.x & 0x1ffff];
-        const float gv = __uint_as_float(en.y);
-        scr[en.x >> 18] = make_float2(xv.x * gv, ((en.x >> 17) & 1) ? -xv.y * gv : xv.y * gv);
+        for (int e = lane; e < ne; e += 32) {
+          const uint2 en = __ldg(ent + e);
+          const float2 xv = Xu[en.x & 0x1ffff];
+          const float gv = __uint_as_float(en.y);
+          su[en.x >> 18] = make_float2(xv.x * gv, ((en.x >> 17) & 1) ? -xv.y * gv : xv.y * gv);
+        }
       }
       __syncwarp();
       switch (m1) {
 #define X_(S) \
-  case S: fwd_step1<S>(a.twM, scr, m2, nch, P.mag2, c_twoff, lane); break;
+  case S: if constexpr (S <= MAXS) fwd_step1<S, MAXS>(a.twM, scr, m2, nvc, P.mag2, c_twoff, lane); break;
         SLICQ_SIZES(X_)
 #undef X_
       }
       __syncwarp();
       switch (m2) {
 #define X_(S) \
-  case S: fwd_step2<S>(scr, out_row, m1, nch, P.mag1, c_off, lane); break;
+  case S: if constexpr (S <= MAXS) fwd_step2<S, MAXS>(scr, out_row, m1, nvc, P.mag1, c_off, lane); break;
         SLICQ_SIZES(X_)
 #undef X_
       }
@@ -479,7 +497,8 @@ __global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_fwd_chan_kernel
   pdl_trigger();
 }
 
-__global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_inv_chan_kernel(const KArgs a) {
+template <int MAXS, int MINB>
+__global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArgs a) {
   extern __shared__ float4 smem4[];
   constexpr int NW = CHAN_T / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -495,49 +514,64 @@ __global__ void __launch_bounds__(CHAN_T, SLICQ_CHAN_MINB) slicq_inv_chan_kernel
     const PacketDev P = a.packets[pk];
     const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
     const bool small = (P.m1m2 >> 17) & 1;
-    const int nch = P.nch;
-    const int ck = __ldg(a.pchans + P.chan_off + (lane < nch ? lane : 0));
-    const int c_off = __ldg(&a.chan[ck].off), c_twoff = __ldg(&a.chan[ck].twoff);
+    const int r = P.nch, nu = P.nu;
+    const int vcl = lane < nu * r ? lane : 0;
+    const int u_l = (vcl * (int)P.magc) >> 16, c_l = vcl - u_l * r;
+    const int ck = __ldg(a.pchans + P.chan_off + c_l);
+    const int c_off0 = __ldg(&a.chan[ck].off);
+    const int c_off = c_off0 + u_l * (int)a.C;
+    const int c_twoff = __ldg(&a.chan[ck].twoff);
     const uint2 *ent = a.ient + P.ient_off;
     const int ne = P.nz;  // contributions of the packet = sum of its L_k
     const int zb = __shfl_sync(FULL, __ldg(&a.chan[ck].goff), 0);  // packet's range in Z
     const int u_lo = (item % ntiles) * a.tile;
     const int u_hi = min(a.nunits, u_lo + a.tile);
-    const int cbase = __shfl_sync(FULL, c_off, 0);
-    const int clen = __shfl_sync(FULL, c_off, nch - 1) - cbase + m1 * m2;
-    for (int ul = u_lo + warp; ul < u_hi; ul += NW) {
-      const float2 *in_row = a.coef_in + (a.unit0 + ul) * a.C;
-      float2 *Zb = a.stage + (int64_t)ul * a.zs + zb;
-      if (ul + NW < u_hi) prefetch_l2(in_row + NW * a.C + cbase, (int64_t)clen * 8, lane);
+    const int cbase = __shfl_sync(FULL, c_off0, 0);
+    const int clen = __shfl_sync(FULL, c_off0, r - 1) - cbase + m1 * m2;
+    const int ntask = (u_hi - u_lo + nu - 1) / nu;
+    for (int t = warp; t < ntask; t += NW) {
+      const int g0 = u_lo + t * nu;
+      const int nuu = min(nu, u_hi - g0);
+      const int nvc = nuu * r;
+      const float2 *in_row = a.coef_in + (a.unit0 + g0) * a.C;
+      if (t + NW < ntask) {
+        const int g1 = g0 + NW * nu, n1u = min(nu, u_hi - g1);
+        for (int u = 0; u < n1u; ++u)
+          prefetch_l2(in_row + (int64_t)(NW * nu + u) * a.C + cbase, (int64_t)clen * 8, lane);
+      }
       if (small) {
         switch (m1) {
 #define X_(S) \
-  case S: inv_small<S>(in_row, scr, nch, c_off, lane); break;
+  case S: if constexpr (S <= MAXS) inv_small<S, MAXS>(in_row, scr, nvc, nu * r, c_off, lane); break;
           SLICQ_SMALL(X_)
 #undef X_
         }
       } else {
         switch (m1) {
 #define X_(S) \
-  case S: inv_step1<S>(a.twM, in_row, scr, m2, nch, P.mag2, c_off, c_twoff, lane); break;
+  case S: if constexpr (S <= MAXS) inv_step1<S, MAXS>(a.twM, in_row, scr, m2, nvc, P.mag2, c_off, c_twoff, lane); break;
           SLICQ_SIZES(X_)
 #undef X_
         }
         __syncwarp();
         switch (m2) {
 #define X_(S) \
-  case S: inv_step2<S>(scr, m1, nch, P.mag1, lane); break;
+  case S: if constexpr (S <= MAXS) inv_step2<S, MAXS>(scr, m1, nvc, P.mag1, lane); break;
           SLICQ_SIZES(X_)
 #undef X_
         }
       }
       __syncwarp();
       // I3a contributions Z[goff_k + d] = F[q] * g~_k[j]/sqrt(M_k), (k, d) contiguous
+      for (int u = 0; u < nuu; ++u) {
+        float2 *Zb = a.stage + (int64_t)(g0 + u) * a.zs + zb;
+        const float2 *su = scr + u * P.ustride;
 #pragma unroll 4
-      for (int e = lane; e < ne; e += 32) {
-        const uint2 en = __ldg(ent + e);
-        const float2 f = scr[en.x];
-        __stcg(Zb + e, cscale(f, __uint_as_float(en.y)));
+        for (int e = lane; e < ne; e += 32) {
+          const uint2 en = __ldg(ent + e);
+          const float2 f = su[en.x];
+          __stcg(Zb + e, cscale(f, __uint_as_float(en.y)));
+        }
       }
       __syncwarp();
     }

@@ -81,6 +81,19 @@ size_t spec_smem_for(int logN, int tr) {
 
 constexpr size_t kSmemCap = 227 * 1024;  // per CTA
 constexpr int kSmallCap = 640;           // float2 scratch entries a small packet may use
+// channel-kernel variants: <largest DFT size, CTAs per SM (register budget)>
+#ifndef SLICQ_LITE_MAX
+#define SLICQ_LITE_MAX 16
+#endif
+#ifndef SLICQ_LITE_MINB
+#define SLICQ_LITE_MINB 3
+#endif
+constexpr int kLiteMax = SLICQ_LITE_MAX, kLiteMinB = SLICQ_LITE_MINB, kFullMax = 32, kFullMinB = 2;
+using ChanFn = void (*)(const KArgs);
+static ChanFn chan_fn(bool fwd, bool lite) {
+  if (fwd) return lite ? slicq_fwd_chan_kernel<kLiteMax, kLiteMinB> : slicq_fwd_chan_kernel<kFullMax, kFullMinB>;
+  return lite ? slicq_inv_chan_kernel<kLiteMax, kLiteMinB> : slicq_inv_chan_kernel<kFullMax, kFullMinB>;
+}
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -144,12 +157,30 @@ int configure_kernels(slicq_plan *p) {
     pk.d.mag1 = (uint32_t)((65536 + m1 - 1) / m1);
     pk.d.mag2 = (uint32_t)((65536 + m2 - 1) / m2);
     while (k < K2 && p->M[k] == M && (int)pk.ks.size() < nch) pk.ks.push_back(k++);
-    pk.d.nch = (int)pk.ks.size();
-    pk.scr = small ? pk.d.nch * M : pk.d.nch * m1 * (m2 | 1);
+    const int r = (int)pk.ks.size();
+    pk.d.nch = r;
+    // units per warp task: fill the lanes (short runs of one M would leave them idle)
+    const int nu = small ? std::max(1, std::min(32 / r, kSmallCap / (r * M)))
+                         : std::max(1, 32 / (r * std::max(m1, m2)));
+    pk.d.nu = nu;
+    pk.d.magc = (uint32_t)((65536 + r - 1) / r);
+    pk.d.ustride = small ? r : r * m1 * (m2 | 1);
+    pk.scr = nu * pk.d.ustride * (small ? M : 1);
     pks.push_back(std::move(pk));
   }
   // shape-sorted (the warps of a channel-kernel CTA run the same code), longer first
-  std::stable_sort(pks.begin(), pks.end(), [](const Pk &x, const Pk &y) { return x.M > y.M; });
+  // lite packets (every DFT size <= kLiteMax) first: they run in the channel-kernel variant
+  // with the smaller register budget (more resident warps), the rest in the full variant
+  auto lite = [](const Pk &x) {
+    const int m1 = x.d.m1m2 & 255, m2 = (x.d.m1m2 >> 8) & 255;
+    return std::max(m1, m2) <= kLiteMax;
+  };
+  std::stable_sort(pks.begin(), pks.end(), [&](const Pk &x, const Pk &y) {
+    const bool lx = lite(x), ly = lite(y);
+    return lx != ly ? lx : x.M > y.M;
+  });
+  kc.nlite = 0;
+  for (const Pk &x : pks) kc.nlite += lite(x) ? 1 : 0;
 
   // ---------------- element tables
   auto bin_of = [&](int j, int &conj) {  // X(j) = X[b] or conj(X[b]) for real input
@@ -223,7 +254,8 @@ int configure_kernels(slicq_plan *p) {
       for (int dd = 0; dd < p->len[k]; ++dd) {
         int q = lo_mod + dd;
         if (q >= M) q -= M;
-        const uint32_t pos = small ? (uint32_t)(q * d.nch + c) : (uint32_t)(c * m1 * S2 + q);
+        // small: scratch q * (nu * nch) + vc; big: vc * M1 * S2 + q (+ u * ustride in-kernel)
+        const uint32_t pos = small ? (uint32_t)(q * d.nu * d.nch + c) : (uint32_t)(c * m1 * S2 + q);
         p->ient.push_back(make_uint2(pos, fbits(p->gdual[p->goff[k] + dd] * sc * half)));
         ++nz;
       }
@@ -402,15 +434,9 @@ int upload(slicq_plan *p) {
     case 15: rc = large_set_attrs<15>(); break;
     case 16: rc = large_set_attrs<16>(); break;
   }
-  if (rc == 0) {
-    cudaError_t e1 = cudaFuncSetAttribute(slicq_fwd_chan_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)p->kc.chan_smem);
-    cudaError_t e2 = cudaFuncSetAttribute(slicq_inv_chan_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)p->kc.chan_smem);
-    rc = e1 != cudaSuccess ? (int)e1 : (int)e2;
-  }
+  for (int v = 0; v < 4 && rc == 0; ++v)
+    rc = (int)cudaFuncSetAttribute(chan_fn(v & 1, v & 2), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)p->kc.chan_smem);
   if (rc != 0)
     return set_error(SLICQ_ECUDA, std::string("cudaFuncSetAttribute: ") +
                                       cudaGetErrorString((cudaError_t)rc));
@@ -443,6 +469,14 @@ WsLayout ws_layout(const slicq_plan *p, int64_t nslices, int64_t batch) {
   return w;
 }
 }  // namespace
+
+int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t batch) {
+  const WsLayout w = ws_layout(p, nslices, batch);
+  const int64_t chunks = (nslices * batch + w.chunk - 1) / w.chunk;
+  const int nchan = (p->kc.nlite > 0) + (p->kc.npackets > p->kc.nlite);
+  const int nspec = !p->kc.large ? 1 : direction == 0 ? 2 : 4;
+  return (int)(chunks * (nchan + nspec));
+}
 
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch) {
   if (!p->has_device) return 0;  // the layout depends on the device configuration
@@ -479,8 +513,8 @@ static int check_device(const slicq_plan *p) {
   return SLICQ_OK;
 }
 
-// persistent channel-kernel grid: resident CTAs (2 per SM), capped by the work items
-static unsigned chan_grid(const slicq_plan *p, const KArgs &a) {
+// persistent channel-kernel grid: resident CTAs per SM, capped by the work items
+static unsigned chan_grid(const slicq_plan *p, const KArgs &a, ChanFn fn) {
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -488,28 +522,38 @@ static unsigned chan_grid(const slicq_plan *p, const KArgs &a) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  const int64_t items = (int64_t)p->kc.npackets * ((a.nunits + a.tile - 1) / a.tile);
-  int per_sm = SLICQ_CHAN_MINB;
+  const int64_t items = (int64_t)a.npackets * ((a.nunits + a.tile - 1) / a.tile);
+  int per_sm = 2;
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slicq_fwd_chan_kernel, CHAN_T,
-                                                    p->kc.chan_smem) == cudaSuccess && occ > 0)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, CHAN_T, p->kc.chan_smem) ==
+          cudaSuccess && occ > 0)
     per_sm = occ;
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)per_sm * nsm));
 }
 
-static cudaError_t launch_chan(bool fwd, const KArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(CHAN_T);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return fwd ? cudaLaunchKernelEx(&cfg, slicq_fwd_chan_kernel, a)
-             : cudaLaunchKernelEx(&cfg, slicq_inv_chan_kernel, a);
+// the channel kernels of one direction: lite packets [0, nlite), then the full variant
+static cudaError_t launch_chan(bool fwd, const slicq_plan *p, KArgs a, cudaStream_t s) {
+  const int np = p->kc.npackets, nl = p->kc.nlite;
+  for (int v = 0; v < 2; ++v) {
+    const bool lite = v == 0;
+    a.packets = p->d.packets + (lite ? 0 : nl);
+    a.npackets = lite ? nl : np - nl;
+    if (a.npackets == 0) continue;
+    const ChanFn fn = chan_fn(fwd, lite);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(chan_grid(p, a, fn));
+    cfg.blockDim = dim3(CHAN_T);
+    cfg.dynamicSmemBytes = p->kc.chan_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 static cudaError_t launch_spec(bool fwd, const slicq_plan *p, const KArgs &a, dim3 grid,
@@ -556,7 +600,7 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
     cudaError_t e = !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), s)
                     : p->kc.logN == 15 ? large_forward<15>(a, s) : large_forward<16>(a, s);
-    if (e == cudaSuccess) e = launch_chan(true, a, dim3(chan_grid(p, a)), p->kc.chan_smem, s);
+    if (e == cudaSuccess) e = launch_chan(true, p, a, s);
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
   }
@@ -596,7 +640,7 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
   for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
     a.unit0 = u0;
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
-    cudaError_t e = launch_chan(false, a, dim3(chan_grid(p, a)), p->kc.chan_smem, s);
+    cudaError_t e = launch_chan(false, p, a, s);
     if (e == cudaSuccess)
       e = !p->kc.large ? launch_spec(false, p, a, dim3((unsigned)a.nunits), s)
           : p->kc.logN == 15 ? large_inverse_spec<15>(a, s) : large_inverse_spec<16>(a, s);

@@ -284,6 +284,11 @@ size_t slicq_workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch
   if (!p || nslices < 1 || batch < 1) return 0;
   return slicq::workspace_bytes(p, nslices, batch);
 }
+int slicq_kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t batch) {
+  if (!p || !p->has_device || nslices < 1 || batch < 1 || (direction != 0 && direction != 1))
+    return 0;
+  return slicq::kernel_launches(p, direction, nslices, batch);
+}
 int64_t slicq_filter_total_length(const slicq_plan *p) {
   if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
   return (int64_t)p->g.size();

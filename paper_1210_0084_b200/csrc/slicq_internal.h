@@ -21,9 +21,10 @@ struct ChanDev {
   int32_t lo_mod;  // lo_k mod M_k in [0, M_k)
 };
 
-// A packet = consecutive channels of one length M.  Big packets (M > 32): four-step
-// M1 x M2 DFT, one task per lane and step (nch*M1, nch*M2 <= 32).  Small packets (M <= 32,
-// flag bit 17): one lane per channel, whole DFT_M in registers.
+// A packet = consecutive channels of one length M, processed for nu consecutive units at
+// once: virtual channel vc = u * nch + c (u < nu, c < nch).  Big packets (M > 32): four-step
+// M1 x M2 DFT, one task per lane and step (nu*nch*M1, nu*nch*M2 <= 32).  Small packets
+// (M <= 32, flag bit 17): one lane per virtual channel, whole DFT_M in registers.
 struct PacketDev {
   int32_t m1m2;     // M1 | (M2 << 8) | SMALL << 17  (small: M1 = M, M2 = 1)
   int32_t nch;      // channels in the packet
@@ -34,6 +35,9 @@ struct PacketDev {
   uint32_t mag1;    // ceil(2^16 / M1): q / M1 = (q * mag1) >> 16 for q < 64
   uint32_t mag2;    // ceil(2^16 / M2)
   int32_t xlo, xhi; // forward: spectrum bins [xlo, xhi] the fold reads (L2 prefetch)
+  int32_t nu;       // units per warp task
+  uint32_t magc;    // ceil(2^16 / nch): vc / nch = (vc * magc) >> 16
+  int32_t ustride;  // scratch entries per unit (small: nch, big: nch * M1 * (M2 | 1))
 };
 
 struct DeviceTables {
@@ -59,6 +63,7 @@ struct KernelConfig {
   int scr = 0;           // channel kernels: per-warp scratch (float2 entries)
   size_t chan_smem = 0;
   int npackets = 0;
+  int nlite = 0;              // packets [0, nlite) run in the lite channel-kernel variant
   int64_t xs = 0, zs = 0;     // staging row strides (float2): X spectra, contributions
   bool large = false;         // 2N >= 65536: four-step FFT through the staging buffer
   int64_t toff_f = 0, toff_i = 0;  // offsets of the four-step intermediate in a unit
@@ -114,4 +119,5 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
 int launch_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,
                        int64_t batch, void *stream);
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
+int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t batch);
 }  // namespace slicq
