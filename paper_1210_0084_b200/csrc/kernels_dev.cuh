@@ -148,8 +148,8 @@ struct KArgs {
   int scr;                  // channel kernels: per-warp scratch entries
   const uint2 *fent;        // forward element table (enc, weight bits)
   const uint2 *ient;        // inverse element table (scratch pos, weight bits)
-  const int32_t *bin_off;   // inverse gather CSR: [N+2]
-  const uint32_t *gents;    // contribution index | conj << 31
+  const uint32_t *dpos;     // inverse overflow run per bin: start | count << 20 (0: none)
+  int64_t zso;              // inverse staging: slot 1 at zso, overflow at 2 zso
   const float *h0;
   const float *h0dual;
   const float2 *tw2n;
@@ -522,8 +522,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
     const int c_off = c_off0 + u_l * (int)a.C;
     const int c_twoff = __ldg(&a.chan[ck].twoff);
     const uint2 *ent = a.ient + P.ient_off;
-    const int ne = P.nz;  // contributions of the packet = sum of its L_k
-    const int zb = __shfl_sync(FULL, __ldg(&a.chan[ck].goff), 0);  // packet's range in Z
+    const int ne = P.nz;  // entries (channel term -> staging slot) of the packet
     const int u_lo = (item % ntiles) * a.tile;
     const int u_hi = min(a.nunits, u_lo + a.tile);
     const int cbase = __shfl_sync(FULL, c_off0, 0);
@@ -562,15 +561,16 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
         }
       }
       __syncwarp();
-      // I3a contributions Z[goff_k + d] = F[q] * g~_k[j]/sqrt(M_k), (k, d) contiguous
+      // I3a terms F[q] * g~_k[j]/sqrt(M_k) (conjugated for mirrored bins) -> their slot of
+      // the unit's half-spectrum staging (I3b sums the slots)
       for (int u = 0; u < nuu; ++u) {
-        float2 *Zb = a.stage + (int64_t)(g0 + u) * a.zs + zb;
+        float2 *Zb = a.stage + (int64_t)(g0 + u) * a.zs;
         const float2 *su = scr + u * P.ustride;
 #pragma unroll 4
         for (int e = lane; e < ne; e += 32) {
           const uint2 en = __ldg(ent + e);
-          const float2 f = su[en.x];
-          __stcg(Zb + e, cscale(f, __uint_as_float(en.y)));
+          const float2 f = cscale(su[en.x & 0x3fff], __uint_as_float(en.y & 0x7fffffffu));
+          __stcg(Zb + (en.x >> 14), make_float2(f.x, (en.y >> 31) ? -f.y : f.y));
         }
       }
       __syncwarp();
@@ -740,44 +740,29 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
   pdl_wait();  // contributions of this chunk come from the channel kernel
   prefetch_l2(a.stage + ul * a.zs, a.zs * 8, tid, T);
 
-  // ---- I3b: per-bin gather of the contributions (Hermitian rule folded into the list)
+  // ---- I3b: half-spectrum bin b = slot0[b] + slot1[b] (+ its overflow run, rare)
   {
     const float2 *Z = a.stage + ul * a.zs;
-    // most bins have <= 2 terms: those loads are issued unconditionally (predicated) for
-    // 4 bins at a time so that ~8 staging loads are in flight per thread
-    constexpr int G = 4;
+    const float2 *Z1 = Z + a.zso, *Zo = Z + 2 * a.zso;
+    constexpr int G = 4;  // 8 independent staging loads in flight per thread
     for (int b0 = tid; b0 <= N; b0 += G * T) {
-      int e0[G], e1[G];
-      uint32_t g0[G], g1[G];
       float2 z0[G], z1[G];
+      uint32_t dp[G];
 #pragma unroll
       for (int q = 0; q < G; ++q) {
-        const int b = b0 + q * T;
-        e0[q] = b <= N ? __ldg(a.bin_off + b) : 0;
-        e1[q] = b <= N ? __ldg(a.bin_off + b + 1) : 0;
-      }
-#pragma unroll
-      for (int q = 0; q < G; ++q) {
-        g0[q] = e0[q] < e1[q] ? __ldg(a.gents + e0[q]) : 0u;
-        g1[q] = e0[q] + 1 < e1[q] ? __ldg(a.gents + e0[q] + 1) : 0u;
-      }
-#pragma unroll
-      for (int q = 0; q < G; ++q) {
-        z0[q] = e0[q] < e1[q] ? __ldcg(Z + (g0[q] & 0x7fffffffu)) : make_float2(0.f, 0.f);
-        z1[q] = e0[q] + 1 < e1[q] ? __ldcg(Z + (g1[q] & 0x7fffffffu)) : make_float2(0.f, 0.f);
+        const int b = min(b0 + q * T, N);
+        z0[q] = __ldcg(Z + b);
+        z1[q] = __ldcg(Z1 + b);
+        dp[q] = __ldg(a.dpos + b);
       }
 #pragma unroll
       for (int q = 0; q < G; ++q) {
         const int b = b0 + q * T;
         if (b > N) continue;
-        float2 acc = make_float2(z0[q].x, (g0[q] >> 31) ? -z0[q].y : z0[q].y);
-        acc.x += z1[q].x;
-        acc.y += (g1[q] >> 31) ? -z1[q].y : z1[q].y;
-        for (int e = e0[q] + 2; e < e1[q]; ++e) {  // deep-overlap bins
-          const uint32_t ge = __ldg(a.gents + e);
-          const float2 z = __ldcg(Z + (ge & 0x7fffffffu));
-          acc.x += z.x;
-          acc.y += (ge >> 31) ? -z.y : z.y;
+        float2 acc = cadd(z0[q], z1[q]);
+        if (dp[q]) {  // deep-overlap bin: overflow terms in order
+          const int st = dp[q] & 0xfffff, cnt = dp[q] >> 20;
+          for (int i = 0; i < cnt; ++i) acc = cadd(acc, __ldcg(Zo + st + i));
         }
         spec[padi(b)] = acc;
       }

@@ -182,6 +182,72 @@ int configure_kernels(slicq_plan *p) {
   kc.nlite = 0;
   for (const Pk &x : pks) kc.nlite += lite(x) ? 1 : 0;
 
+  // ---------------- inverse destinations (I3b gather without index tables): every channel
+  // contribution Z_k[d] goes to half-spectrum bin b by the Hermitian rule of C15 (term at
+  // j mod 2N if <= N, conjugate at -j mod 2N if <= N).  The staging row of a unit holds two
+  // slot arrays [slot][N+1] (slot preferred = channel parity: with the Hann filters' 50%
+  // overlap almost every bin has exactly two terms, one from an even and one from an odd
+  // channel) and an overflow area for the rare deeper bins (ordered by bin, summed in order).
+  // Unused slots receive an explicit zero.  The IA kernel reads slot0[b] + slot1[b] (+ the
+  // overflow run dpos[b]), coalesced and table-free for regular bins.
+  struct Dst {
+    int d;
+    uint32_t dst;
+    int conj;
+    bool zero;
+  };
+  std::vector<std::vector<Dst>> dsts(K2);
+  {
+    const int64_t zso = (N + 2) & ~int64_t(1);
+    std::vector<uint8_t> used(N + 1, 0);
+    std::vector<std::vector<std::pair<int, int>>> ovf(N + 1);  // (k, index into dsts[k])
+    std::vector<std::pair<int, int>> first(N + 1, std::make_pair(-1, -1));
+    for (int k = 0; k < K2; ++k)
+      for (int dd = 0; dd < p->len[k]; ++dd) {
+        const int j = p->lo[k] + dd;
+        int p1 = j % N2;
+        if (p1 < 0) p1 += N2;
+        const int p2 = p1 == 0 ? 0 : N2 - p1;
+        for (int t = 0; t < 2; ++t) {
+          const int b = t == 0 ? p1 : p2;
+          if (b > N) continue;
+          if (first[b].first < 0) first[b] = std::make_pair(k, dd);
+          const int pref = k & 1;
+          int slot = 2;
+          if (!((used[b] >> pref) & 1)) slot = pref;
+          else if (!((used[b] >> (pref ^ 1)) & 1)) slot = pref ^ 1;
+          if (slot < 2) {
+            used[b] |= (uint8_t)(1 << slot);
+            dsts[k].push_back(Dst{dd, (uint32_t)(slot * zso + b), t, false});
+          } else {
+            ovf[b].push_back(std::make_pair(k, (int)dsts[k].size()));
+            dsts[k].push_back(Dst{dd, 0u, t, false});
+          }
+        }
+      }
+    p->dpos.assign(N + 1, 0u);
+    int64_t start = 0;
+    for (int b = 0; b <= N; ++b) {
+      if (first[b].first < 0)
+        return set_error(SLICQ_EINTERNAL, "half-spectrum bin without a channel term");
+      for (int sl = 0; sl < 2; ++sl)  // explicit zeros for unused slots
+        if (!((used[b] >> sl) & 1))
+          dsts[first[b].first].push_back(Dst{first[b].second, (uint32_t)(sl * zso + b), 0, true});
+      if (ovf[b].empty()) continue;
+      const int64_t cnt = (int64_t)ovf[b].size();
+      if (start >= (1 << 20) || cnt >= (1 << 11))
+        return set_error(SLICQ_EUNSUPPORTED, "inverse overflow list too long");
+      p->dpos[b] = (uint32_t)start | ((uint32_t)cnt << 20);
+      for (int64_t i = 0; i < cnt; ++i)
+        dsts[ovf[b][i].first][ovf[b][i].second].dst = (uint32_t)(2 * zso + start + i);
+      start += cnt;
+    }
+    kc.zso = zso;
+    kc.nover = start;
+    if (2 * zso + start >= (int64_t(1) << 18))
+      return set_error(SLICQ_EUNSUPPORTED, "slice too long for the inverse element tables");
+  }
+
   // ---------------- element tables
   auto bin_of = [&](int j, int &conj) {  // X(j) = X[b] or conj(X[b]) for real input
     int jj = j % N2;
@@ -245,18 +311,21 @@ int configure_kernels(slicq_plan *p) {
         }
       }
     }
-    // inverse contribution table: e over (channel, d), Z index goff_first + e
+    // inverse entry table: e over (channel, destination): scratch position | dst << 14,
+    // weight g~_k[j]/sqrt(M_k) (plateaus x 1/2, C15) with the conjugation flag in bit 31
     int nz = 0;
     for (int c = 0; c < d.nch; ++c) {
       const int k = pk.ks[c];
       const int lo_mod = ((p->lo[k] % M) + M) % M;
       const double half = (k == 0 || k == K2 - 1) ? 0.5 : 1.0;  // self-mirrored plateaus (C15)
-      for (int dd = 0; dd < p->len[k]; ++dd) {
-        int q = lo_mod + dd;
+      for (const Dst &ds : dsts[k]) {
+        int q = lo_mod + ds.d;
         if (q >= M) q -= M;
         // small: scratch q * (nu * nch) + vc; big: vc * M1 * S2 + q (+ u * ustride in-kernel)
         const uint32_t pos = small ? (uint32_t)(q * d.nu * d.nch + c) : (uint32_t)(c * m1 * S2 + q);
-        p->ient.push_back(make_uint2(pos, fbits(p->gdual[p->goff[k] + dd] * sc * half)));
+        const double w = ds.zero ? 0.0 : p->gdual[p->goff[k] + ds.d] * sc * half;
+        if (!(w >= 0.0)) return set_error(SLICQ_EUNSUPPORTED, "negative dual filter value");
+        p->ient.push_back(make_uint2(pos | (ds.dst << 14), fbits(w) | ((uint32_t)ds.conj << 31)));
         ++nz;
       }
     }
@@ -286,32 +355,9 @@ int configure_kernels(slicq_plan *p) {
   if (kc.chan_smem > kSmemCap)
     return set_error(SLICQ_EUNSUPPORTED, "channel scratch does not fit in shared memory");
 
-  // ---------------- inverse gather CSR: half-spectrum bin b <- contributions Z[goff_k + d]
-  // with the Hermitian rule of C15 (term at j mod 2N if <= N, conjugate at -j mod 2N if <= N)
-  {
-    std::vector<std::vector<uint32_t>> per(N + 1);
-    for (int k = 0; k < K2; ++k)
-      for (int dd = 0; dd < p->len[k]; ++dd) {
-        const uint32_t zi = (uint32_t)(p->goff[k] + dd);
-        const int j = p->lo[k] + dd;
-        int p1 = j % N2;
-        if (p1 < 0) p1 += N2;
-        if (p1 <= N) per[p1].push_back(zi);
-        const int p2 = p1 == 0 ? 0 : N2 - p1;
-        if (p2 <= N) per[p2].push_back(zi | 0x80000000u);
-      }
-    p->bin_off.assign(N + 2, 0);
-    p->gents.clear();
-    for (int b = 0; b <= N; ++b) {
-      p->bin_off[b] = (int32_t)p->gents.size();
-      p->gents.insert(p->gents.end(), per[b].begin(), per[b].end());
-    }
-    p->bin_off[N + 1] = (int32_t)p->gents.size();
-  }
-
-  // ---------------- staging: X spectra (N+1) and contributions (sum L_k) per unit
+  // ---------------- staging: X spectra (N+1) and inverse slots + overflow per unit
   kc.xs = (p->N + 2) & ~int64_t(1);
-  kc.zs = ((int64_t)p->g.size() + 1) & ~int64_t(1);
+  kc.zs = (2 * kc.zso + kc.nover + 1) & ~int64_t(1);
   if (kc.large) {  // the four-step intermediate (N per unit) follows X / the contributions
     kc.toff_f = kc.xs;
     kc.toff_i = kc.zs;
@@ -389,8 +435,7 @@ int upload(slicq_plan *p) {
       {p->pchans.data(), sizeof(int32_t) * p->pchans.size(), 0},
       {p->fent.data(), sizeof(uint2) * p->fent.size(), 0},
       {p->ient.data(), sizeof(uint2) * p->ient.size(), 0},
-      {p->bin_off.data(), sizeof(int32_t) * p->bin_off.size(), 0},
-      {p->gents.data(), sizeof(uint32_t) * p->gents.size(), 0},
+      {p->dpos.data(), sizeof(uint32_t) * p->dpos.size(), 0},
       {h0.data(), sizeof(float) * h0.size(), 0},
       {h0d.data(), sizeof(float) * h0d.size(), 0},
       {tw.data(), sizeof(float) * tw.size(), 0},
@@ -416,12 +461,11 @@ int upload(slicq_plan *p) {
   p->d.pchans = reinterpret_cast<int32_t *>(b + parts[2].off);
   p->d.fent = reinterpret_cast<uint2 *>(b + parts[3].off);
   p->d.ient = reinterpret_cast<uint2 *>(b + parts[4].off);
-  p->d.bin_off = reinterpret_cast<int32_t *>(b + parts[5].off);
-  p->d.gents = reinterpret_cast<uint32_t *>(b + parts[6].off);
-  p->d.h0 = reinterpret_cast<float *>(b + parts[7].off);
-  p->d.h0dual = reinterpret_cast<float *>(b + parts[8].off);
-  p->d.tw2n = reinterpret_cast<float *>(b + parts[9].off);
-  p->d.twM = reinterpret_cast<float *>(b + parts[10].off);
+  p->d.dpos = reinterpret_cast<uint32_t *>(b + parts[5].off);
+  p->d.h0 = reinterpret_cast<float *>(b + parts[6].off);
+  p->d.h0dual = reinterpret_cast<float *>(b + parts[7].off);
+  p->d.tw2n = reinterpret_cast<float *>(b + parts[8].off);
+  p->d.twM = reinterpret_cast<float *>(b + parts[9].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
@@ -494,8 +538,8 @@ static KArgs base_args(const slicq_plan *p) {
   a.scr = p->kc.scr;
   a.fent = p->d.fent;
   a.ient = p->d.ient;
-  a.bin_off = p->d.bin_off;
-  a.gents = p->d.gents;
+  a.dpos = p->d.dpos;
+  a.zso = p->kc.zso;
   a.h0 = p->d.h0;
   a.h0dual = p->d.h0dual;
   a.tw2n = reinterpret_cast<const float2 *>(p->d.tw2n);

@@ -218,13 +218,12 @@ __global__ void __launch_bounds__(LT) fwd_large_row(const KArgs a) {
 // D = (H[k] - conj H[N-k])/2, O = D e^{+i pi k/N}.
 template <int N>
 __device__ __forceinline__ float2 gather_bin(const KArgs &a, const float2 *Z, int b) {
-  const int e0 = __ldg(a.bin_off + b), e1 = __ldg(a.bin_off + b + 1);
-  float2 acc = make_float2(0.f, 0.f);
-  for (int e = e0; e < e1; ++e) {
-    const uint32_t ge = __ldg(a.gents + e);
-    const float2 z = __ldcg(Z + (ge & 0x7fffffffu));
-    acc.x += z.x;
-    acc.y += (ge >> 31) ? -z.y : z.y;
+  float2 acc = cadd(__ldcg(Z + b), __ldcg(Z + a.zso + b));
+  const uint32_t dp = __ldg(a.dpos + b);
+  if (dp) {  // deep-overlap bin: overflow terms in order
+    const float2 *Zo = Z + 2 * a.zso + (dp & 0xfffff);
+    const int cnt = dp >> 20;
+    for (int i = 0; i < cnt; ++i) acc = cadd(acc, __ldcg(Zo + i));
   }
   return acc;
 }

@@ -46,8 +46,7 @@ struct DeviceTables {
   int32_t *pchans = nullptr;
   uint2 *fent = nullptr;     // forward element table
   uint2 *ient = nullptr;     // inverse element table
-  int32_t *bin_off = nullptr;
-  uint32_t *gents = nullptr;
+  uint32_t *dpos = nullptr;  // inverse overflow run per bin: start | count << 20 (0: none)
   float *h0 = nullptr;      // fp32 h_0[t+N], t in [-N, N)
   float *h0dual = nullptr;  // fp32 h~_0[t+N]
   float *tw2n = nullptr;    // float2: [64] e^{-i pi t/N} for t < 64, then [2N/64] for t = 64 h
@@ -65,6 +64,7 @@ struct KernelConfig {
   int npackets = 0;
   int nlite = 0;              // packets [0, nlite) run in the lite channel-kernel variant
   int64_t xs = 0, zs = 0;     // staging row strides (float2): X spectra, contributions
+  int64_t zso = 0, nover = 0; // inverse staging: slot-1 offset, overflow entries
   bool large = false;         // 2N >= 65536: four-step FFT through the staging buffer
   int64_t toff_f = 0, toff_i = 0;  // offsets of the four-step intermediate in a unit
   int64_t chunk_units = 0;    // units per chunk (staging is sized for one chunk)
@@ -98,8 +98,7 @@ struct slicq_plan {
   std::vector<slicq::PacketDev> packets;
   std::vector<int32_t> pchans;
   std::vector<uint2> fent, ient;
-  std::vector<int32_t> bin_off;
-  std::vector<uint32_t> gents;
+  std::vector<uint32_t> dpos;
 };
 
 namespace slicq {
