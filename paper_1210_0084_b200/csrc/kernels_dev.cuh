@@ -740,31 +740,38 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
   pdl_wait();  // contributions of this chunk come from the channel kernel
   prefetch_l2(a.stage + ul * a.zs, a.zs * 8, tid, T);
 
-  // ---- I3b: half-spectrum bin b = slot0[b] + slot1[b] (+ its overflow run, rare)
+  // ---- I3b: half-spectrum bin b = slot0[b] + slot1[b] (+ its overflow run, rare); two
+  // bins per thread and load (16-byte), 4 pairs in flight
   {
-    const float2 *Z = a.stage + ul * a.zs;
-    const float2 *Z1 = Z + a.zso, *Zo = Z + 2 * a.zso;
-    constexpr int G = 4;  // 8 independent staging loads in flight per thread
-    for (int b0 = tid; b0 <= N; b0 += G * T) {
-      float2 z0[G], z1[G];
-      uint32_t dp[G];
+    const float4 *Z0 = reinterpret_cast<const float4 *>(a.stage + ul * a.zs);
+    const float4 *Z1 = reinterpret_cast<const float4 *>(a.stage + ul * a.zs + a.zso);
+    const float2 *Zo = a.stage + ul * a.zs + 2 * a.zso;
+    const uint2 *dpos2 = reinterpret_cast<const uint2 *>(a.dpos);
+    constexpr int G = 4, NP = N / 2 + 1;  // bin pairs (2i, 2i+1); the pair (N, N+1) is padded
+    for (int i0 = tid; i0 < NP; i0 += G * T) {
+      float4 z0[G], z1[G];
+      uint2 dp[G];
 #pragma unroll
       for (int q = 0; q < G; ++q) {
-        const int b = min(b0 + q * T, N);
-        z0[q] = __ldcg(Z + b);
-        z1[q] = __ldcg(Z1 + b);
-        dp[q] = __ldg(a.dpos + b);
+        const int i = min(i0 + q * T, NP - 1);
+        z0[q] = __ldcg(Z0 + i);
+        z1[q] = __ldcg(Z1 + i);
+        dp[q] = __ldg(dpos2 + i);
       }
 #pragma unroll
       for (int q = 0; q < G; ++q) {
-        const int b = b0 + q * T;
-        if (b > N) continue;
-        float2 acc = cadd(z0[q], z1[q]);
-        if (dp[q]) {  // deep-overlap bin: overflow terms in order
-          const int st = dp[q] & 0xfffff, cnt = dp[q] >> 20;
-          for (int i = 0; i < cnt; ++i) acc = cadd(acc, __ldcg(Zo + st + i));
+        const int i = i0 + q * T;
+        if (i >= NP) continue;
+        float2 acc0 = make_float2(z0[q].x + z1[q].x, z0[q].y + z1[q].y);
+        float2 acc1 = make_float2(z0[q].z + z1[q].z, z0[q].w + z1[q].w);
+        if (dp[q].x | dp[q].y) {  // deep-overlap bins: overflow terms in order
+          for (int e = 0; e < (int)(dp[q].x >> 20); ++e)
+            acc0 = cadd(acc0, __ldcg(Zo + (dp[q].x & 0xfffff) + e));
+          for (int e = 0; e < (int)(dp[q].y >> 20); ++e)
+            acc1 = cadd(acc1, __ldcg(Zo + (dp[q].y & 0xfffff) + e));
         }
-        spec[padi(b)] = acc;
+        spec[padi(2 * i)] = acc0;
+        if (2 * i + 1 <= N) spec[padi(2 * i + 1)] = acc1;
       }
     }
   }
@@ -892,11 +899,15 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       if (!sflag[side]) continue;
       const int b = side == 0 ? bl : br;
       const int64_t mb = a.slice0 + b;  // boundary between global slices mb and mb+1
-      const float *h0p = bnd_row + (int64_t)b * 2 * trp;
-      const float *h1p = h0p + trp;
+      // the partner's half from the workspace, this CTA's own half recomputed from the frame
+      // (a + b is commutative in IEEE arithmetic: the sum does not depend on who is second)
+      const float *hp = bnd_row + ((int64_t)b * 2 + (side == 0 ? 0 : 1)) * trp;
 #pragma unroll 4
       for (int u = tid; u < a.tr - 1; u += T) {
-        const float val = __ldcg(h0p + u) + __ldcg(h1p + u);
+        // __fmul_rn: no contraction into an FMA with the add (the half must round as stored)
+        const float own = side == 0 ? __fmul_rn(fr[N - Bw + 1 + u], htab[Bw - 2 - u - A])
+                                    : __fmul_rn(fr[N + A + 1 + u], htab[u]);
+        const float val = __ldcg(hp + u) + own;
         const int64_t s = mb * N + A + 1 + u;
         if (a.circular) {
           const int64_t sw = s >= a.L ? s - a.L : s;

@@ -225,7 +225,7 @@ int configure_kernels(slicq_plan *p) {
           }
         }
       }
-    p->dpos.assign(N + 1, 0u);
+    p->dpos.assign(N + 2, 0u);  // N + 2: the kernels read bin pairs
     int64_t start = 0;
     for (int b = 0; b <= N; ++b) {
       if (first[b].first < 0)
