@@ -406,6 +406,12 @@ __device__ __noinline__ void inv_small(const float2 *in_row, float2 *reg, int nv
 #define SLICQ_SIZES(X) \
   X(1) X(2) X(3) X(4) X(5) X(6) X(8) X(9) X(10) X(12) X(15) X(16) X(18) X(20) X(24) X(25) X(27) X(30) X(32)
 
+#define SLICQ_PRAGMA_(x) _Pragma(#x)
+#define SLICQ_UNROLL(n) SLICQ_PRAGMA_(unroll n)
+#ifndef SLICQ_FOLD_UNROLL
+#define SLICQ_FOLD_UNROLL 4  // element loops of the channel kernels: loads in flight per lane
+#endif
+
 // ------------------------------------------------------------------ channel kernels
 // Persistent grid; a work item is (packet, tile of units), the CTA's warps split the units.
 // Defined in one translation unit only (kernels_host.cu).
@@ -469,7 +475,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArg
       for (int u = 0; u < nuu; ++u) {
         const float2 *Xu = X + (int64_t)u * a.xs;
         float2 *su = scr + u * P.ustride;
-#pragma unroll 4
+        SLICQ_UNROLL(SLICQ_FOLD_UNROLL)
         for (int e = lane; e < ne; e += 32) {
           const uint2 en = __ldg(ent + e);
           const float2 xv = Xu[en.x & 0x1ffff];
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
       for (int u = 0; u < nuu; ++u) {
         float2 *Zb = a.stage + (int64_t)(g0 + u) * a.zs;
         const float2 *su = scr + u * P.ustride;
-#pragma unroll 4
+        SLICQ_UNROLL(SLICQ_FOLD_UNROLL)
         for (int e = lane; e < ne; e += 32) {
           const uint2 en = __ldg(ent + e);
           const float2 f = cscale(su[en.x & 0x3fff], __uint_as_float(en.y & 0x7fffffffu));
@@ -609,25 +615,34 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
     constexpr int R = CF::F1, TASKS = N / R, PER = (TASKS + T - 1) / T;
     float *fr = reinterpret_cast<float *>(spec);
     const float *xr = a.x + row * a.x_stride;
-    const bool vec = ((reinterpret_cast<uintptr_t>(xr) & 7) == 0);
     const int64_t s0 = (mg - 1) * N - a.base_off;  // local x index of frame sample 0
+    const bool vec = ((reinterpret_cast<uintptr_t>(xr + s0) & 7) == 0);  // 8-byte pairs
     const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
     for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0 + N + A + 1 + u);
     // frame pairs q: samples 2q, 2q+1; window support |2q - N| < Bw for some sample
     const int q_lo = (N - Bw + 1) >> 1, q_hi = (N + Bw - 1) >> 1;  // inclusive
     float2 *fz = reinterpret_cast<float2 *>(fr);
-    for (int q = tid; q < N; q += T)
-      if (q < q_lo || q > q_hi) fz[q] = make_float2(0.f, 0.f);
+    for (int z = tid; z < q_lo + (N - 1 - q_hi); z += T)  // pairs outside [q_lo, q_hi]
+      fz[z < q_lo ? z : z + (q_hi + 1 - q_lo)] = make_float2(0.f, 0.f);
     // samples with frame index i map to x[s0 + i] (wrapped by L for slice 0); all of
     // a thread's loads are issued before any is used (HBM latency overlapped)
     {
       constexpr int MAXP = (N + T - 1) / T;
       float2 xv[MAXP];
+      // interior frames (no wrap, no signal edge, 8-byte aligned row): unchecked pair loads
+      const bool fast = vec && s0 + 2 * q_lo >= 0 && s0 + 2 * q_hi + 1 < a.x_len;
+      const float2 *xp = reinterpret_cast<const float2 *>(xr + (fast ? s0 : 0));
 #pragma unroll
       for (int k = 0; k < MAXP; ++k) {
         const int q = q_lo + tid + k * T;
         float x0 = 0.f, x1 = 0.f;
-        if (q <= q_hi) {
+        if (fast) {
+          if (q <= q_hi) {
+            const float2 t2 = __ldcs(xp + q);
+            x0 = t2.x;
+            x1 = t2.y;
+          }
+        } else if (q <= q_hi) {
           int64_t xi = s0 + 2 * q;
           if (a.wrap && xi < 0) xi += a.L;
           if (vec && xi >= 0 && xi + 1 < a.x_len) {

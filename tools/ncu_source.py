@@ -10,7 +10,10 @@ import sys
 
 rep, kname = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kname}",
+# kernel "name" or "name@i": the i-th matching launch (template variants share a base name)
+kname, _, idx = kname.partition("@")
+sel = ["-s", idx, "-c", "1"] if idx else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kname}", *sel,
                       "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 inst = collections.Counter()
