@@ -74,6 +74,8 @@ template <int LOGN>
 struct Big;
 #ifndef SLICQ_T13
 #define SLICQ_T13 256
+#endif
+#ifndef SLICQ_MINB13
 #define SLICQ_MINB13 2
 #endif
 // MINB = CTAs per SM the shared-memory budget is sized for (two slices in flight per SM
@@ -263,6 +265,20 @@ __device__ __forceinline__ void chan_twiddle(float2 (&v)[M1], int p2, int M, con
 // Programmatic dependent launch: kernels of a call are launched back to back; each waits for
 // its predecessor's memory before touching shared buffers and lets the next one launch
 // when its CTA is done (hides launch gaps, keeps stream order).
+// hide a pointer's derivation from the optimiser so that element accesses p[i] with a
+// 32-bit i compile to one IMAD.WIDE instead of re-associated 64-bit index arithmetic
+// plain global load (default caching), for pointers the compiler cannot classify
+__device__ __forceinline__ float2 ld_global(const float2 *p) {
+  float2 v;
+  asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+template <class P>
+__device__ __forceinline__ P *opaque(P *p) {
+  asm("" : "+l"(p));
+  return p;
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -325,7 +341,8 @@ __device__ __noinline__ void fwd_step2(const float2 *reg, float2 *out_row, int m
 }
 
 // Small forward packet: lane vc = u * nch + c (u < nu) owns channel c of unit u; element p
-// of its fold comes from the table entry p*32 + c (bin | conj << 17, weight; weight 0 for
+// of its fold comes from the table entry p*32 + c (bin, weight with the conjugation flag
+// as its sign; weight 0 for
 // zero padding) -- ent and X arrive offset by c and u.
 template <int M, int V>  // V: channel-kernel variant (separate register budgets)
 __device__ __noinline__ void fwd_small(const uint2 *ent, const float2 *X, float2 *out_row,
@@ -335,9 +352,9 @@ __device__ __noinline__ void fwd_small(const uint2 *ent, const float2 *X, float2
 #pragma unroll
   for (int p = 0; p < M; ++p) {
     const uint2 e = __ldg(ent + p * 32);
-    const float2 xv = X[e.x & 0x1ffff];
-    const float gv = __uint_as_float(e.y);
-    v[p] = make_float2(xv.x * gv, ((e.x >> 17) & 1) ? -xv.y * gv : xv.y * gv);
+    const float2 xv = X[e.x];
+    const float gv = __uint_as_float(e.y);  // sign bit: conjugate X (g >= 0)
+    v[p] = make_float2(xv.x * fabsf(gv), xv.y * gv);
   }
   dft<M, +1>(v);
   float2 *o = out_row + off_lane;
@@ -408,6 +425,9 @@ __device__ __noinline__ void inv_small(const float2 *in_row, float2 *reg, int nv
 
 #define SLICQ_PRAGMA_(x) _Pragma(#x)
 #define SLICQ_UNROLL(n) SLICQ_PRAGMA_(unroll n)
+#ifndef SLICQ_XLOAD
+#define SLICQ_XLOAD __ldg  // fold reads of the staged spectra (prefetched to L2)
+#endif
 #ifndef SLICQ_FOLD_UNROLL
 #define SLICQ_FOLD_UNROLL 4  // element loops of the channel kernels: loads in flight per lane
 #endif
@@ -473,14 +493,14 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArg
       }
       // F3 fold from the element table (coalesced over e; positions conflict-free)
       for (int u = 0; u < nuu; ++u) {
-        const float2 *Xu = X + (int64_t)u * a.xs;
+        const float2 *Xu = opaque(X + (int64_t)u * a.xs);  // 32-bit indexing off one base
         float2 *su = scr + u * P.ustride;
         SLICQ_UNROLL(SLICQ_FOLD_UNROLL)
         for (int e = lane; e < ne; e += 32) {
           const uint2 en = __ldg(ent + e);
-          const float2 xv = Xu[en.x & 0x1ffff];
-          const float gv = __uint_as_float(en.y);
-          su[en.x >> 18] = make_float2(xv.x * gv, ((en.x >> 17) & 1) ? -xv.y * gv : xv.y * gv);
+          const float2 xv = SLICQ_XLOAD(Xu + (en.x & 0x3ffff));
+          const float gv = __uint_as_float(en.y);  // sign bit: conjugate X (g >= 0)
+          su[en.x >> 18] = make_float2(xv.x * fabsf(gv), xv.y * gv);
         }
       }
       __syncwarp();
@@ -570,13 +590,14 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
       // I3a terms F[q] * g~_k[j]/sqrt(M_k) (conjugated for mirrored bins) -> their slot of
       // the unit's half-spectrum staging (I3b sums the slots)
       for (int u = 0; u < nuu; ++u) {
-        float2 *Zb = a.stage + (int64_t)(g0 + u) * a.zs;
+        float2 *Zb = opaque(a.stage + (int64_t)(g0 + u) * a.zs);  // 32-bit indexing
         const float2 *su = scr + u * P.ustride;
         SLICQ_UNROLL(SLICQ_FOLD_UNROLL)
         for (int e = lane; e < ne; e += 32) {
           const uint2 en = __ldg(ent + e);
-          const float2 f = cscale(su[en.x & 0x3fff], __uint_as_float(en.y & 0x7fffffffu));
-          __stcg(Zb + (en.x >> 14), make_float2(f.x, (en.y >> 31) ? -f.y : f.y));
+          const float2 f = su[en.x & 0x3fff];
+          const float w = __uint_as_float(en.y);  // sign bit: conjugate the term (g~ >= 0)
+          __stcg(Zb + (en.x >> 14), make_float2(f.x * fabsf(w), f.y * w));
         }
       }
       __syncwarp();
@@ -607,90 +628,68 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
   pdl_wait();  // the staging buffer may still be read by the previous chunk's kernel
 
-  // ---- F1: the Tukey-windowed frame f^m[i], i in [0, 2N), is staged as a plain float
-  // array in the spectrum buffer (z[p] = (f[2p], f[2p+1]) is then its float2 view):
-  // zero-window samples are stored as zeros without loading, the nonzero window
-  // (N - Bw, N + Bw) is read from HBM as aligned float2 pairs, coalesced across threads.
+  // ---- F1 + first radix pass straight from HBM: task j takes the frame pairs
+  // z[q] = (f[2q], f[2q+1]), q = j + r N/R, of the Tukey-windowed frame f^m[i] = x[s0 + i]
+  // h_0[i - N] (wrapped by L for slice 0).  Zero-window pairs are not loaded; all of
+  // a thread's loads are issued before any is used (HBM latency overlapped with the window
+  // table staging); the window multiplies only the transitions (h_0 = 1 on the flat top).
   {
     constexpr int R = CF::F1, TASKS = N / R, PER = (TASKS + T - 1) / T;
-    float *fr = reinterpret_cast<float *>(spec);
     const float *xr = a.x + row * a.x_stride;
     const int64_t s0 = (mg - 1) * N - a.base_off;  // local x index of frame sample 0
     const bool vec = ((reinterpret_cast<uintptr_t>(xr + s0) & 7) == 0);  // 8-byte pairs
     const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
     for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0 + N + A + 1 + u);
-    // frame pairs q: samples 2q, 2q+1; window support |2q - N| < Bw for some sample
+    // window support: pairs q_lo..q_hi hold at least one nonzero-window sample
     const int q_lo = (N - Bw + 1) >> 1, q_hi = (N + Bw - 1) >> 1;  // inclusive
-    float2 *fz = reinterpret_cast<float2 *>(fr);
-    for (int z = tid; z < q_lo + (N - 1 - q_hi); z += T)  // pairs outside [q_lo, q_hi]
-      fz[z < q_lo ? z : z + (q_hi + 1 - q_lo)] = make_float2(0.f, 0.f);
-    // samples with frame index i map to x[s0 + i] (wrapped by L for slice 0); all of
-    // a thread's loads are issued before any is used (HBM latency overlapped)
-    {
-      constexpr int MAXP = (N + T - 1) / T;
-      float2 xv[MAXP];
-      // interior frames (no wrap, no signal edge, 8-byte aligned row): unchecked pair loads
-      const bool fast = vec && s0 + 2 * q_lo >= 0 && s0 + 2 * q_hi + 1 < a.x_len;
-      const float2 *xp = reinterpret_cast<const float2 *>(xr + (fast ? s0 : 0));
-#pragma unroll
-      for (int k = 0; k < MAXP; ++k) {
-        const int q = q_lo + tid + k * T;
-        float x0 = 0.f, x1 = 0.f;
-        if (fast) {
-          if (q <= q_hi) {
-            const float2 t2 = __ldcs(xp + q);
-            x0 = t2.x;
-            x1 = t2.y;
-          }
-        } else if (q <= q_hi) {
-          int64_t xi = s0 + 2 * q;
-          if (a.wrap && xi < 0) xi += a.L;
-          if (vec && xi >= 0 && xi + 1 < a.x_len) {
-            const float2 t2 = __ldcs(reinterpret_cast<const float2 *>(xr + xi));
-            x0 = t2.x;
-            x1 = t2.y;
-          } else {
-            if (xi >= 0 && xi < a.x_len) x0 = __ldg(xr + xi);
-            if (xi + 1 >= 0 && xi + 1 < a.x_len) x1 = __ldg(xr + xi + 1);
-          }
-        }
-        xv[k] = make_float2(x0, x1);
-      }
-#pragma unroll
-      for (int k = 0; k < MAXP; ++k) {
-        const int q = q_lo + tid + k * T;
-        if (q <= q_hi) fz[q] = xv[k];
-      }
-    }
-    __syncthreads();  // raw samples and window table staged
-    // window: only the transitions need a multiply (h_0 = 1 on the flat top)
-    for (int u = tid; u < 2 * (a.tr - 1); u += T) {
-      const int side = u >= a.tr - 1;
-      const int d = side ? u - (a.tr - 1) : u;  // |t| = A + 1 + d
-      const int i = side ? N + A + 1 + d : N - A - 1 - d;
-      fr[i] *= htab[d];
-    }
-    for (int q = tid; q < 2; q += T) {  // zero-window samples inside the boundary pairs
-      const int i = q == 0 ? N - Bw : N + Bw;
-      if (i >= 0 && i < 2 * N) fr[i] = 0.f;
-    }
-    __syncthreads();
-    // first radix pass from the staged frame (unpadded), written back padded
+    // interior frames (no wrap, no signal edge, 8-byte aligned row): unchecked pair loads
+    const bool fast = vec && s0 + 2 * q_lo >= 0 && s0 + 2 * q_hi + 1 < a.x_len;
+    const float2 *xp = reinterpret_cast<const float2 *>(xr + (fast ? s0 : 0));
     float2 v[PER][R];
 #pragma unroll
     for (int qq = 0; qq < PER; ++qq) {
       const int j = tid + qq * T;
-      if (TASKS % T == 0 || j < TASKS) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[qq][r] = fz[j + r * TASKS];
-        dft<R, -1>(v[qq]);
+      for (int r = 0; r < R; ++r) {
+        const int q = j + r * TASKS;
+        float x0 = 0.f, x1 = 0.f;
+        if ((TASKS % T == 0 || j < TASKS) && q >= q_lo && q <= q_hi) {
+          if (fast) {
+            const float2 t2 = __ldcs(xp + q);
+            x0 = t2.x;
+            x1 = t2.y;
+          } else {
+            int64_t xi = s0 + 2 * q;
+            if (a.wrap && xi < 0) xi += a.L;
+            if (vec && xi >= 0 && xi + 1 < a.x_len) {
+              const float2 t2 = __ldcs(reinterpret_cast<const float2 *>(xr + xi));
+              x0 = t2.x;
+              x1 = t2.y;
+            } else {
+              if (xi >= 0 && xi < a.x_len) x0 = __ldg(xr + xi);
+              if (xi + 1 >= 0 && xi + 1 < a.x_len) x1 = __ldg(xr + xi + 1);
+            }
+          }
+        }
+        v[qq][r] = make_float2(x0, x1);
       }
     }
-    __syncthreads();
+    __syncthreads();  // window table staged (and twiddles)
+    const int qa = (N - A + 1) >> 1, qb = (N + A - 1) >> 1;  // pairs with |t| <= A for both
 #pragma unroll
     for (int qq = 0; qq < PER; ++qq) {
       const int j = tid + qq * T;
       if (TASKS % T == 0 || j < TASKS) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int q = j + r * TASKS;
+          if (q >= qa && q <= qb) continue;  // both samples on the flat top (h_0 = 1)
+          // |t| of the two samples (t = 2q - N and 2q + 1 - N); h_0 = 1 for |t| <= A
+          const int t0 = abs(2 * q - N), t1 = abs(2 * q + 1 - N);
+          if (t0 > A) v[qq][r].x = t0 < Bw ? v[qq][r].x * htab[t0 - A - 1] : 0.f;
+          if (t1 > A) v[qq][r].y = t1 < Bw ? v[qq][r].y * htab[t1 - A - 1] : 0.f;
+        }
+        dft<R, -1>(v[qq]);
 #pragma unroll
         for (int r = 0; r < R; ++r) spec[padi(j * R + r)] = v[qq][r];
       }

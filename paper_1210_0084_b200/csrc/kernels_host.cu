@@ -261,6 +261,8 @@ int configure_kernels(slicq_plan *p) {
     std::memcpy(&u, &f, 4);
     return u;
   };
+  for (double gv : p->g)  // the element tables carry the conjugation flag in the sign bit
+    if (!(gv >= 0.0)) return set_error(SLICQ_EUNSUPPORTED, "negative filter value");
   p->packets.clear();
   p->pchans.clear();
   p->fent.clear();
@@ -275,7 +277,8 @@ int configure_kernels(slicq_plan *p) {
     d.fent_off = (int)p->fent.size();
     d.ient_off = (int)p->ient.size();
     const double sc = 1.0 / std::sqrt((double)M);  // Alg. 1 sqrt(M) IFFT (1/M); Alg. 2 FFT/sqrt(M)
-    // forward fold table (weight 0 and bin 0 for the zero padding)
+    // forward fold table: bin | scratch position << 18, weight g_k/sqrt(M_k) whose sign bit
+    // marks the conjugated (mirrored) bins (g >= 0); weight 0 and bin 0 for the zero padding
     if (small) {
       std::vector<uint2> t(32 * M, make_uint2(0u, 0u));
       for (int c = 0; c < d.nch; ++c) {
@@ -287,8 +290,8 @@ int configure_kernels(slicq_plan *p) {
           if (dd >= p->len[k]) continue;
           int conj = 0;
           const int b = bin_of(p->lo[k] + dd, conj);
-          t[q * 32 + c] = make_uint2((uint32_t)b | ((uint32_t)conj << 17),
-                                     fbits(p->g[p->goff[k] + dd] * sc));
+          t[q * 32 + c] = make_uint2((uint32_t)b, fbits(conj ? -(p->g[p->goff[k] + dd] * sc)
+                                                          : p->g[p->goff[k] + dd] * sc));
         }
       }
       p->fent.insert(p->fent.end(), t.begin(), t.end());
@@ -304,8 +307,8 @@ int configure_kernels(slicq_plan *p) {
           if (dd < p->len[k]) {
             int conj = 0;
             const int b = bin_of(p->lo[k] + dd, conj);
-            e = make_uint2((uint32_t)b | ((uint32_t)conj << 17) | (pos << 18),
-                           fbits(p->g[p->goff[k] + dd] * sc));
+            const double w = p->g[p->goff[k] + dd] * sc;
+            e = make_uint2((uint32_t)b | (pos << 18), fbits(conj ? -w : w));
           }
           p->fent.push_back(e);
         }
@@ -365,6 +368,7 @@ int configure_kernels(slicq_plan *p) {
     kc.zs += p->N;
   }
   kc.tile = (int)std::max<int64_t>(1, env_int("SLICQ_TILE", 128));
+  kc.chan_per_sm = (int)env_int("SLICQ_CHAN_PER_SM", 0);  // dev override: 0 = occupancy
   const int64_t per_unit = sizeof(float2) * std::max(kc.xs, kc.zs);
   const int64_t budget = env_int("SLICQ_STAGE_MB", 48) << 20;
   int64_t cu = env_int("SLICQ_CHUNK_UNITS", int64_t(1) << 40);  // default: no chunking
@@ -572,6 +576,7 @@ static unsigned chan_grid(const slicq_plan *p, const KArgs &a, ChanFn fn) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, CHAN_T, p->kc.chan_smem) ==
           cudaSuccess && occ > 0)
     per_sm = occ;
+  if (p->kc.chan_per_sm > 0) per_sm = std::min(per_sm, p->kc.chan_per_sm);
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)per_sm * nsm));
 }
 

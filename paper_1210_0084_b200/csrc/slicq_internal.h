@@ -69,6 +69,7 @@ struct KernelConfig {
   int64_t toff_f = 0, toff_i = 0;  // offsets of the four-step intermediate in a unit
   int64_t chunk_units = 0;    // units per chunk (staging is sized for one chunk)
   int tile = 16;              // units per channel-kernel tile
+  int chan_per_sm = 0;        // channel-kernel CTAs per SM cap (0: occupancy)
 };
 
 }  // namespace slicq
