@@ -36,6 +36,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "sliCQ fwd+inv input samples/s"
 UNIT = "samples/s"
+E2E_PIECES = 32  # slice ranges of the end-to-end (host-to-host) pipeline
 
 
 def _env_rank():
@@ -298,12 +299,12 @@ def run_gpu(args, cfg):
         xh = torch.from_numpy(x_np).pin_memory()
         yh = torch.empty((B, n), dtype=torch.float32).pin_memory()
         ke = max(2, min(args.steps, 5))
-        api.process_host(plan, xh, yh, pieces=16)
+        api.process_host(plan, xh, yh, pieces=E2E_PIECES)
         torch.cuda.synchronize()
         a0, a1 = ev(), ev()
         a0.record(stream)
         for _ in range(ke):
-            api.process_host(plan, xh, yh, pieces=16)
+            api.process_host(plan, xh, yh, pieces=E2E_PIECES)
         a1.record(stream)
         torch.cuda.synchronize()
         ms_e2e = a0.elapsed_time(a1) / ke
@@ -311,7 +312,7 @@ def run_gpu(args, cfg):
         e2e = {"value": samples / (ms_e2e / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": 4 * B * n, "d2h_bytes_per_step": 4 * B * n,
                "ms_per_step": ms_e2e, "recon_rel_l2": e2e_err,
-               "api": "paper_1210_0084_b200.api.process_host (16 slice ranges, 3 streams)"}
+               "api": f"paper_1210_0084_b200.api.process_host -> slicq_process_host (native executor, {E2E_PIECES} slice ranges, 3 streams)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -182,6 +182,34 @@ SLICQ_API int slicq_inverse_range(const slicq_plan *p, const slicq_c32 *coeffs_l
 SLICQ_API int slicq_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,
                       int64_t batch, void *stream);
 
+/* ------------------------------------------------------------------ streaming executor
+ * slicq_process_host: host-to-host round trip y = inverse(fn(forward(x))) of a long signal,
+ * pipelined over `pieces` contiguous slice ranges (native executor, csrc/stream_exec.cpp):
+ * per range a host -> device copy of its samples plus the left halo (circular for the first
+ * range), slicq_forward_range, the optional hook, slicq_inverse_range, the
+ * overlap-add of its left spill into the previous range (slicq_overlap_add), and a device
+ * -> host copy of the completed range, on three streams forked from `stream` so that the
+ * copies of one range overlap the kernels of another.  The arithmetic is exactly that of
+ * slicq_forward + slicq_inverse.
+ *   x_host, y_host  host float32 [batch][n] (pinned for overlap; pageable works, slower);
+ *                   y_host is fully overwritten
+ *   fn (may be NULL) is called on the host while the work is being enqueued, once per
+ *     range, with the device coefficients [batch][nslices][C] of slices [slice0,
+ *     slice0 + nslices) and the stream its device work must be enqueued on (in-place
+ *     coefficient processing, e.g. masking); a nonzero return aborts with SLICQ_EINVAL
+ *   ws  device, >= slicq_process_host_workspace_bytes(p, n, batch, pieces) bytes,
+ *       256-byte aligned, zero-filled before its first use (a ring of 4 range buffers;
+ *       its size does not grow with n beyond one range)
+ * Asynchronous with respect to the host: synchronise `stream` before reading y_host.
+ * One call per workspace at a time. */
+typedef int (*slicq_coeff_fn)(void *user, slicq_c32 *coeffs, int64_t slice0, int64_t nslices,
+                              int64_t batch, void *stream);
+SLICQ_API size_t slicq_process_host_workspace_bytes(const slicq_plan *p, int64_t n, int64_t batch,
+                                                    int pieces);
+SLICQ_API int slicq_process_host(const slicq_plan *p, const float *x_host, float *y_host, int64_t n,
+                                 int64_t batch, int pieces, slicq_coeff_fn fn, void *user, void *ws,
+                                 size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,6 +29,8 @@ SIGNATURES = {
     "slicq_halo": (_i64, [_p]),
     "slicq_workspace_bytes": (_sz, [_p, _i64, _i64]),
     "slicq_kernel_launches": (_i32, [_p, _i32, _i64, _i64]),
+    "slicq_process_host_workspace_bytes": (_sz, [_p, _i64, _i64, _i32]),
+    "slicq_process_host": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p, _p, _p, _sz, _p]),
     "slicq_plan_export": (_i32, [_p, _p, _p, _p, _p, _p, _p, _p]),
     "slicq_filter_total_length": (_i64, [_p]),
     "slicq_last_error": (C.c_char_p, []),
@@ -71,3 +73,6 @@ def check(rc: int, where: str) -> int:
     if rc < 0:
         raise SlicqError(rc, where)
     return rc
+
+# slicq_coeff_fn(user, coeffs, slice0, nslices, batch, stream) -> int
+COEFF_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p)

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import check, lib
+from ._lib import COEFF_FN, check, lib
 
 
 def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> Optional[int]:
@@ -243,90 +243,61 @@ def plan_for_config(cfg) -> Plan:
                 cfg.rasterize)
 
 
-def process_host(plan: Plan, x_host: torch.Tensor, y_host: Optional[torch.Tensor] = None,
-                 fn=None, pieces: int = 8, device=None) -> torch.Tensor:
-    """Host-to-host sliCQ round trip of a (long) signal, pipelined over slice ranges.
+class _DeviceView:
+    """__cuda_array_interface__ view of library-owned device memory (no copy)."""
 
-    x_host: pinned float32 [batch][n] (CPU).  The S slices are cut into `pieces` contiguous
-    ranges; for each range the input (plus its left halo, circular for range 0) is
-    copied host->device on one stream, slicq_forward_range / optional `fn(coeffs_local,
-    slice0)` (in-place coefficient processing on the device) / slicq_inverse_range run on a
-    second stream, and the synthesised samples go device->host on a third stream as soon as
-    the right neighbour's overlap-add spill has been added (slicq_overlap_add).  Copies of
-    range r+1 / r-1 overlap the kernels of range r.  Returns y_host [batch][n].
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 2}
+
+
+def process_host(plan: Plan, x_host: torch.Tensor, y_host: Optional[torch.Tensor] = None,
+                 fn=None, pieces: int = 32, device=None) -> torch.Tensor:
+    """Host-to-host sliCQ round trip of a (long) signal: slicq_process_host, the library's
+    native streaming executor (csrc/stream_exec.cpp), pipelined over `pieces` slice ranges
+    on three streams so host<->device copies overlap the kernels.
+
+    x_host: float32 [batch][n] CPU tensor (pinned for overlap).  fn(coeffs, slice0), if
+    given, is called once per range with a torch view of that range's device coefficients
+    [batch][nslices][C] under the stream it must enqueue its work on (in-place processing).
+    Returns y_host [batch][n]; asynchronous: synchronise the current stream before use.
     The arithmetic is exactly that of slicq_forward + slicq_inverse (same kernels)."""
     if x_host.dim() == 1:
         x_host = x_host[None]
-    if x_host.is_cuda or x_host.dtype != torch.float32:
-        raise ValueError("x_host must be a float32 CPU tensor (pinned for overlap)")
+    if x_host.is_cuda or x_host.dtype != torch.float32 or not x_host.is_contiguous():
+        raise ValueError("x_host must be a contiguous float32 CPU tensor (pinned for overlap)")
     B, n = x_host.shape
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
     if y_host is None:
         y_host = torch.empty((B, n), dtype=torch.float32, pin_memory=True)
-    N, halo = plan.N, plan.halo
-    S = plan.num_slices(n)
-    L = S * N
-    P = max(1, min(pieces, S // 2))
-    bounds = [r * S // P for r in range(P + 1)]
-    C = plan.coeffs_per_slice
-    st_in, st_k, st_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    cur = torch.cuda.current_stream(dev)
-    for s_ in (st_in, st_k, st_out):
-        s_.wait_stream(cur)
-    xl, co, yl, sp, ev_in, ev_inv = [], [], [], [], [], []
-    for r in range(P):
-        ns = bounds[r + 1] - bounds[r]
-        xl.append(torch.empty((B, halo + ns * N), dtype=torch.float32, device=dev))
-        co.append(torch.empty((B, ns, C), dtype=torch.complex64, device=dev))
-        yl.append(torch.empty((B, ns * N), dtype=torch.float32, device=dev))
-        sp.append(torch.empty((B, halo), dtype=torch.float32, device=dev))
-        ev_in.append(torch.cuda.Event())
-        ev_inv.append(torch.cuda.Event())
+    elif y_host.is_cuda or y_host.dtype != torch.float32 or tuple(y_host.shape) != (B, n) \
+            or not y_host.is_contiguous():
+        raise ValueError("y_host must be a contiguous float32 CPU tensor of x_host's shape")
+    key = (str(dev), "process_host", n, B, pieces)
+    ws = plan._ws.get(key)
+    if ws is None:
+        nb = int(lib().slicq_process_host_workspace_bytes(plan._h, n, B, pieces))
+        if nb == 0:
+            raise ValueError("slicq_process_host_workspace_bytes: invalid arguments")
+        ws = torch.zeros((nb + 15) // 16 * 4, dtype=torch.float32, device=dev)
+        plan._ws[key] = ws
+    cb = None
+    if fn is not None:
+        C_ = plan.coeffs_per_slice
 
-    def copy_in(dst, a, b):  # global samples [a, b) (circular, zero beyond n) -> dst[:, :b-a]
-        pos, o = a, 0
-        while pos < b:
-            g = pos % L
-            seg = min(b - pos, L - g)
-            hi = min(g + seg, n)
-            if hi > g:
-                dst[:, o:o + hi - g].copy_(x_host[:, g:hi], non_blocking=True)
-            if g + seg > max(g, n):
-                dst[:, o + max(hi - g, 0):o + seg].zero_()
-            pos += seg
-            o += seg
-
-    def copy_out(r):
-        a = bounds[r] * N
-        hi = min(bounds[r + 1] * N, n)
-        if hi > a:
-            y_host[:, a:hi].copy_(yl[r][:, :hi - a], non_blocking=True)
-
-    with torch.cuda.stream(st_in):
-        for r in range(P):
-            copy_in(xl[r], bounds[r] * N - halo, bounds[r + 1] * N)
-            ev_in[r].record(st_in)
-    ev_out = [torch.cuda.Event() for _ in range(P)]
-    with torch.cuda.stream(st_k):
-        for r in range(P):
-            s0, ns = bounds[r], bounds[r + 1] - bounds[r]
-            st_k.wait_event(ev_in[r])
-            plan.forward_range(xl[r], halo, s0, ns, S, out=co[r], stream=st_k)
-            if fn is not None:
-                fn(co[r], s0)
-            plan.inverse_range(co[r], s0, ns, S, halo, y_local=yl[r], spill=sp[r], stream=st_k)
-            if r > 0:  # range r's spill completes range r-1's tail
-                Plan.overlap_add(yl[r - 1][:, -halo:], sp[r], stream=st_k)
-                ev_out[r - 1].record(st_k)
-        Plan.overlap_add(yl[P - 1][:, -halo:], sp[0], stream=st_k)  # circular wrap
-        ev_out[P - 1].record(st_k)
-    with torch.cuda.stream(st_out):
-        for r in range(P):
-            st_out.wait_event(ev_out[r])
-            copy_out(r)
-    for s_ in (st_in, st_k, st_out):
-        cur.wait_stream(s_)
-    # keep the buffers alive until the work is done
-    for t in xl + co + yl + sp:
-        t.record_stream(cur)
+        def _hook(user, ptr, slice0, nslices, batch, stream):
+            try:
+                t = torch.as_tensor(_DeviceView(ptr, (batch, nslices, C_), "<c8"), device=dev)
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=dev)):
+                    fn(t, int(slice0))
+                return 0
+            except Exception:  # reported through the library's error path
+                import traceback
+                traceback.print_exc()
+                return 1
+        cb = COEFF_FN(_hook)
+    with torch.cuda.device(dev):
+        check(lib().slicq_process_host(plan._h, x_host.data_ptr(), y_host.data_ptr(), n, B,
+                                       int(pieces), cb, None, ws.data_ptr(), ws.numel() * 4,
+                                       _stream_ptr(None)), "slicq_process_host")
     return y_host

@@ -561,8 +561,8 @@ static int check_device(const slicq_plan *p) {
   return SLICQ_OK;
 }
 
-// persistent channel-kernel grid: resident CTAs per SM, capped by the work items
-static unsigned chan_grid(const slicq_plan *p, const KArgs &a, ChanFn fn) {
+// persistent channel-kernel grid: resident CTAs (occupancy x SMs), capped by the work items
+static int64_t chan_capacity(const slicq_plan *p, ChanFn fn) {
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -570,14 +570,13 @@ static unsigned chan_grid(const slicq_plan *p, const KArgs &a, ChanFn fn) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  const int64_t items = (int64_t)a.npackets * ((a.nunits + a.tile - 1) / a.tile);
   int per_sm = 2;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, CHAN_T, p->kc.chan_smem) ==
           cudaSuccess && occ > 0)
     per_sm = occ;
   if (p->kc.chan_per_sm > 0) per_sm = std::min(per_sm, p->kc.chan_per_sm);
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)per_sm * nsm));
+  return (int64_t)per_sm * nsm;
 }
 
 // the channel kernels of one direction: lite packets [0, nlite), then the full variant
@@ -589,8 +588,15 @@ static cudaError_t launch_chan(bool fwd, const slicq_plan *p, KArgs a, cudaStrea
     a.npackets = lite ? nl : np - nl;
     if (a.npackets == 0) continue;
     const ChanFn fn = chan_fn(fwd, lite);
+    // small calls (e.g. the ranges of the streaming executor): shrink the tile until there
+    // are >= 4 work items per resident CTA (load balance of the persistent grid)
+    const int64_t cap = chan_capacity(p, fn);
+    a.tile = p->kc.tile;
+    while (a.tile > 8 && (int64_t)a.npackets * ((a.nunits + a.tile - 1) / a.tile) < 4 * cap)
+      a.tile /= 2;
+    const int64_t items = (int64_t)a.npackets * ((a.nunits + a.tile - 1) / a.tile);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(chan_grid(p, a, fn));
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(items, cap)));
     cfg.blockDim = dim3(CHAN_T);
     cfg.dynamicSmemBytes = p->kc.chan_smem;
     cfg.stream = s;
