@@ -754,65 +754,150 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
   pdl_wait();  // contributions of this chunk come from the channel kernel
   prefetch_l2(a.stage + ul * a.zs, a.zs * 8, tid, T);
 
-  // ---- I3b: half-spectrum bin b = slot0[b] + slot1[b] (+ its overflow run, rare); two
-  // bins per thread and load (16-byte), 4 pairs in flight
-  {
-    const float4 *Z0 = reinterpret_cast<const float4 *>(a.stage + ul * a.zs);
-    const float4 *Z1 = reinterpret_cast<const float4 *>(a.stage + ul * a.zs + a.zso);
-    const float2 *Zo = a.stage + ul * a.zs + 2 * a.zso;
-    const uint2 *dpos2 = reinterpret_cast<const uint2 *>(a.dpos);
-    constexpr int G = 4, NP = N / 2 + 1;  // bin pairs (2i, 2i+1); the pair (N, N+1) is padded
-    for (int i0 = tid; i0 < NP; i0 += G * T) {
-      float4 z0[G], z1[G];
-      uint2 dp[G];
+  constexpr int R1 = CF::I1, TASKS1 = N / R1;
+  if constexpr (R1 == 16 && TASKS1 == 2 * T) {
+    // ---- I3b + I4a + first radix-16 pass, fused in registers: thread t owns the pass-1
+    // tasks jA = t and jB = TASKS1 - t (t = 0: tasks 0 and TASKS1/2), whose inputs
+    // Z[k], k = j + TASKS1 r, pair up as mirrors: N - (jA + TASKS1 r) = jB + TASKS1 (15 - r),
+    // so every half-spectrum bin H[b] = slot0[b] + slot1[b] (+ overflow) is loaded once
+    // and the c2r packing Z[k] = E + iO, E = (H[k] + conj H[N-k])/2,
+    // O = (H[k] - conj H[N-k]) e^{+i pi k/N} / 2, happens in registers.
+    const float2 *Z0 = a.stage + ul * a.zs;
+    const float2 *Z1 = Z0 + a.zso, *Zo = Z0 + 2 * a.zso;
+    const int jA = tid, jB = tid == 0 ? TASKS1 / 2 : TASKS1 - tid;
+    // e^{+i pi k / N} from the global two-level table (no wait for the shared copy)
+    auto wk = [&](int k) {
+      return cconj(cmul(__ldg(a.tw2n + 64 + (k >> 6)), __ldg(a.tw2n + (k & 63))));
+    };
+    // c2r packing of the pair (k, N - k): Z[k] = E + iO, Z[N-k] = conj(E) + i conj(D) conj(w)
+    auto pack = [&](float2 &hk, float2 &hn, int k) {
+      const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
+      const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+      const float2 w = wk(k);
+      const float2 O = cmul(D, w), O2 = cmul(cconj(D), cconj(w));
+      hk = make_float2(E.x - O.y, E.y + O.x);
+      hn = make_float2(E.x - O2.y, -E.y + O2.x);
+    };
+    // H at the thread's 32 bins jA + TASKS1 r (vA) and jB + TASKS1 r (vB): 4 r per batch,
+    // all 16 slot loads and 8 overflow descriptors of a batch in flight together
+    float2 vA[16], vB[16];
 #pragma unroll
-      for (int q = 0; q < G; ++q) {
-        const int i = min(i0 + q * T, NP - 1);
-        z0[q] = __ldcg(Z0 + i);
-        z1[q] = __ldcg(Z1 + i);
-        dp[q] = __ldg(dpos2 + i);
+    for (int r0 = 0; r0 < 16; r0 += 4) {
+      float2 a0[4], a1[4], b0[4], b1[4];
+      uint32_t da[4], db[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ka = jA + TASKS1 * (r0 + q), kb = jB + TASKS1 * (r0 + q);
+        a0[q] = __ldcg(Z0 + ka);
+        a1[q] = __ldcg(Z1 + ka);
+        b0[q] = __ldcg(Z0 + kb);
+        b1[q] = __ldcg(Z1 + kb);
+        da[q] = __ldg(a.dpos + ka);
+        db[q] = __ldg(a.dpos + kb);
       }
 #pragma unroll
-      for (int q = 0; q < G; ++q) {
-        const int i = i0 + q * T;
-        if (i >= NP) continue;
-        float2 acc0 = make_float2(z0[q].x + z1[q].x, z0[q].y + z1[q].y);
-        float2 acc1 = make_float2(z0[q].z + z1[q].z, z0[q].w + z1[q].w);
-        if (dp[q].x | dp[q].y) {  // deep-overlap bins: overflow terms in order
-          for (int e = 0; e < (int)(dp[q].x >> 20); ++e)
-            acc0 = cadd(acc0, __ldcg(Zo + (dp[q].x & 0xfffff) + e));
-          for (int e = 0; e < (int)(dp[q].y >> 20); ++e)
-            acc1 = cadd(acc1, __ldcg(Zo + (dp[q].y & 0xfffff) + e));
+      for (int q = 0; q < 4; ++q) {
+        vA[r0 + q] = cadd(a0[q], a1[q]);
+        vB[r0 + q] = cadd(b0[q], b1[q]);
+        if (da[q] | db[q]) {  // deep-overlap bins: overflow terms in order
+          for (int e = 0; e < (int)(da[q] >> 20); ++e)
+            vA[r0 + q] = cadd(vA[r0 + q], __ldcg(Zo + (da[q] & 0xfffff) + e));
+          for (int e = 0; e < (int)(db[q] >> 20); ++e)
+            vB[r0 + q] = cadd(vB[r0 + q], __ldcg(Zo + (db[q] & 0xfffff) + e));
         }
-        spec[padi(2 * i)] = acc0;
-        if (2 * i + 1 <= N) spec[padi(2 * i + 1)] = acc1;
       }
     }
-  }
-  __syncthreads();
-  PHASE_MARK(1, 0);
-
-  // ---- I4a: c2r packing  Z[k] = E[k] + i O[k],
-  //   E = (H[k] + conj H[N-k])/2,  O = (H[k] - conj H[N-k]) e^{+i pi k/N} / 2
-  for (int k = tid; k <= N / 2; k += T) {
-    const float2 hk = spec[padi(k)];
-    const float2 hn = spec[padi(N - k)];
-    const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
-    const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
-    const float2 w = cconj(tw_lookup(tw, k));  // e^{+i pi k/N}
-    const float2 O = cmul(D, w);
-    spec[padi(k)] = make_float2(E.x - O.y, E.y + O.x);  // E + iO
-    if (k != 0 && k != N / 2) {
-      // pair N-k: E' = conj(E), O' = conj(D) e^{-i pi k/N}
-      const float2 O2 = cmul(cconj(D), cconj(w));
-      spec[padi(N - k)] = make_float2(E.x - O2.y, -E.y + O2.x);  // conj(E) + i O'
+    if (tid != 0) {
+      // N - (jA + TASKS1 r) = jB + TASKS1 (15 - r)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) pack(vA[r], vB[15 - r], jA + TASKS1 * r);
+    } else {
+      // task 0: bins TASKS1 r pair as (r, 16 - r), r = 8 is N/2, r = 0 pairs with bin N;
+      // task TASKS1/2: bins TASKS1/2 + TASKS1 r pair as (r, 15 - r)
+      float2 hN = cadd(__ldcg(Z0 + N), __ldcg(Z1 + N));
+      {
+        const uint32_t dN = __ldg(a.dpos + N);
+        for (int e = 0; e < (int)(dN >> 20); ++e) hN = cadd(hN, __ldcg(Zo + (dN & 0xfffff) + e));
+      }
+      pack(vA[0], hN, 0);
+#pragma unroll
+      for (int r = 1; r < 8; ++r) pack(vA[r], vA[16 - r], TASKS1 * r);
+      {
+        float2 m = vA[8];
+        pack(vA[8], m, N / 2);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) pack(vB[r], vB[15 - r], TASKS1 / 2 + TASKS1 * r);
     }
-  }
-  __syncthreads();
+    dft<16, +1>(vA);
+    dft<16, +1>(vB);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {  // first Stockham pass (span 1): outputs 16 j + r
+      spec[padi(16 * jA + r)] = vA[r];
+      spec[padi(16 * jB + r)] = vB[r];
+    }
+    __syncthreads();  // (the shared twiddle table is also staged by now)
+  } else {
+    // ---- I3b: half-spectrum bin b = slot0[b] + slot1[b] (+ its overflow run, rare); two
+    // bins per thread and load (16-byte), 4 pairs in flight
+    {
+      const float4 *Z0 = reinterpret_cast<const float4 *>(a.stage + ul * a.zs);
+      const float4 *Z1 = reinterpret_cast<const float4 *>(a.stage + ul * a.zs + a.zso);
+      const float2 *Zo = a.stage + ul * a.zs + 2 * a.zso;
+      const uint2 *dpos2 = reinterpret_cast<const uint2 *>(a.dpos);
+      constexpr int G = 4, NP = N / 2 + 1;  // bin pairs (2i, 2i+1); the pair (N, N+1) is padded
+      for (int i0 = tid; i0 < NP; i0 += G * T) {
+        float4 z0[G], z1[G];
+        uint2 dp[G];
+  #pragma unroll
+        for (int q = 0; q < G; ++q) {
+          const int i = min(i0 + q * T, NP - 1);
+          z0[q] = __ldcg(Z0 + i);
+          z1[q] = __ldcg(Z1 + i);
+          dp[q] = __ldg(dpos2 + i);
+        }
+  #pragma unroll
+        for (int q = 0; q < G; ++q) {
+          const int i = i0 + q * T;
+          if (i >= NP) continue;
+          float2 acc0 = make_float2(z0[q].x + z1[q].x, z0[q].y + z1[q].y);
+          float2 acc1 = make_float2(z0[q].z + z1[q].z, z0[q].w + z1[q].w);
+          if (dp[q].x | dp[q].y) {  // deep-overlap bins: overflow terms in order
+            for (int e = 0; e < (int)(dp[q].x >> 20); ++e)
+              acc0 = cadd(acc0, __ldcg(Zo + (dp[q].x & 0xfffff) + e));
+            for (int e = 0; e < (int)(dp[q].y >> 20); ++e)
+              acc1 = cadd(acc1, __ldcg(Zo + (dp[q].y & 0xfffff) + e));
+          }
+          spec[padi(2 * i)] = acc0;
+          if (2 * i + 1 <= N) spec[padi(2 * i + 1)] = acc1;
+        }
+      }
+    }
+    __syncthreads();
+    PHASE_MARK(1, 0);
 
-  PHASE_MARK(1, 1);
-  // ---- I4b: inverse N-point FFT (unnormalised), first passes in shared memory
-  pass_smem<N, CF::I1, 1, +1, T>(spec, tw);
+    // ---- I4a: c2r packing  Z[k] = E[k] + i O[k],
+    //   E = (H[k] + conj H[N-k])/2,  O = (H[k] - conj H[N-k]) e^{+i pi k/N} / 2
+    for (int k = tid; k <= N / 2; k += T) {
+      const float2 hk = spec[padi(k)];
+      const float2 hn = spec[padi(N - k)];
+      const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
+      const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+      const float2 w = cconj(tw_lookup(tw, k));  // e^{+i pi k/N}
+      const float2 O = cmul(D, w);
+      spec[padi(k)] = make_float2(E.x - O.y, E.y + O.x);  // E + iO
+      if (k != 0 && k != N / 2) {
+        // pair N-k: E' = conj(E), O' = conj(D) e^{-i pi k/N}
+        const float2 O2 = cmul(cconj(D), cconj(w));
+        spec[padi(N - k)] = make_float2(E.x - O2.y, -E.y + O2.x);  // conj(E) + i O'
+      }
+    }
+    __syncthreads();
+
+    PHASE_MARK(1, 1);
+    // ---- I4b: inverse N-point FFT (unnormalised), first passes in shared memory
+    pass_smem<N, CF::I1, 1, +1, T>(spec, tw);
+  }
   PHASE_MARK(1, 2);
   pass_smem<N, CF::I2, CF::I1, +1, T>(spec, tw);
   PHASE_MARK(1, 3);
