@@ -72,6 +72,9 @@ __host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
 // Big-FFT plans: N = 2^LOGN complex points, T threads, radix sequences per direction.
 template <int LOGN>
 struct Big;
+#ifndef SLICQ_IA_GROUP
+#define SLICQ_IA_GROUP 4
+#endif
 #ifndef SLICQ_T13
 #define SLICQ_T13 256
 #endif
@@ -95,7 +98,7 @@ struct Big<12> {
 template <>
 struct Big<13> {
   static constexpr int N = 8192, T = SLICQ_T13, MINB = SLICQ_MINB13;
-  static constexpr int F1 = 16, F2 = 16, F3 = 32;
+  static constexpr int F1 = 16, F2 = 32, F3 = 16;
   static constexpr int I1 = 16, I2 = 32, I3 = 16;
 };
 template <>
@@ -699,33 +702,74 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
   PHASE_MARK(0, 0);
   pass_smem<N, CF::F2, CF::F1, -1, T>(spec, tw);
   PHASE_MARK(0, 1);
-  pass_smem<N, CF::F3, CF::F1 * CF::F2, -1, T>(spec, tw);
-  PHASE_MARK(0, 2);
-
-  // ---- r2c packing: X[k] = E[k] + e^{-i pi k/N} O[k], k = 0..N  (Z[N] := Z[0])
-  for (int k = tid; k <= N / 2; k += T) {
-    const float2 zk = spec[padi(k)];
-    const float2 zn = spec[padi((N - k) & (N - 1))];
-    if (k == 0) {
-      spec[padi(0)] = make_float2(zk.x + zk.y, 0.f);
-      spec[padi(N)] = make_float2(zk.x - zk.y, 0.f);
-    } else {
-      // E = (Zk + conj Zn)/2, O = (Zk - conj Zn)/(2i)
+  constexpr int R3 = CF::F3, TASKS3 = N / R3;
+  if constexpr (R3 == 16 && TASKS3 == 2 * T) {
+    // ---- last radix-16 pass + r2c packing + store, fused in registers: thread t owns the
+    // tasks jA = t and jB = TASKS3 - t (t = 0: 0 and TASKS3/2); their outputs Z[k],
+    // k = j + TASKS3 r, pair up as mirrors N - (jA + TASKS3 r) = jB + TASKS3 (15 - r), so
+    // X[k] = E + e^{-i pi k/N} O and X[N-k] = conj(E) - conj(e^{-i pi k/N} O),
+    // E = (Z[k] + conj Z[N-k])/2, O = (Z[k] - conj Z[N-k])/(2i), come out of registers
+    // and go straight to the staging buffer (coalesced across the warp).
+    const int jA = tid, jB = tid == 0 ? TASKS3 / 2 : TASKS3 - tid;
+    float2 vA[16], vB[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      vA[r] = spec[padi(jA + r * TASKS3)];
+      vB[r] = spec[padi(jB + r * TASKS3)];
+    }
+    pass_twiddle<N, 16, TASKS3, -1>(vA, jA, tw);
+    pass_twiddle<N, 16, TASKS3, -1>(vB, jB, tw);
+    dft<16, -1>(vA);
+    dft<16, -1>(vB);
+    float2 *Xo = a.stage + ul * a.xs;
+    auto r2c = [&](float2 zk, float2 zn, int k, bool mirror) {
       const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
       const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
       const float2 wO = cmul(tw_lookup(tw, k), O);  // e^{-i pi k/N} O
-      spec[padi(k)] = cadd(E, wO);
-      // X[N-k] = conj(E) + e^{-i pi (N-k)/N} conj(O) = conj(E) - conj(wO)
-      if (k != N / 2) spec[padi(N - k)] = csub(cconj(E), cconj(wO));
+      Xo[k] = cadd(E, wO);
+      if (mirror) Xo[N - k] = csub(cconj(E), cconj(wO));
+    };
+    if (tid != 0) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) r2c(vA[r], vB[15 - r], jA + TASKS3 * r, true);
+    } else {
+      Xo[0] = make_float2(vA[0].x + vA[0].y, 0.f);  // X[0], X[N] from Z[0]
+      Xo[N] = make_float2(vA[0].x - vA[0].y, 0.f);
+#pragma unroll
+      for (int r = 1; r < 8; ++r) r2c(vA[r], vA[16 - r], TASKS3 * r, true);
+      r2c(vA[8], vA[8], N / 2, false);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) r2c(vB[r], vB[15 - r], TASKS3 / 2 + TASKS3 * r, true);
     }
-  }
-  __syncthreads();
-  PHASE_MARK(0, 3);
+  } else {
+    pass_smem<N, CF::F3, CF::F1 * CF::F2, -1, T>(spec, tw);
+    PHASE_MARK(0, 2);
 
-  // ---- X[0..N] -> staging (coalesced)
-  {
-    float2 *Xo = a.stage + ul * a.xs;
-    for (int k = tid; k <= N; k += T) Xo[k] = spec[padi(k)];
+    // ---- r2c packing: X[k] = E[k] + e^{-i pi k/N} O[k], k = 0..N  (Z[N] := Z[0])
+    for (int k = tid; k <= N / 2; k += T) {
+      const float2 zk = spec[padi(k)];
+      const float2 zn = spec[padi((N - k) & (N - 1))];
+      if (k == 0) {
+        spec[padi(0)] = make_float2(zk.x + zk.y, 0.f);
+        spec[padi(N)] = make_float2(zk.x - zk.y, 0.f);
+      } else {
+        // E = (Zk + conj Zn)/2, O = (Zk - conj Zn)/(2i)
+        const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
+        const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
+        const float2 wO = cmul(tw_lookup(tw, k), O);  // e^{-i pi k/N} O
+        spec[padi(k)] = cadd(E, wO);
+        // X[N-k] = conj(E) + e^{-i pi (N-k)/N} conj(O) = conj(E) - conj(wO)
+        if (k != N / 2) spec[padi(N - k)] = csub(cconj(E), cconj(wO));
+      }
+    }
+    __syncthreads();
+    PHASE_MARK(0, 3);
+
+    // ---- X[0..N] -> staging (coalesced)
+    {
+      float2 *Xo = a.stage + ul * a.xs;
+      for (int k = tid; k <= N; k += T) Xo[k] = spec[padi(k)];
+    }
   }
   PHASE_MARK(0, 4);
   pdl_trigger();
@@ -781,12 +825,13 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
     // H at the thread's 32 bins jA + TASKS1 r (vA) and jB + TASKS1 r (vB): 4 r per batch,
     // all 16 slot loads and 8 overflow descriptors of a batch in flight together
     float2 vA[16], vB[16];
+    constexpr int IG = SLICQ_IA_GROUP;  // r values per load batch
 #pragma unroll
-    for (int r0 = 0; r0 < 16; r0 += 4) {
-      float2 a0[4], a1[4], b0[4], b1[4];
-      uint32_t da[4], db[4];
+    for (int r0 = 0; r0 < 16; r0 += IG) {
+      float2 a0[IG], a1[IG], b0[IG], b1[IG];
+      uint32_t da[IG], db[IG];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < IG; ++q) {
         const int ka = jA + TASKS1 * (r0 + q), kb = jB + TASKS1 * (r0 + q);
         a0[q] = __ldcg(Z0 + ka);
         a1[q] = __ldcg(Z1 + ka);
@@ -796,7 +841,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
         db[q] = __ldg(a.dpos + kb);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < IG; ++q) {
         vA[r0 + q] = cadd(a0[q], a1[q]);
         vB[r0 + q] = cadd(b0[q], b1[q]);
         if (da[q] | db[q]) {  // deep-overlap bins: overflow terms in order
