@@ -104,7 +104,7 @@ struct Big<13> {
 template <>
 struct Big<14> {
   static constexpr int N = 16384, T = 512, MINB = 1;
-  static constexpr int F1 = 16, F2 = 32, F3 = 32;
+  static constexpr int F1 = 32, F2 = 32, F3 = 16;
   static constexpr int I1 = 16, I2 = 32, I3 = 32;
 };
 
@@ -1038,27 +1038,28 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       sflag[1] = fr;
     }
     __syncthreads();
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      if (!sflag[side]) continue;
-      const int b = side == 0 ? bl : br;
-      const int64_t mb = a.slice0 + b;  // boundary between global slices mb and mb+1
-      // the partner's half from the workspace, this CTA's own half recomputed from the frame
-      // (a + b is commutative in IEEE arithmetic: the sum does not depend on who is second)
-      const float *hp = bnd_row + ((int64_t)b * 2 + (side == 0 ? 0 : 1)) * trp;
-#pragma unroll 4
-      for (int u = tid; u < a.tr - 1; u += T) {
-        // __fmul_rn: no contraction into an FMA with the add (the half must round as stored)
-        const float own = side == 0 ? __fmul_rn(fr[N - Bw + 1 + u], htab[Bw - 2 - u - A])
-                                    : __fmul_rn(fr[N + A + 1 + u], htab[u]);
-        const float val = __ldcg(hp + u) + own;
-        const int64_t s = mb * N + A + 1 + u;
+    // the partner's half from the workspace, this CTA's own half recomputed from the frame
+    // (a + b is commutative in IEEE arithmetic: the sum does not depend on who is second);
+    // both sides in one loop so that all partner loads of a thread are in flight together
+    const bool f0 = sflag[0], f1 = sflag[1];
+    if (f0 || f1) {
+      const float *hp0 = bnd_row + ((int64_t)bl * 2 + 0) * trp;  // left partner's right half
+      const float *hp1 = bnd_row + ((int64_t)br * 2 + 1) * trp;  // right partner's left half
+      const int64_t s0 = (a.slice0 + bl) * N + A + 1, s1 = (a.slice0 + br) * N + A + 1;
+      auto put = [&](int64_t s, float val) {
         if (a.circular) {
           const int64_t sw = s >= a.L ? s - a.L : s;
           if (sw < a.y_len) yrow[sw] = val;
         } else {
           yrow[s - a.y_base] = val;
         }
+      };
+#pragma unroll 4
+      for (int u = tid; u < a.tr - 1; u += T) {
+        const float p0 = f0 ? __ldcg(hp0 + u) : 0.f, p1 = f1 ? __ldcg(hp1 + u) : 0.f;
+        // __fmul_rn: no contraction into an FMA with the add (the half must round as stored)
+        if (f0) put(s0 + u, p0 + __fmul_rn(fr[N - Bw + 1 + u], htab[Bw - 2 - u - A]));
+        if (f1) put(s1 + u, p1 + __fmul_rn(fr[N + A + 1 + u], htab[u]));
       }
     }
   }
