@@ -288,11 +288,11 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 // bring [p, p + bytes) into L2 (one prefetch per 128-byte line, spread over the warp)
 __device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes, int idx, int nthr = 32) {
-  const char *c = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(127));
-  const char *end = reinterpret_cast<const char *>(p) + bytes;
-  for (c += 128 * idx; c < end; c += 128 * nthr) asm volatile("prefetch.global.L2 [%0];" ::"l"(c));
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(127);
+  const int nl = (int)(((reinterpret_cast<uintptr_t>(p) + bytes - 1) >> 7) - (a0 >> 7)) + 1;
+  for (int l = idx; l < nl; l += nthr)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a0 + ((uintptr_t)l << 7)));
 }
-
 // ------------------------------------------------------------------ channel packets
 // A packet = channels of one length M.  Big packets (M > 32) are a four-step M1 x M2 DFT
 // with one task per lane and step; channel ci owns the region ci*M1*S2 (S2 = M2 | 1) of the
@@ -431,6 +431,9 @@ __device__ __noinline__ void inv_small(const float2 *in_row, float2 *reg, int nv
 #ifndef SLICQ_XLOAD
 #define SLICQ_XLOAD __ldg  // fold reads of the staged spectra (prefetched to L2)
 #endif
+#ifndef SLICQ_FB_PREFETCH
+#define SLICQ_FB_PREFETCH 0
+#endif
 #ifndef SLICQ_FOLD_UNROLL
 #define SLICQ_FOLD_UNROLL 4  // element loops of the channel kernels: loads in flight per lane
 #endif
@@ -479,12 +482,14 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArg
       const int nvc = nuu * r;
       const float2 *X = a.stage + (int64_t)g0 * a.xs;
       float2 *out_row = a.coef_out + (a.unit0 + g0) * a.C;
+#if SLICQ_FB_PREFETCH  // (measured: no gain on cfg4; the fold's loads are L2-latency bound)
       if (t + NW < ntask) {  // this warp's next task: its spectrum bins -> L2 (staging in DRAM)
         const int g1 = g0 + NW * nu, n1u = min(nu, u_hi - g1);
         for (int u = 0; u < n1u; ++u)
           prefetch_l2(X + (int64_t)(NW * nu + u) * a.xs + P.xlo, (int64_t)(P.xhi - P.xlo + 1) * 8,
                       lane);
       }
+#endif
       if (small) {
         switch (m1) {
 #define X_(S) \
