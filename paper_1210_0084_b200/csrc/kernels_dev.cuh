@@ -1,27 +1,31 @@
 // sm_100a kernels of the sliCQ hot path (device code).  DESIGN.md "Kernels" describes the
-// design; step names follow SURVEY.md §8(a).  Two kernels per direction, run over chunks of
-// (row, slice) units whose intermediate stays in a workspace staging buffer (sized to stay
-// L2-resident):
+// design; step names follow SURVEY.md §8(a).  Per direction a spectrum kernel and one or two
+// channel kernels (lite / full register variants), over (row, slice) units whose
+// intermediate goes through the workspace staging buffer:
 //
 //   forward
 //     slicq_fwd_spec_kernel<LOGN>   one CTA per unit:
-//       F1  gather the Tukey-windowed slice straight from HBM
-//       F2  r2c FFT_{2N}: complex N-point Stockham FFT in shared memory (register radix
-//           16/32 passes) + packing step -> X[0..N] into the staging buffer
-//     slicq_fwd_chan_kernel         one warp per (packet, tile of units):
+//       F1  first radix pass straight from HBM: Tukey-windowed frame pairs
+//       F2  r2c FFT_{2N}: complex N-point Stockham FFT in shared memory; the last pass, the
+//           packing step and the store of X[0..N] to the staging buffer fused in registers
+//           (mirror-paired tasks)
+//     slicq_fwd_chan_kernel<MAXS,MINB>  one warp task = (packet, nu units) of a tile:
 //       F3  fold: buf[p] = X(j) g_k[j]/sqrt(M_k), j = p mod M_k, from a plan-time element
-//           table (bin, conj flag, scratch position, weight)       (C5)
+//           table (bin | scratch position, weight with the conjugation flag as its sign)
+//                                                                  (C5)
 //       F4  IFFT_{M_k} as a four-step M1 x M2 register DFT (M_k > 32) or a whole DFT_M per
 //           lane (M_k <= 32), compile-time twiddles
 //       F5  store c^m_k                                            (P:320-323 layout view)
 //   inverse
-//     slicq_inv_chan_kernel         one warp per (packet, tile of units):
+//     slicq_inv_chan_kernel<MAXS,MINB>  one warp task = (packet, nu units) of a tile:
 //       I1/I2  load c^m_k, FFT_{M_k} (four-step / per lane)
-//       I3a    contribution Z[k][d] = F_k[j mod M_k] g~_k[j]/sqrt(M_k), j = lo_k + d
+//       I3a    term F_k[j mod M_k] g~_k[j]/sqrt(M_k) (conjugated where C15 mirrors it) into
+//              its bin-major slot of the unit's half spectrum
 //     slicq_inv_spec_kernel<LOGN>   one CTA per unit:
-//       I3b per-bin gather of the contributions with the Hermitian rule of C15 folded into
-//           a plan-time CSR list -- deterministic, no atomics
-//       I4  c2r IFFT_{2N} (packing step + N-point Stockham)
+//       I3b H[b] = slot0[b] + slot1[b] (+ the bin's overflow run, plan order) -- no index
+//           tables, no atomics, deterministic; fused with the c2r packing and the first
+//           radix pass in registers
+//       I4  c2r IFFT_{2N} (N-point Stockham)
 //       I5  multiply by h~_0 and overlap-add; slice-boundary samples are paired across CTAs
 //           through the workspace with a parity counter (no spinning, deterministic a+b)
 //
