@@ -320,10 +320,12 @@ def run_gpu(args, cfg):
     peak, peak_src = peaks()
     bytes_fwd = B * (4 * L_local + 8 * S_local * C)  # read x once, write complex64 coefficients
     bytes_inv = bytes_fwd                             # read coefficients, write y
-    # the dominant direction; each C-ABI call is one spectrum kernel + one channel kernel
+    # the dominant direction; each C-ABI call is one spectrum kernel + the channel kernel
+    # variants its packets need (lite <16,3> and full <32,2>)
     dom = "slicq_inverse" if ms_i >= ms_f else "slicq_forward"
-    kernels = ("slicq_inv_chan_kernel + slicq_inv_spec_kernel" if dom == "slicq_inverse"
-               else "slicq_fwd_spec_kernel + slicq_fwd_chan_kernel")
+    kernels = ("slicq_inv_chan_kernel (lite + full variants) + slicq_inv_spec_kernel"
+               if dom == "slicq_inverse"
+               else "slicq_fwd_spec_kernel + slicq_fwd_chan_kernel (lite + full variants)")
     ms_dom = max(ms_i, ms_f)
     achieved = (bytes_inv if dom == "slicq_inverse" else bytes_fwd) / (ms_dom / 1e3) / 1e9
     traffic = None
@@ -340,7 +342,7 @@ def run_gpu(args, cfg):
     if not sharded and not args.no_e2e:
         # end to end through the public API with host buffers: api.process_host streams the
         # signal host->device, runs forward + inverse (slice ranges) and device->host,
-        # pipelined over 16 ranges on three streams; copies are inside the timed region
+        # pipelined over E2E_PIECES ranges on three streams; copies are inside the timed region
         xh = torch.from_numpy(x_np).pin_memory()
         yh = torch.empty((B, n), dtype=torch.float32).pin_memory()
         ke = max(2, min(args.steps, 5))
@@ -358,6 +360,46 @@ def run_gpu(args, cfg):
                "h2d_bytes_per_step": 4 * B * n, "d2h_bytes_per_step": 4 * B * n,
                "ms_per_step": ms_e2e, "recon_rel_l2": e2e_err,
                "api": f"paper_1210_0084_b200.api.process_host -> slicq_process_host (native executor, {E2E_PIECES} slice ranges, 3 streams)"}
+
+    if sharded and not args.no_e2e:
+        # end to end at N ranks through the public multi-GPU API (dist.SliceRangeShard): each
+        # step copies this rank's input samples from pinned host memory, runs the sharded
+        # forward + inverse (NCCL halo / spill exchange) and copies its output samples back
+        a, b = shard.own
+        hi = max(0, min(b, n) - a)
+        xh = shard.local_input(torch.from_numpy(x_np)).pin_memory()
+        yh = torch.empty((B, hi), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            xl.copy_(xh, non_blocking=True)
+            c_ = shard.forward(xl)
+            y_ = shard.inverse(c_)
+            if hi > 0:
+                yh.copy_(y_[:, :hi], non_blocking=True)
+
+        ke = max(2, min(args.steps, 5))
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a0, a1 = ev(), ev()
+        a0.record(stream)
+        for _ in range(ke):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([a0.elapsed_time(a1) / ke, 4.0 * B * xh.shape[1], 4.0 * B * hi],
+                          dtype=torch.float64, device=dev)
+        mx = tt[:1].clone()
+        if world > 1:
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt)
+        ms_e2e = float(mx[0])
+        e2e = {"value": samples / (ms_e2e / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(tt[1]), "d2h_bytes_per_step": int(tt[2]),
+               "ms_per_step": ms_e2e,
+               "api": "paper_1210_0084_b200.dist.SliceRangeShard (pinned host copies of each "
+                      "rank's range + sharded forward/inverse, max over ranks)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
