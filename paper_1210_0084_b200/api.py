@@ -243,6 +243,42 @@ def plan_for_config(cfg) -> Plan:
                 cfg.rasterize)
 
 
+def two_layer(plan: Plan, c: torch.Tensor):
+    """The paper's coefficient array s = {s^0, s^1} as a view of the
+    slice-major coefficients c [batch][S][C]: per channel k a tensor [batch][2][S M_k / 2]
+    with s^{m mod 2}_k[((m-1) M_k/2 + n) mod (S M_k/2)] = c^m_k[n].  Layer l holds the
+    slices m = l, l+2, ... back to back, rotated by (l-1) M_k / 2 -- index arithmetic only
+    (torch slicing / roll on the tensor's device)."""
+    if c.dim() == 2:
+        c = c[None]
+    B, S, _ = c.shape
+    if S % 2:
+        raise ValueError("a sliced stream has an even number of slices")
+    Ms, offs = plan.channel_lengths(), plan.channel_offsets()
+    out = []
+    for M, off in zip(Ms, offs):
+        layers = []
+        for layer in (0, 1):
+            blk = c[:, layer::2, off:off + M].reshape(B, -1)   # slices m = layer + 2i
+            layers.append(torch.roll(blk, shifts=(layer - 1) * (M // 2), dims=1))
+        out.append(torch.stack(layers, dim=1))
+    return out
+
+
+def from_two_layer(plan: Plan, s) -> torch.Tensor:
+    """Inverse of :func:`two_layer` (the partition of Alg. 4): per-channel
+    [batch][2][S M_k / 2] tensors -> c [batch][S][C]."""
+    Ms, offs = plan.channel_lengths(), plan.channel_offsets()
+    B, _, W0 = s[0].shape
+    S = 2 * W0 // Ms[0]
+    c = torch.empty((B, S, plan.coeffs_per_slice), dtype=s[0].dtype, device=s[0].device)
+    for sk, M, off in zip(s, Ms, offs):
+        for layer in (0, 1):
+            blk = torch.roll(sk[:, layer], shifts=-(layer - 1) * (M // 2), dims=1)
+            c[:, layer::2, off:off + M] = blk.reshape(B, S // 2, M)
+    return c
+
+
 class _DeviceView:
     """__cuda_array_interface__ view of library-owned device memory (no copy)."""
 
