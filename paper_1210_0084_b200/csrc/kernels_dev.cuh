@@ -76,6 +76,15 @@ __host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
 // Big-FFT plans: N = 2^LOGN complex points, T threads, radix sequences per direction.
 template <int LOGN>
 struct Big;
+// store flavours (tunable): coefficients are streamed out, staged terms are re-read by the
+// spectrum kernel
+__device__ __forceinline__ void st_plain(float2 *p, float2 v) { *p = v; }
+#ifndef SLICQ_CSTORE
+#define SLICQ_CSTORE __stcs
+#endif
+#ifndef SLICQ_ZSTORE
+#define SLICQ_ZSTORE __stcs  // (measured: evict-first beats .cg by ~1 % on cfg4)
+#endif
 #ifndef SLICQ_IA_GROUP
 #define SLICQ_IA_GROUP 4
 #endif
@@ -344,7 +353,7 @@ __device__ __noinline__ void fwd_step2(const float2 *reg, float2 *out_row, int m
   dft<M2, +1>(v);
   float2 *o = out_row + off + n1;
 #pragma unroll
-  for (int n2 = 0; n2 < M2; ++n2) __stcs(o + m1 * n2, v[n2]);
+  for (int n2 = 0; n2 < M2; ++n2) SLICQ_CSTORE(o + m1 * n2, v[n2]);
 }
 
 // Small forward packet: lane vc = u * nch + c (u < nu) owns channel c of unit u; element p
@@ -366,7 +375,7 @@ __device__ __noinline__ void fwd_small(const uint2 *ent, const float2 *X, float2
   dft<M, +1>(v);
   float2 *o = out_row + off_lane;
 #pragma unroll
-  for (int n = 0; n < M; ++n) __stcs(o + n, v[n]);
+  for (int n = 0; n < M; ++n) SLICQ_CSTORE(o + n, v[n]);
 }
 
 // I2 step 1: task (ci, p2) loads c[M2 p1 + p2]; DFT_{M1} (sign -); twiddle.
@@ -609,7 +618,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
           const uint2 en = __ldg(ent + e);
           const float2 f = su[en.x & 0x3fff];
           const float w = __uint_as_float(en.y);  // sign bit: conjugate the term (g~ >= 0)
-          __stcg(Zb + (en.x >> 14), make_float2(f.x * fabsf(w), f.y * w));
+          SLICQ_ZSTORE(Zb + (en.x >> 14), make_float2(f.x * fabsf(w), f.y * w));
         }
       }
       __syncwarp();
