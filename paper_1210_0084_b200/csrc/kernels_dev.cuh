@@ -79,6 +79,12 @@ struct Big;
 // store flavours (tunable): coefficients are streamed out, staged terms are re-read by the
 // spectrum kernel
 __device__ __forceinline__ void st_plain(float2 *p, float2 v) { *p = v; }
+#ifndef SLICQ_XSTORE
+#define SLICQ_XSTORE st_plain
+#endif
+#ifndef SLICQ_ZLOAD
+#define SLICQ_ZLOAD __ldcg
+#endif
 #ifndef SLICQ_CSTORE
 #define SLICQ_CSTORE __stcs
 #endif
@@ -744,15 +750,15 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
       const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
       const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
       const float2 wO = cmul(tw_lookup(tw, k), O);  // e^{-i pi k/N} O
-      Xo[k] = cadd(E, wO);
-      if (mirror) Xo[N - k] = csub(cconj(E), cconj(wO));
+      SLICQ_XSTORE(Xo + k, cadd(E, wO));
+      if (mirror) SLICQ_XSTORE(Xo + (N - k), csub(cconj(E), cconj(wO)));
     };
     if (tid != 0) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) r2c(vA[r], vB[15 - r], jA + TASKS3 * r, true);
     } else {
-      Xo[0] = make_float2(vA[0].x + vA[0].y, 0.f);  // X[0], X[N] from Z[0]
-      Xo[N] = make_float2(vA[0].x - vA[0].y, 0.f);
+      SLICQ_XSTORE(Xo, make_float2(vA[0].x + vA[0].y, 0.f));  // X[0], X[N] from Z[0]
+      SLICQ_XSTORE(Xo + N, make_float2(vA[0].x - vA[0].y, 0.f));
 #pragma unroll
       for (int r = 1; r < 8; ++r) r2c(vA[r], vA[16 - r], TASKS3 * r, true);
       r2c(vA[8], vA[8], N / 2, false);
@@ -851,10 +857,10 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
 #pragma unroll
       for (int q = 0; q < IG; ++q) {
         const int ka = jA + TASKS1 * (r0 + q), kb = jB + TASKS1 * (r0 + q);
-        a0[q] = __ldcg(Z0 + ka);
-        a1[q] = __ldcg(Z1 + ka);
-        b0[q] = __ldcg(Z0 + kb);
-        b1[q] = __ldcg(Z1 + kb);
+        a0[q] = SLICQ_ZLOAD(Z0 + ka);
+        a1[q] = SLICQ_ZLOAD(Z1 + ka);
+        b0[q] = SLICQ_ZLOAD(Z0 + kb);
+        b1[q] = SLICQ_ZLOAD(Z1 + kb);
         da[q] = __ldg(a.dpos + ka);
         db[q] = __ldg(a.dpos + kb);
       }
