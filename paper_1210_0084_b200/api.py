@@ -243,6 +243,39 @@ def plan_for_config(cfg) -> Plan:
                 cfg.rasterize)
 
 
+def transpose_bins(plan: Plan, c: torch.Tensor, shift: int) -> torch.Tensor:
+    """Pitch transposition by `shift` CQ bins (B bins = one octave, SURVEY
+    NEXT-4): CQ channel k takes channel (k - shift)'s coefficients, vacated channels are
+    zero, the DC / Nyquist plateaus are kept.  Needs one coefficient count M for all CQ
+    channels (a rasterised plan, C10; the paper's "rectangular representation").
+
+    The library's coefficients carry absolute phase (C6): channel k's content at bin j sits
+    at folded frequency j mod M.  Moving it to channel k' is the demodulated ("verbatim")
+    copy of the paper's toolbox, which in absolute phase is a modulation by the difference
+    of the two channels' centre bins: c'_{k'}[n] = c_k[n] e^{2 pi i (w_k' - w_k) n / M}."""
+    if c.dim() == 2:
+        c = c[None]
+    ex = plan.export()
+    Ms, offs, lo, ln = ex["M"], ex["off"], ex["lo"], ex["len"]
+    K = len(Ms) - 2
+    if len(set(int(m) for m in Ms[1:K + 1])) != 1:
+        raise ValueError("transpose_bins needs equal M_k over the CQ channels (rasterize=2)")
+    M = int(Ms[1])
+    centre = lo.astype(np.float64) + (ln.astype(np.float64) - 1.0) / 2.0
+    out = c.clone()
+    out[:, :, int(offs[1]):int(offs[K + 1])] = 0
+    s = int(shift)
+    n = torch.arange(M, device=c.device, dtype=torch.float64)
+    for k in range(1, K + 1):
+        src = k - s
+        if not 1 <= src <= K:
+            continue
+        d = int(round(centre[k] - centre[src]))
+        ph = torch.polar(torch.ones_like(n), 2.0 * np.pi * d * n / M).to(c.dtype)
+        out[:, :, int(offs[k]):int(offs[k]) + M] = c[:, :, int(offs[src]):int(offs[src]) + M] * ph
+    return out
+
+
 def two_layer(plan: Plan, c: torch.Tensor):
     """The paper's coefficient array s = {s^0, s^1} as a view of the
     slice-major coefficients c [batch][S][C]: per channel k a tensor [batch][2][S M_k / 2]

@@ -1,0 +1,63 @@
+"""Paper-level behaviour checks on the GPU path: T7 runtime linear in L, T8
+transposition moves the argmax channel, through the library's kernels."""
+import time
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_t7_runtime_linear_in_length():
+    """the sliCQ costs O(L); log-log slope of forward + inverse time vs L in
+    [0.85, 1.15] once the GPU is filled (>= 2^23 samples)."""
+    from paper_1210_0084_b200 import api
+    from synth.configs import CONFIGS
+    plan = api.plan_for_config(CONFIGS[4])
+    ns = [1 << 23, 1 << 24, 1 << 25, 1 << 26]
+    ts = []
+    for n in ns:
+        x = torch.randn(1, n, device="cuda") * 0.1
+        c = plan.forward(x)
+        y = plan.inverse(c, n)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            plan.forward(x, out=c)
+            plan.inverse(c, n, out=y)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 5)
+        del x, c, y
+    slope = np.polyfit(np.log(ns), np.log(ts), 1)[0]
+    assert 0.85 <= slope <= 1.15, (slope, ts)
+
+
+def test_t8_transposition_moves_argmax_channel():
+    """shifting the CQ coefficients by +B bins (one octave) and resynthesising moves
+    a tone's energy maximum by B channels (rasterised plan, equal M_k)."""
+    from paper_1210_0084_b200 import api
+    fs, B = 44100.0, 24
+    plan = api.Plan(fs, 55.0, 22050.0, B, 16384, 2048, 2)
+    n = 8 * 16384
+    t = np.arange(n) / fs
+    x = torch.from_numpy((0.5 * np.sin(2 * np.pi * 440.0 * t)).astype(np.float32))[None].cuda()
+    c = plan.forward(x)
+    Ms, offs = plan.channel_lengths(), plan.channel_offsets()
+    K = len(Ms) - 2
+
+    def argmax_channel(cc):
+        e = (cc.abs() ** 2).sum(dim=(0, 1)).cpu().numpy()
+        en = [e[offs[k]:offs[k + 1]].sum() for k in range(1, K + 1)]
+        return 1 + int(np.argmax(en))
+
+    k0 = argmax_channel(c)
+    y = plan.inverse(api.transpose_bins(plan, c, B), n)
+    k1 = argmax_channel(plan.forward(y))
+    assert k1 == k0 + B, (k0, k1)
+    # the transposed tone is an octave up: the spectrum peak moves from 440 to ~880 Hz
+    Y = np.abs(np.fft.rfft(y[0].cpu().numpy()))
+    f_peak = np.argmax(Y) * fs / n
+    assert abs(f_peak - 880.0) < 20.0, f_peak
