@@ -243,6 +243,22 @@ def plan_for_config(cfg) -> Plan:
                 cfg.rasterize)
 
 
+def apply_mask(c: torch.Tensor, mask, db: bool = True) -> torch.Tensor:
+    """Coefficient masking (paper §VI): c * a, with a = 10^(-5 (1 - mask)) for
+    dB-scaled masks ("0 in the mask corresponds to 10^-5 (-100 dB) and 1 corresponds to 1
+    (0 dB)"), else a = mask.  `mask` broadcasts against c [batch][S][C] (e.g. a per-column
+    [C] or full [batch][S][C] grid); real-valued, on c's device."""
+    m = torch.as_tensor(mask, device=c.device, dtype=torch.float64)
+    a = torch.pow(10.0, -5.0 * (1.0 - m)) if db else m
+    return c * a.to(torch.float32 if c.dtype == torch.complex64 else torch.float64)
+
+
+def spectrogram(plan: Plan, c: torch.Tensor):
+    """The paper's sliCQ spectrogram |s^0 + s^1|^2 per channel: a list of
+    [batch][S M_k / 2] real tensors, time-ordered with hop 2N/M_k samples per entry."""
+    return [(s[:, 0] + s[:, 1]).abs() ** 2 for s in two_layer(plan, c)]
+
+
 def transpose_bins(plan: Plan, c: torch.Tensor, shift: int) -> torch.Tensor:
     """Pitch transposition by `shift` CQ bins (B bins = one octave, SURVEY
     NEXT-4): CQ channel k takes channel (k - shift)'s coefficients, vacated channels are

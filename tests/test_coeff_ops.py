@@ -69,3 +69,30 @@ def test_transpose_bins_relocates_magnitudes():
     with pytest.raises(ValueError):
         api.transpose_bins(api.Plan(44100.0, 55.0, 22050.0, 24, 16384, 2048, 0, host_only=True),
                            c[..., :1], 1)
+
+
+def test_apply_mask_db_convention():
+    """mask 0 -> 10^-5 (-100 dB), 1 -> 1 (0 dB), linear in dB in between."""
+    from paper_1210_0084_b200 import api
+    c = torch.full((1, 2, 6), 2.0 + 1.0j, dtype=torch.complex128)
+    assert torch.equal(api.apply_mask(c, 1.0), c)
+    assert torch.allclose(api.apply_mask(c, 0.0), c * 1e-5, rtol=1e-14, atol=0)
+    m = torch.tensor([0.0, 0.25, 0.5, 0.75, 1.0, 0.5], dtype=torch.float64)
+    out = api.apply_mask(c, m)
+    want = 10.0 ** (-5.0 * (1.0 - m))
+    assert torch.allclose(out[0, 1].abs() / c[0, 1].abs(), want, rtol=1e-12, atol=0)
+    assert torch.allclose(20 * torch.log10(out[0, 0].abs() / c[0, 0].abs()), -100 * (1 - m))
+    assert torch.equal(api.apply_mask(c, m, db=False), c * m)
+
+
+def test_spectrogram_is_two_layer_sum():
+    from paper_1210_0084_b200 import api
+    plan = api.Plan(*plan_args(CONFIGS[1]), host_only=True)
+    rng = np.random.default_rng(11)
+    S, C = 8, plan.coeffs_per_slice
+    c = torch.from_numpy(rng.standard_normal((1, S, C)) + 1j * rng.standard_normal((1, S, C)))
+    sp = api.spectrogram(plan, c)
+    s = api.two_layer(plan, c)
+    for k in (0, 7, plan.num_channels - 1):
+        assert torch.allclose(sp[k], (s[k][:, 0] + s[k][:, 1]).abs() ** 2)
+        assert sp[k].shape[1] == S * int(plan.channel_lengths()[k]) // 2

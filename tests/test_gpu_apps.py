@@ -61,3 +61,24 @@ def test_t8_transposition_moves_argmax_channel():
     Y = np.abs(np.fft.rfft(y[0].cpu().numpy()))
     f_peak = np.argmax(Y) * fs / n
     assert abs(f_peak - 880.0) < 20.0, f_peak
+
+
+def test_mask_decomposition_adds_up():
+    """a mask and its complement split a signal into parts that add back to it
+    (synthesis is linear; the masks are applied to the coefficients on the device)."""
+    from paper_1210_0084_b200 import api
+    from synth.configs import CONFIGS
+    from synth.signals import make_signal
+    plan = api.plan_for_config(CONFIGS[1])
+    x = torch.from_numpy(make_signal(1)).cuda()
+    n = x.shape[1]
+    c = plan.forward(x)
+    g = torch.Generator().manual_seed(1)
+    m = torch.rand(c.shape, generator=g, dtype=torch.float64).cuda()
+    y1 = plan.inverse(api.apply_mask(c, m, db=False), n)
+    y2 = plan.inverse(api.apply_mask(c, 1.0 - m, db=False), n)
+    err = ((y1 + y2 - x).norm() / x.norm()).item()
+    assert err <= 1e-5, err
+    # -100 dB everywhere: the output is x scaled by 1e-5
+    y0 = plan.inverse(api.apply_mask(c, 0.0), n)
+    assert ((y0 - 1e-5 * x).norm() / (1e-5 * x.norm())).item() <= 1e-5
