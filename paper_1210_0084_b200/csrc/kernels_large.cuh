@@ -95,13 +95,12 @@ __global__ void __launch_bounds__(LT) fwd_large_col(const KArgs a) {
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N1>();
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  float2 *tw = buf + LB * CS;
+  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1 (17 KB at N = 65536)
   const int tid = threadIdx.x;
   const int64_t ul = blockIdx.x;
   int64_t row, mloc, mg;
   unit_coords(a, ul, row, mloc, mg);
   const int p2_0 = blockIdx.y * LB;
-  for (int i = tid; i < tw_entries_n<N>(); i += LT) tw[i] = a.tw2n[i];
   pdl_wait();
   // F1: windowed z[N2 p1 + p2] = (f[2p], f[2p+1]) * h_0, 16 consecutive p2 per row p1
   {
@@ -155,11 +154,10 @@ __global__ void __launch_bounds__(LT) fwd_large_row(const KArgs a) {
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N2>();
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  float2 *tw = buf + LB * CS;
+  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1 (17 KB at N = 65536)
   const int tid = threadIdx.x;
   const int64_t ul = blockIdx.x;
   const int kb = blockIdx.y * 8;  // rows kb..kb+7 (<= N1/2) and their partners N1 - k1
-  for (int i = tid; i < tw_entries_n<N>(); i += LT) tw[i] = a.tw2n[i];
   pdl_wait();
   const float2 *T = a.stage + ul * a.xs + a.toff;
   auto slot_row = [&](int s) -> int {  // -1: empty slot
@@ -178,8 +176,10 @@ __global__ void __launch_bounds__(LT) fwd_large_row(const KArgs a) {
   // buf[slot][k2] = Z[k1 + N1 k2].  r2c packing (as in slicq_fwd_spec_kernel):
   // X[k] = E + w O, X[N-k] = conj(E) - conj(w O), w = e^{-i pi k/N}
   float2 *Xo = a.stage + ul * a.xs;
+  // consecutive threads take consecutive rows k1 of one column k2: the outputs
+  // X[k1 + N1 k2] (and their mirrors) are stored as 8-entry contiguous runs
   for (int idx = tid; idx < 8 * N2; idx += LT) {
-    const int s = idx / N2, k2 = idx % N2;
+    const int s = idx % 8, k2 = idx / 8;
     const int k1 = kb + s;
     if (k1 > N1 / 2) continue;
     int ps, pk2;  // partner slot / column of Z[N - k]
@@ -232,10 +232,7 @@ template <int LOGN>
 __global__ void __launch_bounds__(LT) inv_large_pack(const KArgs a) {
   using G = Large<LOGN>;
   constexpr int N = G::N;
-  extern __shared__ float4 smem4[];
-  float2 *tw = reinterpret_cast<float2 *>(smem4);
-  for (int i = threadIdx.x; i < tw_entries_n<N>(); i += LT) tw[i] = a.tw2n[i];
-  __syncthreads();
+  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1
   pdl_wait();
   const int64_t ul = blockIdx.x;
   const float2 *Z = a.stage + ul * a.zs;
@@ -263,11 +260,10 @@ __global__ void __launch_bounds__(LT) inv_large_col(const KArgs a) {
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N1>();
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  float2 *tw = buf + LB * CS;
+  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1 (17 KB at N = 65536)
   const int tid = threadIdx.x;
   const int64_t ul = blockIdx.x;
   const int p2_0 = blockIdx.y * LB;
-  for (int i = tid; i < tw_entries_n<N>(); i += LT) tw[i] = a.tw2n[i];
   pdl_wait();
   float2 *W = a.stage + ul * a.zs + a.toff;
   for (int idx = tid; idx < LB * N1; idx += LT) {
@@ -295,13 +291,12 @@ __global__ void __launch_bounds__(LT) inv_large_row(const KArgs a) {
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N2>();
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  float2 *tw = buf + LB * CS;
+  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1 (17 KB at N = 65536)
   const int tid = threadIdx.x;
   const int64_t ul = blockIdx.x;
   int64_t row, mloc, mg;
   unit_coords(a, ul, row, mloc, mg);
   const int n1_0 = blockIdx.y * LB;
-  for (int i = tid; i < tw_entries_n<N>(); i += LT) tw[i] = a.tw2n[i];
   pdl_wait();
   const float2 *W = a.stage + ul * a.zs + a.toff;
   for (int idx = tid; idx < LB * N2; idx += LT) {
@@ -393,7 +388,7 @@ __global__ void __launch_bounds__(LT) inv_large_bnd(const KArgs a) {
 
 template <int LOGN>
 constexpr size_t large_smem_bytes() {
-  return sizeof(float2) * (size_t)(LB * colstride<256>() + tw_entries_n<Large<LOGN>::N>());
+  return sizeof(float2) * (size_t)(LB * colstride<256>());
 }
 
 // entry points (kernels_large.cu)

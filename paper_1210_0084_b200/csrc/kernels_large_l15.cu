@@ -48,7 +48,7 @@ cudaError_t large_inverse_spec<SLICQ_LOGN>(const KArgs &a, cudaStream_t s) {
   using G = Large<SLICQ_LOGN>;
   const size_t sm = large_smem_bytes<SLICQ_LOGN>();
   const unsigned nu = (unsigned)a.nunits;
-  cudaError_t e = lpdl(inv_large_pack<SLICQ_LOGN>, a, dim3(nu, (G::N / 2 + 1 + LT - 1) / LT), sm, s);
+  cudaError_t e = lpdl(inv_large_pack<SLICQ_LOGN>, a, dim3(nu, (G::N / 2 + 1 + LT - 1) / LT), 0, s);
   if (e == cudaSuccess) e = lpdl(inv_large_col<SLICQ_LOGN>, a, dim3(nu, G::N2 / LB), sm, s);
   if (e == cudaSuccess) e = lpdl(inv_large_row<SLICQ_LOGN>, a, dim3(nu, G::N1 / LB), sm, s);
   if (e == cudaSuccess)
