@@ -81,6 +81,10 @@ size_t spec_smem_for(int logN, int tr) {
 
 constexpr size_t kSmemCap = 227 * 1024;  // per CTA
 constexpr int kSmallCap = 640;           // float2 scratch entries a small packet may use
+#ifndef SLICQ_SMALL_MAX
+#define SLICQ_SMALL_MAX 32
+#endif
+constexpr int kSmallMax = SLICQ_SMALL_MAX;  // channels with M <= this: one lane per channel
 // channel-kernel variants: <largest DFT size, CTAs per SM (register budget)>
 #ifndef SLICQ_LITE_MAX
 #define SLICQ_LITE_MAX 16
@@ -147,7 +151,7 @@ int configure_kernels(slicq_plan *p) {
   std::vector<Pk> pks;
   for (int k = 0; k < K2;) {
     const int M = p->M[k];
-    const bool small = M <= 32 && in_small(M);
+    const bool small = M <= kSmallMax && in_small(M);
     const int m1 = fac[M].first, m2 = fac[M].second;
     const int nch = small ? std::min(32, kSmallCap / M) : std::max(1, 32 / std::max(m1, m2));
     Pk pk;
