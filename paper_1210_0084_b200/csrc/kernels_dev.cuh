@@ -707,9 +707,14 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
     for (int qq = 0; qq < PER; ++qq) {
       const int j = tid + qq * T;
       if (TASKS % T == 0 || j < TASKS) {
+        const int jw = (tid & ~31) + qq * T;  // this warp's first task
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int q = j + r * TASKS;
+          // warp-uniform skip: the warp's 32 pairs all on the flat top (h_0 = 1), or all
+          // outside the window support (not loaded: zeros)
+          const int w0 = jw + r * TASKS, w1 = w0 + 31;
+          if ((w0 >= qa && w1 <= qb) || w1 < q_lo || w0 > q_hi) continue;
           if (q >= qa && q <= qb) continue;  // both samples on the flat top (h_0 = 1)
           // |t| of the two samples (t = 2q - N and 2q + 1 - N); h_0 = 1 for |t| <= A
           const int t0 = abs(2 * q - N), t1 = abs(2 * q + 1 - N);
