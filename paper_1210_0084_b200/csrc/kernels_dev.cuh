@@ -1017,17 +1017,26 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
     }
     __syncthreads();
     const int64_t sbase = (mg - 1) * N;  // global sample of frame index 0
-    // exclusive part |t| <= A: h~_0 = 1
-    for (int i = N - A + tid; i <= N + A; i += T) {
-      const float val = fr[i];
-      const int64_t sg = sbase + i;
-      if (a.circular) {
-        const int64_t sw = sg < 0 ? sg + a.L : (sg >= a.L ? sg - a.L : sg);
-        if (sw < a.y_len) yrow[sw] = val;
-      } else {
-        const int64_t li = sg - a.y_base;
-        if (li >= 0) yrow[li] = val;
-        else a.spill[row * a.halo + (li + a.halo)] = val;
+    // exclusive part |t| <= A: h~_0 = 1.  Interior frames (no wrap, no trim, no spill): a
+    // plain coalesced copy; the others take the per-sample index logic.
+    const bool excl_direct =
+        a.circular ? (sbase + N - A >= 0 && sbase + N + A < a.L && sbase + N + A < a.y_len)
+                   : (sbase + N - A - a.y_base >= 0);
+    if (excl_direct) {
+      float *yo = yrow + (a.circular ? sbase : sbase - a.y_base);
+      for (int i = N - A + tid; i <= N + A; i += T) yo[i] = fr[i];
+    } else {
+      for (int i = N - A + tid; i <= N + A; i += T) {
+        const float val = fr[i];
+        const int64_t sg = sbase + i;
+        if (a.circular) {
+          const int64_t sw = sg < 0 ? sg + a.L : (sg >= a.L ? sg - a.L : sg);
+          if (sw < a.y_len) yrow[sw] = val;
+        } else {
+          const int64_t li = sg - a.y_base;
+          if (li >= 0) yrow[li] = val;
+          else a.spill[row * a.halo + (li + a.halo)] = val;
+        }
       }
     }
     // transitions, u = 0 .. tr-2 (|t| = A + 1 + u on the right, Bw - 1 - u on the left)
