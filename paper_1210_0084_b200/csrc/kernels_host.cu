@@ -373,10 +373,13 @@ int configure_kernels(slicq_plan *p) {
   }
   kc.tile = (int)std::max<int64_t>(1, env_int("SLICQ_TILE", 128));
   kc.chan_per_sm = (int)env_int("SLICQ_CHAN_PER_SM", 0);  // dev override: 0 = occupancy
+  // staging is sized for one chunk of units; calls with more units run chunk by chunk
+  // (each chunk costs kernel tails, so the default budget keeps every BASELINE config in a
+  // single chunk: 8 GB of staging = 61 K slices of 2N = 16384)
   const int64_t per_unit = sizeof(float2) * std::max(kc.xs, kc.zs);
-  const int64_t budget = env_int("SLICQ_STAGE_MB", 48) << 20;
-  int64_t cu = env_int("SLICQ_CHUNK_UNITS", int64_t(1) << 40);  // default: no chunking
-  (void)budget;
+  const int64_t budget = env_int("SLICQ_STAGE_MB", 8192) << 20;
+  int64_t cu = env_int("SLICQ_CHUNK_UNITS", std::max<int64_t>(1, budget / per_unit));
+  cu = std::min<int64_t>(cu, 0x7fffffff);  // grid x dimension of the spectrum kernels
   cu = std::max<int64_t>(kc.tile, cu / kc.tile * kc.tile);
   kc.chunk_units = cu;
   return SLICQ_OK;

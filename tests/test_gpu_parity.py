@@ -299,3 +299,26 @@ def test_process_host_matches_device_path(api, pieces, n, batch):
     y2 = api.process_host(plan, x, pieces=pieces, fn=lambda c, s0: c.mul_(2.0))
     torch.cuda.synchronize()
     assert torch.allclose(y2, 2 * yd, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_chunked_staging_is_bit_identical(api, monkeypatch):
+    """Calls larger than the staging budget run chunk by chunk (SLICQ_CHUNK_UNITS /
+    SLICQ_STAGE_MB, read at plan creation): identical results, including the slice
+    boundaries paired across chunks."""
+    n, batch = 37 * 8192 + 77, 8  # 304 units: three chunks of 128 (the tile)
+    x = torch.from_numpy(random_signal(777, batch, n)).cuda()
+    plan = api.plan_for_config(CONFIGS[1])
+    c = plan.forward(x)
+    y = plan.inverse(c, n)
+    monkeypatch.setenv("SLICQ_CHUNK_UNITS", "128")
+    chunked = api.plan_for_config(CONFIGS[1])
+    monkeypatch.delenv("SLICQ_CHUNK_UNITS")
+    assert chunked.workspace_bytes(c.shape[1], batch) < plan.workspace_bytes(c.shape[1], batch)
+    assert chunked.kernel_launches("forward", c.shape[1], batch) > \
+        plan.kernel_launches("forward", c.shape[1], batch)
+    c2 = chunked.forward(x)
+    y2 = chunked.inverse(c2, n)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
+    assert torch.equal(y, y2)
