@@ -24,6 +24,30 @@ namespace {
 constexpr int kSlots = 4;
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Range boundaries over S slices: the first and last kRamp ranges are shorter (weights
+// 1/kRamp, 2/kRamp, ...) so that the pipeline fills and drains quickly -- the first
+// copy-in and the last copy-out are not overlapped with anything.
+constexpr int kRamp = 4;
+std::vector<int64_t> range_bounds(int64_t S, int P) {
+  std::vector<double> w(P);
+  double tot = 0.0;
+  for (int r = 0; r < P; ++r) {
+    const int d = std::min(r + 1, P - r);
+    w[r] = d >= kRamp ? 1.0 : (double)d / kRamp;
+    tot += w[r];
+  }
+  std::vector<int64_t> b(P + 1, 0);
+  double acc = 0.0;
+  for (int r = 0; r < P; ++r) {
+    acc += w[r];
+    b[r + 1] = (int64_t)(S * acc / tot + 0.5);
+    b[r + 1] = std::max(b[r + 1], b[r] + 1);                 // every range >= 1 slice
+    b[r + 1] = std::min(b[r + 1], S - (int64_t)(P - 1 - r));  // room for the rest
+  }
+  b[P] = S;
+  return b;
+}
+
 struct ExecLayout {
   int P = 0;             // ranges
   int64_t S = 0, N = 0, halo = 0, nsmax = 0, C = 0;
@@ -40,7 +64,10 @@ ExecLayout exec_layout(const slicq_plan *p, int64_t n, int64_t batch, int pieces
   e.S = Lpad / p->N;
   e.P = (int)std::max<int64_t>(1, std::min<int64_t>(pieces, e.S / 2));
   e.halo = ((p->N + p->tr) / 2 + 1) & ~int64_t(1);  // >= slicq_halo, even
-  e.nsmax = (e.S + e.P - 1) / e.P;
+  {
+    const std::vector<int64_t> b = range_bounds(e.S, e.P);
+    for (int r = 0; r < e.P; ++r) e.nsmax = std::max(e.nsmax, b[r + 1] - b[r]);
+  }
   e.C = p->C;
   e.xw = e.halo + e.nsmax * p->N;
   e.yw = e.nsmax * p->N;
@@ -79,8 +106,7 @@ int slicq_process_host(const slicq_plan *p, const float *x_host, float *y_host, 
   if ((uintptr_t)ws % 256) return set_error(SLICQ_ESHAPE, "workspace must be 256-byte aligned");
   const int64_t N = e.N, S = e.S, L = S * N, halo = e.halo, B = batch;
   const int P = e.P;
-  std::vector<int64_t> bounds(P + 1);
-  for (int r = 0; r <= P; ++r) bounds[r] = (int64_t)r * S / P;
+  const std::vector<int64_t> bounds = range_bounds(S, P);
   char *base = static_cast<char *>(ws);
   auto slot_x = [&](int r) { return reinterpret_cast<float *>(base + (r % kSlots) * e.slot + e.x); };
   auto slot_c = [&](int r) {
