@@ -187,12 +187,19 @@ struct KArgs {
 __device__ __forceinline__ float2 tw_lookup(const float2 *tw, int e) {
   return cmul(tw[64 + (e >> 6)], tw[e & 63]);
 }
+// the same table read from global memory through the read-only (L1) path
+struct GlobalTw {
+  const float2 *p;
+};
+__device__ __forceinline__ float2 tw_lookup(GlobalTw tw, int e) {
+  return cmul(__ldg(tw.p + 64 + (e >> 6)), __ldg(tw.p + (e & 63)));
+}
 
 // Stockham twiddles for task j of a radix-R pass with span NS (applied before the
 // butterfly): w^r for r = 1..R-1, w = e^{SIGN 2 pi i (j mod NS)/(NS R)}.  w^{4q} comes
 // from the table, w^{4q+s} = w^{4q} * w^s (s = 1..3): at most two roundings deep.
-template <int N, int R, int NS, int SIGN>
-__device__ __forceinline__ void pass_twiddle(float2 (&v)[R], int j, const float2 *tw) {
+template <int N, int R, int NS, int SIGN, class TW>
+__device__ __forceinline__ void pass_twiddle(float2 (&v)[R], int j, TW tw) {
   if constexpr (NS > 1) {
     static_assert(R % 4 == 0, "big-FFT radices are multiples of 4");
     constexpr int STEP = 2 * (N / (NS * R));  // units of e^{-i pi/N}

@@ -42,8 +42,8 @@ constexpr int colstride() {
 }
 
 // B = LB independent P-point Stockham passes in shared memory (column c at c * CS)
-template <int NTAB, int P, int R, int NS, int SIGN>
-__device__ __forceinline__ void bpass(float2 *buf, const float2 *tw) {
+template <int NTAB, int P, int R, int NS, int SIGN, class TW>
+__device__ __forceinline__ void bpass(float2 *buf, TW tw) {
   constexpr int TPC = P / R, TASKS = LB * TPC, PER = (TASKS + LT - 1) / LT;
   constexpr int CS = colstride<P>();
   float2 v[PER][R];
@@ -75,8 +75,8 @@ __device__ __forceinline__ void bpass(float2 *buf, const float2 *tw) {
 }
 
 // e^{-i pi e/N}, e any integer (reduced mod 2N)
-template <int N>
-__device__ __forceinline__ float2 tw_any(const float2 *tw, int64_t e) {
+template <int N, class TW>
+__device__ __forceinline__ float2 tw_any(TW tw, int64_t e) {
   return tw_lookup(tw, (int)(e & (2 * N - 1)));
 }
 
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(LT) fwd_large_col(const KArgs a) {
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N1>();
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1 (17 KB at N = 65536)
+  const GlobalTw tw{a.tw2n};  // two-level twiddle table, read through L1 (17 KB at N = 65536)
   const int tid = threadIdx.x;
   const int64_t ul = blockIdx.x;
   int64_t row, mloc, mg;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(LT) fwd_large_row(const KArgs a) {
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N2>();
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1 (17 KB at N = 65536)
+  const GlobalTw tw{a.tw2n};  // two-level twiddle table, read through L1 (17 KB at N = 65536)
   const int tid = threadIdx.x;
   const int64_t ul = blockIdx.x;
   const int kb = blockIdx.y * 8;  // rows kb..kb+7 (<= N1/2) and their partners N1 - k1
@@ -165,10 +165,20 @@ __global__ void __launch_bounds__(LT) fwd_large_row(const KArgs a) {
     const int k1 = kb + s - 8;
     return (k1 > 0 && k1 < N1 / 2) ? N1 - k1 : -1;
   };
-  for (int idx = tid; idx < LB * N2; idx += LT) {
-    const int s = idx / N2, k2 = idx % N2;
-    const int r = slot_row(s);
-    buf[s * CS + padi(k2)] = r >= 0 ? T[(int64_t)r * N2 + k2] : make_float2(0.f, 0.f);
+  {  // all of a thread's row loads in flight together (streaming, L2 only)
+    constexpr int PERL = LB * N2 / LT;
+    float2 v[PERL];
+#pragma unroll
+    for (int q = 0; q < PERL; ++q) {
+      const int idx = tid + q * LT, s = idx / N2, k2 = idx % N2;
+      const int r = slot_row(s);
+      v[q] = r >= 0 ? __ldcs(T + (int64_t)r * N2 + k2) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < PERL; ++q) {
+      const int idx = tid + q * LT;
+      buf[(idx / N2) * CS + padi(idx % N2)] = v[q];
+    }
   }
   __syncthreads();
   bpass<N, N2, R_ROW, 1, -1>(buf, tw);
@@ -232,7 +242,7 @@ template <int LOGN>
 __global__ void __launch_bounds__(LT) inv_large_pack(const KArgs a) {
   using G = Large<LOGN>;
   constexpr int N = G::N;
-  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1
+  const GlobalTw tw{a.tw2n};  // two-level twiddle table, read through L1
   pdl_wait();
   const int64_t ul = blockIdx.x;
   const float2 *Z = a.stage + ul * a.zs;
@@ -260,15 +270,25 @@ __global__ void __launch_bounds__(LT) inv_large_col(const KArgs a) {
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N1>();
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1 (17 KB at N = 65536)
+  const GlobalTw tw{a.tw2n};  // two-level twiddle table, read through L1 (17 KB at N = 65536)
   const int tid = threadIdx.x;
   const int64_t ul = blockIdx.x;
   const int p2_0 = blockIdx.y * LB;
   pdl_wait();
   float2 *W = a.stage + ul * a.zs + a.toff;
-  for (int idx = tid; idx < LB * N1; idx += LT) {
-    const int c = idx % LB, p1 = idx / LB;
-    buf[c * CS + padi(p1)] = W[(int64_t)N2 * p1 + p2_0 + c];
+  {  // all of a thread's column loads in flight together (streaming, L2 only)
+    constexpr int PERL = LB * N1 / LT;
+    float2 v[PERL];
+#pragma unroll
+    for (int q = 0; q < PERL; ++q) {
+      const int idx = tid + q * LT;
+      v[q] = __ldcs(W + (int64_t)N2 * (idx / LB) + p2_0 + idx % LB);
+    }
+#pragma unroll
+    for (int q = 0; q < PERL; ++q) {
+      const int idx = tid + q * LT;
+      buf[(idx % LB) * CS + padi(idx / LB)] = v[q];
+    }
   }
   __syncthreads();
   bpass<N, N1, G::C1, 1, +1>(buf, tw);
@@ -291,7 +311,7 @@ __global__ void __launch_bounds__(LT) inv_large_row(const KArgs a) {
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N2>();
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  const float2 *tw = a.tw2n;  // two-level twiddle table, read through L1 (17 KB at N = 65536)
+  const GlobalTw tw{a.tw2n};  // two-level twiddle table, read through L1 (17 KB at N = 65536)
   const int tid = threadIdx.x;
   const int64_t ul = blockIdx.x;
   int64_t row, mloc, mg;
@@ -299,9 +319,19 @@ __global__ void __launch_bounds__(LT) inv_large_row(const KArgs a) {
   const int n1_0 = blockIdx.y * LB;
   pdl_wait();
   const float2 *W = a.stage + ul * a.zs + a.toff;
-  for (int idx = tid; idx < LB * N2; idx += LT) {
-    const int s = idx / N2, p2 = idx % N2;
-    buf[s * CS + padi(p2)] = W[(int64_t)(n1_0 + s) * N2 + p2];
+  {  // all of a thread's row loads in flight together (streaming, L2 only)
+    constexpr int PERL = LB * N2 / LT;
+    float2 v[PERL];
+#pragma unroll
+    for (int q = 0; q < PERL; ++q) {
+      const int idx = tid + q * LT;
+      v[q] = __ldcs(W + (int64_t)(n1_0 + idx / N2) * N2 + idx % N2);
+    }
+#pragma unroll
+    for (int q = 0; q < PERL; ++q) {
+      const int idx = tid + q * LT;
+      buf[(idx / N2) * CS + padi(idx % N2)] = v[q];
+    }
   }
   __syncthreads();
   bpass<N, N2, R_ROW, 1, +1>(buf, tw);
