@@ -152,15 +152,19 @@ def cfg5_signal(c: SlicqConfig, batch: int | None = None, n: int | None = None) 
     n_full = c.n
     n = n_full if n is None else n
     out = np.empty((b, n), dtype=np.float32)
-    t = np.arange(n, dtype=np.float64) / c.fs
+    blk = 4096  # angle addition per block: sin(w(t0+u)+p) = sin(wt0+p)cos(wu) + cos(wt0+p)sin(wu)
+    nb = -(-n // blk)
+    u = np.arange(blk, dtype=np.float64) / c.fs
+    t0 = np.arange(nb, dtype=np.float64) * (blk / c.fs)
     for i in range(b):
         f = np.exp(rng.uniform(math.log(27.5), math.log(20000.0), size=64))
         ph = rng.uniform(0.0, 2 * np.pi, size=64)
         noise = 0.05 * rng.standard_normal(n_full)[:n]
-        x = noise.copy()
-        for q in range(64):
-            x += 0.125 * np.sin(2 * np.pi * f[q] * t + ph[q])
-        out[i] = x.astype(np.float32)
+        w = 2 * np.pi * f
+        arg0 = np.outer(t0, w) + ph                      # [nb][64] phase at each block start
+        cu, su = np.cos(np.outer(w, u)), np.sin(np.outer(w, u))  # [64][blk]
+        x = (np.sin(arg0) @ cu + np.cos(arg0) @ su).reshape(-1)[:n]
+        out[i] = (noise + 0.125 * x).astype(np.float32)
     return out
 
 

@@ -322,3 +322,40 @@ def test_chunked_staging_is_bit_identical(api, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(c, c2)
     assert torch.equal(y, y2)
+
+
+def _full_size_launch_check(api, cfg_id, pairs_per_row=2, rows=(0, -1)):
+    """Full BASELINE size in bench.py's launch configuration (all rows in one call):
+    sampled (row, slice) coefficients against the oracle, reconstruction of every row."""
+    cfg = CONFIGS[cfg_id]
+    plan = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    x = make_signal(cfg_id)
+    B, n = x.shape
+    xt = torch.from_numpy(x).cuda()
+    c = plan.forward(xt)
+    y = plan.inverse(c, n)
+    torch.cuda.synchronize()
+    S = c.shape[1]
+    rng = np.random.default_rng(cfg_id)
+    worst = 0.0
+    for b in [r % B for r in rows] + rng.integers(0, B, 2).tolist():
+        ms = sorted(set([0, S - 1] + rng.integers(0, S, pairs_per_row).tolist()))
+        cr = oslicq.forward(x[b:b + 1], ref, slices=ms)[0]
+        worst = max(worst, float(slice_errors(c[b, ms].cpu().numpy(), cr).max()))
+    assert worst <= TOL, worst
+    num = torch.linalg.vector_norm((y - xt).double(), dim=1)
+    den = torch.linalg.vector_norm(xt.double(), dim=1)
+    assert float((num / den).max()) <= TOL
+
+
+@pytest.mark.slow
+def test_cfg3_full_size_launch(api):
+    """BASELINE configs[2]: 128 channel-signals of 2^20 samples in one call."""
+    _full_size_launch_check(api, 3)
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_launch(api):
+    """BASELINE configs[4]: 16 signals of 2^22 samples in one call (2N = 131072)."""
+    _full_size_launch_check(api, 5)
