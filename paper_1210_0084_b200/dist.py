@@ -11,6 +11,7 @@ neighbouring slices (the paper's hop-N overlap, with circular indices
 
 Both exchanges are one grouped point-to-point send/recv pair per call
 (torch.distributed.batch_isend_irecv; NCCL over NVLink on GPUs, gloo in the CPU tests).
+Batches of independent signals are split by rows instead (BatchShard: no exchange at all).
 All transform arithmetic runs in the backend's range calls (libslicq.so for the product;
 the tests substitute the oracle to check this host logic without a GPU).
 """
@@ -137,6 +138,34 @@ class SliceRangeShard:
             return None
         full = torch.cat([o[:, :sizes[r] * self.N] for r, o in enumerate(out)], dim=1)
         return full[:, :self.n]
+
+
+class BatchShard:
+    """Independent signals (cfg3's 128 channel-signals, cfg5's 16 signals): rank r
+    owns rows [floor(r B / G), floor((r+1) B / G)) and transforms them whole with no data-path
+    collective (slicq_forward / slicq_inverse on its rows)."""
+
+    def __init__(self, plan, n: int, batch: int, rank: Optional[int] = None,
+                 world: Optional[int] = None, group=None):
+        self.plan = plan
+        self.n = n
+        self.batch = batch
+        self.group = group
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.world = dist.get_world_size(group) if world is None else world
+        if batch < self.world:
+            raise ValueError(f"{batch} signals cannot be split over {self.world} ranks")
+        b = slice_bounds(batch, self.world)
+        self.r0, self.r1 = b[self.rank], b[self.rank + 1]
+
+    def local_input(self, x_full: torch.Tensor, device=None) -> torch.Tensor:
+        return x_full[self.r0:self.r1].to(device if device is not None else x_full.device)
+
+    def forward(self, xl: torch.Tensor, out=None) -> torch.Tensor:
+        return self.plan.forward(xl, out=out)
+
+    def inverse(self, c: torch.Tensor, out=None) -> torch.Tensor:
+        return self.plan.inverse(c, self.n, out=out)
 
 
 class LibBackend:
