@@ -349,6 +349,41 @@ __device__ __noinline__ void fwd_step1(const float2 *twM, float2 *reg, int m2, i
   }
 }
 
+// F3 fold fused into F4 step 1: task (ci, p2) reads its column q = M2 p1 + p2, p1 < M1, of
+// the folded vector straight from the element table (entry c M + q: bin | ..., weight with
+// the conjugation flag as its sign) and the unit's staged spectrum -- M1 independent loads
+// in flight per lane, no shared-memory round trip; DFT_{M1} (sign +), twiddle, stores
+// A[n1 S2 + p2].  Virtual channel ci = u * r + c (unit u of the task, channel c).
+template <int M1, int V>  // V: channel-kernel variant (separate register budgets)
+__device__ __noinline__ void fwd_step1f(const uint2 *ent, const float2 *X, int64_t xs, int r,
+                                           unsigned magc, const float2 *twM, float2 *reg, int m2,
+                                           int nch, unsigned mag2, int twoff_lane, int lane) {
+  const int nt = nch * m2;
+  const bool act = lane < nt;
+  const int ci = act ? (lane * (int)mag2) >> 16 : 0;
+  const int p2 = act ? lane - ci * m2 : 0;
+  const int twoff = __shfl_sync(FULL, twoff_lane, ci);
+  if (!act) return;
+  const int u = (ci * (int)magc) >> 16, c = ci - u * r;
+  const int M = M1 * m2;
+  const uint2 *e0 = ent + c * M + p2;
+  const float2 *Xu = X + u * xs;
+  float2 v[M1];
+#pragma unroll
+  for (int p1 = 0; p1 < M1; ++p1) {
+    const uint2 en = __ldg(e0 + m2 * p1);
+    const float2 xv = __ldg(Xu + (en.x & 0x3ffff));
+    const float gv = __uint_as_float(en.y);  // sign bit: conjugate X (g >= 0)
+    v[p1] = make_float2(xv.x * fabsf(gv), xv.y * gv);
+  }
+  dft<M1, +1>(v);
+  chan_twiddle<M1, +1>(v, p2, M, twM + twoff);
+  const int S2 = m2 | 1;
+  float2 *base = reg + ci * M1 * S2;
+#pragma unroll
+  for (int n1 = 0; n1 < M1; ++n1) base[n1 * S2 + p2] = v[n1];
+}
+
 // F4 step 2 + F5: task (ci, n1): DFT_{M2} over p2 -> c[n1 + M1 n2] (coalesced over n1).
 template <int M2, int V>  // V: channel-kernel variant (separate register budgets)
 __device__ __noinline__ void fwd_step2(const float2 *reg, float2 *out_row, int m1, int nch,
@@ -525,22 +560,14 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArg
         }
         continue;
       }
-      // F3 fold from the element table (coalesced over e; positions conflict-free)
-      for (int u = 0; u < nuu; ++u) {
-        const float2 *Xu = opaque(X + (int64_t)u * a.xs);  // 32-bit indexing off one base
-        float2 *su = scr + u * P.ustride;
-        SLICQ_UNROLL(SLICQ_FOLD_UNROLL)
-        for (int e = lane; e < ne; e += 32) {
-          const uint2 en = __ldg(ent + e);
-          const float2 xv = SLICQ_XLOAD(Xu + (en.x & 0x3ffff));
-          const float gv = __uint_as_float(en.y);  // sign bit: conjugate X (g >= 0)
-          su[en.x >> 18] = make_float2(xv.x * fabsf(gv), xv.y * gv);
-        }
-      }
-      __syncwarp();
+      // F3 fold fused into step 1 (loads straight from the element table and the spectrum)
+      (void)ne;
       switch (m1) {
-#define X_(S) \
-  case S: if constexpr (S <= MAXS) fwd_step1<S, MAXS>(a.twM, scr, m2, nvc, P.mag2, c_twoff, lane); break;
+#define X_(S)                                                                               \
+  case S:                                                                                   \
+    if constexpr (S <= MAXS)                                                                \
+      fwd_step1f<S, MAXS>(ent, X, a.xs, r, P.magc, a.twM, scr, m2, nvc, P.mag2, c_twoff, lane); \
+    break;
         SLICQ_SIZES(X_)
 #undef X_
       }
