@@ -1036,20 +1036,24 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
         dft<R, +1>(v[q]);
       }
     }
-    // stage the output frame (unpadded float array in the spectrum buffer), then write the
-    // exclusive part and the two transitions as contiguous, coalesced runs
-    __syncthreads();  // every thread has read its last-pass inputs
-    float2 *fz = reinterpret_cast<float2 *>(spec);
-    const float *fr = reinterpret_cast<const float *>(spec);
+    // stage the output frame z[p] = (f[2p], f[2p+1]) in place: the last pass's outputs
+    // j + r NS are exactly the padded entries its task read (NS = N / R), so no barrier is
+    // needed between the reads and the writes; then write the exclusive part and the two
+    // transitions as contiguous, coalesced runs
+    static_assert(NS == TASKS, "the last Stockham pass is in place");
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = tid + q * T;
       if (TASKS % T == 0 || j < TASKS) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) fz[j + r * NS] = cscale(v[q][r], invN);
+        for (int r = 0; r < R; ++r) spec[padi(j + r * NS)] = cscale(v[q][r], invN);
       }
     }
     __syncthreads();
+    auto fr = [&](int i) {  // frame sample i
+      const float2 z = spec[padi(i >> 1)];
+      return (i & 1) ? z.y : z.x;
+    };
     const int64_t sbase = (mg - 1) * N;  // global sample of frame index 0
     // exclusive part |t| <= A: h~_0 = 1.  Interior frames (no wrap, no trim, no spill): a
     // plain coalesced copy; the others take the per-sample index logic.
@@ -1058,10 +1062,10 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
                    : (sbase + N - A - a.y_base >= 0);
     if (excl_direct) {
       float *yo = yrow + (a.circular ? sbase : sbase - a.y_base);
-      for (int i = N - A + tid; i <= N + A; i += T) yo[i] = fr[i];
+      for (int i = N - A + tid; i <= N + A; i += T) yo[i] = fr(i);
     } else {
       for (int i = N - A + tid; i <= N + A; i += T) {
-        const float val = fr[i];
+        const float val = fr(i);
         const int64_t sg = sbase + i;
         if (a.circular) {
           const int64_t sw = sg < 0 ? sg + a.L : (sg >= a.L ? sg - a.L : sg);
@@ -1076,12 +1080,12 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
     // transitions, u = 0 .. tr-2 (|t| = A + 1 + u on the right, Bw - 1 - u on the left)
     for (int u = tid; u < a.tr - 1; u += T) {
       const int il = N - Bw + 1 + u;  // left: t = u - Bw + 1
-      const float vl = fr[il] * htab[Bw - 2 - u - A];
+      const float vl = fr(il) * htab[Bw - 2 - u - A];
       const int64_t sl = sbase + il;
       if (left_paired) bnd_row[((int64_t)bl * 2 + 1) * trp + u] = vl;
       else a.spill[row * a.halo + (sl - a.y_base + a.halo)] = vl;
       const int ir = N + A + 1 + u;   // right: t = A + 1 + u
-      const float vr = fr[ir] * htab[u];
+      const float vr = fr(ir) * htab[u];
       if (right_paired) bnd_row[((int64_t)br * 2 + 0) * trp + u] = vr;
       else yrow[sbase + ir - a.y_base] = vr;
     }
@@ -1102,12 +1106,12 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
     __shared__ int sflag[2];
     if (tid == 0) {
       __threadfence();
-      int fl = 0, fr = 0;
-      if (left_paired) fl = (atomicAdd(a.cnt + row * S + bl, 1u) & 1u) ? 1 : 0;
-      if (right_paired) fr = (atomicAdd(a.cnt + row * S + br, 1u) & 1u) ? 1 : 0;
+      int second_l = 0, second_r = 0;
+      if (left_paired) second_l = (atomicAdd(a.cnt + row * S + bl, 1u) & 1u) ? 1 : 0;
+      if (right_paired) second_r = (atomicAdd(a.cnt + row * S + br, 1u) & 1u) ? 1 : 0;
       __threadfence();
-      sflag[0] = fl;
-      sflag[1] = fr;
+      sflag[0] = second_l;
+      sflag[1] = second_r;
     }
     __syncthreads();
     // the partner's half from the workspace, this CTA's own half recomputed from the frame
@@ -1130,8 +1134,8 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       for (int u = tid; u < a.tr - 1; u += T) {
         const float p0 = f0 ? __ldcg(hp0 + u) : 0.f, p1 = f1 ? __ldcg(hp1 + u) : 0.f;
         // __fmul_rn: no contraction into an FMA with the add (the half must round as stored)
-        if (f0) put(s0 + u, p0 + __fmul_rn(fr[N - Bw + 1 + u], htab[Bw - 2 - u - A]));
-        if (f1) put(s1 + u, p1 + __fmul_rn(fr[N + A + 1 + u], htab[u]));
+        if (f0) put(s0 + u, p0 + __fmul_rn(fr(N - Bw + 1 + u), htab[Bw - 2 - u - A]));
+        if (f1) put(s1 + u, p1 + __fmul_rn(fr(N + A + 1 + u), htab[u]));
       }
     }
   }
