@@ -80,7 +80,10 @@ size_t spec_smem_for(int logN, int tr) {
 }
 
 constexpr size_t kSmemCap = 227 * 1024;  // per CTA
-constexpr int kSmallCap = 640;           // float2 scratch entries a small packet may use
+#ifndef SLICQ_SMALL_CAP
+#define SLICQ_SMALL_CAP 640
+#endif
+constexpr int kSmallCap = SLICQ_SMALL_CAP;  // float2 scratch entries a small packet may use
 #ifndef SLICQ_SMALL_MAX
 #define SLICQ_SMALL_MAX 32
 #endif
