@@ -325,30 +325,6 @@ __device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes, int id
 // warp scratch: first the length-M vector (fold / F), in between A[n1][p2].  Small packets
 // (M <= 32) give each lane a whole channel.
 
-// F4 step 1, in place: task (ci, p2) takes buf[M2 p1 + p2], p1 < M1; DFT_{M1} (sign +);
-// twiddle e^{+2 pi i p2 n1 / M}; stores A[n1 S2 + p2].
-template <int M1, int V>  // V: channel-kernel variant (separate register budgets)
-__device__ __noinline__ void fwd_step1(const float2 *twM, float2 *reg, int m2, int nch,
-                                          unsigned mag2, int twoff_lane, int lane) {
-  const int nt = nch * m2;
-  const bool act = lane < nt;
-  const int ci = act ? (lane * (int)mag2) >> 16 : 0;
-  const int p2 = act ? lane - ci * m2 : 0;
-  const int S2 = m2 | 1;
-  float2 *base = reg + ci * M1 * S2;
-  float2 v[M1];
-#pragma unroll
-  for (int p1 = 0; p1 < M1; ++p1) v[p1] = base[m2 * p1 + p2];
-  const int twoff = __shfl_sync(FULL, twoff_lane, ci);
-  __syncwarp();
-  if (act) {
-    dft<M1, +1>(v);
-    chan_twiddle<M1, +1>(v, p2, M1 * m2, twM + twoff);
-#pragma unroll
-    for (int n1 = 0; n1 < M1; ++n1) base[n1 * S2 + p2] = v[n1];
-  }
-}
-
 // F3 fold fused into F4 step 1: task (ci, p2) reads its column q = M2 p1 + p2, p1 < M1, of
 // the folded vector straight from the element table (entry c M + q: bin | ..., weight with
 // the conjugation flag as its sign) and the unit's staged spectrum -- M1 independent loads
