@@ -359,3 +359,38 @@ def test_cfg3_full_size_launch(api):
 def test_cfg5_full_size_launch(api):
     """BASELINE configs[4]: 16 signals of 2^22 samples in one call (2N = 131072)."""
     _full_size_launch_check(api, 5)
+
+
+@pytest.mark.gpu
+def test_hot_path_error_returns(api):
+    """The C ABI rejects bad calls with SLICQ_ESHAPE (include/slicq.h) instead of launching:
+    workspace too small or misaligned, NULL buffers, n < 1, batch < 1, misaligned
+    coefficients; the library stays usable afterwards."""
+    import ctypes as C
+    from paper_1210_0084_b200 import _lib
+    L = _lib.lib()
+    plan = api.plan_for_config(CONFIGS[1])
+    n, B = 3 * 8192, 1
+    S = plan.num_slices(n)
+    x = torch.randn(B, n, device="cuda")
+    c = torch.empty((B, S, plan.coeffs_per_slice), dtype=torch.complex64, device="cuda")
+    y = torch.empty((B, n), device="cuda")
+    nb = plan.workspace_bytes(S, B)
+    ws = torch.zeros(nb // 4 + 64, dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    h = plan._h
+    ES = -3
+    assert L.slicq_forward(h, x.data_ptr(), n, B, c.data_ptr(), ws.data_ptr(), nb - 16, st) == ES
+    assert L.slicq_forward(h, x.data_ptr(), n, B, c.data_ptr(), ws.data_ptr() + 4, nb, st) == ES
+    assert L.slicq_forward(h, None, n, B, c.data_ptr(), ws.data_ptr(), nb, st) == ES
+    assert L.slicq_forward(h, x.data_ptr(), 0, B, c.data_ptr(), ws.data_ptr(), nb, st) == ES
+    assert L.slicq_forward(h, x.data_ptr(), n, 0, c.data_ptr(), ws.data_ptr(), nb, st) == ES
+    assert L.slicq_forward(h, x.data_ptr(), n, B, c.data_ptr() + 4, ws.data_ptr(), nb, st) == ES
+    assert L.slicq_inverse(h, c.data_ptr(), n, B, None, ws.data_ptr(), nb, st) == ES
+    assert L.slicq_inverse(h, c.data_ptr(), n, B, y.data_ptr(), ws.data_ptr(), 16, st) == ES
+    assert b"workspace" in L.slicq_last_error() or L.slicq_last_error()
+    # still usable
+    assert L.slicq_forward(h, x.data_ptr(), n, B, c.data_ptr(), ws.data_ptr(), nb, st) == 0
+    assert L.slicq_inverse(h, c.data_ptr(), n, B, y.data_ptr(), ws.data_ptr(), nb, st) == 0
+    torch.cuda.synchronize()
+    assert ((y - x).norm() / x.norm()).item() <= TOL
