@@ -155,6 +155,16 @@ SLICQ_API int slicq_forward(const slicq_plan *p, const float *x, int64_t n, int6
 SLICQ_API int slicq_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n, int64_t batch,
                   float *y, void *ws, size_t ws_bytes, void *stream);
 
+/* slicq_inverse_masked: slicq_inverse of (coeffs * a), the coefficient mask fused into the
+ * inverse's coefficient loads (paper §VI masking):
+ *   mask  device float32 [batch][S][C], the layout of coeffs, 4-byte aligned
+ *   mask_db  0: a = mask (linear amplitude); 1: dB-scaled, a = 10^(-5 (1 - mask)), i.e.
+ *            0 -> -100 dB, 1 -> 0 dB, linear in dB in between
+ * Errors as slicq_inverse (NULL mask -> SLICQ_ESHAPE). */
+SLICQ_API int slicq_inverse_masked(const slicq_plan *p, const slicq_c32 *coeffs, const float *mask,
+                                   int mask_db, int64_t n, int64_t batch, float *y, void *ws,
+                                   size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------ slice-range shards
  * Multi-GPU partition of one long stream: a rank owns slices
  * [slice0, slice0 + nslices) of total_slices = S and input samples

@@ -157,8 +157,11 @@ class Plan:
         return out
 
     def inverse(self, c: torch.Tensor, n: int, out: Optional[torch.Tensor] = None,
-                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
-        """slicq_inverse: complex64 [batch][S][C] -> float32 [batch][n]."""
+                stream: Optional[torch.cuda.Stream] = None, mask: Optional[torch.Tensor] = None,
+                mask_db: bool = True) -> torch.Tensor:
+        """slicq_inverse: complex64 [batch][S][C] -> float32 [batch][n].  With `mask` (float32
+        [batch][S][C]), slicq_inverse_masked: the coefficient mask (dB-scaled unless
+        mask_db=False, paper §VI) is applied inside the inverse's coefficient loads."""
         if c.dim() == 2:
             c = c[None]
         B = c.shape[0]
@@ -169,6 +172,13 @@ class Plan:
         else:
             _check_tensor(out, torch.float32, "out", (B, n))
         ws = self.workspace(S, B, c.device)
+        if mask is not None:
+            _check_tensor(mask, torch.float32, "mask", (B, S, self.coeffs_per_slice))
+            check(lib().slicq_inverse_masked(self._h, c.data_ptr(), mask.data_ptr(),
+                                             1 if mask_db else 0, n, B, out.data_ptr(),
+                                             ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)),
+                  "slicq_inverse_masked")
+            return out
         check(lib().slicq_inverse(self._h, c.data_ptr(), n, B, out.data_ptr(), ws.data_ptr(),
                                   ws.numel() * 4, _stream_ptr(stream)), "slicq_inverse")
         return out

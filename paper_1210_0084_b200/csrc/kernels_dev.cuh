@@ -160,6 +160,8 @@ struct KArgs {
   int64_t C;
   float2 *coef_out;
   const float2 *coef_in;
+  const float *mask;     // inverse: optional real mask [batch][S][C] fused into the loads
+  int mask_db;           // 1: dB-scaled mask, amplitude 10^(-5 (1 - m))
   // staging (workspace): X spectra [unit][xs], contributions [unit][zs]
   float2 *stage;
   int64_t xs, zs;
@@ -402,11 +404,24 @@ __device__ __noinline__ void fwd_small(const uint2 *ent, const float2 *X, float2
   for (int n = 0; n < M; ++n) SLICQ_CSTORE(o + n, v[n]);
 }
 
+// NEXT-4 coefficient mask fused into the inverse's coefficient loads (paper §VI):
+// MK = 0 none, 1 linear amplitude m, 2 dB-scaled amplitude 10^(-5 (1 - m))
+template <int MK>
+__device__ __forceinline__ float2 mask_coef(float2 c, const float *m) {
+  if constexpr (MK == 0) {
+    return c;
+  } else {
+    const float mv = __ldcs(m);
+    const float amp = MK == 1 ? mv : exp10f(-5.0f * (1.0f - mv));
+    return make_float2(c.x * amp, c.y * amp);
+  }
+}
+
 // I2 step 1: task (ci, p2) loads c[M2 p1 + p2]; DFT_{M1} (sign -); twiddle.
-template <int M1, int V>  // V: channel-kernel variant (separate register budgets)
+template <int M1, int V, int MK = 0>  // V: channel-kernel variant; MK: fused mask mode
 __device__ __noinline__ void inv_step1(const float2 *twM, const float2 *in_row, float2 *reg,
                                           int m2, int nch, unsigned mag2, int off_lane,
-                                          int twoff_lane, int lane) {
+                                          int twoff_lane, int lane, const float *mrow = nullptr) {
   const int nt = nch * m2;
   const int ci = lane < nt ? (lane * (int)mag2) >> 16 : 0;
   const int p2 = lane - ci * m2;
@@ -416,6 +431,10 @@ __device__ __noinline__ void inv_step1(const float2 *twM, const float2 *in_row, 
   const float2 *src = in_row + off + p2;
 #pragma unroll
   for (int p1 = 0; p1 < M1; ++p1) v[p1] = __ldcs(src + p1 * m2);
+  if constexpr (MK != 0) {
+#pragma unroll
+    for (int p1 = 0; p1 < M1; ++p1) v[p1] = mask_coef<MK>(v[p1], mrow + off + p2 + p1 * m2);
+  }
   dft<M1, -1>(v);
   chan_twiddle<M1, -1>(v, p2, M1 * m2, twM + twoff);
   const int S2 = m2 | 1;
@@ -446,14 +465,18 @@ __device__ __noinline__ void inv_step2(float2 *reg, int m1, int nch, unsigned ma
 }
 
 // Small inverse packet: lane vc loads virtual channel vc, FFT_M, F[q] -> scratch q*nv + vc.
-template <int M, int V>  // V: channel-kernel variant (separate register budgets)
+template <int M, int V, int MK = 0>  // V: channel-kernel variant; MK: fused mask mode
 __device__ __noinline__ void inv_small(const float2 *in_row, float2 *reg, int nvc, int nv,
-                                          int off_lane, int lane) {
+                                          int off_lane, int lane, const float *mrow = nullptr) {
   if (lane >= nvc) return;
   const float2 *src = in_row + off_lane;
   float2 v[M];
 #pragma unroll
   for (int n = 0; n < M; ++n) v[n] = __ldcs(src + n);
+  if constexpr (MK != 0) {
+#pragma unroll
+    for (int n = 0; n < M; ++n) v[n] = mask_coef<MK>(v[n], mrow + off_lane + n);
+  }
   dft<M, -1>(v);
 #pragma unroll
   for (int q = 0; q < M; ++q) reg[q * nv + lane] = v[q];
@@ -560,7 +583,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArg
   pdl_trigger();
 }
 
-template <int MAXS, int MINB>
+template <int MAXS, int MINB, int MK = 0>
 __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArgs a) {
   extern __shared__ float4 smem4[];
   constexpr int NW = CHAN_T / 32;
@@ -596,6 +619,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
       const int nuu = min(nu, u_hi - g0);
       const int nvc = nuu * r;
       const float2 *in_row = a.coef_in + (a.unit0 + g0) * a.C;
+      const float *mrow = MK ? a.mask + (a.unit0 + g0) * a.C : nullptr;
       if (t + NW < ntask) {
         const int g1 = g0 + NW * nu, n1u = min(nu, u_hi - g1);
         for (int u = 0; u < n1u; ++u)
@@ -604,14 +628,14 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
       if (small) {
         switch (m1) {
 #define X_(S) \
-  case S: if constexpr (S <= MAXS) inv_small<S, MAXS>(in_row, scr, nvc, nu * r, c_off, lane); break;
+  case S: if constexpr (S <= MAXS) inv_small<S, MAXS, MK>(in_row, scr, nvc, nu * r, c_off, lane, mrow); break;
           SLICQ_SMALL(X_)
 #undef X_
         }
       } else {
         switch (m1) {
 #define X_(S) \
-  case S: if constexpr (S <= MAXS) inv_step1<S, MAXS>(a.twM, in_row, scr, m2, nvc, P.mag2, c_off, c_twoff, lane); break;
+  case S: if constexpr (S <= MAXS) inv_step1<S, MAXS, MK>(a.twM, in_row, scr, m2, nvc, P.mag2, c_off, c_twoff, lane, mrow); break;
           SLICQ_SIZES(X_)
 #undef X_
         }

@@ -97,8 +97,13 @@ constexpr int kSmallMax = SLICQ_SMALL_MAX;  // channels with M <= this: one lane
 #endif
 constexpr int kLiteMax = SLICQ_LITE_MAX, kLiteMinB = SLICQ_LITE_MINB, kFullMax = 32, kFullMinB = 2;
 using ChanFn = void (*)(const KArgs);
-static ChanFn chan_fn(bool fwd, bool lite) {
+// mask: inverse with a fused coefficient mask (0 none, 1 linear, 2 dB)
+static ChanFn chan_fn(bool fwd, bool lite, int mask = 0) {
   if (fwd) return lite ? slicq_fwd_chan_kernel<kLiteMax, kLiteMinB> : slicq_fwd_chan_kernel<kFullMax, kFullMinB>;
+  switch (mask) {
+    case 1: return lite ? slicq_inv_chan_kernel<kLiteMax, kLiteMinB, 1> : slicq_inv_chan_kernel<kFullMax, kFullMinB, 1>;
+    case 2: return lite ? slicq_inv_chan_kernel<kLiteMax, kLiteMinB, 2> : slicq_inv_chan_kernel<kFullMax, kFullMinB, 2>;
+  }
   return lite ? slicq_inv_chan_kernel<kLiteMax, kLiteMinB> : slicq_inv_chan_kernel<kFullMax, kFullMinB>;
 }
 
@@ -492,9 +497,9 @@ int upload(slicq_plan *p) {
     case 15: rc = large_set_attrs<15>(); break;
     case 16: rc = large_set_attrs<16>(); break;
   }
-  for (int v = 0; v < 4 && rc == 0; ++v)
-    rc = (int)cudaFuncSetAttribute(chan_fn(v & 1, v & 2), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)p->kc.chan_smem);
+  for (int v = 0; v < 12 && rc == 0; ++v)  // bit 0: forward, bit 1: lite, v >> 2: mask mode
+    rc = (int)cudaFuncSetAttribute(chan_fn(v & 1, v & 2, v >> 2),
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->kc.chan_smem);
   if (rc != 0)
     return set_error(SLICQ_ECUDA, std::string("cudaFuncSetAttribute: ") +
                                       cudaGetErrorString((cudaError_t)rc));
@@ -597,7 +602,7 @@ static cudaError_t launch_chan(bool fwd, const slicq_plan *p, KArgs a, cudaStrea
     a.packets = p->d.packets + (lite ? 0 : nl);
     a.npackets = lite ? nl : np - nl;
     if (a.npackets == 0) continue;
-    const ChanFn fn = chan_fn(fwd, lite);
+    const ChanFn fn = chan_fn(fwd, lite, fwd || !a.mask ? 0 : (a.mask_db ? 2 : 1));
     // small calls (e.g. the ranges of the streaming executor): shrink the tile until there
     // are >= 4 work items per resident CTA (load balance of the persistent grid)
     const int64_t cap = chan_capacity(p, fn);
@@ -675,7 +680,7 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
 int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0, int64_t nslices,
                    int64_t total_slices, int64_t batch, int circular, int64_t n_valid, int64_t L,
                    float *y, int64_t y_stride, int64_t y_base, float *left_spill, int64_t halo,
-                   void *ws, size_t ws_bytes, void *stream) {
+                   void *ws, size_t ws_bytes, void *stream, const float *mask, int mask_db) {
   (void)total_slices;
   int rc = check_device(p);
   if (rc) return rc;
@@ -685,6 +690,8 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
   if ((uintptr_t)ws % 16) return set_error(SLICQ_ESHAPE, "workspace must be 16-byte aligned");
   KArgs a = base_args(p);
   a.coef_in = reinterpret_cast<const float2 *>(coeffs);
+  a.mask = mask;
+  a.mask_db = mask_db;
   a.y = y;
   a.y_len = n_valid;
   a.y_stride = y_stride;

@@ -339,6 +339,21 @@ int slicq_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n, int64
                                ws_bytes, stream);
 }
 
+int slicq_inverse_masked(const slicq_plan *p, const slicq_c32 *coeffs, const float *mask,
+                         int mask_db, int64_t n, int64_t batch, float *y, void *ws,
+                         size_t ws_bytes, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (n < 1 || batch < 1) return set_error(SLICQ_ESHAPE, "n and batch must be >= 1");
+  if (!y || !coeffs || !mask) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)y % 4 || (uintptr_t)coeffs % 8 || (uintptr_t)mask % 4)
+    return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  const int64_t L = slicq_padded_length(p, n);
+  const int64_t S = L / p->N;
+  return slicq::launch_inverse(p, coeffs, 0, S, S, batch, 1, n, L, y, n, 0, nullptr, 0, ws,
+                               ws_bytes, stream, mask, mask_db ? 1 : 0);
+}
+
 int slicq_forward_range(const slicq_plan *p, const float *x_local, int64_t x_len,
                         int64_t x_stride, int64_t halo, int64_t slice0, int64_t nslices,
                         int64_t total_slices, int64_t batch, slicq_c32 *coeffs_local,

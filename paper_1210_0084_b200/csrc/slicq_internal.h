@@ -115,7 +115,8 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
 int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0, int64_t nslices,
                    int64_t total_slices, int64_t batch, int circular, int64_t n_valid,
                    int64_t L, float *y, int64_t y_stride, int64_t y_base, float *left_spill,
-                   int64_t halo, void *ws, size_t ws_bytes, void *stream);
+                   int64_t halo, void *ws, size_t ws_bytes, void *stream,
+                   const float *mask = nullptr, int mask_db = 0);
 int launch_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,
                        int64_t batch, void *stream);
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);

@@ -82,3 +82,26 @@ def test_mask_decomposition_adds_up():
     # -100 dB everywhere: the output is x scaled by 1e-5
     y0 = plan.inverse(api.apply_mask(c, 0.0), n)
     assert ((y0 - 1e-5 * x).norm() / (1e-5 * x.norm())).item() <= 1e-5
+
+
+def test_masked_inverse_fused_equals_separate_mask():
+    """slicq_inverse_masked (the mask fused into the inverse's coefficient loads, NEXT-4)
+    equals masking the coefficients first and running slicq_inverse; a mask of ones gives
+    exactly the unmasked inverse; covers lite/full packets (cfg1) and the large path (cfg5
+    plan, 2N = 131072)."""
+    from paper_1210_0084_b200 import api
+    from synth.configs import CONFIGS
+    for cfg_id, n in ((1, 65536), (5, 3 * 131072 + 5)):
+        plan = api.plan_for_config(CONFIGS[cfg_id])
+        x = torch.randn(2, n, device="cuda") * 0.1
+        c = plan.forward(x)
+        g = torch.Generator().manual_seed(cfg_id)
+        m = torch.rand(c.shape, generator=g).cuda()
+        for db in (True, False):
+            y_f = plan.inverse(c, n, mask=m, mask_db=db)
+            y_s = plan.inverse(api.apply_mask(c, m, db=db), n)
+            err = ((y_f - y_s).norm() / y_s.norm()).item()
+            assert err <= 1e-5, (cfg_id, db, err)
+        ones = torch.ones(c.shape, device="cuda")
+        assert torch.equal(plan.inverse(c, n, mask=ones, mask_db=False), plan.inverse(c, n))
+        assert torch.equal(plan.inverse(c, n, mask=ones, mask_db=True), plan.inverse(c, n))
