@@ -165,6 +165,21 @@ SLICQ_API int slicq_inverse_masked(const slicq_plan *p, const slicq_c32 *coeffs,
                                    int mask_db, int64_t n, int64_t batch, float *y, void *ws,
                                    size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------ full-length CQ-NSGT
+ * slicq_nsgt_forward / slicq_nsgt_inverse: the CQ-NSGT of Alg. 1 / Alg. 2 of a
+ * whole signal of length L = sl_len (for L up to the library's 2^17):
+ * the frame is x itself (zero padded from n to L), no slicing window, no overlap; the plan's
+ * channels are the CQ-NSGT's at length L.
+ *   x, y    device float32 [batch][n], 1 <= n <= sl_len
+ *   coeffs  device slicq_c32 [batch][C] (C = slicq_coeffs_per_slice, channel k at
+ *           slicq_channel_offsets[k]; mirror channels not stored, C15)
+ *   ws      >= slicq_workspace_bytes(p, 1, batch) bytes, as for slicq_forward
+ * Errors as slicq_forward / slicq_inverse; n > sl_len gives SLICQ_ESHAPE. */
+SLICQ_API int slicq_nsgt_forward(const slicq_plan *p, const float *x, int64_t n, int64_t batch,
+                                 slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream);
+SLICQ_API int slicq_nsgt_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
+                                 int64_t batch, float *y, void *ws, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------ slice-range shards
  * Multi-GPU partition of one long stream: a rank owns slices
  * [slice0, slice0 + nslices) of total_slices = S and input samples

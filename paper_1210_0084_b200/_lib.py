@@ -29,6 +29,8 @@ SIGNATURES = {
     "slicq_halo": (_i64, [_p]),
     "slicq_workspace_bytes": (_sz, [_p, _i64, _i64]),
     "slicq_kernel_launches": (_i32, [_p, _i32, _i64, _i64]),
+    "slicq_nsgt_forward": (_i32, [_p, _p, _i64, _i64, _p, _p, _sz, _p]),
+    "slicq_nsgt_inverse": (_i32, [_p, _p, _i64, _i64, _p, _p, _sz, _p]),
     "slicq_inverse_masked": (_i32, [_p, _p, _p, _i32, _i64, _i64, _p, _p, _sz, _p]),
     "slicq_process_host_workspace_bytes": (_sz, [_p, _i64, _i64, _i32]),
     "slicq_process_host": (_i32, [_p, _p, _p, _i64, _i64, _i32, _p, _p, _p, _sz, _p]),

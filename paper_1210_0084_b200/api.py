@@ -183,6 +183,37 @@ class Plan:
                                   ws.numel() * 4, _stream_ptr(stream)), "slicq_inverse")
         return out
 
+    def nsgt_forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+                     stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """slicq_nsgt_forward: full-length CQ-NSGT (Alg. 1) of x float32 [batch][n],
+        n <= sl_len -> complex64 [batch][C]."""
+        if x.dim() == 1:
+            x = x[None]
+        _check_tensor(x, torch.float32, "x")
+        B, n = x.shape
+        if out is None:
+            out = torch.empty((B, self.coeffs_per_slice), dtype=torch.complex64, device=x.device)
+        else:
+            _check_tensor(out, torch.complex64, "out", (B, self.coeffs_per_slice))
+        ws = self.workspace(1, B, x.device)
+        check(lib().slicq_nsgt_forward(self._h, x.data_ptr(), n, B, out.data_ptr(), ws.data_ptr(),
+                                       ws.numel() * 4, _stream_ptr(stream)), "slicq_nsgt_forward")
+        return out
+
+    def nsgt_inverse(self, c: torch.Tensor, n: int, out: Optional[torch.Tensor] = None,
+                     stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """slicq_nsgt_inverse: full-length CQ-NSGT synthesis (Alg. 2) -> float32 [batch][n]."""
+        if c.dim() == 1:
+            c = c[None]
+        B = c.shape[0]
+        _check_tensor(c, torch.complex64, "coeffs", (B, self.coeffs_per_slice))
+        if out is None:
+            out = torch.empty((B, n), dtype=torch.float32, device=c.device)
+        ws = self.workspace(1, B, c.device)
+        check(lib().slicq_nsgt_inverse(self._h, c.data_ptr(), n, B, out.data_ptr(), ws.data_ptr(),
+                                       ws.numel() * 4, _stream_ptr(stream)), "slicq_nsgt_inverse")
+        return out
+
     def forward_range(self, x_local: torch.Tensor, halo: int, slice0: int, nslices: int,
                       total_slices: int, out: Optional[torch.Tensor] = None,
                       x_len: Optional[int] = None,

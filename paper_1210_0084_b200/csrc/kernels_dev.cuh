@@ -670,7 +670,10 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
 #endif  // SLICQ_DEFINE_CHAN_KERNELS
 
 // ------------------------------------------------------------------ forward spectrum kernel
-template <int LOGN>
+// MODE 0: sliCQ slice m (Tukey window, hop N, circular indices).  MODE 1: full-length
+// CQ-NSGT (Alg. 1): the frame is the whole signal x[0..2N) (zeros past
+// x_len), no window; one unit per row.
+template <int LOGN, int MODE = 0>
 __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_kernel(const KArgs a) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T;
@@ -699,10 +702,11 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
     const float *xr = a.x + row * a.x_stride;
     const int64_t s0 = (mg - 1) * N - a.base_off;  // local x index of frame sample 0
     const bool vec = ((reinterpret_cast<uintptr_t>(xr + s0) & 7) == 0);  // 8-byte pairs
-    const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
-    for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0 + N + A + 1 + u);
+    const int A = MODE ? N : (N - a.tr) / 2, Bw = MODE ? N + 1 : (N + a.tr) / 2;
+    if constexpr (MODE == 0)
+      for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0 + N + A + 1 + u);
     // window support: pairs q_lo..q_hi hold at least one nonzero-window sample
-    const int q_lo = (N - Bw + 1) >> 1, q_hi = (N + Bw - 1) >> 1;  // inclusive
+    const int q_lo = MODE ? 0 : (N - Bw + 1) >> 1, q_hi = MODE ? N - 1 : (N + Bw - 1) >> 1;
     // interior frames (no wrap, no signal edge, 8-byte aligned row): unchecked pair loads
     const bool fast = vec && s0 + 2 * q_lo >= 0 && s0 + 2 * q_hi + 1 < a.x_len;
     const float2 *xp = reinterpret_cast<const float2 *>(xr + (fast ? s0 : 0));
@@ -747,6 +751,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
           const int q = j + r * TASKS;
           // warp-uniform skip: the warp's 32 pairs all on the flat top (h_0 = 1), or all
           // outside the window support (not loaded: zeros)
+          if constexpr (MODE == 1) continue;  // no window
           const int w0 = jw + r * TASKS, w1 = w0 + 31;
           if ((w0 >= qa && w1 <= qb) || w1 < q_lo || w0 > q_hi) continue;
           if (q >= qa && q <= qb) continue;  // both samples on the flat top (h_0 = 1)
@@ -839,7 +844,9 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
 }
 
 // ------------------------------------------------------------------ inverse spectrum kernel
-template <int LOGN>
+// MODE 0: sliCQ (dual window, overlap-add, paired boundaries).  MODE 1: full-length CQ-NSGT
+// synthesis (Alg. 2): y[row][i] = the frame sample i for i < y_len, nothing else.
+template <int LOGN, int MODE = 0>
 __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_kernel(const KArgs a) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T;
@@ -856,7 +863,9 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
 
   PHASE_INIT();
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
-  for (int u2 = tid; u2 < a.tr - 1; u2 += T) htab[u2] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u2);
+  if constexpr (MODE == 0)
+    for (int u2 = tid; u2 < a.tr - 1; u2 += T)
+      htab[u2] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u2);
   constexpr bool hsm = true;
   pdl_wait();  // contributions of this chunk come from the channel kernel
   prefetch_l2(a.stage + ul * a.zs, a.zs * 8, tid, T);
@@ -1054,6 +1063,13 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       const float2 z = spec[padi(i >> 1)];
       return (i & 1) ? z.y : z.x;
     };
+    if constexpr (MODE == 1) {  // full-length synthesis: the frame is the signal
+      const int cnt = (int)min((int64_t)(2 * N), a.y_len);
+      for (int i = tid; i < cnt; i += T) yrow[i] = fr(i);
+      (void)A; (void)Bw; (void)left_paired; (void)right_paired; (void)bl; (void)br; (void)bnd_row;
+      pdl_trigger();
+      return;
+    }
     const int64_t sbase = (mg - 1) * N;  // global sample of frame index 0
     // exclusive part |t| <= A: h~_0 = 1.  Interior frames (no wrap, no trim, no spill): a
     // plain coalesced copy; the others take the per-sample index logic.
@@ -1155,9 +1171,11 @@ int phase_times(unsigned long long *out32, int reset);
 template <int LOGN>
 int set_attrs(size_t smem);
 template <int LOGN>
-cudaError_t launch_fwd_spec(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s, bool pdl);
+cudaError_t launch_fwd_spec(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s, bool pdl,
+                            int mode = 0);
 template <int LOGN>
-cudaError_t launch_inv_spec(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s, bool pdl);
+cudaError_t launch_inv_spec(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s, bool pdl,
+                            int mode = 0);
 
 }  // namespace kern
 }  // namespace slicq

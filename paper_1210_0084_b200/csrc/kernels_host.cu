@@ -627,24 +627,26 @@ static cudaError_t launch_chan(bool fwd, const slicq_plan *p, KArgs a, cudaStrea
 }
 
 static cudaError_t launch_spec(bool fwd, const slicq_plan *p, const KArgs &a, dim3 grid,
-                               cudaStream_t s) {
+                               cudaStream_t s, int mode) {
   const size_t sm = p->kc.spec_smem;
   switch (p->kc.logN) {
-    case 11:
-      return fwd ? launch_fwd_spec<11>(a, grid, sm, s, true) : launch_inv_spec<11>(a, grid, sm, s, true);
-    case 12:
-      return fwd ? launch_fwd_spec<12>(a, grid, sm, s, true) : launch_inv_spec<12>(a, grid, sm, s, true);
-    case 13:
-      return fwd ? launch_fwd_spec<13>(a, grid, sm, s, true) : launch_inv_spec<13>(a, grid, sm, s, true);
-    case 14:
-      return fwd ? launch_fwd_spec<14>(a, grid, sm, s, true) : launch_inv_spec<14>(a, grid, sm, s, true);
+#define CASE_(L)                                                                           \
+  case L:                                                                                  \
+    return fwd ? launch_fwd_spec<L>(a, grid, sm, s, true, mode)                            \
+               : launch_inv_spec<L>(a, grid, sm, s, true, mode);
+    CASE_(11)
+    CASE_(12)
+    CASE_(13)
+    CASE_(14)
+#undef CASE_
   }
   return cudaErrorInvalidValue;
 }
 
 int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x_stride,
                    int64_t base_off, int64_t L, int wrap, int64_t slice0, int64_t nslices,
-                   int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream) {
+                   int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream,
+                   int mode) {
   int rc = check_device(p);
   if (rc) return rc;
   if (nslices > 0x7fffffff) return set_error(SLICQ_ESHAPE, "too many slices");
@@ -668,8 +670,9 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
   for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
     a.unit0 = u0;
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
-    cudaError_t e = !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), s)
-                    : p->kc.logN == 15 ? large_forward<15>(a, s) : large_forward<16>(a, s);
+    cudaError_t e = !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), s, mode)
+                    : p->kc.logN == 15 ? large_forward<15>(a, s, mode)
+                                       : large_forward<16>(a, s, mode);
     if (e == cudaSuccess) e = launch_chan(true, p, a, s);
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
@@ -680,7 +683,8 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
 int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0, int64_t nslices,
                    int64_t total_slices, int64_t batch, int circular, int64_t n_valid, int64_t L,
                    float *y, int64_t y_stride, int64_t y_base, float *left_spill, int64_t halo,
-                   void *ws, size_t ws_bytes, void *stream, const float *mask, int mask_db) {
+                   void *ws, size_t ws_bytes, void *stream, const float *mask, int mask_db,
+                   int mode) {
   (void)total_slices;
   int rc = check_device(p);
   if (rc) return rc;
@@ -714,8 +718,9 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
     cudaError_t e = launch_chan(false, p, a, s);
     if (e == cudaSuccess)
-      e = !p->kc.large ? launch_spec(false, p, a, dim3((unsigned)a.nunits), s)
-          : p->kc.logN == 15 ? large_inverse_spec<15>(a, s) : large_inverse_spec<16>(a, s);
+      e = !p->kc.large ? launch_spec(false, p, a, dim3((unsigned)a.nunits), s, mode)
+          : p->kc.logN == 15 ? large_inverse_spec<15>(a, s, mode)
+                             : large_inverse_spec<16>(a, s, mode);
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
   }

@@ -8,12 +8,15 @@ namespace kern {
 
 template <>
 int set_attrs<SLICQ_LOGN>(size_t smem) {
-  cudaError_t e1 = cudaFuncSetAttribute(slicq_fwd_spec_kernel<SLICQ_LOGN>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaError_t e2 = cudaFuncSetAttribute(slicq_inv_spec_kernel<SLICQ_LOGN>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e1 != cudaSuccess) return (int)e1;
-  if (e2 != cudaSuccess) return (int)e2;
+  const void *fns[] = {(const void *)slicq_fwd_spec_kernel<SLICQ_LOGN, 0>,
+                       (const void *)slicq_inv_spec_kernel<SLICQ_LOGN, 0>,
+                       (const void *)slicq_fwd_spec_kernel<SLICQ_LOGN, 1>,
+                       (const void *)slicq_inv_spec_kernel<SLICQ_LOGN, 1>};
+  for (const void *f : fns) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
   return 0;
 }
 
@@ -35,14 +38,20 @@ static cudaError_t launch_pdl(K kernel, const KArgs &a, dim3 grid, int threads, 
 
 template <>
 cudaError_t launch_fwd_spec<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s,
-                                        bool pdl) {
-  return launch_pdl(slicq_fwd_spec_kernel<SLICQ_LOGN>, a, grid, Big<SLICQ_LOGN>::T, smem, s, pdl);
+                                        bool pdl, int mode) {
+  if (mode == 1)
+    return launch_pdl(slicq_fwd_spec_kernel<SLICQ_LOGN, 1>, a, grid, Big<SLICQ_LOGN>::T, smem, s,
+                      pdl);
+  return launch_pdl(slicq_fwd_spec_kernel<SLICQ_LOGN, 0>, a, grid, Big<SLICQ_LOGN>::T, smem, s, pdl);
 }
 
 template <>
 cudaError_t launch_inv_spec<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s,
-                                        bool pdl) {
-  return launch_pdl(slicq_inv_spec_kernel<SLICQ_LOGN>, a, grid, Big<SLICQ_LOGN>::T, smem, s, pdl);
+                                        bool pdl, int mode) {
+  if (mode == 1)
+    return launch_pdl(slicq_inv_spec_kernel<SLICQ_LOGN, 1>, a, grid, Big<SLICQ_LOGN>::T, smem, s,
+                      pdl);
+  return launch_pdl(slicq_inv_spec_kernel<SLICQ_LOGN, 0>, a, grid, Big<SLICQ_LOGN>::T, smem, s, pdl);
 }
 
 template <>

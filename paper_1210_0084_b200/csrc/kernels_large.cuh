@@ -89,7 +89,7 @@ __device__ __forceinline__ void unit_coords(const KArgs &a, int64_t ul, int64_t 
 }
 
 // ------------------------------------------------------------------ forward
-template <int LOGN>
+template <int LOGN, int MODE = 0>  // MODE 1: full-length CQ-NSGT frame (no window)
 __global__ void __launch_bounds__(LT) fwd_large_col(const KArgs a) {
   using G = Large<LOGN>;
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N1>();
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(LT) fwd_large_col(const KArgs a) {
       const int at0 = t0 < 0 ? -t0 : t0;
       const int at1 = (t0 + 1) < 0 ? -(t0 + 1) : (t0 + 1);
       float x0 = 0.f, x1 = 0.f;
-      if (at0 < Bw || at1 < Bw) {
+      if (MODE == 1 || at0 < Bw || at1 < Bw) {
         int64_t xi = s0 + i0;
         if (a.wrap && xi < 0) xi += a.L;
         if (vec && xi >= 0 && xi + 1 < a.x_len) {
@@ -126,10 +126,12 @@ __global__ void __launch_bounds__(LT) fwd_large_col(const KArgs a) {
           if (xi >= 0 && xi < a.x_len) x0 = __ldg(xr + xi);
           if (xi + 1 >= 0 && xi + 1 < a.x_len) x1 = __ldg(xr + xi + 1);
         }
-        const float ha = at0 <= A ? 1.f : (at0 < Bw ? __ldg(a.h0 + i0) : 0.f);
-        const float hb = at1 <= A ? 1.f : (at1 < Bw ? __ldg(a.h0 + i0 + 1) : 0.f);
-        x0 *= ha;
-        x1 *= hb;
+        if constexpr (MODE == 0) {
+          const float ha = at0 <= A ? 1.f : (at0 < Bw ? __ldg(a.h0 + i0) : 0.f);
+          const float hb = at1 <= A ? 1.f : (at1 < Bw ? __ldg(a.h0 + i0 + 1) : 0.f);
+          x0 *= ha;
+          x1 *= hb;
+        }
       }
       buf[c * CS + padi(p1)] = make_float2(x0, x1);
     }
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(LT) inv_large_col(const KArgs a) {
 // rows n1 in [16 b, 16 b + 16): z[n1 + N1 n2] -> samples 2n, 2n+1, times h~_0 / N.
 // Exclusive samples go to y; transition samples of a paired boundary to the workspace
 // (combined by inv_large_bnd); unpaired ones (slice-range edges) straight to y / the spill.
-template <int LOGN>
+template <int LOGN, int MODE = 0>  // MODE 1: full-length CQ-NSGT synthesis (frame -> y)
 __global__ void __launch_bounds__(LT) inv_large_row(const KArgs a) {
   using G = Large<LOGN>;
   constexpr int N = G::N, N1 = G::N1, N2 = G::N2, CS = colstride<N2>();
@@ -345,6 +347,19 @@ __global__ void __launch_bounds__(LT) inv_large_row(const KArgs a) {
   const int trp = a.tr;
   float *yrow = a.y + row * a.y_stride;
   float *bnd_row = a.bnd + row * (int64_t)S * 2 * trp;
+  if constexpr (MODE == 1) {  // the frame is the signal: samples 2p, 2p+1 -> y (p < N)
+    for (int idx = tid; idx < LB * N2; idx += LT) {
+      const int s = idx % LB, n2 = idx / LB;
+      const float2 z = buf[s * CS + padi(n2)];
+      const int64_t i = 2 * (int64_t)(n1_0 + s + N1 * n2);
+      if (i < a.y_len) yrow[i] = z.x * invN;
+      if (i + 1 < a.y_len) yrow[i + 1] = z.y * invN;
+    }
+    (void)A; (void)Bw; (void)left_paired; (void)right_paired; (void)bl; (void)br; (void)trp;
+    (void)bnd_row; (void)S;
+    pdl_trigger();
+    return;
+  }
   // consecutive threads take consecutive n1 (16 rows) of one n2: 32 consecutive samples
   for (int idx = tid; idx < LB * N2; idx += LT) {
     const int s = idx % LB, n2 = idx / LB;
@@ -425,9 +440,9 @@ constexpr size_t large_smem_bytes() {
 template <int LOGN>
 int large_set_attrs();
 template <int LOGN>
-cudaError_t large_forward(const KArgs &a, cudaStream_t s);
+cudaError_t large_forward(const KArgs &a, cudaStream_t s, int mode = 0);
 template <int LOGN>
-cudaError_t large_inverse_spec(const KArgs &a, cudaStream_t s);
+cudaError_t large_inverse_spec(const KArgs &a, cudaStream_t s, int mode = 0);
 
 }  // namespace kern
 }  // namespace slicq

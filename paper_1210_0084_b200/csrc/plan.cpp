@@ -339,6 +339,31 @@ int slicq_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n, int64
                                ws_bytes, stream);
 }
 
+int slicq_nsgt_forward(const slicq_plan *p, const float *x, int64_t n, int64_t batch,
+                       slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (n < 1 || batch < 1 || n > 2 * p->N)
+    return set_error(SLICQ_ESHAPE, "need 1 <= n <= sl_len and batch >= 1");
+  if (!x || !coeffs) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)x % 4 || (uintptr_t)coeffs % 8) return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  // one frame per row: "slice" 1 of a 2-slice stream starts at sample 0, no wrap, no window
+  return slicq::launch_forward(p, x, n, n, 0, 2 * p->N, 0, 1, 1, batch, coeffs, ws, ws_bytes,
+                               stream, 1);
+}
+
+int slicq_nsgt_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n, int64_t batch,
+                       float *y, void *ws, size_t ws_bytes, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (n < 1 || batch < 1 || n > 2 * p->N)
+    return set_error(SLICQ_ESHAPE, "need 1 <= n <= sl_len and batch >= 1");
+  if (!y || !coeffs) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)y % 4 || (uintptr_t)coeffs % 8) return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  return slicq::launch_inverse(p, coeffs, 1, 1, 2, batch, 0, n, 2 * p->N, y, n, 0, nullptr, 0, ws,
+                               ws_bytes, stream, nullptr, 0, 1);
+}
+
 int slicq_inverse_masked(const slicq_plan *p, const slicq_c32 *coeffs, const float *mask,
                          int mask_db, int64_t n, int64_t batch, float *y, void *ws,
                          size_t ws_bytes, void *stream) {

@@ -111,12 +111,13 @@ int upload(slicq_plan *p);             // allocates + copies device tables
 void free_device(slicq_plan *p);
 int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x_stride,
                    int64_t base_off, int64_t L, int wrap, int64_t slice0, int64_t nslices,
-                   int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream);
+                   int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream,
+                   int mode = 0);  // mode 1: full-length CQ-NSGT (one frame per row)
 int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0, int64_t nslices,
                    int64_t total_slices, int64_t batch, int circular, int64_t n_valid,
                    int64_t L, float *y, int64_t y_stride, int64_t y_base, float *left_spill,
                    int64_t halo, void *ws, size_t ws_bytes, void *stream,
-                   const float *mask = nullptr, int mask_db = 0);
+                   const float *mask = nullptr, int mask_db = 0, int mode = 0);
 int launch_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,
                        int64_t batch, void *stream);
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
