@@ -182,6 +182,10 @@ struct KArgs {
   const float2 *twM;
   unsigned *cnt;  // inverse workspace: [batch][nslices] pairing counters
   float *bnd;     // inverse workspace: [batch][nslices][2][tr] boundary halves
+  // long full-length CQ-NSGT (kernels_long.cuh): fp32 g_k / sqrt(M_k), g~_k / sqrt(M_k)
+  // (x 1/2 on the plateaus, C15) at the filter offsets goff_k; per-bin term lists (CSR)
+  const float *gw, *gdw;
+  const uint32_t *lrow, *lent;
 };
 
 

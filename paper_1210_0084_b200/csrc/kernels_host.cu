@@ -16,6 +16,11 @@
 #include "kernels_large.cuh"
 
 namespace slicq {
+namespace kern {  // kernels_long.cu (full-length CQ-NSGT of long signals)
+int long_set_attrs(int logN, size_t chan_smem);
+cudaError_t long_forward(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s);
+cudaError_t long_inverse(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s);
+}  // namespace kern
 namespace {
 using namespace slicq::kern;
 
@@ -117,14 +122,92 @@ int64_t env_int(const char *name, int64_t dflt) {
 
 }  // namespace
 
-int device_supports(int logN) { return logN >= 11 && logN <= 16; }
+// logN 11..16: sliCQ (and full-length CQ-NSGT) slices; 17..21: full-length CQ-NSGT only
+int device_supports(int logN) { return logN >= 11 && logN <= 21; }
+
+namespace {
+// Long mode (sl_len = 2^18 .. 2^22): the full-length CQ-NSGT of kernels_long.cuh.  No
+// packets or element tables: per-channel fp32 weights and, for the synthesis, the list of
+// channel terms of every half-spectrum bin (Hermitian rule C15, plan order).
+int configure_long(slicq_plan *p, int logN) {
+  KernelConfig &kc = p->kc;
+  kc.logN = logN;
+  kc.large = false;
+  kc.longmode = true;
+  kc.npackets = kc.nlite = 0;
+  const int K2 = p->K + 2;
+  const int64_t N = p->N, N2 = 2 * N;
+  int maxM = 0;
+  for (int k = 0; k < K2; ++k) maxM = std::max(maxM, (int)p->M[k]);
+  kc.lchan_smem = sizeof(float2) * (size_t)(padi(maxM) + 1);
+  if (kc.lchan_smem > kSmemCap)
+    return set_error(SLICQ_EUNSUPPORTED, "channel length M_k = " + std::to_string(maxM) +
+                                             " exceeds the shared-memory channel FFT of the "
+                                             "long full-length path (M_k <= 27000)");
+  const int64_t nterms = (int64_t)p->g.size();
+  if (nterms >= (int64_t(1) << 31)) return set_error(SLICQ_EUNSUPPORTED, "too many filter terms");
+  p->lgw.assign(nterms, 0.f);
+  p->lgdw.assign(nterms, 0.f);
+  std::vector<uint32_t> cnt(N + 2, 0u);
+  auto bins = [&](int64_t j, int64_t &b1, int64_t &b2) {  // direct bin, conjugate bin (or -1)
+    int64_t p1 = j % N2;
+    if (p1 < 0) p1 += N2;
+    const int64_t p2 = p1 == 0 ? 0 : N2 - p1;
+    b1 = p1 <= N ? p1 : -1;
+    b2 = p2 <= N ? p2 : -1;
+  };
+  for (int k = 0; k < K2; ++k) {
+    const double sc = 1.0 / std::sqrt((double)p->M[k]);
+    const double half = (k == 0 || k == K2 - 1) ? 0.5 : 1.0;  // self-mirrored plateaus (C15)
+    for (int dd = 0; dd < p->len[k]; ++dd) {
+      const int64_t e = p->goff[k] + dd;
+      p->lgw[e] = (float)(p->g[e] * sc);
+      p->lgdw[e] = (float)(p->gdual[e] * sc * half);
+      int64_t b1, b2;
+      bins(p->lo[k] + dd, b1, b2);
+      if (b1 >= 0) ++cnt[b1];
+      if (b2 >= 0) ++cnt[b2];
+    }
+  }
+  p->lrow.assign(N + 2, 0u);
+  for (int64_t b = 0; b <= N; ++b) {
+    if (!cnt[b]) return set_error(SLICQ_EINTERNAL, "half-spectrum bin without a channel term");
+    p->lrow[b + 1] = p->lrow[b] + cnt[b];
+  }
+  p->lent.assign(p->lrow[N + 1], 0u);
+  std::vector<uint32_t> fill(p->lrow.begin(), p->lrow.end() - 1);
+  for (int k = 0; k < K2; ++k)
+    for (int dd = 0; dd < p->len[k]; ++dd) {
+      const uint32_t e = (uint32_t)(p->goff[k] + dd);
+      int64_t b1, b2;
+      bins(p->lo[k] + dd, b1, b2);
+      if (b1 >= 0) p->lent[fill[b1]++] = e;
+      if (b2 >= 0) p->lent[fill[b2]++] = e | 0x80000000u;
+    }
+  // staging per row: X[0..N] then the four-step intermediate (forward); the channel terms
+  // then the packed spectrum W (inverse)
+  kc.toff_f = (N + 2) & ~int64_t(1);
+  kc.xs = kc.toff_f + N;
+  kc.toff_i = (nterms + 1) & ~int64_t(1);
+  kc.zs = kc.toff_i + N;
+  kc.zso = 0;
+  kc.nover = 0;
+  kc.tile = 1;
+  const int64_t per_unit = sizeof(float2) * std::max(kc.xs, kc.zs);
+  const int64_t budget = env_int("SLICQ_STAGE_MB", 8192) << 20;
+  kc.chunk_units = std::min<int64_t>(65535, std::max<int64_t>(1, budget / per_unit));
+  return SLICQ_OK;
+}
+}  // namespace
 
 int configure_kernels(slicq_plan *p) {
   int logN = 0;
   while ((int64_t(1) << logN) < p->N) ++logN;
   if ((int64_t(1) << logN) != p->N || !device_supports(logN))
     return set_error(SLICQ_EUNSUPPORTED,
-                     "CUDA path implements sl_len = 2^12 .. 2^17");
+                     "CUDA path implements sl_len = 2^12 .. 2^17 (sliCQ) and up to 2^22 "
+                     "(full-length CQ-NSGT)");
+  if (logN >= 17) return configure_long(p, logN);
   KernelConfig &kc = p->kc;
   kc.logN = logN;
   kc.large = logN >= 15;
@@ -459,6 +542,10 @@ int upload(slicq_plan *p) {
       {h0d.data(), sizeof(float) * h0d.size(), 0},
       {tw.data(), sizeof(float) * tw.size(), 0},
       {twM.data(), sizeof(float) * twM.size(), 0},
+      {p->lgw.data(), sizeof(float) * p->lgw.size(), 0},
+      {p->lgdw.data(), sizeof(float) * p->lgdw.size(), 0},
+      {p->lrow.data(), sizeof(uint32_t) * p->lrow.size(), 0},
+      {p->lent.data(), sizeof(uint32_t) * p->lent.size(), 0},
   };
   size_t o = 0;
   for (Part &pt : parts) {
@@ -485,6 +572,10 @@ int upload(slicq_plan *p) {
   p->d.h0dual = reinterpret_cast<float *>(b + parts[7].off);
   p->d.tw2n = reinterpret_cast<float *>(b + parts[8].off);
   p->d.twM = reinterpret_cast<float *>(b + parts[9].off);
+  p->d.gw = reinterpret_cast<float *>(b + parts[10].off);
+  p->d.gdw = reinterpret_cast<float *>(b + parts[11].off);
+  p->d.lrow = reinterpret_cast<uint32_t *>(b + parts[12].off);
+  p->d.lent = reinterpret_cast<uint32_t *>(b + parts[13].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
@@ -496,8 +587,9 @@ int upload(slicq_plan *p) {
     case 14: rc = set_attrs<14>(p->kc.spec_smem); break;
     case 15: rc = large_set_attrs<15>(); break;
     case 16: rc = large_set_attrs<16>(); break;
+    default: rc = long_set_attrs(p->kc.logN, p->kc.lchan_smem); break;
   }
-  for (int v = 0; v < 12 && rc == 0; ++v)  // bit 0: forward, bit 1: lite, v >> 2: mask mode
+  for (int v = 0; v < 12 && rc == 0 && !p->kc.longmode; ++v)  // bit 0: forward, bit 1: lite, v >> 2: mask mode
     rc = (int)cudaFuncSetAttribute(chan_fn(v & 1, v & 2, v >> 2),
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->kc.chan_smem);
   if (rc != 0)
@@ -536,6 +628,7 @@ WsLayout ws_layout(const slicq_plan *p, int64_t nslices, int64_t batch) {
 int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t batch) {
   const WsLayout w = ws_layout(p, nslices, batch);
   const int64_t chunks = (nslices * batch + w.chunk - 1) / w.chunk;
+  if (p->kc.longmode) return (int)(chunks * (direction == 0 ? 3 : 4));
   const int nchan = (p->kc.nlite > 0) + (p->kc.npackets > p->kc.nlite);
   const int nspec = !p->kc.large ? 1 : direction == 0 ? 2 : 4;
   return (int)(chunks * (nchan + nspec));
@@ -566,6 +659,10 @@ static KArgs base_args(const slicq_plan *p) {
   a.xs = p->kc.xs;
   a.zs = p->kc.zs;
   a.tile = p->kc.tile;
+  a.gw = p->d.gw;
+  a.gdw = p->d.gdw;
+  a.lrow = p->d.lrow;
+  a.lent = p->d.lent;
   return a;
 }
 
@@ -667,6 +764,19 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t units = nslices * batch;
   a.toff = p->kc.toff_f;
+  if (p->kc.longmode) {  // full-length CQ-NSGT only (kernels_long.cuh)
+    if (mode != 1 || nslices != 1)
+      return set_error(SLICQ_EUNSUPPORTED, "sl_len > 2^17: only the full-length CQ-NSGT "
+                                           "(slicq_nsgt_forward / slicq_nsgt_inverse)");
+    for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
+      a.unit0 = u0;
+      a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
+      const cudaError_t e = long_forward(p->kc.logN, a, p->K + 2, p->kc.lchan_smem, s);
+      if (e != cudaSuccess)
+        return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
+    }
+    return SLICQ_OK;
+  }
   for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
     a.unit0 = u0;
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
@@ -713,6 +823,19 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t units = nslices * batch;
   a.toff = p->kc.toff_i;
+  if (p->kc.longmode) {  // full-length CQ-NSGT only (kernels_long.cuh)
+    if (mode != 1 || nslices != 1 || mask)
+      return set_error(SLICQ_EUNSUPPORTED, "sl_len > 2^17: only the full-length CQ-NSGT "
+                                           "(slicq_nsgt_forward / slicq_nsgt_inverse)");
+    for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
+      a.unit0 = u0;
+      a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
+      const cudaError_t e = long_inverse(p->kc.logN, a, p->K + 2, p->kc.lchan_smem, s);
+      if (e != cudaSuccess)
+        return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
+    }
+    return SLICQ_OK;
+  }
   for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
     a.unit0 = u0;
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);

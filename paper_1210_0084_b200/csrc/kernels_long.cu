@@ -1,0 +1,104 @@
+// Full-length CQ-NSGT of long signals (L = 2^18 .. 2^22), see kernels_long.cuh.
+#include "kernels_long.cuh"
+
+namespace slicq {
+namespace kern {
+
+template <class K>
+static cudaError_t pdl_launch(K kernel, const KArgs &a, dim3 grid, int threads, size_t smem,
+                              cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
+template <int LOGN>
+static int set_attrs_logn() {
+  const int cs = (int)long_col_smem<LOGN>(), rs = (int)large_smem_bytes<LOGN>();
+  cudaError_t e = cudaFuncSetAttribute(long_fwd_col<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(long_inv_col<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fwd_large_row<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(inv_large_row<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
+  return (int)e;
+}
+
+int long_set_attrs(int logN, size_t chan_smem) {
+  int rc = 0;
+  switch (logN) {
+    case 17: rc = set_attrs_logn<17>(); break;
+    case 18: rc = set_attrs_logn<18>(); break;
+    case 19: rc = set_attrs_logn<19>(); break;
+    case 20: rc = set_attrs_logn<20>(); break;
+    case 21: rc = set_attrs_logn<21>(); break;
+    default: return (int)cudaErrorInvalidValue;
+  }
+  if (rc) return rc;
+  cudaError_t e = cudaFuncSetAttribute(long_chan_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chan_smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(long_chan_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chan_smem);
+  return (int)e;
+}
+
+template <int LOGN>
+static cudaError_t fwd_logn(const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s) {
+  using G = Large<LOGN>;
+  const unsigned nu = (unsigned)a.nunits;
+  cudaError_t e = pdl_launch(long_fwd_col<LOGN>, a, dim3(nu, G::N2 / LongCol<LOGN>::NB), LCT,
+                             long_col_smem<LOGN>(), s);
+  if (e == cudaSuccess)
+    e = pdl_launch(fwd_large_row<LOGN>, a, dim3(nu, (G::N1 / 2 + 1 + 7) / 8), LT,
+                   large_smem_bytes<LOGN>(), s);
+  if (e == cudaSuccess) e = pdl_launch(long_chan_fwd, a, dim3((unsigned)nchan, nu), LKT, chan_smem, s);
+  return e;
+}
+
+template <int LOGN>
+static cudaError_t inv_logn(const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s) {
+  using G = Large<LOGN>;
+  const unsigned nu = (unsigned)a.nunits;
+  cudaError_t e = pdl_launch(long_chan_inv, a, dim3((unsigned)nchan, nu), LKT, chan_smem, s);
+  if (e == cudaSuccess)
+    e = pdl_launch(long_inv_pack, a, dim3(nu, (G::N / 2 + 1 + LT - 1) / LT), LT, 0, s);
+  if (e == cudaSuccess)
+    e = pdl_launch(long_inv_col<LOGN>, a, dim3(nu, G::N2 / LongCol<LOGN>::NB), LCT,
+                   long_col_smem<LOGN>(), s);
+  if (e == cudaSuccess)
+    e = pdl_launch(inv_large_row<LOGN, 1>, a, dim3(nu, G::N1 / LB), LT, large_smem_bytes<LOGN>(), s);
+  return e;
+}
+
+cudaError_t long_forward(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s) {
+  switch (logN) {
+    case 17: return fwd_logn<17>(a, nchan, chan_smem, s);
+    case 18: return fwd_logn<18>(a, nchan, chan_smem, s);
+    case 19: return fwd_logn<19>(a, nchan, chan_smem, s);
+    case 20: return fwd_logn<20>(a, nchan, chan_smem, s);
+    case 21: return fwd_logn<21>(a, nchan, chan_smem, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t long_inverse(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s) {
+  switch (logN) {
+    case 17: return inv_logn<17>(a, nchan, chan_smem, s);
+    case 18: return inv_logn<18>(a, nchan, chan_smem, s);
+    case 19: return inv_logn<19>(a, nchan, chan_smem, s);
+    case 20: return inv_logn<20>(a, nchan, chan_smem, s);
+    case 21: return inv_logn<21>(a, nchan, chan_smem, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace kern
+}  // namespace slicq

@@ -1,0 +1,377 @@
+// Full-length CQ-NSGT for long signals, L = 2N = 2^18 .. 2^22:
+// Alg. 1 / Alg. 2 on the whole signal, one "unit" per batch row.  The sliCQ
+// path's per-slice machinery (packet tables, 14/17-bit element encodings, one-CTA spectra)
+// is sized for slices <= 2^17; a whole signal needs the same steps at larger sizes:
+//
+//   FFT_L (r2c)   four-step N = N1 * 256 through the staging buffer: long_fwd_col (NB
+//                 columns of N1 points per CTA, three Stockham passes in shared memory,
+//                 twiddle) -> fwd_large_row (256-point rows + r2c packing, kernels_large.cuh)
+//   channels      long_chan_fwd: one CTA per (channel, row): fold X(j) g_k[j]/sqrt(M_k) into
+//                 a shared-memory vector of M_k (painless: one term per position, M_k >= L_k),
+//                 in-place mixed-radix (2/3/4/5/8/9/16/25) decimation-in-frequency IFFT_{M_k}
+//                 (runtime radix sequence, table twiddles e^{2 pi i t/M_k}), coefficients
+//                 stored from the digit-reversed positions
+//   synthesis     long_chan_inv: FFT_{M_k} of c_k, term F_k[j mod M_k] g~_k[j]/sqrt(M_k) per
+//                 support bin to the row's term array (channel k at goff_k);
+//                 long_inv_pack: per half-spectrum bin the sum of its terms in plan order
+//                 (CSR: term index | conj << 31, Hermitian rule C15) + c2r packing;
+//                 long_inv_col + inv_large_row<LOGN, 1> (c2r IFFT_L, 1/N, y)
+//
+// Deterministic (no atomics).  M_k is limited by shared memory (M_k <= 27 000, checked at
+// plan time); the radix sequence is the greedy rule long_radix() on both sides (the
+// butterflies and the digit reversal of the output).
+#pragma once
+#include "kernels_large.cuh"
+
+namespace slicq {
+namespace kern {
+
+template <>
+struct Large<17> {
+  static constexpr int N = 1 << 17, N1 = 512, N2 = 256;
+};
+template <>
+struct Large<18> {
+  static constexpr int N = 1 << 18, N1 = 1024, N2 = 256;
+};
+template <>
+struct Large<19> {
+  static constexpr int N = 1 << 19, N1 = 2048, N2 = 256;
+};
+template <>
+struct Large<20> {
+  static constexpr int N = 1 << 20, N1 = 4096, N2 = 256;
+};
+template <>
+struct Large<21> {
+  static constexpr int N = 1 << 21, N1 = 8192, N2 = 256;
+};
+
+// column FFTs of the four-step: P = N1 points, NB columns per CTA (NB * P = 8192 points,
+// 16 per thread), radices R1 R2 R3 (R3 = 1: two passes)
+template <int LOGN>
+struct LongCol;
+template <>
+struct LongCol<17> {
+  static constexpr int P = 512, NB = 16, R1 = 16, R2 = 32, R3 = 1;
+};
+template <>
+struct LongCol<18> {
+  static constexpr int P = 1024, NB = 8, R1 = 32, R2 = 32, R3 = 1;
+};
+template <>
+struct LongCol<19> {
+  static constexpr int P = 2048, NB = 4, R1 = 16, R2 = 16, R3 = 8;
+};
+template <>
+struct LongCol<20> {
+  static constexpr int P = 4096, NB = 2, R1 = 16, R2 = 16, R3 = 16;
+};
+template <>
+struct LongCol<21> {
+  static constexpr int P = 8192, NB = 1, R1 = 16, R2 = 16, R3 = 32;
+};
+constexpr int LCT = 512;  // column-kernel threads
+constexpr int LKT = 512;  // channel-kernel threads
+
+template <int LOGN>
+constexpr size_t long_col_smem() {
+  return sizeof(float2) * (size_t)(LongCol<LOGN>::NB * colstride<LongCol<LOGN>::P>());
+}
+
+// NB independent P-point Stockham passes in shared memory (column c at c * CS), LCT threads
+template <int NTAB, int P, int NB, int R, int NS, int SIGN, class TW>
+__device__ __forceinline__ void cpass(float2 *buf, TW tw) {
+  if constexpr (R > 1) {
+    constexpr int TPC = P / R, TASKS = NB * TPC, PER = (TASKS + LCT - 1) / LCT;
+    constexpr int CS = colstride<P>();
+    float2 v[PER][R];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int t = threadIdx.x + q * LCT;
+      if (TASKS % LCT == 0 || t < TASKS) {
+        const int c = t / TPC, j = t - c * TPC;
+        const float2 *col = buf + c * CS;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[q][r] = col[padi(j + r * TPC)];
+        pass_twiddle<NTAB, R, NS, SIGN>(v[q], j, tw);
+        dft<R, SIGN>(v[q]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int t = threadIdx.x + q * LCT;
+      if (TASKS % LCT == 0 || t < TASKS) {
+        const int c = t / TPC, j = t - c * TPC;
+        float2 *col = buf + c * CS;
+        const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+        for (int r = 0; r < R; ++r) col[padi(base + r * NS)] = v[q][r];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// forward four-step, first half: z[N2 p1 + p2] = (x[2p], x[2p+1]) (zero past n), DFT_N1 over
+// p1 for NB consecutive columns p2, twiddle w_N^{p2 k1}, T[k1][p2] to the staging buffer
+template <int LOGN>
+__global__ void __launch_bounds__(LCT) long_fwd_col(const KArgs a) {
+  using G = LongCol<LOGN>;
+  constexpr int N = 1 << LOGN, P = G::P, NB = G::NB, N2 = 256, CS = colstride<P>();
+  static_assert(P * N2 == N, "four-step split");
+  extern __shared__ float4 smem4[];
+  float2 *buf = reinterpret_cast<float2 *>(smem4);
+  const GlobalTw tw{a.tw2n};
+  const int tid = threadIdx.x;
+  const int64_t ul = blockIdx.x;
+  const int64_t row = a.unit0 + ul;
+  const int p2_0 = blockIdx.y * NB;
+  pdl_wait();
+  const float *xr = a.x + row * a.x_stride;
+  const bool vec = ((reinterpret_cast<uintptr_t>(xr) & 7) == 0);
+  for (int idx = tid; idx < NB * P; idx += LCT) {
+    const int c = idx % NB, p1 = idx / NB;
+    const int64_t i0 = 2 * (int64_t)(N2 * p1 + p2_0 + c);
+    float x0 = 0.f, x1 = 0.f;
+    if (vec && i0 + 1 < a.x_len) {
+      const float2 xv = __ldcs(reinterpret_cast<const float2 *>(xr + i0));
+      x0 = xv.x;
+      x1 = xv.y;
+    } else {
+      if (i0 < a.x_len) x0 = __ldg(xr + i0);
+      if (i0 + 1 < a.x_len) x1 = __ldg(xr + i0 + 1);
+    }
+    buf[c * CS + padi(p1)] = make_float2(x0, x1);
+  }
+  __syncthreads();
+  cpass<N, P, NB, G::R1, 1, -1>(buf, tw);
+  cpass<N, P, NB, G::R2, G::R1, -1>(buf, tw);
+  cpass<N, P, NB, G::R3, G::R1 * G::R2, -1>(buf, tw);
+  float2 *T = a.stage + ul * a.xs + a.toff;
+  for (int idx = tid; idx < NB * P; idx += LCT) {
+    const int c = idx % NB, k1 = idx / NB;
+    const int p2 = p2_0 + c;
+    T[(int64_t)k1 * N2 + p2] = cmul(buf[c * CS + padi(k1)], tw_any<N>(tw, 2 * (int64_t)p2 * k1));
+  }
+  pdl_trigger();
+}
+
+// inverse four-step, first half (in place): DFT_N1 (sign +) over n1 of W[N2 n1 + p2] for NB
+// columns, twiddle conj(w_N^{p2 n1}); inv_large_row<LOGN, 1> finishes the rows
+template <int LOGN>
+__global__ void __launch_bounds__(LCT) long_inv_col(const KArgs a) {
+  using G = LongCol<LOGN>;
+  constexpr int N = 1 << LOGN, P = G::P, NB = G::NB, N2 = 256, CS = colstride<P>();
+  extern __shared__ float4 smem4[];
+  float2 *buf = reinterpret_cast<float2 *>(smem4);
+  const GlobalTw tw{a.tw2n};
+  const int tid = threadIdx.x;
+  const int64_t ul = blockIdx.x;
+  const int p2_0 = blockIdx.y * NB;
+  pdl_wait();
+  float2 *W = a.stage + ul * a.zs + a.toff;
+  {
+    constexpr int PERL = NB * P / LCT;
+    float2 v[PERL];
+#pragma unroll
+    for (int q = 0; q < PERL; ++q) {
+      const int idx = tid + q * LCT;
+      v[q] = __ldcs(W + (int64_t)N2 * (idx / NB) + p2_0 + idx % NB);
+    }
+#pragma unroll
+    for (int q = 0; q < PERL; ++q) {
+      const int idx = tid + q * LCT;
+      buf[(idx % NB) * CS + padi(idx / NB)] = v[q];
+    }
+  }
+  __syncthreads();
+  cpass<N, P, NB, G::R1, 1, +1>(buf, tw);
+  cpass<N, P, NB, G::R2, G::R1, +1>(buf, tw);
+  cpass<N, P, NB, G::R3, G::R1 * G::R2, +1>(buf, tw);
+  for (int idx = tid; idx < NB * P; idx += LCT) {
+    const int c = idx % NB, n1 = idx / NB;
+    const int p2 = p2_0 + c;
+    W[(int64_t)n1 * N2 + p2] =
+        cmul(buf[c * CS + padi(n1)], cconj(tw_any<N>(tw, 2 * (int64_t)p2 * n1)));
+  }
+  pdl_trigger();
+}
+
+// ------------------------------------------------------------------ channel FFTs
+// greedy radix of a remaining (2/3/5-smooth) transform size m; the same rule orders the
+// butterflies and the output digits
+__device__ __forceinline__ int long_radix(int m) {
+  return (m & 15) == 0 ? 16
+         : (m & 7) == 0 ? 8
+         : (m & 3) == 0 ? 4
+         : (m & 1) == 0 ? 2
+         : m % 9 == 0   ? 9
+         : m % 3 == 0   ? 3
+         : m % 25 == 0  ? 25
+                        : 5;
+}
+
+// one decimation-in-frequency stage over all M/Ms blocks of size Ms (in place):
+// y_k1[n'] = w_Ms^{SIGN n' k1} sum_r x[n' + r Q] w_R^{SIGN r k1} -> position n' + k1 Q
+template <int R, int SIGN>
+__device__ __forceinline__ void dif_stage(float2 *buf, int M, int Ms, const float2 *tw) {
+  const int Q = Ms / R, tasks = M / R, tstep = M / Ms;
+  for (int t = threadIdx.x; t < tasks; t += LKT) {
+    const int blk = t / Q, np = t - blk * Q;
+    const int base = blk * Ms + np;
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = buf[padi(base + r * Q)];
+    dft<R, SIGN>(v);
+    if (np) {
+      const int e1 = np * tstep;  // e^{2 pi i n' k1 / Ms} = table[n' k1 M/Ms], index < M
+      int e = 0;
+#pragma unroll
+      for (int k = 1; k < R; ++k) {
+        e += e1;
+        float2 w = __ldg(tw + e);
+        if (SIGN < 0) w = cconj(w);
+        v[k] = cmul(v[k], w);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[padi(base + r * Q)] = v[r];
+  }
+}
+
+// DFT_M (unnormalised, sign SIGN) of buf[padi(0..M)) in place; X[k] ends at dif_pos(k, M)
+template <int SIGN>
+__device__ __noinline__ void dif_fft(float2 *buf, int M, const float2 *tw) {
+  int Ms = M;
+  while (Ms > 1) {
+    const int R = long_radix(Ms);
+    switch (R) {
+      case 16: dif_stage<16, SIGN>(buf, M, Ms, tw); break;
+      case 8: dif_stage<8, SIGN>(buf, M, Ms, tw); break;
+      case 4: dif_stage<4, SIGN>(buf, M, Ms, tw); break;
+      case 2: dif_stage<2, SIGN>(buf, M, Ms, tw); break;
+      case 9: dif_stage<9, SIGN>(buf, M, Ms, tw); break;
+      case 3: dif_stage<3, SIGN>(buf, M, Ms, tw); break;
+      case 25: dif_stage<25, SIGN>(buf, M, Ms, tw); break;
+      default: dif_stage<5, SIGN>(buf, M, Ms, tw); break;
+    }
+    Ms /= R;
+    __syncthreads();
+  }
+}
+
+// position of output k: k = d1 + R1 d2 + R1 R2 d3 + ... sits at d1 M/R1 + d2 M/(R1 R2) + ...
+__device__ __forceinline__ int dif_pos(int k, int M) {
+  int pos = 0, Ms = M;
+  while (Ms > 1) {
+    const int R = long_radix(Ms);
+    Ms /= R;
+    const int q = k / R;
+    pos += (k - q * R) * Ms;
+    k = q;
+  }
+  return pos;
+}
+
+// Alg. 1 per channel: c_k = sqrt(M_k) IFFT_{M_k}(fold of X g_k)  (C1, C5, C15)
+__global__ void __launch_bounds__(LKT) long_chan_fwd(const KArgs a) {
+  extern __shared__ float4 smem4[];
+  float2 *buf = reinterpret_cast<float2 *>(smem4);
+  const ChanDev ch = a.chan[blockIdx.x];
+  const int64_t ul = blockIdx.y, row = a.unit0 + ul;
+  const int N2x = (int)a.L, N = N2x / 2;
+  const int M = ch.M;
+  pdl_wait();
+  const float2 *X = a.stage + ul * a.xs;
+  for (int q = threadIdx.x; q < M; q += LKT) {
+    int dd = q - ch.lo_mod;
+    if (dd < 0) dd += M;
+    float2 v = make_float2(0.f, 0.f);
+    if (dd < ch.len) {  // unwrapped bin j = lo + dd in (-2N, 2N); real input: X(j) = conj X(2N-j)
+      int jj = ch.lo + dd;
+      if (jj < 0) jj += N2x;
+      else if (jj >= N2x) jj -= N2x;
+      const bool cj = jj > N;
+      const float2 xv = __ldcg(X + (cj ? N2x - jj : jj));
+      const float w = __ldg(a.gw + ch.goff + dd);
+      v = make_float2(xv.x * w, cj ? -xv.y * w : xv.y * w);
+    }
+    buf[padi(q)] = v;
+  }
+  __syncthreads();
+  dif_fft<+1>(buf, M, a.twM + ch.twoff);
+  float2 *out = a.coef_out + row * a.C + ch.off;
+  for (int m = threadIdx.x; m < M; m += LKT) __stcs(out + m, buf[padi(dif_pos(m, M))]);
+  pdl_trigger();
+}
+
+// Alg. 2 per channel: terms FFT_{M_k}(c_k)[j mod M_k] g~_k[j] / sqrt(M_k)
+__global__ void __launch_bounds__(LKT) long_chan_inv(const KArgs a) {
+  extern __shared__ float4 smem4[];
+  float2 *buf = reinterpret_cast<float2 *>(smem4);
+  const ChanDev ch = a.chan[blockIdx.x];
+  const int64_t ul = blockIdx.y, row = a.unit0 + ul;
+  const int M = ch.M;
+  pdl_wait();
+  const float2 *in = a.coef_in + row * a.C + ch.off;
+  for (int m = threadIdx.x; m < M; m += LKT) buf[padi(m)] = __ldcs(in + m);
+  __syncthreads();
+  dif_fft<-1>(buf, M, a.twM + ch.twoff);
+  float2 *terms = a.stage + ul * a.zs + ch.goff;
+  for (int dd = threadIdx.x; dd < ch.len; dd += LKT) {
+    int q = ch.lo_mod + dd;
+    if (q >= M) q -= M;
+    const float2 F = buf[padi(dif_pos(q, M))];
+    const float w = __ldg(a.gdw + ch.goff + dd);
+    __stcg(terms + dd, make_float2(F.x * w, F.y * w));
+  }
+  pdl_trigger();
+}
+
+// half-spectrum bin b: sum of its channel terms in plan order (conjugated where C15 mirrors)
+__device__ __forceinline__ float2 long_gather(const KArgs &a, const float2 *Tm, int b) {
+  float2 acc = make_float2(0.f, 0.f);
+  const uint32_t e0 = __ldg(a.lrow + b), e1 = __ldg(a.lrow + b + 1);
+  for (uint32_t i = e0; i < e1; ++i) {
+    const uint32_t e = __ldg(a.lent + i);
+    float2 t = __ldcg(Tm + (e & 0x7fffffffu));
+    if (e >> 31) t.y = -t.y;
+    acc = cadd(acc, t);
+  }
+  return acc;
+}
+
+// H -> c2r-packed W (as inv_large_pack, kernels_large.cuh)
+__global__ void __launch_bounds__(LT) long_inv_pack(const KArgs a) {
+  const GlobalTw tw{a.tw2n};
+  const int N = (int)(a.L / 2);
+  pdl_wait();
+  const int64_t ul = blockIdx.x;
+  const float2 *Tm = a.stage + ul * a.zs;
+  float2 *W = a.stage + ul * a.zs + a.toff;
+  const int k = blockIdx.y * LT + threadIdx.x;
+  if (k <= N / 2) {
+    const float2 hk = long_gather(a, Tm, k);
+    const float2 hn = long_gather(a, Tm, N - k);
+    const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
+    const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+    const float2 w = cconj(tw_lookup(tw, k));  // e^{+i pi k/N}
+    const float2 O = cmul(D, w);
+    W[k] = make_float2(E.x - O.y, E.y + O.x);
+    if (k != 0 && k != N / 2) {
+      const float2 O2 = cmul(cconj(D), cconj(w));
+      W[N - k] = make_float2(E.x - O2.y, -E.y + O2.x);
+    }
+  }
+  pdl_trigger();
+}
+
+// entry points (kernels_long.cu)
+int long_set_attrs(int logN, size_t chan_smem);
+cudaError_t long_forward(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s);
+cudaError_t long_inverse(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s);
+
+}  // namespace kern
+}  // namespace slicq

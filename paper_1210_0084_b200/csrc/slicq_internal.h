@@ -51,6 +51,10 @@ struct DeviceTables {
   float *h0dual = nullptr;  // fp32 h~_0[t+N]
   float *tw2n = nullptr;    // float2: [64] e^{-i pi t/N} for t < 64, then [2N/64] for t = 64 h
   float *twM = nullptr;     // float2 tables e^{+2 pi i t / M}
+  float *gw = nullptr;      // long mode: g_k / sqrt(M_k) (fp32, at goff_k)
+  float *gdw = nullptr;     // long mode: g~_k / sqrt(M_k) (x 1/2 on the plateaus)
+  uint32_t *lrow = nullptr; // long mode: per-bin term list start [N + 2]
+  uint32_t *lent = nullptr; // long mode: term index | conj << 31
   void *block = nullptr;    // single allocation holding all of the above
   size_t bytes = 0;
 };
@@ -70,6 +74,8 @@ struct KernelConfig {
   int64_t chunk_units = 0;    // units per chunk (staging is sized for one chunk)
   int tile = 16;              // units per channel-kernel tile
   int chan_per_sm = 0;        // channel-kernel CTAs per SM cap (0: occupancy)
+  bool longmode = false;      // sl_len 2^18..2^22: full-length CQ-NSGT only (kernels_long.cuh)
+  size_t lchan_smem = 0;      // long mode: channel-FFT shared memory (max M_k)
 };
 
 }  // namespace slicq
@@ -100,6 +106,8 @@ struct slicq_plan {
   std::vector<int32_t> pchans;
   std::vector<uint2> fent, ient;
   std::vector<uint32_t> dpos;
+  std::vector<float> lgw, lgdw;          // long mode filter weights
+  std::vector<uint32_t> lrow, lent;      // long mode per-bin term lists
 };
 
 namespace slicq {

@@ -38,6 +38,47 @@ def test_nsgt_matches_oracle_and_reconstructs(L, n, B, bpo, fmin, raster):
         assert ry <= TOL, (b, ry)
 
 
+@pytest.mark.parametrize("L,n,B,bpo,fmin", [
+    (2 ** 18, 2 ** 18, 2, 48, 50.0), (2 ** 19, 400000, 1, 24, 50.0),
+    (2 ** 20, 2 ** 20, 2, 48, 50.0), (2 ** 21, 2 ** 21 - 1000, 1, 96, 60.0)])
+def test_long_nsgt_matches_oracle_and_reconstructs(L, n, B, bpo, fmin):
+    """Long signals (kernels_long.cuh): four-step FFT_L with N1 = 512 .. 8192 columns and
+    shared-memory mixed-radix channel FFTs up to M_k = 15 360."""
+    from paper_1210_0084_b200 import api
+    args = (44100.0, fmin, 22050.0, bpo, L, 64, 0)
+    plan = api.Plan(*args)
+    ref = cqplan.make_plan(*args)
+    assert list(plan.channel_lengths()) == list(ref.M)
+    x = random_signal(L + n + 7, B, n)
+    xt = torch.from_numpy(x).cuda()
+    c = plan.nsgt_forward(xt)
+    y = plan.nsgt_inverse(c, n)
+    torch.cuda.synchronize()
+    cg = c.cpu().numpy().astype(np.complex128)
+    for b in range(B):
+        xp = np.zeros(L)
+        xp[:n] = x[b]
+        cr = onsgt.analysis_real(xp, ref)
+        crc = np.concatenate(cr)
+        err = np.linalg.norm(cg[b] - crc) / np.linalg.norm(crc)
+        assert err <= TOL, (b, err)
+        # per channel too (the small channels must not hide behind the big ones' energy)
+        off = np.cumsum([0] + [len(v) for v in cr])
+        rms = np.sqrt(np.mean(np.abs(crc) ** 2))
+        for k, v in enumerate(cr):
+            d = np.linalg.norm(cg[b, off[k]:off[k + 1]] - v) / max(np.linalg.norm(v), rms * np.sqrt(len(v)))
+            assert d <= TOL, (b, k, d)
+        ry = np.linalg.norm(y[b].cpu().numpy() - x[b]) / np.linalg.norm(x[b])
+        assert ry <= TOL, (b, ry)
+
+
+def test_long_plan_serves_only_the_full_length_transform():
+    from paper_1210_0084_b200 import api
+    plan = api.Plan(44100.0, 50.0, 22050.0, 48, 2 ** 18, 64, 0)
+    with pytest.raises(Exception, match="full-length"):
+        plan.forward(torch.zeros(1, 2 ** 18, device="cuda"))
+
+
 def test_nsgt_rejects_long_input():
     from paper_1210_0084_b200 import api
     plan = api.Plan(44100.0, 50.0, 22050.0, 24, 4096, 64, 0)
