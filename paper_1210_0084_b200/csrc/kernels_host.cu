@@ -14,13 +14,9 @@
 #define SLICQ_DEFINE_CHAN_KERNELS
 #include "kernels_dev.cuh"
 #include "kernels_large.cuh"
+#include "kernels_long_api.h"
 
 namespace slicq {
-namespace kern {  // kernels_long.cu (full-length CQ-NSGT of long signals)
-int long_set_attrs(int logN, size_t chan_smem);
-cudaError_t long_forward(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s);
-cudaError_t long_inverse(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s);
-}  // namespace kern
 namespace {
 using namespace slicq::kern;
 
@@ -137,13 +133,29 @@ int configure_long(slicq_plan *p, int logN) {
   kc.npackets = kc.nlite = 0;
   const int K2 = p->K + 2;
   const int64_t N = p->N, N2 = 2 * N;
-  int maxM = 0;
-  for (int k = 0; k < K2; ++k) maxM = std::max(maxM, (int)p->M[k]);
-  kc.lchan_smem = sizeof(float2) * (size_t)(padi(maxM) + 1);
-  if (kc.lchan_smem > kSmemCap)
-    return set_error(SLICQ_EUNSUPPORTED, "channel length M_k = " + std::to_string(maxM) +
-                                             " exceeds the shared-memory channel FFT of the "
-                                             "long full-length path (M_k <= 27000)");
+  // channels by size class (kernels_long_api.h); the class list replaces the packet list
+  p->pchans.clear();
+  int maxm[kLongClasses] = {};
+  for (int c = 0; c < kLongClasses; ++c) {
+    kc.lcls.off[c] = (int)p->pchans.size();
+    for (int k = 0; k < K2; ++k) {
+      const int M = p->M[k];
+      int cls = 0;
+      while (cls + 1 < kLongClasses && M > long_class_maxm(cls)) ++cls;
+      if (cls != c) continue;
+      if (M > long_class_maxm(kLongClasses - 1))
+        return set_error(SLICQ_EUNSUPPORTED, "channel length M_k = " + std::to_string(M) +
+                                                 " exceeds the shared-memory channel FFT of the "
+                                                 "long full-length path (M_k <= 26000)");
+      p->pchans.push_back(k);
+      maxm[c] = std::max(maxm[c], M);
+    }
+    kc.lcls.smem[c] = maxm[c] ? sizeof(float2) * (size_t)(padi(maxm[c]) + 1 +
+                                                          long_twiddle_entries(maxm[c]) +
+                                                          kDifPlanEntries)
+                              : 0;
+  }
+  kc.lcls.off[kLongClasses] = (int)p->pchans.size();
   const int64_t nterms = (int64_t)p->g.size();
   if (nterms >= (int64_t(1) << 31)) return set_error(SLICQ_EUNSUPPORTED, "too many filter terms");
   p->lgw.assign(nterms, 0.f);
@@ -587,7 +599,7 @@ int upload(slicq_plan *p) {
     case 14: rc = set_attrs<14>(p->kc.spec_smem); break;
     case 15: rc = large_set_attrs<15>(); break;
     case 16: rc = large_set_attrs<16>(); break;
-    default: rc = long_set_attrs(p->kc.logN, p->kc.lchan_smem); break;
+    default: rc = long_set_attrs(p->kc.logN, p->kc.lcls); break;
   }
   for (int v = 0; v < 12 && rc == 0 && !p->kc.longmode; ++v)  // bit 0: forward, bit 1: lite, v >> 2: mask mode
     rc = (int)cudaFuncSetAttribute(chan_fn(v & 1, v & 2, v >> 2),
@@ -771,7 +783,7 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
       a.unit0 = u0;
       a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
-      const cudaError_t e = long_forward(p->kc.logN, a, p->K + 2, p->kc.lchan_smem, s);
+      const cudaError_t e = long_forward(p->kc.logN, a, p->kc.lcls, s);
       if (e != cudaSuccess)
         return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
     }
@@ -830,7 +842,7 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
       a.unit0 = u0;
       a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
-      const cudaError_t e = long_inverse(p->kc.logN, a, p->K + 2, p->kc.lchan_smem, s);
+      const cudaError_t e = long_inverse(p->kc.logN, a, p->kc.lcls, s);
       if (e != cudaSuccess)
         return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
     }

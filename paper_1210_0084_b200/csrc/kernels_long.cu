@@ -1,6 +1,8 @@
 // Full-length CQ-NSGT of long signals (L = 2^18 .. 2^22), see kernels_long.cuh.
 #include "kernels_long.cuh"
 
+#include <algorithm>
+
 namespace slicq {
 namespace kern {
 
@@ -33,7 +35,29 @@ static int set_attrs_logn() {
   return (int)e;
 }
 
-int long_set_attrs(int logN, size_t chan_smem) {
+static void (*chan_kernel(bool fwd, int c))(const KArgs) {
+  switch (c) {
+    case 0: return fwd ? long_chan_fwd<long_class_threads(0)> : long_chan_inv<long_class_threads(0)>;
+    case 1: return fwd ? long_chan_fwd<long_class_threads(1)> : long_chan_inv<long_class_threads(1)>;
+  }
+  return fwd ? long_chan_fwd<512> : long_chan_inv<512>;
+}
+
+// the channel kernels of one direction, one launch per non-empty size class
+static cudaError_t launch_classes(bool fwd, KArgs a, const LongClasses &cls, cudaStream_t s) {
+  const int32_t *list = a.pchans;
+  for (int c = 0; c < kLongClasses; ++c) {
+    const int n = cls.off[c + 1] - cls.off[c];
+    if (!n) continue;
+    a.pchans = list + cls.off[c];
+    const cudaError_t e = pdl_launch(chan_kernel(fwd, c), a, dim3((unsigned)n, (unsigned)a.nunits),
+                                     long_class_threads(c), cls.smem[c], s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int long_set_attrs(int logN, const LongClasses &cls) {
   int rc = 0;
   switch (logN) {
     case 17: rc = set_attrs_logn<17>(); break;
@@ -44,14 +68,16 @@ int long_set_attrs(int logN, size_t chan_smem) {
     default: return (int)cudaErrorInvalidValue;
   }
   if (rc) return rc;
-  cudaError_t e = cudaFuncSetAttribute(long_chan_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chan_smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(long_chan_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chan_smem);
+  cudaError_t e = cudaSuccess;
+  for (int c = 0; c < kLongClasses && e == cudaSuccess; ++c)
+    for (int f = 0; f < 2 && e == cudaSuccess; ++f)
+      e = cudaFuncSetAttribute(chan_kernel(f == 0, c), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::max<size_t>(cls.smem[c], 1024));
   return (int)e;
 }
 
 template <int LOGN>
-static cudaError_t fwd_logn(const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s) {
+static cudaError_t fwd_logn(const KArgs &a, const LongClasses &cls, cudaStream_t s) {
   using G = Large<LOGN>;
   const unsigned nu = (unsigned)a.nunits;
   cudaError_t e = pdl_launch(long_fwd_col<LOGN>, a, dim3(nu, G::N2 / LongCol<LOGN>::NB), LCT,
@@ -59,15 +85,15 @@ static cudaError_t fwd_logn(const KArgs &a, int nchan, size_t chan_smem, cudaStr
   if (e == cudaSuccess)
     e = pdl_launch(fwd_large_row<LOGN>, a, dim3(nu, (G::N1 / 2 + 1 + 7) / 8), LT,
                    large_smem_bytes<LOGN>(), s);
-  if (e == cudaSuccess) e = pdl_launch(long_chan_fwd, a, dim3((unsigned)nchan, nu), LKT, chan_smem, s);
+  if (e == cudaSuccess) e = launch_classes(true, a, cls, s);
   return e;
 }
 
 template <int LOGN>
-static cudaError_t inv_logn(const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s) {
+static cudaError_t inv_logn(const KArgs &a, const LongClasses &cls, cudaStream_t s) {
   using G = Large<LOGN>;
   const unsigned nu = (unsigned)a.nunits;
-  cudaError_t e = pdl_launch(long_chan_inv, a, dim3((unsigned)nchan, nu), LKT, chan_smem, s);
+  cudaError_t e = launch_classes(false, a, cls, s);
   if (e == cudaSuccess)
     e = pdl_launch(long_inv_pack, a, dim3(nu, (G::N / 2 + 1 + LT - 1) / LT), LT, 0, s);
   if (e == cudaSuccess)
@@ -78,24 +104,24 @@ static cudaError_t inv_logn(const KArgs &a, int nchan, size_t chan_smem, cudaStr
   return e;
 }
 
-cudaError_t long_forward(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s) {
+cudaError_t long_forward(int logN, const KArgs &a, const LongClasses &cls, cudaStream_t s) {
   switch (logN) {
-    case 17: return fwd_logn<17>(a, nchan, chan_smem, s);
-    case 18: return fwd_logn<18>(a, nchan, chan_smem, s);
-    case 19: return fwd_logn<19>(a, nchan, chan_smem, s);
-    case 20: return fwd_logn<20>(a, nchan, chan_smem, s);
-    case 21: return fwd_logn<21>(a, nchan, chan_smem, s);
+    case 17: return fwd_logn<17>(a, cls, s);
+    case 18: return fwd_logn<18>(a, cls, s);
+    case 19: return fwd_logn<19>(a, cls, s);
+    case 20: return fwd_logn<20>(a, cls, s);
+    case 21: return fwd_logn<21>(a, cls, s);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t long_inverse(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s) {
+cudaError_t long_inverse(int logN, const KArgs &a, const LongClasses &cls, cudaStream_t s) {
   switch (logN) {
-    case 17: return inv_logn<17>(a, nchan, chan_smem, s);
-    case 18: return inv_logn<18>(a, nchan, chan_smem, s);
-    case 19: return inv_logn<19>(a, nchan, chan_smem, s);
-    case 20: return inv_logn<20>(a, nchan, chan_smem, s);
-    case 21: return inv_logn<21>(a, nchan, chan_smem, s);
+    case 17: return inv_logn<17>(a, cls, s);
+    case 18: return inv_logn<18>(a, cls, s);
+    case 19: return inv_logn<19>(a, cls, s);
+    case 20: return inv_logn<20>(a, cls, s);
+    case 21: return inv_logn<21>(a, cls, s);
   }
   return cudaErrorInvalidValue;
 }

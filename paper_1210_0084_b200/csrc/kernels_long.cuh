@@ -22,6 +22,7 @@
 // butterflies and the digit reversal of the output).
 #pragma once
 #include "kernels_large.cuh"
+#include "kernels_long_api.h"
 
 namespace slicq {
 namespace kern {
@@ -72,7 +73,6 @@ struct LongCol<21> {
   static constexpr int P = 8192, NB = 1, R1 = 16, R2 = 16, R3 = 32;
 };
 constexpr int LCT = 512;  // column-kernel threads
-constexpr int LKT = 512;  // channel-kernel threads
 
 template <int LOGN>
 constexpr size_t long_col_smem() {
@@ -209,18 +209,45 @@ __device__ __forceinline__ int long_radix(int m) {
          : (m & 1) == 0 ? 2
          : m % 9 == 0   ? 9
          : m % 3 == 0   ? 3
-         : m % 25 == 0  ? 25
                         : 5;
 }
 
-// one decimation-in-frequency stage over all M/Ms blocks of size Ms (in place):
+// The stage plan of DFT_M (built once per CTA in shared memory): stage s has radix R[s] and
+// span Q[s] = Ms / R[s] (Ms: the block size the stage splits), twiddle stride M / Ms, and
+// exact reciprocals for the index arithmetic: x / d = umulhi(x, ceil(2^32 / d)) for
+// x, d < 2^16 (M_k <= 26000).
+struct DifPlan {
+  int ns;
+  int R[kDifMaxStages], Q[kDifMaxStages], tstep[kDifMaxStages];
+  unsigned magR[kDifMaxStages], magQ[kDifMaxStages];
+};
+__device__ __forceinline__ unsigned recip32(int d) {  // d >= 2 (d = 1 is special-cased)
+  return (unsigned)((0x100000000ull + (unsigned)d - 1) / (unsigned)d);
+}
+__device__ __forceinline__ void build_dif_plan(DifPlan &pl, int M) {  // one thread
+  int Ms = M, s = 0;
+  while (Ms > 1) {
+    const int R = long_radix(Ms);
+    pl.R[s] = R;
+    pl.Q[s] = Ms / R;
+    pl.tstep[s] = M / Ms;
+    pl.magR[s] = recip32(R);
+    pl.magQ[s] = recip32(Ms / R);
+    Ms /= R;
+    ++s;
+  }
+  pl.ns = s;
+}
+
+// one decimation-in-frequency stage over all M/Ms blocks of size Ms = R Q (in place):
 // y_k1[n'] = w_Ms^{SIGN n' k1} sum_r x[n' + r Q] w_R^{SIGN r k1} -> position n' + k1 Q
-template <int R, int SIGN>
-__device__ __forceinline__ void dif_stage(float2 *buf, int M, int Ms, const float2 *tw) {
-  const int Q = Ms / R, tasks = M / R, tstep = M / Ms;
-  for (int t = threadIdx.x; t < tasks; t += LKT) {
-    const int blk = t / Q, np = t - blk * Q;
-    const int base = blk * Ms + np;
+template <int R, int SIGN, int T>
+__device__ __forceinline__ void dif_stage(float2 *buf, int M, int Q, int tstep, unsigned magQ,
+                                          const float2 *tw) {
+  const int tasks = M / R;
+  for (int t = threadIdx.x; t < tasks; t += T) {
+    const int blk = Q == 1 ? t : (int)__umulhi((unsigned)t, magQ), np = t - blk * Q;
+    const int base = blk * (R * Q) + np;
     float2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = buf[padi(base + r * Q)];
@@ -231,7 +258,7 @@ __device__ __forceinline__ void dif_stage(float2 *buf, int M, int Ms, const floa
 #pragma unroll
       for (int k = 1; k < R; ++k) {
         e += e1;
-        float2 w = __ldg(tw + e);
+        float2 w = cmul(tw[e & 63], tw[64 + (e >> 6)]);  // shared two-level table
         if (SIGN < 0) w = cconj(w);
         v[k] = cmul(v[k], w);
       }
@@ -241,51 +268,71 @@ __device__ __forceinline__ void dif_stage(float2 *buf, int M, int Ms, const floa
   }
 }
 
-// DFT_M (unnormalised, sign SIGN) of buf[padi(0..M)) in place; X[k] ends at dif_pos(k, M)
-template <int SIGN>
-__device__ __noinline__ void dif_fft(float2 *buf, int M, const float2 *tw) {
-  int Ms = M;
-  while (Ms > 1) {
-    const int R = long_radix(Ms);
-    switch (R) {
-      case 16: dif_stage<16, SIGN>(buf, M, Ms, tw); break;
-      case 8: dif_stage<8, SIGN>(buf, M, Ms, tw); break;
-      case 4: dif_stage<4, SIGN>(buf, M, Ms, tw); break;
-      case 2: dif_stage<2, SIGN>(buf, M, Ms, tw); break;
-      case 9: dif_stage<9, SIGN>(buf, M, Ms, tw); break;
-      case 3: dif_stage<3, SIGN>(buf, M, Ms, tw); break;
-      case 25: dif_stage<25, SIGN>(buf, M, Ms, tw); break;
-      default: dif_stage<5, SIGN>(buf, M, Ms, tw); break;
+// shared-memory two-level twiddle table of e^{2 pi i t/M}: tw[l] (l < 64), tw[64 + h] = t = 64 h,
+// from the plan's full table twM (global)
+template <int T>
+__device__ __forceinline__ void load_twiddles(float2 *tw, const float2 *twM, int M) {
+  const int nh = (M + 63) >> 6;
+  for (int i = threadIdx.x; i < 64 + nh; i += T) {
+    const int t = i < 64 ? i : 64 * (i - 64);
+    tw[i] = t < M ? __ldg(twM + t) : make_float2(1.f, 0.f);
+  }
+}
+
+// DFT_M (unnormalised, sign SIGN) of buf[padi(0..M)) in place; X[k] ends at dif_pos(k)
+// (tw: the shared table of load_twiddles; pl: the shared stage plan)
+template <int SIGN, int T>
+__device__ __noinline__ void dif_fft(float2 *buf, int M, const float2 *tw, const DifPlan &pl) {
+  for (int s = 0; s < pl.ns; ++s) {
+    const int Q = pl.Q[s], ts = pl.tstep[s];
+    const unsigned mq = pl.magQ[s];
+    switch (pl.R[s]) {
+      case 16: dif_stage<16, SIGN, T>(buf, M, Q, ts, mq, tw); break;
+      case 8: dif_stage<8, SIGN, T>(buf, M, Q, ts, mq, tw); break;
+      case 4: dif_stage<4, SIGN, T>(buf, M, Q, ts, mq, tw); break;
+      case 2: dif_stage<2, SIGN, T>(buf, M, Q, ts, mq, tw); break;
+      case 9: dif_stage<9, SIGN, T>(buf, M, Q, ts, mq, tw); break;
+      case 3: dif_stage<3, SIGN, T>(buf, M, Q, ts, mq, tw); break;
+      default: dif_stage<5, SIGN, T>(buf, M, Q, ts, mq, tw); break;
     }
-    Ms /= R;
     __syncthreads();
   }
 }
 
-// position of output k: k = d1 + R1 d2 + R1 R2 d3 + ... sits at d1 M/R1 + d2 M/(R1 R2) + ...
-__device__ __forceinline__ int dif_pos(int k, int M) {
-  int pos = 0, Ms = M;
-  while (Ms > 1) {
-    const int R = long_radix(Ms);
-    Ms /= R;
-    const int q = k / R;
-    pos += (k - q * R) * Ms;
+// position of output k: k = d1 + R1 d2 + R1 R2 d3 + ... sits at d1 Q1 + d2 Q2 + ...
+__device__ __forceinline__ int dif_pos(int k, const DifPlan &pl) {
+  int pos = 0;
+  for (int s = 0; s < pl.ns; ++s) {
+    const int q = (int)__umulhi((unsigned)k, pl.magR[s]);
+    pos += (k - q * pl.R[s]) * pl.Q[s];
     k = q;
   }
   return pos;
 }
 
+// shared-memory layout of a channel CTA: buf [padi(M) + 1], twiddles, stage plan
+__device__ __forceinline__ float2 *long_tw_ptr(float2 *buf, int M) { return buf + padi(M) + 1; }
+__device__ __forceinline__ DifPlan *long_plan_ptr(float2 *buf, int M) {
+  return reinterpret_cast<DifPlan *>(long_tw_ptr(buf, M) + long_twiddle_entries(M));
+}
+
 // Alg. 1 per channel: c_k = sqrt(M_k) IFFT_{M_k}(fold of X g_k)  (C1, C5, C15)
-__global__ void __launch_bounds__(LKT) long_chan_fwd(const KArgs a) {
+// (grid x: the channels of one size class, listed in a.pchans; 64 registers per thread)
+template <int T>
+__global__ void __launch_bounds__(T, 65536 / (64 * T)) long_chan_fwd(const KArgs a) {
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  const ChanDev ch = a.chan[blockIdx.x];
+  const ChanDev ch = a.chan[a.pchans[blockIdx.x]];
   const int64_t ul = blockIdx.y, row = a.unit0 + ul;
   const int N2x = (int)a.L, N = N2x / 2;
   const int M = ch.M;
   pdl_wait();
   const float2 *X = a.stage + ul * a.xs;
-  for (int q = threadIdx.x; q < M; q += LKT) {
+  float2 *tws = long_tw_ptr(buf, M);
+  DifPlan &pl = *long_plan_ptr(buf, M);
+  if (threadIdx.x == 0) build_dif_plan(pl, M);
+  load_twiddles<T>(tws, a.twM + ch.twoff, M);
+  for (int q = threadIdx.x; q < M; q += T) {
     int dd = q - ch.lo_mod;
     if (dd < 0) dd += M;
     float2 v = make_float2(0.f, 0.f);
@@ -301,29 +348,34 @@ __global__ void __launch_bounds__(LKT) long_chan_fwd(const KArgs a) {
     buf[padi(q)] = v;
   }
   __syncthreads();
-  dif_fft<+1>(buf, M, a.twM + ch.twoff);
+  dif_fft<+1, T>(buf, M, tws, pl);
   float2 *out = a.coef_out + row * a.C + ch.off;
-  for (int m = threadIdx.x; m < M; m += LKT) __stcs(out + m, buf[padi(dif_pos(m, M))]);
+  for (int m = threadIdx.x; m < M; m += T) __stcs(out + m, buf[padi(dif_pos(m, pl))]);
   pdl_trigger();
 }
 
 // Alg. 2 per channel: terms FFT_{M_k}(c_k)[j mod M_k] g~_k[j] / sqrt(M_k)
-__global__ void __launch_bounds__(LKT) long_chan_inv(const KArgs a) {
+template <int T>
+__global__ void __launch_bounds__(T, 65536 / (64 * T)) long_chan_inv(const KArgs a) {
   extern __shared__ float4 smem4[];
   float2 *buf = reinterpret_cast<float2 *>(smem4);
-  const ChanDev ch = a.chan[blockIdx.x];
+  const ChanDev ch = a.chan[a.pchans[blockIdx.x]];
   const int64_t ul = blockIdx.y, row = a.unit0 + ul;
   const int M = ch.M;
   pdl_wait();
   const float2 *in = a.coef_in + row * a.C + ch.off;
-  for (int m = threadIdx.x; m < M; m += LKT) buf[padi(m)] = __ldcs(in + m);
+  float2 *tws = long_tw_ptr(buf, M);
+  DifPlan &pl = *long_plan_ptr(buf, M);
+  if (threadIdx.x == 0) build_dif_plan(pl, M);
+  load_twiddles<T>(tws, a.twM + ch.twoff, M);
+  for (int m = threadIdx.x; m < M; m += T) buf[padi(m)] = __ldcs(in + m);
   __syncthreads();
-  dif_fft<-1>(buf, M, a.twM + ch.twoff);
+  dif_fft<-1, T>(buf, M, tws, pl);
   float2 *terms = a.stage + ul * a.zs + ch.goff;
-  for (int dd = threadIdx.x; dd < ch.len; dd += LKT) {
+  for (int dd = threadIdx.x; dd < ch.len; dd += T) {
     int q = ch.lo_mod + dd;
     if (q >= M) q -= M;
-    const float2 F = buf[padi(dif_pos(q, M))];
+    const float2 F = buf[padi(dif_pos(q, pl))];
     const float w = __ldg(a.gdw + ch.goff + dd);
     __stcg(terms + dd, make_float2(F.x * w, F.y * w));
   }
@@ -369,9 +421,6 @@ __global__ void __launch_bounds__(LT) long_inv_pack(const KArgs a) {
 }
 
 // entry points (kernels_long.cu)
-int long_set_attrs(int logN, size_t chan_smem);
-cudaError_t long_forward(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s);
-cudaError_t long_inverse(int logN, const KArgs &a, int nchan, size_t chan_smem, cudaStream_t s);
 
 }  // namespace kern
 }  // namespace slicq

@@ -1,0 +1,37 @@
+// Host interface of the long full-length CQ-NSGT kernels (kernels_long.cuh / .cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+namespace slicq {
+namespace kern {
+struct KArgs;
+
+// channel-kernel size classes: CTA threads and the largest M_k of each (shared memory is
+// sized per class, so the many short channels do not pay for the longest one's buffer)
+constexpr int kLongClasses = 4;
+__host__ __device__ constexpr int long_class_threads(int c) { return c == 0 ? 128 : c == 1 ? 256 : 512; }
+__host__ __device__ constexpr int long_class_maxm(int c) {
+  return c == 0 ? 1536 : c == 1 ? 6144 : c == 2 ? 12288 : 26000;
+}
+
+// largest stage count of a channel DFT (radices >= 2: log2(26000) < 15)
+constexpr int kDifMaxStages = 16;
+// shared bytes of the per-CTA stage plan (kernels_long.cuh DifPlan), rounded to float2
+constexpr int kDifPlanEntries = (4 + 5 * 4 * kDifMaxStages + 7) / 8;
+
+// shared two-level twiddle table entries of a channel of length M (kernels_long.cuh)
+__host__ __device__ constexpr int long_twiddle_entries(int M) { return 64 + ((M + 63) >> 6); }
+
+// per size class c: channels [off[c], off[c+1]) of the device channel list (KArgs::pchans)
+// and the class's dynamic shared-memory bytes
+struct LongClasses {
+  int off[kLongClasses + 1];
+  size_t smem[kLongClasses];
+};
+int long_set_attrs(int logN, const LongClasses &cls);
+cudaError_t long_forward(int logN, const KArgs &a, const LongClasses &cls, cudaStream_t s);
+cudaError_t long_inverse(int logN, const KArgs &a, const LongClasses &cls, cudaStream_t s);
+}  // namespace kern
+}  // namespace slicq

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "../../include/slicq.h"
+#include "kernels_long_api.h"
 
 namespace slicq {
 
@@ -75,7 +76,7 @@ struct KernelConfig {
   int tile = 16;              // units per channel-kernel tile
   int chan_per_sm = 0;        // channel-kernel CTAs per SM cap (0: occupancy)
   bool longmode = false;      // sl_len 2^18..2^22: full-length CQ-NSGT only (kernels_long.cuh)
-  size_t lchan_smem = 0;      // long mode: channel-FFT shared memory (max M_k)
+  kern::LongClasses lcls{};   // long mode: channel size classes (kernels_long_api.h)
 };
 
 }  // namespace slicq
