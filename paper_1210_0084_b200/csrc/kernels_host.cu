@@ -135,6 +135,7 @@ int configure_long(slicq_plan *p, int logN) {
   const int64_t N = p->N, N2 = 2 * N;
   // channels by size class (kernels_long_api.h); the class list replaces the packet list
   p->pchans.clear();
+  p->lm1.assign(K2, 0);
   int maxm[kLongClasses] = {};
   for (int c = 0; c < kLongClasses; ++c) {
     kc.lcls.off[c] = (int)p->pchans.size();
@@ -143,12 +144,21 @@ int configure_long(slicq_plan *p, int logN) {
       int cls = 0;
       while (cls + 1 < kLongClasses && M > long_class_maxm(cls)) ++cls;
       if (cls != c) continue;
-      if (M > long_class_maxm(kLongClasses - 1))
-        return set_error(SLICQ_EUNSUPPORTED, "channel length M_k = " + std::to_string(M) +
-                                                 " exceeds the shared-memory channel FFT of the "
-                                                 "long full-length path (M_k <= 26000)");
+      int Msm = M;  // the shared-memory DFT size of the channel
+      if (c == kLongClasses - 1) {  // four-step M1 x M2 (kernels_long.cuh)
+        for (int m1 : {2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16})
+          if (M % m1 == 0 && M / m1 <= kLongSmemMax) {
+            p->lm1[k] = m1;
+            break;
+          }
+        if (!p->lm1[k])
+          return set_error(SLICQ_EUNSUPPORTED, "channel length M_k = " + std::to_string(M) +
+                                                   " has no factor M1 <= 16 with M_k / M1 <= " +
+                                                   std::to_string(kLongSmemMax));
+        Msm = M / p->lm1[k];
+      }
       p->pchans.push_back(k);
-      maxm[c] = std::max(maxm[c], M);
+      maxm[c] = std::max(maxm[c], Msm);
     }
     kc.lcls.smem[c] = maxm[c] ? sizeof(float2) * (size_t)(padi(maxm[c]) + 1 +
                                                           long_twiddle_entries(maxm[c]) +
@@ -202,6 +212,23 @@ int configure_long(slicq_plan *p, int logN) {
   kc.xs = kc.toff_f + N;
   kc.toff_i = (nterms + 1) & ~int64_t(1);
   kc.zs = kc.toff_i + N;
+  // four-step channels: their M_k-entry scratch after both layouts (same offset per channel
+  // in the forward and the inverse row)
+  p->lsoff.assign(K2, 0);
+  {
+    int64_t so = std::max(kc.xs, kc.zs);
+    bool any = false;
+    for (int k = 0; k < K2; ++k)
+      if (p->lm1[k]) {
+        p->lsoff[k] = so;
+        so += (p->M[k] + 1) & ~1;
+        any = true;
+      }
+    if (any) {
+      if (so >= (int64_t(1) << 31)) return set_error(SLICQ_EUNSUPPORTED, "staging row too long");
+      kc.xs = kc.zs = so;
+    }
+  }
   kc.zso = 0;
   kc.nover = 0;
   kc.tile = 1;
@@ -520,6 +547,10 @@ int upload(slicq_plan *p) {
     c.twoff = twoff[c.M];
     c.scale = (float)(1.0 / std::sqrt((double)c.M));
     c.lo_mod = ((c.lo % c.M) + c.M) % c.M;
+    if (p->kc.longmode) {
+      c.m1 = p->lm1[k];
+      c.soff = (int32_t)p->lsoff[k];
+    }
   }
   std::vector<float> h0(N2), h0d(N2);
   for (int64_t i = 0; i < N2; ++i) {

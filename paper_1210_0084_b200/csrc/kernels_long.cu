@@ -36,6 +36,7 @@ static int set_attrs_logn() {
 }
 
 static void (*chan_kernel(bool fwd, int c))(const KArgs) {
+  if (c == kLongClasses - 1) return fwd ? long_chan_fwd_big : long_chan_inv_big;
   switch (c) {
     case 0: return fwd ? long_chan_fwd<long_class_threads(0)> : long_chan_inv<long_class_threads(0)>;
     case 1: return fwd ? long_chan_fwd<long_class_threads(1)> : long_chan_inv<long_class_threads(1)>;

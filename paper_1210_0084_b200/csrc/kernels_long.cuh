@@ -270,12 +270,13 @@ __device__ __forceinline__ void dif_stage(float2 *buf, int M, int Q, int tstep, 
 
 // shared-memory two-level twiddle table of e^{2 pi i t/M}: tw[l] (l < 64), tw[64 + h] = t = 64 h,
 // from the plan's full table twM (global)
+// (stride s: the table of M / s from the table of M, e^{2 pi i t/(M/s)} = twM[s t])
 template <int T>
-__device__ __forceinline__ void load_twiddles(float2 *tw, const float2 *twM, int M) {
+__device__ __forceinline__ void load_twiddles(float2 *tw, const float2 *twM, int M, int s = 1) {
   const int nh = (M + 63) >> 6;
   for (int i = threadIdx.x; i < 64 + nh; i += T) {
     const int t = i < 64 ? i : 64 * (i - 64);
-    tw[i] = t < M ? __ldg(twM + t) : make_float2(1.f, 0.f);
+    tw[i] = t < M ? __ldg(twM + (int64_t)t * s) : make_float2(1.f, 0.f);
   }
 }
 
@@ -378,6 +379,121 @@ __global__ void __launch_bounds__(T, 65536 / (64 * T)) long_chan_inv(const KArgs
     const float2 F = buf[padi(dif_pos(q, pl))];
     const float w = __ldg(a.gdw + ch.goff + dd);
     __stcg(terms + dd, make_float2(F.x * w, F.y * w));
+  }
+  pdl_trigger();
+}
+
+// ------------------------------------------------------------------ M_k > 26000
+// Four-step M = M1 M2 (M2 <= 26000): q = M2 n1 + n2, k = k1 + M1 k2,
+//   Y[k1 + M1 k2] = sum_n2 w_M2^{n2 k2} w_M^{n2 k1} sum_n1 y[M2 n1 + n2] w_M1^{n1 k1}
+// (w = e^{SIGN 2 pi i / .}).  Step 1 (register DFT_M1 per n2, twiddle) writes the rows
+// A[k1][n2] to the channel's staging scratch; step 2 runs each row's DFT_M2 in shared memory.
+template <int M1, int SIGN, class LD>
+__device__ __forceinline__ void big_step1(float2 *A, int M, int M2, const float2 *twM, LD load) {
+  for (int n2 = threadIdx.x; n2 < M2; n2 += 512) {
+    float2 v[M1];
+#pragma unroll
+    for (int n1 = 0; n1 < M1; ++n1) v[n1] = load(M2 * n1 + n2);
+    dft<M1, SIGN>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < M1; ++k1) {
+      float2 w = __ldg(twM + n2 * k1);  // e^{2 pi i n2 k1 / M}, index < M
+      if (SIGN < 0) w = cconj(w);
+      __stcg(A + (int64_t)k1 * M2 + n2, k1 ? cmul(v[k1], w) : v[k1]);
+    }
+  }
+}
+template <int SIGN, class LD>
+__device__ __forceinline__ void big_step1_any(int M1, float2 *A, int M, int M2, const float2 *twM,
+                                              LD load) {
+  switch (M1) {
+    case 2: big_step1<2, SIGN>(A, M, M2, twM, load); break;
+    case 3: big_step1<3, SIGN>(A, M, M2, twM, load); break;
+    case 4: big_step1<4, SIGN>(A, M, M2, twM, load); break;
+    case 5: big_step1<5, SIGN>(A, M, M2, twM, load); break;
+    case 6: big_step1<6, SIGN>(A, M, M2, twM, load); break;
+    case 8: big_step1<8, SIGN>(A, M, M2, twM, load); break;
+    case 9: big_step1<9, SIGN>(A, M, M2, twM, load); break;
+    case 10: big_step1<10, SIGN>(A, M, M2, twM, load); break;
+    case 12: big_step1<12, SIGN>(A, M, M2, twM, load); break;
+    case 15: big_step1<15, SIGN>(A, M, M2, twM, load); break;
+    default: big_step1<16, SIGN>(A, M, M2, twM, load); break;
+  }
+}
+
+__global__ void __launch_bounds__(512, 1) long_chan_fwd_big(const KArgs a) {
+  extern __shared__ float4 smem4[];
+  float2 *buf = reinterpret_cast<float2 *>(smem4);
+  const ChanDev ch = a.chan[a.pchans[blockIdx.x]];
+  const int64_t ul = blockIdx.y, row = a.unit0 + ul;
+  const int N2x = (int)a.L, N = N2x / 2;
+  const int M = ch.M, M1 = ch.m1, M2 = M / M1;
+  const float2 *twM = a.twM + ch.twoff;
+  float2 *tws = long_tw_ptr(buf, M2);
+  DifPlan &pl = *long_plan_ptr(buf, M2);
+  if (threadIdx.x == 0) build_dif_plan(pl, M2);
+  load_twiddles<512>(tws, twM, M2, M1);
+  pdl_wait();
+  const float2 *X = a.stage + ul * a.xs;
+  float2 *A = a.stage + ul * a.xs + ch.soff;
+  big_step1_any<+1>(M1, A, M, M2, twM, [&](int q) {  // the fold, as in long_chan_fwd
+    int dd = q - ch.lo_mod;
+    if (dd < 0) dd += M;
+    float2 v = make_float2(0.f, 0.f);
+    if (dd < ch.len) {
+      int jj = ch.lo + dd;
+      if (jj < 0) jj += N2x;
+      else if (jj >= N2x) jj -= N2x;
+      const bool cj = jj > N;
+      const float2 xv = __ldcg(X + (cj ? N2x - jj : jj));
+      const float w = __ldg(a.gw + ch.goff + dd);
+      v = make_float2(xv.x * w, cj ? -xv.y * w : xv.y * w);
+    }
+    return v;
+  });
+  __syncthreads();
+  float2 *out = a.coef_out + row * a.C + ch.off;
+  for (int k1 = 0; k1 < M1; ++k1) {
+    for (int n2 = threadIdx.x; n2 < M2; n2 += 512) buf[padi(n2)] = __ldcg(A + (int64_t)k1 * M2 + n2);
+    __syncthreads();
+    dif_fft<+1, 512>(buf, M2, tws, pl);
+    for (int k2 = threadIdx.x; k2 < M2; k2 += 512) __stcs(out + k1 + M1 * k2, buf[padi(dif_pos(k2, pl))]);
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
+__global__ void __launch_bounds__(512, 1) long_chan_inv_big(const KArgs a) {
+  extern __shared__ float4 smem4[];
+  float2 *buf = reinterpret_cast<float2 *>(smem4);
+  const ChanDev ch = a.chan[a.pchans[blockIdx.x]];
+  const int64_t ul = blockIdx.y, row = a.unit0 + ul;
+  const int M = ch.M, M1 = ch.m1, M2 = M / M1;
+  const float2 *twM = a.twM + ch.twoff;
+  float2 *tws = long_tw_ptr(buf, M2);
+  DifPlan &pl = *long_plan_ptr(buf, M2);
+  if (threadIdx.x == 0) build_dif_plan(pl, M2);
+  load_twiddles<512>(tws, twM, M2, M1);
+  pdl_wait();
+  const float2 *in = a.coef_in + row * a.C + ch.off;
+  float2 *A = a.stage + ul * a.zs + ch.soff;
+  big_step1_any<-1>(M1, A, M, M2, twM, [&](int q) { return __ldcs(in + q); });
+  __syncthreads();
+  float2 *terms = a.stage + ul * a.zs + ch.goff;
+  for (int k1 = 0; k1 < M1; ++k1) {
+    for (int n2 = threadIdx.x; n2 < M2; n2 += 512) buf[padi(n2)] = __ldcg(A + (int64_t)k1 * M2 + n2);
+    __syncthreads();
+    dif_fft<-1, 512>(buf, M2, tws, pl);
+    // F[q], q = k1 + M1 k2 -> the support bins dd = q - lo_mod (mod M) < L_k
+    for (int k2 = threadIdx.x; k2 < M2; k2 += 512) {
+      int dd = k1 + M1 * k2 - ch.lo_mod;
+      if (dd < 0) dd += M;
+      if (dd >= ch.len) continue;
+      const float2 F = buf[padi(dif_pos(k2, pl))];
+      const float w = __ldg(a.gdw + ch.goff + dd);
+      __stcg(terms + dd, make_float2(F.x * w, F.y * w));
+    }
+    __syncthreads();
   }
   pdl_trigger();
 }

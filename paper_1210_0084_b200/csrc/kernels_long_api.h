@@ -10,10 +10,13 @@ struct KArgs;
 
 // channel-kernel size classes: CTA threads and the largest M_k of each (shared memory is
 // sized per class, so the many short channels do not pay for the longest one's buffer)
-constexpr int kLongClasses = 4;
+// class 4 (kLongClasses - 1): M_k > 26000, a four-step M1 x M2 through the row's staging
+// scratch with M2 <= 26000 in shared memory
+constexpr int kLongClasses = 5;
+constexpr int kLongSmemMax = 26000;  // largest shared-memory DFT
 __host__ __device__ constexpr int long_class_threads(int c) { return c == 0 ? 128 : c == 1 ? 256 : 512; }
 __host__ __device__ constexpr int long_class_maxm(int c) {
-  return c == 0 ? 1536 : c == 1 ? 6144 : c == 2 ? 12288 : 26000;
+  return c == 0 ? 1536 : c == 1 ? 6144 : c == 2 ? 12288 : c == 3 ? kLongSmemMax : 16 * kLongSmemMax;
 }
 
 // largest stage count of a channel DFT (radices >= 2: log2(26000) < 15)

@@ -20,6 +20,8 @@ struct ChanDev {
   int32_t twoff;   // offset of the e^{+2 pi i t / M_k} table
   float scale;     // 1/sqrt(M_k)  (Alg. 1 sqrt(M)*IFFT incl. 1/M, Alg. 2 FFT/sqrt(M); C1)
   int32_t lo_mod;  // lo_k mod M_k in [0, M_k)
+  int32_t m1 = 0;   // long mode, M_k > 26000: four-step factor M1 (M_k = M1 * M2)
+  int32_t soff = 0; // long mode, M_k > 26000: offset of the channel's staging scratch
 };
 
 // A packet = consecutive channels of one length M, processed for nu consecutive units at
@@ -109,6 +111,8 @@ struct slicq_plan {
   std::vector<uint32_t> dpos;
   std::vector<float> lgw, lgdw;          // long mode filter weights
   std::vector<uint32_t> lrow, lent;      // long mode per-bin term lists
+  std::vector<int32_t> lm1;              // long mode: four-step factor of M_k > 26000 (else 0)
+  std::vector<int64_t> lsoff;            // long mode: staging scratch offset of those channels
 };
 
 namespace slicq {

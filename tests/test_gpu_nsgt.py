@@ -40,10 +40,12 @@ def test_nsgt_matches_oracle_and_reconstructs(L, n, B, bpo, fmin, raster):
 
 @pytest.mark.parametrize("L,n,B,bpo,fmin", [
     (2 ** 18, 2 ** 18, 2, 48, 50.0), (2 ** 19, 400000, 1, 24, 50.0),
-    (2 ** 20, 2 ** 20, 2, 48, 50.0), (2 ** 21, 2 ** 21 - 1000, 1, 96, 60.0)])
+    (2 ** 20, 2 ** 20, 2, 48, 50.0), (2 ** 21, 2 ** 21 - 1000, 1, 96, 60.0),
+    (2 ** 22, 2 ** 22, 1, 96, 60.0), (2 ** 22, 3000000, 1, 48, 60.0)])
 def test_long_nsgt_matches_oracle_and_reconstructs(L, n, B, bpo, fmin):
-    """Long signals (kernels_long.cuh): four-step FFT_L with N1 = 512 .. 8192 columns and
-    shared-memory mixed-radix channel FFTs up to M_k = 15 360."""
+    """Long signals (kernels_long.cuh): four-step FFT_L with N1 = 512 .. 8192 columns,
+    shared-memory mixed-radix channel FFTs (M_k <= 26000) and, at L = 2^22, the four-step
+    channel FFTs through the staging scratch (M_k = 30720 = 2 x 15360, 60750 = 3 x 20250)."""
     from paper_1210_0084_b200 import api
     args = (44100.0, fmin, 22050.0, bpo, L, 64, 0)
     plan = api.Plan(*args)
