@@ -90,12 +90,14 @@ enum { SLICQ_PLAN_HOST_ONLY = 1 }; /* plan_create_ex flag: host tables only, no 
  *   bins_per_octave  B >= 1
  *   sl_len           2N: divisible by 4 and 2/3/5-smooth.  The CUDA path implements
  *                    2N = 2^12 .. 2^17 (4096 .. 131072; 2N >= 65536 use a four-step FFT
- *                    through the workspace); other valid values give SLICQ_EUNSUPPORTED
- *                    unless SLICQ_PLAN_HOST_ONLY is set.
+ *                    through the workspace) for every entry point, and 2N = 2^18 .. 2^22
+ *                    for the full-length CQ-NSGT (slicq_nsgt_*) only; other valid values
+ *                    give SLICQ_EUNSUPPORTED unless SLICQ_PLAN_HOST_ONLY is set.
  *   tr_area          Tukey transition length (the paper's M): even, 2 <= tr < N
  *   rasterize        SLICQ_RASTER_*
  *   out              receives the plan (NULL on failure)
- * The plan allocates its device tables (a few MB) on the device current at the call.
+ * The plan allocates its device tables (a few MB; up to ~100 MB for 2N = 2^22) on the device
+ * current at the call.
  * Returns SLICQ_EINVAL, SLICQ_ENOTFRAME, SLICQ_EUNSUPPORTED, SLICQ_ECUDA, SLICQ_ENOMEM. */
 SLICQ_API int plan_create(double fs, double fmin, double fmax, int bins_per_octave, int64_t sl_len,
                 int64_t tr_area, int rasterize, slicq_plan **out);
@@ -167,7 +169,9 @@ SLICQ_API int slicq_inverse_masked(const slicq_plan *p, const slicq_c32 *coeffs,
 
 /* ------------------------------------------------------------------ full-length CQ-NSGT
  * slicq_nsgt_forward / slicq_nsgt_inverse: the CQ-NSGT of Alg. 1 / Alg. 2 of a
- * whole signal of length L = sl_len (for L up to the library's 2^17):
+ * whole signal of length L = sl_len (L = 2^12 .. 2^22 — plans with
+ * sl_len = 2^18 .. 2^22 serve only these two calls, the sliCQ calls on them return
+ * SLICQ_EUNSUPPORTED; channel lengths up to 16 x 26000):
  * the frame is x itself (zero padded from n to L), no slicing window, no overlap; the plan's
  * channels are the CQ-NSGT's at length L.
  *   x, y    device float32 [batch][n], 1 <= n <= sl_len

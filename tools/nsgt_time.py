@@ -5,9 +5,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1210_0084_b200 import api
 CASES = ((16384, 1024, 24, 50.0), (131072, 128, 96, 60.0), (2 ** 18, 64, 48, 50.0),
-         (2 ** 20, 16, 48, 50.0), (2 ** 21, 8, 96, 60.0))
+         (2 ** 20, 16, 48, 50.0), (2 ** 21, 8, 96, 60.0), (2 ** 22, 4, 96, 60.0),
+         (2 ** 22, 4, 48, 60.0))
 if len(sys.argv) > 1:
-    CASES = [c for c in CASES if c[0] == int(sys.argv[1])]
+    CASES = [c for c in CASES if c[0] == int(sys.argv[1])][:1]
 for L, B, bpo, fmin in CASES:
     plan = api.Plan(44100.0, fmin, 22050.0, bpo, L, 64, 0)
     x = torch.randn(B, L, device="cuda") * 0.1
