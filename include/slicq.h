@@ -81,6 +81,9 @@ enum {
 };
 
 enum { SLICQ_PLAN_HOST_ONLY = 1 }; /* plan_create_ex flag: host tables only, no device */
+/* filter shape H of P:262: Hann (C7) or the 4-term Blackman-Harris of the paper's
+ * approximation experiments (reading C20) */
+enum { SLICQ_WINDOW_HANN = 0, SLICQ_WINDOW_BLACKMAN_HARRIS = 1 };
 
 /* ------------------------------------------------------------------ plans
  * plan_create: build the CQ-NSGT system for slices of length sl_len = 2N.
@@ -103,6 +106,24 @@ SLICQ_API int plan_create(double fs, double fmin, double fmax, int bins_per_octa
                 int64_t tr_area, int rasterize, slicq_plan **out);
 SLICQ_API int plan_create_ex(double fs, double fmin, double fmax, int bins_per_octave, int64_t sl_len,
                    int64_t tr_area, int rasterize, unsigned flags, slicq_plan **out);
+/* plan_create_ex2: plan_create_ex with the filter options of the paper's approximation
+ * experiments (Sec. V-A; Prop. 4):
+ *   window        SLICQ_WINDOW_HANN (plan_create_ex) or SLICQ_WINDOW_BLACKMAN_HARRIS
+ *   min_width     lower bound on the filter width in bins, >= 1 (plan_create_ex: 4; the x
+ *                 axis of Fig. CoeffQual)
+ *   sampled_from  0, or 2N' (a multiple of 4 dividing sl_len): build the full-length system
+ *                 G(g^L, a) of Prop. 4 -- filters whose samples every sl_len/2N' bins are the
+ *                 2N' system's (g_k[j] = g^L_k[j sl_len/2N'], the width clamp acting on the
+ *                 2N' grid) and counts M_k = (sl_len/2N') M'_k (the same hops a_k; reading
+ *                 C21).  Such a system need not be painless (M_k < L_k where the support is
+ *                 longer than the hops allow): only slicq_nsgt_forward is defined on it
+ *                 (other calls return SLICQ_EUNSUPPORTED), and its device path requires
+ *                 sl_len >= 2^18 (the fold of the long path sums aliased bins).
+ * Errors as plan_create_ex; SLICQ_EINVAL for a bad window / min_width / sampled_from. */
+SLICQ_API int plan_create_ex2(double fs, double fmin, double fmax, int bins_per_octave,
+                              int64_t sl_len, int64_t tr_area, int rasterize, unsigned flags,
+                              int window, double min_width, int64_t sampled_from,
+                              slicq_plan **out);
 /* NULL-safe; frees the plan-owned device tables.  No call may be in flight on the plan. */
 SLICQ_API void plan_destroy(slicq_plan *p);
 
@@ -183,6 +204,26 @@ SLICQ_API int slicq_nsgt_forward(const slicq_plan *p, const float *x, int64_t n,
                                  slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream);
 SLICQ_API int slicq_nsgt_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
                                  int64_t batch, float *y, void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ Prop. 4 / Sec. V-A
+ * slicq_approx_error: the sliCQ's approximation of the full-length CQ-NSGT (Prop. 4,
+ * P:377-391; the experiment of P:475-497).  Per row b and stored
+ * channel k, in the Prop. 4 normalisation c_{n,k} = <f, T_{n a_k} g^L_k-check> (reading C22:
+ * the library's Alg. 1 coefficients divided by sqrt(L a_k), slices by sqrt(2N a_k)):
+ *   out[b][k][0] = sum_n |c_{n,k}|^2
+ *   out[b][k][1] = sum_n |c_{n,k} - (s^0_{n,k} + s^1_{n,k})|^2,  n < L/a_k,
+ * with s^0 + s^1 at n = m N/a_k + n' (n' < N/a_k) = c^m_{n' + N/a_k, k} + c^{m+1}_{n', k}
+ * (the two-layer array of Alg. 3; slices circular).  SNR = 10 log10(sum [0] /
+ * sum [1]).
+ *   ps   sliCQ plan (slices 2N); pl: plan_create_ex2(..., sampled_from = 2N) with sl_len
+ *        L, a multiple of 2N, and the same CQ parameters
+ *   s    device slicq_c32 [batch][S][C_ps], S = L/N: slicq_forward(ps, x, n = L)
+ *   c    device slicq_c32 [batch][C_pl]: slicq_nsgt_forward(pl, x, n = L)
+ *   out  device double [batch][K+2][2], fully overwritten
+ * Enqueued on `stream`.  SLICQ_EINVAL if (ps, pl) is not such a pair; SLICQ_ESHAPE for
+ * NULL / misaligned buffers or batch < 1. */
+SLICQ_API int slicq_approx_error(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
+                                 const slicq_c32 *c, int64_t batch, double *out, void *stream);
 
 /* ------------------------------------------------------------------ slice-range shards
  * Multi-GPU partition of one long stream: a rank owns slices

@@ -3,6 +3,8 @@
 Everything here is the paper's construction written out directly:
   * Table 1 layout and the constant Q ............ P:242-260 (readings C3, C4)
   * sampled Hann filters g_k and plateaus ........ P:262 (readings C7, C8)
+  * Blackman-Harris filters, minimal width,
+    filters sampled from a length-L system ....... P:377-386 (Prop. 4), P:475-490 (C20-C22)
   * coefficient counts M_k = L/a_k >= L_k ........ P:168-170, P:264-265 (C9, C10)
   * frame diagonal and canonical dual ............ P:219-228, Prop. 2 (C1, C16)
   * Tukey slicing window h_0 and its dual ........ P:353-356, P:363-374 (C11, C12)
@@ -68,6 +70,7 @@ class Plan:
     dual_full: List[np.ndarray]
     h0: np.ndarray                 # h_0[t], t = -N..N-1  (index t+N)
     h0dual: np.ndarray             # canonical dual slicing window, same indexing
+    painless: bool = True          # M_k >= L_k for every channel (False only for sampled_from)
 
     @property
     def N(self) -> int:
@@ -119,18 +122,42 @@ def hann(x: np.ndarray) -> np.ndarray:
     return np.where(np.abs(x) <= 0.5, np.cos(np.pi * np.clip(x, -0.5, 0.5)) ** 2, 0.0)
 
 
-def cq_filter(xi: float, Om: float, fs: float, Ls: int):
+# 4-term Blackman-Harris (the window of the paper's approximation experiments),
+# centred on [-1/2, 1/2] (reading C20): H(x) = a0 + a1 cos 2 pi x + a2 cos 4 pi x + a3 cos 6 pi x
+BH = (0.35875, 0.48829, 0.14128, 0.01168)
+
+
+def blackman_harris(x: np.ndarray) -> np.ndarray:
+    x = np.asarray(x, dtype=np.float64)
+    a0, a1, a2, a3 = BH
+    v = a0 + a1 * np.cos(2 * np.pi * x) + a2 * np.cos(4 * np.pi * x) + a3 * np.cos(6 * np.pi * x)
+    return np.where(np.abs(x) <= 0.5, v, 0.0)
+
+
+WINDOWS = {"hann": hann, "blackman_harris": blackman_harris}
+
+
+def cq_filter(xi: float, Om: float, fs: float, Ls: int, window: str = "hann",
+              min_width: float = MIN_WIDTH, grid: Optional[int] = None):
     """g_k[j] = H((j fs/Ls - xi_k)/Omega_k) with width clamp (reading C7).
 
-    omega = xi Ls/fs (fractional), W = max(Omega Ls/fs, 4) bins,
+    omega = xi Ls/fs (fractional), W = max(Omega Ls/fs, min_width) bins,
     J = [ceil(omega - W/2 - eps), floor(omega + W/2 + eps)], g = H((j - omega)/W).
-    Returns (lo, g, omega, W)."""
-    omega = xi * Ls / fs
-    W = max(Om * Ls / fs, MIN_WIDTH)
+    grid = 2N (Prop. 4, reading C21): the filter of a length-Ls system whose samples at the
+    multiples of s = Ls/2N are the length-2N system's filter, g_k[j] = g^L_k[j Ls/2N]:
+    omega = s (xi 2N/fs), W = s max(Omega 2N/fs, min_width) -- the width clamp acts on the
+    2N grid.  Returns (lo, g, omega, W)."""
+    if grid is None:
+        omega = xi * Ls / fs
+        W = max(Om * Ls / fs, min_width)
+    else:
+        sc = Ls // grid
+        omega = sc * (xi * grid / fs)
+        W = sc * max(Om * grid / fs, min_width)
     lo = math.ceil(omega - W / 2 - EDGE_EPS)
     hi = math.floor(omega + W / 2 + EDGE_EPS)
     j = np.arange(lo, hi + 1, dtype=np.float64)
-    return lo, hann((j - omega) / W), omega, W
+    return lo, WINDOWS[window]((j - omega) / W), omega, W
 
 
 def _eval_on(lo: int, g: np.ndarray, j: np.ndarray) -> np.ndarray:
@@ -253,24 +280,49 @@ def dual_slicing_window(h0: np.ndarray, N: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- the plan
+def _raw_filters(lay: Layout, fs: float, Ls: int, window: str, min_width: float,
+                 grid: Optional[int]):
+    cq = [cq_filter(lay.xi[i], lay.Omega[i], fs, Ls, window, min_width, grid)
+          for i in range(lay.K)]
+    (lo0, g0), (loN, gN) = plateau_filters(cq, Ls)
+    return [(lo0, g0, "dc")] + [(lo, g, "cq") for (lo, g, _, _) in cq] + [(loN, gN, "nyq")]
+
+
 def make_plan(fs: float, fmin: float, fmax: Optional[float], B: int, sl_len: int, tr: int,
-              rasterize: int = 0) -> Plan:
-    """Precompute everything Alg. 3/4 need for slices of length 2N = sl_len."""
+              rasterize: int = 0, window: str = "hann", min_width: float = MIN_WIDTH,
+              sampled_from: Optional[int] = None) -> Plan:
+    """Precompute everything Alg. 3/4 need for slices of length 2N = sl_len.
+
+    window: "hann" or "blackman_harris"; min_width: the lower bound on
+    the filter width in bins (C7; the x axis of the paper's Fig. CoeffQual).
+    sampled_from = 2N' (Prop. 4; reading C21): the length-sl_len system whose
+    filters, sampled every sl_len/2N' bins, are those of the length-2N' system with the same
+    parameters, and whose counts are M_k = (sl_len/2N') M'_k (the same hops a_k) -- the
+    full-length CQ-NSGT that the sliCQ with slices 2N' approximates."""
     if sl_len % 4 != 0 or not is_235_smooth(sl_len):
         raise ValueError("sl_len must be divisible by 4 and 2/3/5-smooth")
     N = sl_len // 2
     if tr % 2 != 0 or tr < 2 or tr >= N:
         raise ValueError("tr_area must be even, >= 2 and < sl_len/2 (P:373: M < N)")
+    if not min_width >= 1.0:
+        raise ValueError("min_width must be >= 1 bin")
     lay = cq_layout(fs, fmin, fmax, B)
     Ls = sl_len
-    cq = [cq_filter(lay.xi[i], lay.Omega[i], fs, Ls) for i in range(lay.K)]
-    (lo0, g0), (loN, gN) = plateau_filters(cq, Ls)
-    raw = [(lo0, g0, "dc")] + [(lo, g, "cq") for (lo, g, _, _) in cq] + [(loN, gN, "nyq")]
-    Ms = channel_lengths([g.shape[0] for _, g, _ in raw], B, rasterize)
+    if sampled_from is not None and (sampled_from <= 0 or Ls % sampled_from != 0):
+        raise ValueError("sampled_from must divide sl_len")
+    raw = _raw_filters(lay, fs, Ls, window, min_width, sampled_from)
+    if sampled_from is None:
+        Ms = channel_lengths([g.shape[0] for _, g, _ in raw], B, rasterize)
+    else:
+        raw0 = _raw_filters(lay, fs, sampled_from, window, min_width, None)
+        Ms = [(Ls // sampled_from) * m
+              for m in channel_lengths([g.shape[0] for _, g, _ in raw0], B, rasterize)]
     stored = [Channel(lo, g, M, kind) for (lo, g, kind), M in zip(raw, Ms)]
-    for c in stored:
-        if c.M < c.L:
-            raise ValueError("painless condition M_k >= L_k violated (P:170)")
+    painless = all(c.M >= c.L for c in stored)
+    # a sampled_from system keeps the slice system's hops even where its support is longer
+    # than M_k (Prop. 4 needs only the analysis, which Alg. 1 folds; reading C21)
+    if not painless and sampled_from is None:
+        raise ValueError("painless condition M_k >= L_k violated (P:170)")
     K = lay.K
     # mirrors K+2..2K+1 of Table 1 (P:252): channel 2K+2-k mirrors k = K..1 about Nyquist
     mirrors = []
@@ -285,4 +337,4 @@ def make_plan(fs: float, fmin: float, fmax: Optional[float], B: int, sl_len: int
     return Plan(fs=fs, fmin=fmin, fmax=fs / 2 if fmax is None else fmax, B=B, sl_len=sl_len,
                 tr=tr, rasterize=rasterize, layout=lay, stored=stored, full=full, D=D,
                 dual_stored=dual_full[:K + 2], dual_full=dual_full, h0=h0,
-                h0dual=dual_slicing_window(h0, N))
+                h0dual=dual_slicing_window(h0, N), painless=painless)

@@ -11,12 +11,16 @@ SLICQ_OK = 0
 ERRORS = {-1: "EINVAL", -2: "ENOTFRAME", -3: "ESHAPE", -4: "ECUDA", -5: "ENOMEM",
           -6: "EINTERNAL", -7: "EUNSUPPORTED"}
 PLAN_HOST_ONLY = 1
+WINDOWS = {"hann": 0, "blackman_harris": 1}
 
 # every symbol include/slicq.h declares, with (restype, argtypes)
 _p, _i64, _i32, _d, _sz, _u = C.c_void_p, C.c_int64, C.c_int, C.c_double, C.c_size_t, C.c_uint
 SIGNATURES = {
     "plan_create": (_i32, [_d, _d, _d, _i32, _i64, _i64, _i32, C.POINTER(_p)]),
     "plan_create_ex": (_i32, [_d, _d, _d, _i32, _i64, _i64, _i32, _u, C.POINTER(_p)]),
+    "plan_create_ex2": (_i32, [_d, _d, _d, _i32, _i64, _i64, _i32, _u, _i32, _d, _i64,
+                               C.POINTER(_p)]),
+    "slicq_approx_error": (_i32, [_p, _p, _p, _p, _i64, _p, _p]),
     "plan_destroy": (None, [_p]),
     "slicq_num_channels": (_i32, [_p]),
     "slicq_num_cq_channels": (_i32, [_p]),

@@ -27,16 +27,23 @@ class Plan:
     """plan_create(fs, fmin, fmax, bins_per_octave, sl_len, tr_area, rasterize)."""
 
     def __init__(self, fs: float, fmin: float, fmax: float, bins_per_octave: int, sl_len: int,
-                 tr_area: int, rasterize: int = 0, host_only: bool = False):
+                 tr_area: int, rasterize: int = 0, host_only: bool = False,
+                 window: str = "hann", min_width: float = 4.0, sampled_from: int = 0):
+        """window / min_width / sampled_from: plan_create_ex2 (the filter options of the
+        paper's approximation experiments; sampled_from = 2N builds Prop. 4's full-length
+        system for slices of 2N)."""
         L = lib()
         h = C.c_void_p()
         flags = _lib.PLAN_HOST_ONLY if host_only else 0
-        check(L.plan_create_ex(float(fs), float(fmin), float(fmax), int(bins_per_octave),
-                               int(sl_len), int(tr_area), int(rasterize), flags, C.byref(h)),
+        check(L.plan_create_ex2(float(fs), float(fmin), float(fmax), int(bins_per_octave),
+                                int(sl_len), int(tr_area), int(rasterize), flags,
+                                _lib.WINDOWS[window], float(min_width), int(sampled_from),
+                                C.byref(h)),
               "plan_create")
         self._h = h
         self.host_only = host_only
         self.params = (fs, fmin, fmax, bins_per_octave, sl_len, tr_area, rasterize)
+        self.options = dict(window=window, min_width=min_width, sampled_from=sampled_from)
         self._ws = {}
 
     # ------------------------------------------------------------ lifetime
@@ -282,6 +289,28 @@ def plan_for_config(cfg) -> Plan:
     """Plan for a synth.configs.SlicqConfig."""
     return Plan(cfg.fs, cfg.fmin, cfg.fmax_eff, cfg.bins_per_octave, cfg.sl_len, cfg.tr_area,
                 cfg.rasterize)
+
+
+def approximation_error(x: torch.Tensor, ps: Plan, pl: Plan, stream=None):
+    """Prop. 4 / Sec. V-A: how closely the sliCQ
+    with plan ps (slices 2N) approximates the full-length CQ-NSGT with pl (created with
+    sampled_from = 2N, sl_len L).  x: float32 [batch][L] on the device.  Runs slicq_forward,
+    slicq_nsgt_forward and slicq_approx_error; returns (snr_db [batch] float64 tensor,
+    sums [batch][K+2][2] float64: per channel sum |c|^2 and sum |c - (s^0 + s^1)|^2 in the
+    Prop. 4 normalisation)."""
+    if x.dim() == 1:
+        x = x[None]
+    _check_tensor(x, torch.float32, "x")
+    B, L = x.shape
+    if L != pl.sl_len:
+        raise ValueError("x must hold L = pl.sl_len samples per row")
+    s = ps.forward(x, stream=stream)
+    c = pl.nsgt_forward(x, stream=stream)
+    out = torch.empty((B, ps.num_channels, 2), dtype=torch.float64, device=x.device)
+    check(lib().slicq_approx_error(ps._h, pl._h, s.data_ptr(), c.data_ptr(), B, out.data_ptr(),
+                                   _stream_ptr(stream)), "slicq_approx_error")
+    tot = out.sum(dim=1)
+    return 10.0 * torch.log10(tot[:, 0] / tot[:, 1]), out
 
 
 def apply_mask(c: torch.Tensor, mask, db: bool = True) -> torch.Tensor:

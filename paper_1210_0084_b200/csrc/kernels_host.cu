@@ -28,6 +28,48 @@ __global__ void overlap_add_kernel(float *y, int64_t y_stride, const float *spil
     y[row * y_stride + i] += spill[row * count + i];
 }
 
+// Prop. 4 sums (slicq_approx_error): one CTA per (stored channel, row).  c_P4 = c sqrt(M^L)/L,
+// s_P4 = s sqrt(M)/(2N) (reading C22); (s^0 + s^1)[m h + n'] = c^m[n' + h] + c^{m+1}[n'],
+// h = M/2 = N/a_k (two-layer array of Alg. 3, slices circular).
+__global__ void __launch_bounds__(256) approx_kernel(const ChanDev *chs, const ChanDev *chl,
+                                                     const float2 *s, const float2 *c, int64_t Cs,
+                                                     int64_t Cl, int S, float scs, float scl_num,
+                                                     double *out) {
+  const int k = blockIdx.x, K2 = gridDim.x;
+  const int64_t b = blockIdx.y;
+  const ChanDev a = chs[k], l = chl[k];
+  const int h = a.M / 2;
+  const float ss = sqrtf((float)a.M) * scs, sl = sqrtf((float)l.M) * scl_num;
+  const float2 *srow = s + b * (int64_t)S * Cs + a.off;
+  const float2 *crow = c + b * Cl + l.off;
+  double e0 = 0.0, e1 = 0.0;
+  for (int n = threadIdx.x; n < l.M; n += 256) {
+    const int m = n / h, np = n - m * h;
+    const int m1 = m + 1 == S ? 0 : m + 1;
+    const float2 v0 = srow[(int64_t)m * Cs + np + h], v1 = srow[(int64_t)m1 * Cs + np];
+    const float2 cv = crow[n];
+    const float cr = cv.x * sl, ci = cv.y * sl;
+    const float dr = cr - (v0.x + v1.x) * ss, di = ci - (v0.y + v1.y) * ss;
+    e0 += (double)cr * cr + (double)ci * ci;
+    e1 += (double)dr * dr + (double)di * di;
+  }
+  __shared__ double r0[256], r1[256];
+  r0[threadIdx.x] = e0;
+  r1[threadIdx.x] = e1;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      r0[threadIdx.x] += r0[threadIdx.x + w];
+      r1[threadIdx.x] += r1[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[(b * K2 + k) * 2 + 0] = r0[0];
+    out[(b * K2 + k) * 2 + 1] = r1[0];
+  }
+}
+
 const int kSizes[] = {1, 2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16, 18, 20, 24, 25, 27, 30, 32};
 const int kSmall[] = {4, 6, 8, 10, 12, 16, 18, 20, 24, 30, 32};
 
@@ -247,6 +289,9 @@ int configure_kernels(slicq_plan *p) {
                      "CUDA path implements sl_len = 2^12 .. 2^17 (sliCQ) and up to 2^22 "
                      "(full-length CQ-NSGT)");
   if (logN >= 17) return configure_long(p, logN);
+  if (!p->painless)  // the element tables hold one term per fold position
+    return set_error(SLICQ_EUNSUPPORTED, "a system with M_k < L_k (sampled_from) needs "
+                                         "sl_len >= 2^18 on the device");
   KernelConfig &kc = p->kc;
   kc.logN = logN;
   kc.large = logN >= 15;
@@ -622,19 +667,19 @@ int upload(slicq_plan *p) {
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
+  // (the dynamic shared-memory limit: the device cap, allow_max_dyn_smem)
   int rc = 0;
   switch (p->kc.logN) {
-    case 11: rc = set_attrs<11>(p->kc.spec_smem); break;
-    case 12: rc = set_attrs<12>(p->kc.spec_smem); break;
-    case 13: rc = set_attrs<13>(p->kc.spec_smem); break;
-    case 14: rc = set_attrs<14>(p->kc.spec_smem); break;
+    case 11: rc = set_attrs<11>(kSmemCap); break;
+    case 12: rc = set_attrs<12>(kSmemCap); break;
+    case 13: rc = set_attrs<13>(kSmemCap); break;
+    case 14: rc = set_attrs<14>(kSmemCap); break;
     case 15: rc = large_set_attrs<15>(); break;
     case 16: rc = large_set_attrs<16>(); break;
     default: rc = long_set_attrs(p->kc.logN, p->kc.lcls); break;
   }
   for (int v = 0; v < 12 && rc == 0 && !p->kc.longmode; ++v)  // bit 0: forward, bit 1: lite, v >> 2: mask mode
-    rc = (int)cudaFuncSetAttribute(chan_fn(v & 1, v & 2, v >> 2),
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->kc.chan_smem);
+    rc = (int)allow_max_dyn_smem((const void *)chan_fn(v & 1, v & 2, v >> 2));
   if (rc != 0)
     return set_error(SLICQ_ECUDA, std::string("cudaFuncSetAttribute: ") +
                                       cudaGetErrorString((cudaError_t)rc));
@@ -866,6 +911,8 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t units = nslices * batch;
   a.toff = p->kc.toff_i;
+  if (!p->painless)
+    return set_error(SLICQ_EUNSUPPORTED, "synthesis needs a painless system (M_k >= L_k, P:170)");
   if (p->kc.longmode) {  // full-length CQ-NSGT only (kernels_long.cuh)
     if (mode != 1 || nslices != 1 || mask)
       return set_error(SLICQ_EUNSUPPORTED, "sl_len > 2^17: only the full-length CQ-NSGT "
@@ -890,6 +937,24 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
   }
+  return SLICQ_OK;
+}
+
+int launch_approx(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
+                  const slicq_c32 *c, int64_t batch, double *out, void *stream) {
+  int rc = check_device(ps);
+  if (!rc) rc = check_device(pl);
+  if (rc) return rc;
+  if (batch > 65535) return set_error(SLICQ_ESHAPE, "batch too large");
+  const int S = (int)(pl->sl_len / ps->N);
+  approx_kernel<<<dim3((unsigned)(ps->K + 2), (unsigned)batch), 256, 0,
+                  static_cast<cudaStream_t>(stream)>>>(
+      ps->d.chan, pl->d.chan, reinterpret_cast<const float2 *>(s),
+      reinterpret_cast<const float2 *>(c), ps->C, pl->C, S, (float)(1.0 / (double)ps->sl_len),
+      (float)(1.0 / (double)pl->sl_len), out);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return set_error(SLICQ_ECUDA, std::string("approx launch: ") + cudaGetErrorString(e));
   return SLICQ_OK;
 }
 

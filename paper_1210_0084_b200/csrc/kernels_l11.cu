@@ -2,6 +2,7 @@
 // Instantiation of the per-slice spectrum kernels for N = 2^SLICQ_LOGN (one translation
 // unit per size so that the sizes compile in parallel).
 #include "kernels_dev.cuh"
+#include "kernels_long_api.h"
 
 namespace slicq {
 namespace kern {
@@ -13,8 +14,8 @@ int set_attrs<SLICQ_LOGN>(size_t smem) {
                        (const void *)slicq_fwd_spec_kernel<SLICQ_LOGN, 1>,
                        (const void *)slicq_inv_spec_kernel<SLICQ_LOGN, 1>};
   for (const void *f : fns) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    (void)smem;
+    const cudaError_t e = allow_max_dyn_smem(f);
     if (e != cudaSuccess) return (int)e;
   }
   return 0;

@@ -72,8 +72,7 @@ int long_set_attrs(int logN, const LongClasses &cls) {
   cudaError_t e = cudaSuccess;
   for (int c = 0; c < kLongClasses && e == cudaSuccess; ++c)
     for (int f = 0; f < 2 && e == cudaSuccess; ++f)
-      e = cudaFuncSetAttribute(chan_kernel(f == 0, c), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)std::max<size_t>(cls.smem[c], 1024));
+      e = allow_max_dyn_smem((const void *)chan_kernel(f == 0, c));  // not the plan's size
   return (int)e;
 }
 

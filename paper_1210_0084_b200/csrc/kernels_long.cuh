@@ -317,6 +317,27 @@ __device__ __forceinline__ DifPlan *long_plan_ptr(float2 *buf, int M) {
   return reinterpret_cast<DifPlan *>(long_tw_ptr(buf, M) + long_twiddle_entries(M));
 }
 
+// fold position q of channel k: sum over the support bins j = lo + dd, dd = q - lo (mod M),
+// of X(j) g_k[j]/sqrt(M_k) (one term for a painless system; the aliases dd + M, dd + 2M ...
+// of a sampled_from system, reading C21); real input: X(j) = conj X(2N - j), j in (-2N, 2N)
+__device__ __forceinline__ float2 long_fold(const KArgs &a, const ChanDev &ch, const float2 *X,
+                                            int q, int N2x, int N) {
+  int dd = q - ch.lo_mod;
+  if (dd < 0) dd += ch.M;
+  float2 v = make_float2(0.f, 0.f);
+  for (; dd < ch.len; dd += ch.M) {
+    int jj = ch.lo + dd;
+    if (jj < 0) jj += N2x;
+    else if (jj >= N2x) jj -= N2x;
+    const bool cj = jj > N;
+    const float2 xv = __ldcg(X + (cj ? N2x - jj : jj));
+    const float w = __ldg(a.gw + ch.goff + dd);
+    v.x = fmaf(xv.x, w, v.x);
+    v.y = fmaf(cj ? -xv.y : xv.y, w, v.y);
+  }
+  return v;
+}
+
 // Alg. 1 per channel: c_k = sqrt(M_k) IFFT_{M_k}(fold of X g_k)  (C1, C5, C15)
 // (grid x: the channels of one size class, listed in a.pchans; 64 registers per thread)
 template <int T>
@@ -333,21 +354,7 @@ __global__ void __launch_bounds__(T, 65536 / (64 * T)) long_chan_fwd(const KArgs
   DifPlan &pl = *long_plan_ptr(buf, M);
   if (threadIdx.x == 0) build_dif_plan(pl, M);
   load_twiddles<T>(tws, a.twM + ch.twoff, M);
-  for (int q = threadIdx.x; q < M; q += T) {
-    int dd = q - ch.lo_mod;
-    if (dd < 0) dd += M;
-    float2 v = make_float2(0.f, 0.f);
-    if (dd < ch.len) {  // unwrapped bin j = lo + dd in (-2N, 2N); real input: X(j) = conj X(2N-j)
-      int jj = ch.lo + dd;
-      if (jj < 0) jj += N2x;
-      else if (jj >= N2x) jj -= N2x;
-      const bool cj = jj > N;
-      const float2 xv = __ldcg(X + (cj ? N2x - jj : jj));
-      const float w = __ldg(a.gw + ch.goff + dd);
-      v = make_float2(xv.x * w, cj ? -xv.y * w : xv.y * w);
-    }
-    buf[padi(q)] = v;
-  }
+  for (int q = threadIdx.x; q < M; q += T) buf[padi(q)] = long_fold(a, ch, X, q, N2x, N);
   __syncthreads();
   dif_fft<+1, T>(buf, M, tws, pl);
   float2 *out = a.coef_out + row * a.C + ch.off;
@@ -436,21 +443,7 @@ __global__ void __launch_bounds__(512, 1) long_chan_fwd_big(const KArgs a) {
   pdl_wait();
   const float2 *X = a.stage + ul * a.xs;
   float2 *A = a.stage + ul * a.xs + ch.soff;
-  big_step1_any<+1>(M1, A, M, M2, twM, [&](int q) {  // the fold, as in long_chan_fwd
-    int dd = q - ch.lo_mod;
-    if (dd < 0) dd += M;
-    float2 v = make_float2(0.f, 0.f);
-    if (dd < ch.len) {
-      int jj = ch.lo + dd;
-      if (jj < 0) jj += N2x;
-      else if (jj >= N2x) jj -= N2x;
-      const bool cj = jj > N;
-      const float2 xv = __ldcg(X + (cj ? N2x - jj : jj));
-      const float w = __ldg(a.gw + ch.goff + dd);
-      v = make_float2(xv.x * w, cj ? -xv.y * w : xv.y * w);
-    }
-    return v;
-  });
+  big_step1_any<+1>(M1, A, M, M2, twM, [&](int q) { return long_fold(a, ch, X, q, N2x, N); });
   __syncthreads();
   float2 *out = a.coef_out + row * a.C + ch.off;
   for (int k1 = 0; k1 < M1; ++k1) {

@@ -8,6 +8,22 @@ namespace slicq {
 namespace kern {
 struct KArgs;
 
+// Allow a kernel the device's whole opt-in shared memory (minus its static shared memory).
+// The dynamic shared-memory limit is a per-function attribute shared by every plan in the
+// process; each launch passes its own size, so a later plan with a smaller configuration
+// cannot invalidate an earlier plan's launches.
+inline cudaError_t allow_max_dyn_smem(const void *f) {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - (int)fa.sharedSizeBytes);
+  return e;
+}
+
 // channel-kernel size classes: CTA threads and the largest M_k of each (shared memory is
 // sized per class, so the many short channels do not pay for the longest one's buffer)
 // class 4 (kLongClasses - 1): M_k > 26000, a four-step M1 x M2 through the row's staging

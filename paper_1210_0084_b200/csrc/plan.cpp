@@ -15,7 +15,6 @@ namespace {
 thread_local std::string g_last_error;
 constexpr double kEdgeEps = 1e-9;  // C7/C18 support-edge guard
 constexpr double kKEps = 1e-12;    // C4/C18 guard on B log2(.)
-constexpr double kMinWidth = 4.0;  // C7 minimum filter width in bins
 constexpr double kPi = 3.14159265358979323846;
 
 bool smooth235(int64_t m) {
@@ -38,6 +37,12 @@ double hann(double x) {
   double c = std::cos(kPi * x);
   return c * c;
 }
+// 4-term Blackman-Harris centred on [-1/2, 1/2] (reading C20)
+double blackman_harris(double x) {
+  if (std::fabs(x) > 0.5) return 0.0;
+  return 0.35875 + 0.48829 * std::cos(2.0 * kPi * x) + 0.14128 * std::cos(4.0 * kPi * x) +
+         0.01168 * std::cos(6.0 * kPi * x);
+}
 
 struct Filt {
   int64_t lo;
@@ -58,6 +63,78 @@ int set_error(int code, const std::string &msg) {
 
 using slicq::set_error;
 
+// Filters of the stored channels 0..K+1 on a length-Ls DFT grid (reading C7):
+// fractional centre omega = xi Ls/fs, width W = max(Omega Ls/fs, min_width) bins,
+// J = [ceil(omega - W/2 - eps), floor(omega + W/2 + eps)], g[j] = H((j - omega)/W), then the
+// plateaus (C8).  grid = 2N' > 0 (Prop. 4, reading C21): omega = s (xi 2N'/fs),
+// W = s max(Omega 2N'/fs, min_width), s = Ls/2N' -- sampled every s bins this is the 2N'
+// system's filter.
+static int cq_filters(const slicq_plan *p, int64_t Ls, int64_t grid, std::vector<Filt> &f) {
+  const double fs = p->fs;
+  const int64_t K = p->K;
+  double (*H)(double) = p->window == SLICQ_WINDOW_BLACKMAN_HARRIS ? blackman_harris : hann;
+  f.assign(K + 2, Filt{});
+  std::vector<double> omega(K + 2, 0.0);
+  for (int64_t k = 1; k <= K; ++k) {
+    const double xi = p->xi[k - 1], Om = xi / p->Q;
+    double om, W;
+    if (grid) {
+      const double sc = (double)(Ls / grid);
+      om = sc * (xi * grid / fs);
+      W = sc * std::max(Om * grid / fs, p->min_width);
+    } else {
+      om = xi * Ls / fs;
+      W = std::max(Om * Ls / fs, p->min_width);
+    }
+    const int64_t lo = (int64_t)std::ceil(om - W / 2 - kEdgeEps);
+    const int64_t hi = (int64_t)std::floor(om + W / 2 + kEdgeEps);
+    if (hi < lo) return set_error(SLICQ_ENOTFRAME, "empty filter support");
+    f[k].lo = lo;
+    f[k].v.resize(hi - lo + 1);
+    for (int64_t j = lo; j <= hi; ++j) f[k].v[j - lo] = H(((double)j - om) / W);
+    omega[k] = om;
+  }
+  // plateaus (Table 1 rows 0 and K+1; reading C8)
+  const int64_t a = (int64_t)std::floor(omega[1]);
+  f[0].lo = -a;
+  f[0].v.resize(2 * a + 1);
+  for (int64_t j = -a; j <= a; ++j) f[0].v[j + a] = 1.0 - f[1].at(j < 0 ? -j : j);
+  const int64_t b0 = (int64_t)std::ceil(omega[K]);
+  const int64_t b1 = (int64_t)std::floor((double)Ls - omega[K]);
+  if (b1 < b0) return set_error(SLICQ_ENOTFRAME, "empty filter support");
+  f[K + 1].lo = b0;
+  f[K + 1].v.resize(b1 - b0 + 1);
+  for (int64_t j = b0; j <= b1; ++j) {
+    double v = 1.0 - f[K].at(j) - f[K].at(Ls - j);
+    f[K + 1].v[j - b0] = v > 0.0 ? v : 0.0;
+  }
+  return SLICQ_OK;
+}
+
+// M_k = L/a_k >= L_k (readings C9, C10)
+static int channel_counts(const slicq_plan *p, const std::vector<Filt> &f, std::vector<int64_t> &M) {
+  const int64_t K = p->K, B = p->B;
+  M.assign(K + 2, 0);
+  auto len = [&](int64_t k) { return (int64_t)f[k].v.size(); };
+  if (p->raster == SLICQ_RASTER_NONE) {
+    for (int64_t k = 0; k < K + 2; ++k) M[k] = even_smooth_ge(len(k));
+  } else if (p->raster == SLICQ_RASTER_FULL) {
+    int64_t mx = 0;
+    for (int64_t k = 0; k < K + 2; ++k) mx = std::max(mx, len(k));
+    for (int64_t k = 0; k < K + 2; ++k) M[k] = even_smooth_ge(mx);
+  } else {  // per octave: groups {0}, {K+1}, CQ octaves floor((k-1)/B)
+    M[0] = even_smooth_ge(len(0));
+    M[K + 1] = even_smooth_ge(len(K + 1));
+    for (int64_t k0 = 1; k0 <= K; k0 += B) {
+      const int64_t k1 = std::min(k0 + B - 1, K);
+      int64_t mx = 0;
+      for (int64_t k = k0; k <= k1; ++k) mx = std::max(mx, len(k));
+      for (int64_t k = k0; k <= k1; ++k) M[k] = even_smooth_ge(mx);
+    }
+  }
+  return SLICQ_OK;
+}
+
 static int build_host_plan(slicq_plan *p) {
   const double fs = p->fs, fmin = p->fmin, fmax = p->fmax;
   const int B = p->B;
@@ -76,70 +153,41 @@ static int build_host_plan(slicq_plan *p) {
   p->xi.resize(K);
   for (int64_t k = 1; k <= K; ++k) p->xi[k - 1] = fmin * std::pow(2.0, (double)(k - 1) / B);
 
-  // ---- CQ filters at length Ls (reading C7): fractional centre omega = xi Ls/fs,
-  // width W = max(Omega Ls/fs, 4) bins, J = [ceil(om - W/2 - eps), floor(om + W/2 + eps)],
-  // g[j] = H((j - omega)/W).
-  std::vector<Filt> f(K + 2);
-  std::vector<double> omega(K + 2, 0.0);
-  for (int64_t k = 1; k <= K; ++k) {
-    const double om = p->xi[k - 1] * Ls / fs;
-    double W = (p->xi[k - 1] / p->Q) * Ls / fs;
-    if (W < kMinWidth) W = kMinWidth;
-    const int64_t lo = (int64_t)std::ceil(om - W / 2 - kEdgeEps);
-    const int64_t hi = (int64_t)std::floor(om + W / 2 + kEdgeEps);
-    f[k].lo = lo;
-    f[k].v.resize(hi - lo + 1);
-    for (int64_t j = lo; j <= hi; ++j) f[k].v[j - lo] = hann(((double)j - om) / W);
-    omega[k] = om;
+  // ---- CQ filters and plateaus (readings C7, C8); coefficient counts (C9, C10)
+  std::vector<Filt> f;
+  std::vector<int64_t> Mk;
+  int rc = cq_filters(p, Ls, p->sampled_from, f);
+  if (rc) return rc;
+  if (!p->sampled_from) {
+    rc = channel_counts(p, f, Mk);
+  } else {  // Prop. 4 (reading C21): the counts of the 2N' system times L/2N'
+    std::vector<Filt> f0;
+    rc = cq_filters(p, p->sampled_from, 0, f0);
+    if (!rc) rc = channel_counts(p, f0, Mk);
+    for (int64_t &m : Mk) m *= Ls / p->sampled_from;
   }
-  // ---- plateaus (Table 1 rows 0 and K+1; reading C8)
-  {
-    const int64_t a = (int64_t)std::floor(omega[1]);
-    f[0].lo = -a;
-    f[0].v.resize(2 * a + 1);
-    for (int64_t j = -a; j <= a; ++j) f[0].v[j + a] = 1.0 - f[1].at(j < 0 ? -j : j);
-    const int64_t b0 = (int64_t)std::ceil(omega[K]);
-    const int64_t b1 = (int64_t)std::floor((double)Ls - omega[K]);
-    f[K + 1].lo = b0;
-    f[K + 1].v.resize(b1 - b0 + 1);
-    for (int64_t j = b0; j <= b1; ++j) {
-      double v = 1.0 - f[K].at(j) - f[K].at(Ls - j);
-      f[K + 1].v[j - b0] = v > 0.0 ? v : 0.0;
-    }
-  }
-  // ---- coefficient counts M_k = L/a_k >= L_k (readings C9, C10)
+  if (rc) return rc;
   p->lo.resize(K + 2);
   p->len.resize(K + 2);
   p->M.resize(K + 2);
   for (int64_t k = 0; k < K + 2; ++k) {
     p->lo[k] = (int32_t)f[k].lo;
     p->len[k] = (int32_t)f[k].v.size();
-    if (p->len[k] < 1) return set_error(SLICQ_ENOTFRAME, "empty filter support");
-  }
-  if (p->raster == SLICQ_RASTER_NONE) {
-    for (int64_t k = 0; k < K + 2; ++k) p->M[k] = (int32_t)even_smooth_ge(p->len[k]);
-  } else if (p->raster == SLICQ_RASTER_FULL) {
-    int64_t mx = 0;
-    for (int64_t k = 0; k < K + 2; ++k) mx = p->len[k] > mx ? p->len[k] : mx;
-    const int64_t m = even_smooth_ge(mx);
-    for (int64_t k = 0; k < K + 2; ++k) p->M[k] = (int32_t)m;
-  } else {  // per octave: groups {0}, {K+1}, CQ octaves floor((k-1)/B)
-    p->M[0] = (int32_t)even_smooth_ge(p->len[0]);
-    p->M[K + 1] = (int32_t)even_smooth_ge(p->len[K + 1]);
-    for (int64_t k0 = 1; k0 <= K; k0 += B) {
-      const int64_t k1 = (k0 + B - 1 < K) ? k0 + B - 1 : K;
-      int64_t mx = 0;
-      for (int64_t k = k0; k <= k1; ++k) mx = p->len[k] > mx ? p->len[k] : mx;
-      const int64_t m = even_smooth_ge(mx);
-      for (int64_t k = k0; k <= k1; ++k) p->M[k] = (int32_t)m;
-    }
+    if (Mk[k] > INT32_MAX) return set_error(SLICQ_EINVAL, "channel length overflows int32");
+    p->M[k] = (int32_t)Mk[k];
   }
   p->off.assign(K + 3, 0);
   p->goff.assign(K + 2, 0);
   int64_t gl = 0;
+  p->painless = true;
   for (int64_t k = 0; k < K + 2; ++k) {
-    if (p->M[k] < p->len[k])
-      return set_error(SLICQ_ENOTFRAME, "painless condition M_k >= L_k violated (P:170)");
+    if (p->M[k] < p->len[k]) {
+      // a sampled_from system keeps the slice system's hops (Prop. 4, reading C21): only
+      // its analysis is defined (Alg. 1 folds); everything else must be painless
+      if (!p->sampled_from)
+        return set_error(SLICQ_ENOTFRAME, "painless condition M_k >= L_k violated (P:170)");
+      p->painless = false;
+    }
     p->off[k + 1] = p->off[k] + p->M[k];
     p->goff[k] = gl;
     gl += p->len[k];
@@ -193,7 +241,21 @@ extern "C" {
 
 int plan_create_ex(double fs, double fmin, double fmax, int bins_per_octave, int64_t sl_len,
                    int64_t tr_area, int rasterize, unsigned flags, slicq_plan **out) {
+  return plan_create_ex2(fs, fmin, fmax, bins_per_octave, sl_len, tr_area, rasterize, flags,
+                         SLICQ_WINDOW_HANN, 4.0, 0, out);
+}
+
+int plan_create_ex2(double fs, double fmin, double fmax, int bins_per_octave, int64_t sl_len,
+                    int64_t tr_area, int rasterize, unsigned flags, int window, double min_width,
+                    int64_t sampled_from, slicq_plan **out) {
   if (!out) return set_error(SLICQ_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (window != SLICQ_WINDOW_HANN && window != SLICQ_WINDOW_BLACKMAN_HARRIS)
+    return set_error(SLICQ_EINVAL, "window must be SLICQ_WINDOW_HANN or _BLACKMAN_HARRIS");
+  if (!(min_width >= 1.0) || !std::isfinite(min_width))
+    return set_error(SLICQ_EINVAL, "min_width must be >= 1 bin");
+  if (sampled_from < 0 || (sampled_from > 0 && (sampled_from % 4 != 0 || sl_len % sampled_from != 0)))
+    return set_error(SLICQ_EINVAL, "sampled_from must be 0 or a multiple of 4 dividing sl_len");
   *out = nullptr;
   if (!(fs > 0) || !std::isfinite(fs)) return set_error(SLICQ_EINVAL, "fs must be > 0");
   if (!(fmin > 0) || !(fmin < fs / 2)) return set_error(SLICQ_EINVAL, "need 0 < fmin < fs/2");
@@ -215,6 +277,9 @@ int plan_create_ex(double fs, double fmin, double fmax, int bins_per_octave, int
   p->N = sl_len / 2;
   p->tr = tr_area;
   p->raster = rasterize;
+  p->window = window;
+  p->min_width = min_width;
+  p->sampled_from = sampled_from;
   int rc = build_host_plan(p);
   if (rc == SLICQ_OK && !(flags & SLICQ_PLAN_HOST_ONLY)) {
     rc = slicq::configure_kernels(p);
@@ -410,6 +475,24 @@ int slicq_inverse_range(const slicq_plan *p, const slicq_c32 *coeffs_local, int6
   return slicq::launch_inverse(p, coeffs_local, slice0, nslices, total_slices, batch, 0,
                                nslices * p->N, L, y_local, y_stride, slice0 * p->N, left_spill,
                                halo, ws, ws_bytes, stream);
+}
+
+int slicq_approx_error(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
+                       const slicq_c32 *c, int64_t batch, double *out, void *stream) {
+  int rc = check_dev_plan(ps);
+  if (!rc) rc = check_dev_plan(pl);
+  if (rc) return rc;
+  const int64_t N2 = ps->sl_len, L = pl->sl_len;
+  if (pl->sampled_from != N2 || L % N2 || ps->K != pl->K || ps->B != pl->B)
+    return set_error(SLICQ_EINVAL, "pl must be created with sampled_from = sl_len of ps");
+  for (int k = 0; k < ps->K + 2; ++k)
+    if ((int64_t)pl->M[k] != (L / N2) * ps->M[k] || ps->M[k] % 2)
+      return set_error(SLICQ_EINVAL, "channel counts are not (L/2N) M_k");
+  if (batch < 1) return set_error(SLICQ_ESHAPE, "batch must be >= 1");
+  if (!s || !c || !out) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)s % 8 || (uintptr_t)c % 8 || (uintptr_t)out % 8)
+    return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  return slicq::launch_approx(ps, pl, s, c, batch, out, stream);
 }
 
 int slicq_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,

@@ -89,6 +89,10 @@ struct slicq_plan {
   int B;
   int64_t sl_len, N, tr;
   int raster;
+  int window = 0;              // SLICQ_WINDOW_*
+  double min_width = 4.0;      // C7 lower bound on the filter width (bins)
+  int64_t sampled_from = 0;    // Prop. 4: 2N' whose filters this system samples (0: none)
+  bool painless = true;        // M_k >= L_k for all k (false only with sampled_from)
   // Table 1 layout
   int K;
   double Q;
@@ -133,6 +137,8 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
                    const float *mask = nullptr, int mask_db = 0, int mode = 0);
 int launch_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,
                        int64_t batch, void *stream);
+int launch_approx(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
+                  const slicq_c32 *c, int64_t batch, double *out, void *stream);
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
 int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t batch);
 }  // namespace slicq
