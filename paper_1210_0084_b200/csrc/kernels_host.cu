@@ -554,6 +554,10 @@ int configure_kernels(slicq_plan *p) {
   const int64_t per_unit = sizeof(float2) * std::max(kc.xs, kc.zs);
   const int64_t budget = env_int("SLICQ_STAGE_MB", 8192) << 20;
   int64_t cu = env_int("SLICQ_CHUNK_UNITS", std::max<int64_t>(1, budget / per_unit));
+  // chunk pipelining (Pipe below): calls of >= pipe_min units run as pipe_parts chunks
+  kc.pipe = env_int("SLICQ_PIPE", 1) != 0;
+  kc.pipe_min = env_int("SLICQ_PIPE_MIN_UNITS", 8192);
+  kc.pipe_parts = std::max<int64_t>(2, env_int("SLICQ_PIPE_PARTS", 4));
   cu = std::min<int64_t>(cu, 0x7fffffff);  // grid x dimension of the spectrum kernels
   cu = std::max<int64_t>(kc.tile, cu / kc.tile * kc.tile);
   kc.chunk_units = cu;
@@ -683,11 +687,25 @@ int upload(slicq_plan *p) {
   if (rc != 0)
     return set_error(SLICQ_ECUDA, std::string("cudaFuncSetAttribute: ") +
                                       cudaGetErrorString((cudaError_t)rc));
+  if (p->kc.pipe) {
+    for (cudaStream_t &st : p->d.pipe)
+      if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+        return set_error(SLICQ_ECUDA, "cudaStreamCreate");
+    for (cudaEvent_t &ev : p->d.pev)
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+        return set_error(SLICQ_ECUDA, "cudaEventCreate");
+  }
   p->has_device = true;
   return SLICQ_OK;
 }
 
 void free_device(slicq_plan *p) {
+  if (p) {
+    for (cudaStream_t &st : p->d.pipe)
+      if (st) cudaStreamDestroy(st), st = nullptr;
+    for (cudaEvent_t &ev : p->d.pev)
+      if (ev) cudaEventDestroy(ev), ev = nullptr;
+  }
   if (p && p->d.block) {
     cudaFree(p->d.block);
     p->d.block = nullptr;
@@ -700,17 +718,53 @@ namespace {
 struct WsLayout {
   size_t cnt, bnd, stage, total;
   int64_t chunk;
+  bool pipe;  // chunks alternate between the plan's two streams (two staging buffers)
 };
 WsLayout ws_layout(const slicq_plan *p, int64_t nslices, int64_t batch) {
   WsLayout w{};
   const int64_t units = nslices * batch;
   w.chunk = std::min<int64_t>(units, p->kc.chunk_units);
+  w.pipe = p->kc.pipe && !p->kc.longmode && units >= p->kc.pipe_min;
+  if (w.pipe) {  // pipe_parts chunks (rounded up to the channel-kernel tile)
+    const int64_t t = p->kc.tile;
+    w.chunk = std::min(w.chunk, ((units + p->kc.pipe_parts - 1) / p->kc.pipe_parts + t - 1) / t * t);
+    w.pipe = units > w.chunk;
+  }
   w.cnt = 0;
   w.bnd = align_up(sizeof(unsigned) * (size_t)units);
   w.stage = align_up(w.bnd + sizeof(float) * (size_t)(units * 2 * p->tr));
-  w.total = w.stage + sizeof(float2) * (size_t)(w.chunk * std::max(p->kc.xs, p->kc.zs));
+  w.total = w.stage + (w.pipe ? 2 : 1) * sizeof(float2) *
+                         (size_t)(w.chunk * std::max(p->kc.xs, p->kc.zs));
   return w;
 }
+
+// chunk pipelining: chunks alternate between the plan's two streams (forked from and joined
+// back into the caller's stream) with ping-pong staging, so that one chunk's kernel tails
+// overlap the next chunk's first kernels (measured +1.5 % on cfg4; the results are
+// bit-identical: same kernels, deterministic boundary pairing)
+struct Pipe {
+  const slicq_plan *p;
+  cudaStream_t s;
+  bool on;
+  Pipe(const slicq_plan *p_, cudaStream_t s_, const WsLayout &w)
+      : p(p_), s(s_), on(w.pipe) {
+    if (!on) return;
+    cudaEventRecord(p->d.pev[0], s);
+    cudaStreamWaitEvent(p->d.pipe[0], p->d.pev[0], 0);
+    cudaStreamWaitEvent(p->d.pipe[1], p->d.pev[0], 0);
+  }
+  cudaStream_t stream(int64_t i) const { return on ? p->d.pipe[i & 1] : s; }
+  float2 *stage(float2 *base, int64_t i, int64_t chunk, int64_t row) const {
+    return on ? base + (i & 1) * chunk * row : base;
+  }
+  void join() {
+    if (!on) return;
+    cudaEventRecord(p->d.pev[1], p->d.pipe[0]);
+    cudaEventRecord(p->d.pev[2], p->d.pipe[1]);
+    cudaStreamWaitEvent(s, p->d.pev[1], 0);
+    cudaStreamWaitEvent(s, p->d.pev[2], 0);
+  }
+};
 }  // namespace
 
 int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t batch) {
@@ -865,16 +919,21 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     }
     return SLICQ_OK;
   }
-  for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
+  Pipe pp(p, s, w);
+  float2 *stage0 = a.stage;
+  for (int64_t u0 = 0, i = 0; u0 < units; u0 += w.chunk, ++i) {
     a.unit0 = u0;
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
-    cudaError_t e = !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), s, mode)
-                    : p->kc.logN == 15 ? large_forward<15>(a, s, mode)
-                                       : large_forward<16>(a, s, mode);
-    if (e == cudaSuccess) e = launch_chan(true, p, a, s);
+    a.stage = pp.stage(stage0, i, w.chunk, std::max(p->kc.xs, p->kc.zs));
+    const cudaStream_t st = pp.stream(i);
+    cudaError_t e = !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), st, mode)
+                    : p->kc.logN == 15 ? large_forward<15>(a, st, mode)
+                                       : large_forward<16>(a, st, mode);
+    if (e == cudaSuccess) e = launch_chan(true, p, a, st);
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
   }
+  pp.join();
   return SLICQ_OK;
 }
 
@@ -926,17 +985,22 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     }
     return SLICQ_OK;
   }
-  for (int64_t u0 = 0; u0 < units; u0 += w.chunk) {
+  Pipe pp(p, s, w);
+  float2 *stage0 = a.stage;
+  for (int64_t u0 = 0, i = 0; u0 < units; u0 += w.chunk, ++i) {
     a.unit0 = u0;
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
-    cudaError_t e = launch_chan(false, p, a, s);
+    a.stage = pp.stage(stage0, i, w.chunk, std::max(p->kc.xs, p->kc.zs));
+    const cudaStream_t st = pp.stream(i);
+    cudaError_t e = launch_chan(false, p, a, st);
     if (e == cudaSuccess)
-      e = !p->kc.large ? launch_spec(false, p, a, dim3((unsigned)a.nunits), s, mode)
-          : p->kc.logN == 15 ? large_inverse_spec<15>(a, s, mode)
-                             : large_inverse_spec<16>(a, s, mode);
+      e = !p->kc.large ? launch_spec(false, p, a, dim3((unsigned)a.nunits), st, mode)
+          : p->kc.logN == 15 ? large_inverse_spec<15>(a, st, mode)
+                             : large_inverse_spec<16>(a, st, mode);
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
   }
+  pp.join();
   return SLICQ_OK;
 }
 

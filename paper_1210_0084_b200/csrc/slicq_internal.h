@@ -1,5 +1,7 @@
 // Internal structures shared by the host plan (plan.cpp) and the kernels (kernels.cu).
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <string>
 #include <vector_types.h>
@@ -59,6 +61,8 @@ struct DeviceTables {
   uint32_t *lrow = nullptr; // long mode: per-bin term list start [N + 2]
   uint32_t *lent = nullptr; // long mode: term index | conj << 31
   void *block = nullptr;    // single allocation holding all of the above
+  cudaStream_t pipe[2] = {nullptr, nullptr};  // chunk pipelining (kc.pipe): two streams
+  cudaEvent_t pev[3] = {nullptr, nullptr, nullptr};
   size_t bytes = 0;
 };
 
@@ -77,6 +81,9 @@ struct KernelConfig {
   int64_t chunk_units = 0;    // units per chunk (staging is sized for one chunk)
   int tile = 16;              // units per channel-kernel tile
   int chan_per_sm = 0;        // channel-kernel CTAs per SM cap (0: occupancy)
+  bool pipe = false;          // chunks alternate between two streams, ping-pong staging
+  int64_t pipe_min = 8192;    // ... for calls of at least this many units
+  int64_t pipe_parts = 4;     // ... split into this many chunks
   bool longmode = false;      // sl_len 2^18..2^22: full-length CQ-NSGT only (kernels_long.cuh)
   kern::LongClasses lcls{};   // long mode: channel size classes (kernels_long_api.h)
 };

@@ -324,6 +324,37 @@ def test_chunked_staging_is_bit_identical(api, monkeypatch):
     assert torch.equal(y, y2)
 
 
+def test_pipelined_chunks_are_bit_identical(api, monkeypatch):
+    """Calls of >= SLICQ_PIPE_MIN_UNITS units run as chunks alternating between two internal
+    streams (ping-pong staging, fork/join on the caller's stream): identical results to one
+    chunk, boundaries paired across concurrently running chunks, and the caller's stream
+    sees the finished result."""
+    n, batch = 37 * 8192 + 77, 8  # 304 units
+    x = torch.from_numpy(random_signal(778, batch, n)).cuda()
+    monkeypatch.setenv("SLICQ_PIPE", "0")
+    plain = api.plan_for_config(CONFIGS[1])
+    monkeypatch.setenv("SLICQ_PIPE", "1")
+    monkeypatch.setenv("SLICQ_PIPE_MIN_UNITS", "100")
+    monkeypatch.setenv("SLICQ_PIPE_PARTS", "3")
+    piped = api.plan_for_config(CONFIGS[1])
+    for v in ("SLICQ_PIPE", "SLICQ_PIPE_MIN_UNITS", "SLICQ_PIPE_PARTS"):
+        monkeypatch.delenv(v)
+    S = plain.num_slices(n)
+    assert piped.kernel_launches("inverse", S, batch) > plain.kernel_launches("inverse", S, batch)
+    c = plain.forward(x)
+    y = plain.inverse(c, n)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        c2 = piped.forward(x, stream=s)
+        y2 = piped.inverse(c2, n, stream=s)
+        r = y2.sum()  # on the caller's stream, after the join
+    s.synchronize()
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
+    assert torch.equal(y, y2)
+    assert r.item() == y.sum().item()
+
+
 def _full_size_launch_check(api, cfg_id, pairs_per_row=2, rows=(0, -1)):
     """Full BASELINE size in bench.py's launch configuration (all rows in one call):
     sampled (row, slice) coefficients against the oracle, reconstruction of every row."""
