@@ -114,11 +114,22 @@ struct Big<12> {
   static constexpr int F1 = 16, F2 = 16, F3 = 16;
   static constexpr int I1 = 16, I2 = 16, I3 = 16;
 };
+// radix sequences (tunable at build time: SLICQ_F13A/B/C, SLICQ_I13A/B/C)
+#ifndef SLICQ_F13A
+#define SLICQ_F13A 16
+#define SLICQ_F13B 32
+#define SLICQ_F13C 16
+#endif
+#ifndef SLICQ_I13A
+#define SLICQ_I13A 16
+#define SLICQ_I13B 32
+#define SLICQ_I13C 16
+#endif
 template <>
 struct Big<13> {
   static constexpr int N = 8192, T = SLICQ_T13, MINB = SLICQ_MINB13;
-  static constexpr int F1 = 16, F2 = 32, F3 = 16;
-  static constexpr int I1 = 16, I2 = 32, I3 = 16;
+  static constexpr int F1 = SLICQ_F13A, F2 = SLICQ_F13B, F3 = SLICQ_F13C;
+  static constexpr int I1 = SLICQ_I13A, I2 = SLICQ_I13B, I3 = SLICQ_I13C;
 };
 template <>
 struct Big<14> {
