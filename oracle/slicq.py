@@ -194,3 +194,59 @@ def inverse_range(c_local: np.ndarray, slice0: int, nslices: int, plan: Plan, ha
         assert np.all(fm[~ok] == 0)
         np.add.at(y, li[ok], fm[ok])
     return y[halo:], y[:halo]
+
+
+# ------------------------------------------------------------------ complex input
+# Alg. 3 / Alg. 4 for complex signals f in C^L (the paper's general setting, and its
+# Set 1): every slice goes through the full 2K+2-channel CQ-NSGT_2N (Table 1 incl.
+# the mirror channels K+2..2K+1).  Coefficient rows are [sum over all 2K+2 M_k] in
+# Table-1 channel order (stored channels 0..K+1, then the mirrors of K..1).
+from .nsgt import analysis as _analysis, synthesis as _synthesis  # noqa: E402
+
+
+def offsets_full(plan: Plan) -> np.ndarray:
+    return np.concatenate([[0], np.cumsum([c.M for c in plan.full])]).astype(np.int64)
+
+
+def slice_frame_complex(x: np.ndarray, m: int, plan: Plan, L: int) -> np.ndarray:
+    """f^m[j] = f[((m-1)N + j) mod L] h_0[j - N] for complex f."""
+    N = plan.N
+    idx = np.mod((m - 1) * N + np.arange(2 * N), L)
+    v = np.zeros(2 * N, dtype=np.complex128)
+    ok = idx < x.shape[0]
+    v[ok] = x[idx[ok]]
+    return v * plan.h0
+
+
+def forward_complex(x: np.ndarray, plan: Plan) -> np.ndarray:
+    """Alg. 3 for complex signals x[batch][n] -> c[batch][S][sum over 2K+2 channels M_k]."""
+    x = np.atleast_2d(np.asarray(x, dtype=np.complex128))
+    B, n = x.shape
+    L = padded_length(n, plan.sl_len)
+    S = 2 * L // plan.sl_len
+    out = np.zeros((B, S, int(offsets_full(plan)[-1])), dtype=np.complex128)
+    for b in range(B):
+        for m in range(S):
+            out[b, m] = concat(_analysis(slice_frame_complex(x[b], m, plan, L), plan.full,
+                                         plan.sl_len))
+    return out
+
+
+def inverse_complex(c: np.ndarray, plan: Plan, n: int) -> np.ndarray:
+    """Alg. 4 for complex signals: all 2K+2 channels through Alg. 2, dual window,
+    overlap-add (P:336-346) -> y[batch][n] complex."""
+    c = np.asarray(c)
+    if c.ndim == 2:
+        c = c[None]
+    B, S, _ = c.shape
+    L = padded_length(n, plan.sl_len)
+    N = plan.N
+    off = offsets_full(plan)
+    y = np.zeros((B, L), dtype=np.complex128)
+    for b in range(B):
+        for m in range(S):
+            chans = [c[b, m, off[k]:off[k + 1]] for k in range(len(plan.full))]
+            fm = _synthesis(chans, plan.full, plan.dual_full, plan.sl_len)
+            pos = np.mod((m - 1) * N + np.arange(2 * N), L)
+            np.add.at(y[b], pos, fm * plan.h0dual)
+    return y[:, :n]
