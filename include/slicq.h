@@ -205,6 +205,30 @@ SLICQ_API int slicq_nsgt_forward(const slicq_plan *p, const float *x, int64_t n,
 SLICQ_API int slicq_nsgt_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
                                  int64_t batch, float *y, void *ws, size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------ complex input
+ * slicq_forward_complex / slicq_inverse_complex: the sliCQ of complex signals f in C^L
+ * (Alg. 3/4) over all 2K+2 channels of Table 1: no Hermitian
+ * reduction, the mirror channels K+2..2K+1 are stored.
+ *   x, y    device slicq_c32 [batch][n] (interleaved re, im), 8-byte aligned
+ *   coeffs  device slicq_c32 [batch][S][Cf], Cf = slicq_coeffs_per_slice_full(p): channels
+ *           in Table-1 order -- 0..K+1 at slicq_channel_offsets[k] as in the real layout,
+ *           then the mirrors of channels K, K-1, .., 1 (M_{2K+2-k} = M_k)
+ *   ws      >= slicq_workspace_bytes_complex(p, S, batch, n) bytes, 256-byte aligned
+ * Computed through the real-input kernels by linearity (f = Re f + i Im f; the mirror
+ * channels of a real input are e^{2 pi i 2N n/M_k} conj(c_{n,k}), C15): forward = real
+ * transform of the 2 batch rows (Re, Im) + a combine kernel; inverse = split into two
+ * real-consistent coefficient sets + real synthesis of 2 batch rows + interleave.  Errors
+ * as slicq_forward / slicq_inverse. */
+SLICQ_API int64_t slicq_coeffs_per_slice_full(const slicq_plan *p);  /* sum over 2K+2 M_k */
+SLICQ_API size_t slicq_workspace_bytes_complex(const slicq_plan *p, int64_t nslices,
+                                               int64_t batch, int64_t n);
+SLICQ_API int slicq_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n,
+                                    int64_t batch, slicq_c32 *coeffs, void *ws,
+                                    size_t ws_bytes, void *stream);
+SLICQ_API int slicq_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
+                                    int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes,
+                                    void *stream);
+
 /* ------------------------------------------------------------------ Prop. 4 / Sec. V-A
  * slicq_approx_error: the sliCQ's approximation of the full-length CQ-NSGT (Prop. 4,
  * P:377-391; the experiment of P:475-497).  Per row b and stored

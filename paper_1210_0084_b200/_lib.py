@@ -21,6 +21,10 @@ SIGNATURES = {
     "plan_create_ex2": (_i32, [_d, _d, _d, _i32, _i64, _i64, _i32, _u, _i32, _d, _i64,
                                C.POINTER(_p)]),
     "slicq_approx_error": (_i32, [_p, _p, _p, _p, _i64, _p, _p]),
+    "slicq_coeffs_per_slice_full": (_i64, [_p]),
+    "slicq_workspace_bytes_complex": (_sz, [_p, _i64, _i64, _i64]),
+    "slicq_forward_complex": (_i32, [_p, _p, _i64, _i64, _p, _p, _sz, _p]),
+    "slicq_inverse_complex": (_i32, [_p, _p, _i64, _i64, _p, _p, _sz, _p]),
     "plan_destroy": (None, [_p]),
     "slicq_num_channels": (_i32, [_p]),
     "slicq_num_cq_channels": (_i32, [_p]),

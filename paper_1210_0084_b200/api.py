@@ -106,6 +106,11 @@ class Plan:
     def num_slices(self, n: int) -> int:
         return check(lib().slicq_num_slices(self._h, int(n)), "slicq_num_slices")
 
+    @property
+    def coeffs_per_slice_full(self) -> int:
+        """sum of M_k over all 2K+2 channels (complex-input layout)."""
+        return check(lib().slicq_coeffs_per_slice_full(self._h), "slicq_coeffs_per_slice_full")
+
     def workspace_bytes(self, nslices: int, batch: int) -> int:
         return int(lib().slicq_workspace_bytes(self._h, int(nslices), int(batch)))
 
@@ -188,6 +193,52 @@ class Plan:
             return out
         check(lib().slicq_inverse(self._h, c.data_ptr(), n, B, out.data_ptr(), ws.data_ptr(),
                                   ws.numel() * 4, _stream_ptr(stream)), "slicq_inverse")
+        return out
+
+    def _workspace_complex(self, nslices: int, batch: int, n: int, device) -> torch.Tensor:
+        key = (str(device), nslices, batch, ("complex", n))
+        ws = self._ws.get(key)
+        if ws is None:
+            nb = int(lib().slicq_workspace_bytes_complex(self._h, nslices, batch, n))
+            ws = torch.zeros((nb + 15) // 16 * 4, dtype=torch.float32, device=device)
+            self._ws[key] = ws
+        return ws
+
+    def forward_complex(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+                        stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """slicq_forward_complex: complex64 [batch][n] -> complex64 [batch][S][Cf] over all
+        2K+2 channels (Table-1 order: stored 0..K+1, then the mirrors of K..1)."""
+        if x.dim() == 1:
+            x = x[None]
+        _check_tensor(x, torch.complex64, "x")
+        B, n = x.shape
+        S = self.num_slices(n)
+        if out is None:
+            out = torch.empty((B, S, self.coeffs_per_slice_full), dtype=torch.complex64,
+                              device=x.device)
+        else:
+            _check_tensor(out, torch.complex64, "out", (B, S, self.coeffs_per_slice_full))
+        ws = self._workspace_complex(S, B, n, x.device)
+        check(lib().slicq_forward_complex(self._h, x.data_ptr(), n, B, out.data_ptr(),
+                                          ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)),
+              "slicq_forward_complex")
+        return out
+
+    def inverse_complex(self, c: torch.Tensor, n: int, out: Optional[torch.Tensor] = None,
+                        stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """slicq_inverse_complex: complex64 [batch][S][Cf] -> complex64 [batch][n]."""
+        if c.dim() == 2:
+            c = c[None]
+        B, S = c.shape[0], self.num_slices(n)
+        _check_tensor(c, torch.complex64, "coeffs", (B, S, self.coeffs_per_slice_full))
+        if out is None:
+            out = torch.empty((B, n), dtype=torch.complex64, device=c.device)
+        else:
+            _check_tensor(out, torch.complex64, "out", (B, n))
+        ws = self._workspace_complex(S, B, n, c.device)
+        check(lib().slicq_inverse_complex(self._h, c.data_ptr(), n, B, out.data_ptr(),
+                                          ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)),
+              "slicq_inverse_complex")
         return out
 
     def nsgt_forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,

@@ -1,0 +1,153 @@
+// Complex-input sliCQ (Alg. 3/4 on f in C^L over all 2K+2 channels of Table 1)
+// through the real-input kernels.  By linearity c(f) = c(Re f) + i c(Im f) for every channel,
+// and for a real input the mirror channel 2K+2-k of CQ channel k is
+//   c_{n,2K+2-k} = w_n conj(c_{n,k}),  w_n = e^{2 pi i 2N n / M_k}      (C15)
+// so the forward runs the real transform on the 2B rows (Re f_b, Im f_b) and combines:
+//   stored k:  c_k = a_k + i b_k,   mirror of k:  w (conj a_k + i conj b_k)
+// The synthesis splits the 2K+2-channel coefficients into two real-consistent sets
+//   u_k = (c_k + z_k) / 2,  v_k = (c_k - z_k) / (2i),  z_k = w conj(c_{mirror(k)})
+// (mirror(0) = 0 with w = 1: the DC plateau of a real input is real; mirror(K+1) = K+1:
+// the Nyquist plateau is its own mirror), runs the real synthesis on the 2B rows (u_b, v_b)
+// (exact on real-consistent sets, C15) and interleaves y = y_u + i y_v.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "fft_dev.cuh"
+#include "slicq_internal.h"
+
+namespace slicq {
+namespace {
+using namespace slicq::dev;
+
+__global__ void cx_split_rows(const float2 *x, int64_t n, float *r) {  // [B][n] -> [2B][n]
+  const int64_t b = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = x[b * n + i];
+    r[(2 * b) * n + i] = v.x;
+    r[(2 * b + 1) * n + i] = v.y;
+  }
+}
+
+__global__ void cx_join_rows(const float *r, int64_t n, float2 *y) {  // [2B][n] -> [B][n]
+  const int64_t b = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[b * n + i] = make_float2(r[(2 * b) * n + i], r[(2 * b + 1) * n + i]);
+}
+
+// w_n = e^{2 pi i 2N n / M} from the plan's e^{2 pi i t / M} table
+__device__ __forceinline__ float2 mirror_phase(const float2 *tw, int64_t n2, int n, int M) {
+  return tw[(int)(((n2 % M) * (int64_t)n) % M)];
+}
+
+// one CTA per (coefficient row (b, m), stored channel k); T: [2B][S][C], out: [B][S][Cf]
+__global__ void cx_combine(const ChanDev *ch, const float2 *twM, const float2 *T, float2 *out,
+                           int64_t S, int64_t C, int64_t Cf, int K, int64_t n2) {
+  const int64_t row = blockIdx.x, b = row / S, m = row - b * S;
+  const int k = blockIdx.y;
+  const ChanDev c = ch[k];
+  const float2 *a = T + ((2 * b) * S + m) * C + c.off;
+  const float2 *bb = T + ((2 * b + 1) * S + m) * C + c.off;
+  float2 *o = out + row * Cf;
+  const bool mirrored = k >= 1 && k <= K;
+  const int64_t moff = C + (ch[K + 1].off - (c.off + c.M));  // mirrors of K..1 after stored
+  for (int n = threadIdx.x; n < c.M; n += blockDim.x) {
+    const float2 av = a[n], bv = bb[n];
+    o[c.off + n] = make_float2(av.x - bv.y, av.y + bv.x);
+    if (mirrored)  // w (conj a + i conj b) = w (a.x + b.y, b.x - a.y)
+      o[moff + n] = cmul(mirror_phase(twM + c.twoff, n2, n, c.M),
+                         make_float2(av.x + bv.y, bv.x - av.y));
+  }
+}
+
+// c: [B][S][Cf] -> U: [2B][S][C] (rows u_b, v_b)
+__global__ void cx_split(const ChanDev *ch, const float2 *twM, const float2 *cf, float2 *U,
+                         int64_t S, int64_t C, int64_t Cf, int K, int64_t n2) {
+  const int64_t row = blockIdx.x, b = row / S, m = row - b * S;
+  const int k = blockIdx.y;
+  const ChanDev c = ch[k];
+  const float2 *ck = cf + row * Cf + c.off;
+  const int64_t moff = (k >= 1 && k <= K) ? C + (ch[K + 1].off - (c.off + c.M)) : c.off;
+  const float2 *cm = cf + row * Cf + moff;
+  float2 *u = U + ((2 * b) * S + m) * C + c.off;
+  float2 *v = U + ((2 * b + 1) * S + m) * C + c.off;
+  for (int n = threadIdx.x; n < c.M; n += blockDim.x) {
+    const float2 w = k == 0 ? make_float2(1.f, 0.f) : mirror_phase(twM + c.twoff, n2, n, c.M);
+    const float2 z = cmul(w, cconj(cm[n]));
+    const float2 x = ck[n];
+    u[n] = make_float2(0.5f * (x.x + z.x), 0.5f * (x.y + z.y));
+    v[n] = make_float2(0.5f * (x.y - z.y), -0.5f * (x.x - z.x));  // (x - z) / (2i)
+  }
+}
+
+int cuda_err(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return SLICQ_OK;
+  return set_error(SLICQ_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
+int64_t coeffs_full(const slicq_plan *p) {
+  int64_t c = p->C;
+  for (int k = 1; k <= p->K; ++k) c += p->M[k];
+  return c;
+}
+
+// workspace: [real-path workspace for 2B rows][real buffer 2B x n][coefficients 2B x S x C]
+static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+size_t workspace_bytes_complex(const slicq_plan *p, int64_t nslices, int64_t batch, int64_t n) {
+  return al(workspace_bytes(p, nslices, 2 * batch)) + al(sizeof(float) * 2 * batch * n) +
+         sizeof(float2) * (size_t)(2 * batch * nslices * p->C);
+}
+
+int launch_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n, int64_t batch,
+                           slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream) {
+  const int64_t L = (n + p->sl_len - 1) / p->sl_len * p->sl_len, S = L / p->N;
+  if (ws_bytes < workspace_bytes_complex(p, S, batch, n))
+    return set_error(SLICQ_ESHAPE, "workspace too small");
+  if (batch > 65535) return set_error(SLICQ_ESHAPE, "batch too large");
+  char *w = static_cast<char *>(ws);
+  const size_t wr = al(workspace_bytes(p, S, 2 * batch));
+  float *R = reinterpret_cast<float *>(w + wr);
+  float2 *T = reinterpret_cast<float2 *>(w + wr + al(sizeof(float) * 2 * batch * n));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cx_split_rows<<<dim3((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)batch), 256, 0, s>>>(
+      reinterpret_cast<const float2 *>(x), n, R);
+  int rc = cuda_err(cudaGetLastError(), "complex split");
+  if (rc) return rc;
+  rc = launch_forward(p, R, n, n, 0, L, 1, 0, S, 2 * batch, reinterpret_cast<slicq_c32 *>(T), ws,
+                      wr, stream);
+  if (rc) return rc;
+  cx_combine<<<dim3((unsigned)(batch * S), (unsigned)(p->K + 2)), 128, 0, s>>>(
+      p->d.chan, reinterpret_cast<const float2 *>(p->d.twM), T,
+      reinterpret_cast<float2 *>(coeffs), S, p->C, coeffs_full(p), p->K, p->sl_len);
+  return cuda_err(cudaGetLastError(), "complex combine");
+}
+
+int launch_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
+                           int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes, void *stream) {
+  const int64_t L = (n + p->sl_len - 1) / p->sl_len * p->sl_len, S = L / p->N;
+  if (ws_bytes < workspace_bytes_complex(p, S, batch, n))
+    return set_error(SLICQ_ESHAPE, "workspace too small");
+  if (batch > 65535) return set_error(SLICQ_ESHAPE, "batch too large");
+  char *w = static_cast<char *>(ws);
+  const size_t wr = al(workspace_bytes(p, S, 2 * batch));
+  float *Y = reinterpret_cast<float *>(w + wr);
+  float2 *U = reinterpret_cast<float2 *>(w + wr + al(sizeof(float) * 2 * batch * n));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cx_split<<<dim3((unsigned)(batch * S), (unsigned)(p->K + 2)), 128, 0, s>>>(
+      p->d.chan, reinterpret_cast<const float2 *>(p->d.twM),
+      reinterpret_cast<const float2 *>(coeffs), U, S, p->C, coeffs_full(p), p->K, p->sl_len);
+  int rc = cuda_err(cudaGetLastError(), "complex split");
+  if (rc) return rc;
+  rc = launch_inverse(p, reinterpret_cast<const slicq_c32 *>(U), 0, S, S, 2 * batch, 1, n, L, Y,
+                      n, 0, nullptr, 0, ws, wr, stream);
+  if (rc) return rc;
+  cx_join_rows<<<dim3((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)batch), 256, 0, s>>>(
+      Y, n, reinterpret_cast<float2 *>(y));
+  return cuda_err(cudaGetLastError(), "complex join");
+}
+
+}  // namespace slicq

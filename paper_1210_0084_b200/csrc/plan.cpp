@@ -477,6 +477,39 @@ int slicq_inverse_range(const slicq_plan *p, const slicq_c32 *coeffs_local, int6
                                halo, ws, ws_bytes, stream);
 }
 
+int64_t slicq_coeffs_per_slice_full(const slicq_plan *p) {
+  if (!p) return set_error(SLICQ_EINVAL, "plan is NULL");
+  return slicq::coeffs_full(p);
+}
+
+size_t slicq_workspace_bytes_complex(const slicq_plan *p, int64_t nslices, int64_t batch,
+                                     int64_t n) {
+  if (!p || !p->has_device || nslices < 1 || batch < 1 || n < 1) return 0;
+  return slicq::workspace_bytes_complex(p, nslices, batch, n);
+}
+
+int slicq_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n, int64_t batch,
+                          slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (n < 1 || batch < 1) return set_error(SLICQ_ESHAPE, "n and batch must be >= 1");
+  if (!x || !coeffs || !ws) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)x % 8 || (uintptr_t)coeffs % 8 || (uintptr_t)ws % 256)
+    return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  return slicq::launch_forward_complex(p, x, n, batch, coeffs, ws, ws_bytes, stream);
+}
+
+int slicq_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n, int64_t batch,
+                          slicq_c32 *y, void *ws, size_t ws_bytes, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (n < 1 || batch < 1) return set_error(SLICQ_ESHAPE, "n and batch must be >= 1");
+  if (!y || !coeffs || !ws) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)y % 8 || (uintptr_t)coeffs % 8 || (uintptr_t)ws % 256)
+    return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  return slicq::launch_inverse_complex(p, coeffs, n, batch, y, ws, ws_bytes, stream);
+}
+
 int slicq_approx_error(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
                        const slicq_c32 *c, int64_t batch, double *out, void *stream) {
   int rc = check_dev_plan(ps);
