@@ -228,6 +228,16 @@ SLICQ_API int slicq_forward_complex(const slicq_plan *p, const slicq_c32 *x, int
 SLICQ_API int slicq_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
                                     int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes,
                                     void *stream);
+/* slicq_nsgt_forward_complex / slicq_nsgt_inverse_complex: the full-length CQ-NSGT (Alg. 1/2)
+ * of complex signals, 1 <= n <= sl_len, coefficients [batch][Cf] in the layout above;
+ * ws >= slicq_workspace_bytes_complex(p, 1, batch, n).  Same construction as the sliced
+ * calls; plans with M_k < L_k (sampled_from) serve only the forward. */
+SLICQ_API int slicq_nsgt_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n,
+                                         int64_t batch, slicq_c32 *coeffs, void *ws,
+                                         size_t ws_bytes, void *stream);
+SLICQ_API int slicq_nsgt_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
+                                         int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes,
+                                         void *stream);
 
 /* ------------------------------------------------------------------ Prop. 4 / Sec. V-A
  * slicq_approx_error: the sliCQ's approximation of the full-length CQ-NSGT (Prop. 4,
@@ -248,6 +258,13 @@ SLICQ_API int slicq_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs
  * NULL / misaligned buffers or batch < 1. */
 SLICQ_API int slicq_approx_error(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
                                  const slicq_c32 *c, int64_t batch, double *out, void *stream);
+/* slicq_approx_error_complex: the same sums for complex signals over all 2K+2 channels:
+ *   s    [batch][S][Cf_ps] from slicq_forward_complex(ps, x, n = L)
+ *   c    [batch][Cf_pl]    from slicq_nsgt_forward_complex(pl, x, n = L)
+ *   out  device double [batch][2K+2][2] (Table-1 channel order) */
+SLICQ_API int slicq_approx_error_complex(const slicq_plan *ps, const slicq_plan *pl,
+                                         const slicq_c32 *s, const slicq_c32 *c, int64_t batch,
+                                         double *out, void *stream);
 
 /* ------------------------------------------------------------------ slice-range shards
  * Multi-GPU partition of one long stream: a rank owns slices

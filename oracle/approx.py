@@ -77,6 +77,37 @@ def channel_sums(f: np.ndarray, plan_s: Plan, plan_L: Plan) -> np.ndarray:
     return np.array([[np.sum(np.abs(ck) ** 2), np.sum(np.abs(ck - sk) ** 2)] for ck, sk in zip(c, s)])
 
 
+# ------------------------------------------------------------------ complex input (Set 1)
+def _two_layer_sum(c_rows: np.ndarray, chans, off, L: int, N2: int) -> List[np.ndarray]:
+    """s^0 + s^1 per channel from slice rows c[S][...] (Alg. 3 lines P:320-323, any layout)."""
+    S = c_rows.shape[0]
+    out = []
+    for k, ch in enumerate(chans):
+        M = ch.M
+        width = L * M // N2
+        s = np.zeros((2, width), dtype=np.complex128)
+        for m in range(S):
+            idx = np.mod((m - 1) * (M // 2) + np.arange(M), width)
+            s[m % 2, idx] = c_rows[m, off[k]:off[k + 1]]
+        out.append(s[0] + s[1])
+    return out
+
+
+def channel_sums_complex(f: np.ndarray, plan_s: Plan, plan_L: Plan) -> np.ndarray:
+    """Complex f (the paper's Set 1): per channel of all 2K+2 (Table-1 order)
+    [sum |c|^2, sum |c - (s^0 + s^1)|^2], P4-normalised (C22)."""
+    from .nsgt import analysis
+    from .slicq import forward_complex, offsets_full
+    check_pair(plan_s, plan_L)
+    L, N2 = plan_L.sl_len, plan_s.sl_len
+    f = np.asarray(f, np.complex128)
+    c = [ck * p4_scale(ch.M, L) for ck, ch in zip(analysis(f, plan_L.full, L), plan_L.full)]
+    rows = forward_complex(f[None], plan_s)[0]
+    s = _two_layer_sum(rows, plan_s.full, offsets_full(plan_s), L, N2)
+    s = [sk * p4_scale(ch.M, N2) for sk, ch in zip(s, plan_s.full)]
+    return np.array([[np.sum(np.abs(ck) ** 2), np.sum(np.abs(ck - sk) ** 2)] for ck, sk in zip(c, s)])
+
+
 # ------------------------------------------------------------------ Prop. 4, term by term
 def atom(ch, L: int, x: float = 0.0) -> np.ndarray:
     """T_x g^L_k-check, g-check = F^{-1} g^L_k with the non-unitary inverse DFT (reading
@@ -97,17 +128,17 @@ def slicing_windows(plan_s: Plan, L: int, m: int) -> np.ndarray:
     return h
 
 
-def residual_and_bound(f: np.ndarray, plan_s: Plan, plan_L: Plan, k: int):
+def residual_and_bound(f: np.ndarray, plan_s: Plan, plan_L: Plan, k: int, full: bool = False):
     """For channel k and every n = m N/a_k + n^s: R[n] of the proof by direct
     inner products over C^L, and the right-hand side of eq:inner_outer.
     Returns (R, bound), both P4-normalised arrays of length L/a_k."""
     L = plan_L.sl_len
     N = plan_s.sl_len // 2
     sc = check_pair(plan_s, plan_L)
-    ch = plan_L.stored[k]
+    ch = (plan_L.full if full else plan_L.stored)[k]  # full: all 2K+2 channels (complex f)
     M = ch.M
     a = L / M                                          # a_k (possibly fractional)
-    half = plan_s.stored[k].M // 2                     # N / a_k
+    half = (plan_s.full if full else plan_s.stored)[k].M // 2   # N / a_k
     nf = np.linalg.norm(f)
     R = np.zeros(M, dtype=np.complex128)
     bound = np.zeros(M)

@@ -241,6 +241,40 @@ class Plan:
               "slicq_inverse_complex")
         return out
 
+    def nsgt_forward_complex(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+                             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """slicq_nsgt_forward_complex: full-length CQ-NSGT of complex64 [batch][n], n <= sl_len
+        -> complex64 [batch][Cf] (all 2K+2 channels)."""
+        if x.dim() == 1:
+            x = x[None]
+        _check_tensor(x, torch.complex64, "x")
+        B, n = x.shape
+        if out is None:
+            out = torch.empty((B, self.coeffs_per_slice_full), dtype=torch.complex64,
+                              device=x.device)
+        else:
+            _check_tensor(out, torch.complex64, "out", (B, self.coeffs_per_slice_full))
+        ws = self._workspace_complex(1, B, n, x.device)
+        check(lib().slicq_nsgt_forward_complex(self._h, x.data_ptr(), n, B, out.data_ptr(),
+                                               ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)),
+              "slicq_nsgt_forward_complex")
+        return out
+
+    def nsgt_inverse_complex(self, c: torch.Tensor, n: int, out: Optional[torch.Tensor] = None,
+                             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """slicq_nsgt_inverse_complex: complex64 [batch][Cf] -> complex64 [batch][n]."""
+        if c.dim() == 1:
+            c = c[None]
+        B = c.shape[0]
+        _check_tensor(c, torch.complex64, "coeffs", (B, self.coeffs_per_slice_full))
+        if out is None:
+            out = torch.empty((B, n), dtype=torch.complex64, device=c.device)
+        ws = self._workspace_complex(1, B, n, c.device)
+        check(lib().slicq_nsgt_inverse_complex(self._h, c.data_ptr(), n, B, out.data_ptr(),
+                                               ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)),
+              "slicq_nsgt_inverse_complex")
+        return out
+
     def nsgt_forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
                      stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
         """slicq_nsgt_forward: full-length CQ-NSGT (Alg. 1) of x float32 [batch][n],
@@ -345,21 +379,30 @@ def plan_for_config(cfg) -> Plan:
 def approximation_error(x: torch.Tensor, ps: Plan, pl: Plan, stream=None):
     """Prop. 4 / Sec. V-A: how closely the sliCQ
     with plan ps (slices 2N) approximates the full-length CQ-NSGT with pl (created with
-    sampled_from = 2N, sl_len L).  x: float32 [batch][L] on the device.  Runs slicq_forward,
-    slicq_nsgt_forward and slicq_approx_error; returns (snr_db [batch] float64 tensor,
-    sums [batch][K+2][2] float64: per channel sum |c|^2 and sum |c - (s^0 + s^1)|^2 in the
-    Prop. 4 normalisation)."""
+    sampled_from = 2N, sl_len L).  x: float32 [batch][L] (stored channels) or complex64
+    [batch][L] (all 2K+2 channels, the paper's Set 1) on the device.  Runs the sliCQ, the
+    full-length CQ-NSGT and slicq_approx_error(_complex); returns (snr_db [batch] float64
+    tensor, sums [batch][channels][2] float64: per channel sum |c|^2 and sum |c - (s^0 + s^1)|^2
+    in the Prop. 4 normalisation)."""
     if x.dim() == 1:
         x = x[None]
-    _check_tensor(x, torch.float32, "x")
     B, L = x.shape
     if L != pl.sl_len:
         raise ValueError("x must hold L = pl.sl_len samples per row")
-    s = ps.forward(x, stream=stream)
-    c = pl.nsgt_forward(x, stream=stream)
-    out = torch.empty((B, ps.num_channels, 2), dtype=torch.float64, device=x.device)
-    check(lib().slicq_approx_error(ps._h, pl._h, s.data_ptr(), c.data_ptr(), B, out.data_ptr(),
-                                   _stream_ptr(stream)), "slicq_approx_error")
+    if x.is_complex():  # the paper's Set 1: all 2K+2 channels (slicq_approx_error_complex)
+        _check_tensor(x, torch.complex64, "x")
+        s = ps.forward_complex(x, stream=stream)
+        c = pl.nsgt_forward_complex(x, stream=stream)
+        out = torch.empty((B, 2 * ps.K + 2, 2), dtype=torch.float64, device=x.device)
+        fn, name = lib().slicq_approx_error_complex, "slicq_approx_error_complex"
+    else:
+        _check_tensor(x, torch.float32, "x")
+        s = ps.forward(x, stream=stream)
+        c = pl.nsgt_forward(x, stream=stream)
+        out = torch.empty((B, ps.num_channels, 2), dtype=torch.float64, device=x.device)
+        fn, name = lib().slicq_approx_error, "slicq_approx_error"
+    check(fn(ps._h, pl._h, s.data_ptr(), c.data_ptr(), B, out.data_ptr(), _stream_ptr(stream)),
+          name)
     tot = out.sum(dim=1)
     return 10.0 * torch.log10(tot[:, 0] / tot[:, 1]), out
 

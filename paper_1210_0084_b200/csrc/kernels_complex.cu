@@ -102,9 +102,12 @@ size_t workspace_bytes_complex(const slicq_plan *p, int64_t nslices, int64_t bat
          sizeof(float2) * (size_t)(2 * batch * nslices * p->C);
 }
 
+// nsgt = 1: the full-length CQ-NSGT of the whole signal (one frame per row, n <= sl_len)
 int launch_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n, int64_t batch,
-                           slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream) {
-  const int64_t L = (n + p->sl_len - 1) / p->sl_len * p->sl_len, S = L / p->N;
+                           slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream,
+                           int nsgt) {
+  const int64_t L = nsgt ? p->sl_len : (n + p->sl_len - 1) / p->sl_len * p->sl_len;
+  const int64_t S = nsgt ? 1 : L / p->N;
   if (ws_bytes < workspace_bytes_complex(p, S, batch, n))
     return set_error(SLICQ_ESHAPE, "workspace too small");
   if (batch > 65535) return set_error(SLICQ_ESHAPE, "batch too large");
@@ -117,8 +120,10 @@ int launch_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n, i
       reinterpret_cast<const float2 *>(x), n, R);
   int rc = cuda_err(cudaGetLastError(), "complex split");
   if (rc) return rc;
-  rc = launch_forward(p, R, n, n, 0, L, 1, 0, S, 2 * batch, reinterpret_cast<slicq_c32 *>(T), ws,
-                      wr, stream);
+  rc = nsgt ? launch_forward(p, R, n, n, 0, L, 0, 1, 1, 2 * batch,
+                             reinterpret_cast<slicq_c32 *>(T), ws, wr, stream, 1)
+            : launch_forward(p, R, n, n, 0, L, 1, 0, S, 2 * batch,
+                             reinterpret_cast<slicq_c32 *>(T), ws, wr, stream);
   if (rc) return rc;
   cx_combine<<<dim3((unsigned)(batch * S), (unsigned)(p->K + 2)), 128, 0, s>>>(
       p->d.chan, reinterpret_cast<const float2 *>(p->d.twM), T,
@@ -127,8 +132,10 @@ int launch_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n, i
 }
 
 int launch_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
-                           int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes, void *stream) {
-  const int64_t L = (n + p->sl_len - 1) / p->sl_len * p->sl_len, S = L / p->N;
+                           int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes, void *stream,
+                           int nsgt) {
+  const int64_t L = nsgt ? p->sl_len : (n + p->sl_len - 1) / p->sl_len * p->sl_len;
+  const int64_t S = nsgt ? 1 : L / p->N;
   if (ws_bytes < workspace_bytes_complex(p, S, batch, n))
     return set_error(SLICQ_ESHAPE, "workspace too small");
   if (batch > 65535) return set_error(SLICQ_ESHAPE, "batch too large");
@@ -142,8 +149,10 @@ int launch_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t
       reinterpret_cast<const float2 *>(coeffs), U, S, p->C, coeffs_full(p), p->K, p->sl_len);
   int rc = cuda_err(cudaGetLastError(), "complex split");
   if (rc) return rc;
-  rc = launch_inverse(p, reinterpret_cast<const slicq_c32 *>(U), 0, S, S, 2 * batch, 1, n, L, Y,
-                      n, 0, nullptr, 0, ws, wr, stream);
+  rc = nsgt ? launch_inverse(p, reinterpret_cast<const slicq_c32 *>(U), 1, 1, 2, 2 * batch, 0, n,
+                             L, Y, n, 0, nullptr, 0, ws, wr, stream, nullptr, 0, 1)
+            : launch_inverse(p, reinterpret_cast<const slicq_c32 *>(U), 0, S, S, 2 * batch, 1, n,
+                             L, Y, n, 0, nullptr, 0, ws, wr, stream);
   if (rc) return rc;
   cx_join_rows<<<dim3((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)batch), 256, 0, s>>>(
       Y, n, reinterpret_cast<float2 *>(y));

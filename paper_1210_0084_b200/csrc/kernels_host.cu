@@ -31,17 +31,28 @@ __global__ void overlap_add_kernel(float *y, int64_t y_stride, const float *spil
 // Prop. 4 sums (slicq_approx_error): one CTA per (stored channel, row).  c_P4 = c sqrt(M^L)/L,
 // s_P4 = s sqrt(M)/(2N) (reading C22); (s^0 + s^1)[m h + n'] = c^m[n' + h] + c^{m+1}[n'],
 // h = M/2 = N/a_k (two-layer array of Alg. 3, slices circular).
+// full = 1 (complex input): the layouts of slicq_forward_complex / slicq_nsgt_forward_complex,
+// channel index k' over all 2K+2 channels (mirror k' = 2K+2-k: M_k, after the stored ones)
+__device__ __forceinline__ int64_t full_off(const ChanDev *ch, int kk, int K, int64_t C) {
+  if (kk <= K + 1) return ch[kk].off;
+  const int k = 2 * K + 2 - kk;
+  return C + ch[K + 1].off - (ch[k].off + ch[k].M);
+}
 __global__ void __launch_bounds__(256) approx_kernel(const ChanDev *chs, const ChanDev *chl,
                                                      const float2 *s, const float2 *c, int64_t Cs,
                                                      int64_t Cl, int S, float scs, float scl_num,
-                                                     double *out) {
-  const int k = blockIdx.x, K2 = gridDim.x;
+                                                     double *out, int full, int K, int64_t Cs0,
+                                                     int64_t Cl0) {
+  const int kk = blockIdx.x, K2 = gridDim.x;
+  const int k = kk <= K + 1 ? kk : 2 * K + 2 - kk;
   const int64_t b = blockIdx.y;
   const ChanDev a = chs[k], l = chl[k];
+  const int64_t aoff = full ? full_off(chs, kk, K, Cs0) : a.off;
+  const int64_t loff = full ? full_off(chl, kk, K, Cl0) : l.off;
   const int h = a.M / 2;
   const float ss = sqrtf((float)a.M) * scs, sl = sqrtf((float)l.M) * scl_num;
-  const float2 *srow = s + b * (int64_t)S * Cs + a.off;
-  const float2 *crow = c + b * Cl + l.off;
+  const float2 *srow = s + b * (int64_t)S * Cs + aoff;
+  const float2 *crow = c + b * Cl + loff;
   double e0 = 0.0, e1 = 0.0;
   for (int n = threadIdx.x; n < l.M; n += 256) {
     const int m = n / h, np = n - m * h;
@@ -65,8 +76,8 @@ __global__ void __launch_bounds__(256) approx_kernel(const ChanDev *chs, const C
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    out[(b * K2 + k) * 2 + 0] = r0[0];
-    out[(b * K2 + k) * 2 + 1] = r1[0];
+    out[(b * K2 + kk) * 2 + 0] = r0[0];
+    out[(b * K2 + kk) * 2 + 1] = r1[0];
   }
 }
 
@@ -1005,17 +1016,19 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
 }
 
 int launch_approx(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
-                  const slicq_c32 *c, int64_t batch, double *out, void *stream) {
+                  const slicq_c32 *c, int64_t batch, double *out, void *stream, int full) {
   int rc = check_device(ps);
   if (!rc) rc = check_device(pl);
   if (rc) return rc;
   if (batch > 65535) return set_error(SLICQ_ESHAPE, "batch too large");
   const int S = (int)(pl->sl_len / ps->N);
-  approx_kernel<<<dim3((unsigned)(ps->K + 2), (unsigned)batch), 256, 0,
+  const int nch = full ? 2 * ps->K + 2 : ps->K + 2;
+  approx_kernel<<<dim3((unsigned)nch, (unsigned)batch), 256, 0,
                   static_cast<cudaStream_t>(stream)>>>(
       ps->d.chan, pl->d.chan, reinterpret_cast<const float2 *>(s),
-      reinterpret_cast<const float2 *>(c), ps->C, pl->C, S, (float)(1.0 / (double)ps->sl_len),
-      (float)(1.0 / (double)pl->sl_len), out);
+      reinterpret_cast<const float2 *>(c), full ? coeffs_full(ps) : ps->C,
+      full ? coeffs_full(pl) : pl->C, S, (float)(1.0 / (double)ps->sl_len),
+      (float)(1.0 / (double)pl->sl_len), out, full, ps->K, ps->C, pl->C);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("approx launch: ") + cudaGetErrorString(e));

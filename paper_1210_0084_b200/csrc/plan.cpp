@@ -510,8 +510,35 @@ int slicq_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t 
   return slicq::launch_inverse_complex(p, coeffs, n, batch, y, ws, ws_bytes, stream);
 }
 
-int slicq_approx_error(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
-                       const slicq_c32 *c, int64_t batch, double *out, void *stream) {
+int slicq_nsgt_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n,
+                               int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes,
+                               void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (n < 1 || batch < 1 || n > p->sl_len)
+    return set_error(SLICQ_ESHAPE, "need 1 <= n <= sl_len and batch >= 1");
+  if (!x || !coeffs || !ws) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)x % 8 || (uintptr_t)coeffs % 8 || (uintptr_t)ws % 256)
+    return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  return slicq::launch_forward_complex(p, x, n, batch, coeffs, ws, ws_bytes, stream, 1);
+}
+
+int slicq_nsgt_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
+                               int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes,
+                               void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (n < 1 || batch < 1 || n > p->sl_len)
+    return set_error(SLICQ_ESHAPE, "need 1 <= n <= sl_len and batch >= 1");
+  if (!y || !coeffs || !ws) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)y % 8 || (uintptr_t)coeffs % 8 || (uintptr_t)ws % 256)
+    return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  return slicq::launch_inverse_complex(p, coeffs, n, batch, y, ws, ws_bytes, stream, 1);
+}
+
+static int approx_common(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
+                         const slicq_c32 *c, int64_t batch, double *out, void *stream,
+                         int full) {
   int rc = check_dev_plan(ps);
   if (!rc) rc = check_dev_plan(pl);
   if (rc) return rc;
@@ -525,7 +552,17 @@ int slicq_approx_error(const slicq_plan *ps, const slicq_plan *pl, const slicq_c
   if (!s || !c || !out) return set_error(SLICQ_ESHAPE, "NULL buffer");
   if ((uintptr_t)s % 8 || (uintptr_t)c % 8 || (uintptr_t)out % 8)
     return set_error(SLICQ_ESHAPE, "misaligned buffer");
-  return slicq::launch_approx(ps, pl, s, c, batch, out, stream);
+  return slicq::launch_approx(ps, pl, s, c, batch, out, stream, full);
+}
+
+int slicq_approx_error_complex(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
+                               const slicq_c32 *c, int64_t batch, double *out, void *stream) {
+  return approx_common(ps, pl, s, c, batch, out, stream, 1);
+}
+
+int slicq_approx_error(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
+                       const slicq_c32 *c, int64_t batch, double *out, void *stream) {
+  return approx_common(ps, pl, s, c, batch, out, stream, 0);
 }
 
 int slicq_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t count,

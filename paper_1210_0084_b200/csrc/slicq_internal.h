@@ -148,11 +148,13 @@ int launch_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t c
 int64_t coeffs_full(const slicq_plan *p);
 size_t workspace_bytes_complex(const slicq_plan *p, int64_t nslices, int64_t batch, int64_t n);
 int launch_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n, int64_t batch,
-                           slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream);
+                           slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream,
+                           int nsgt = 0);
 int launch_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
-                           int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes, void *stream);
+                           int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes, void *stream,
+                           int nsgt = 0);
 int launch_approx(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
-                  const slicq_c32 *c, int64_t batch, double *out, void *stream);
+                  const slicq_c32 *c, int64_t batch, double *out, void *stream, int full = 0);
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
 int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t batch);
 }  // namespace slicq

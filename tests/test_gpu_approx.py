@@ -57,3 +57,43 @@ def test_sampled_system_analysis_and_refusals():
         pl.nsgt_inverse(torch.from_numpy(c.astype(np.complex64)).cuda()[None], L)
     with pytest.raises(Exception):  # a non-painless system below the long path
         api.Plan(*base, 65536, 1024, 0, window="blackman_harris", min_width=4, sampled_from=N2)
+
+
+def test_approx_error_complex_matches_oracle():
+    """Complex Set-1-like signals over all 2K+2 channels (slicq_approx_error_complex)."""
+    from paper_1210_0084_b200 import api
+    N2, L = 4096, 2 ** 18
+    base = (44100.0, 50.0, 22050.0, 24)
+    ps = api.Plan(*base, N2, 1024, 0, window="blackman_harris", min_width=8)
+    pl = api.Plan(*base, L, 1024, 0, window="blackman_harris", min_width=8, sampled_from=N2)
+    ops = cqplan.make_plan(*base, N2, 1024, 0, window="blackman_harris", min_width=8)
+    opl = cqplan.make_plan(*base, L, 1024, 0, window="blackman_harris", min_width=8,
+                           sampled_from=N2)
+    x = (random_signal(31, 1, L) + 1j * random_signal(32, 1, L)).astype(np.complex64)
+    snr, sums = api.approximation_error(torch.from_numpy(x).cuda(), ps, pl)
+    torch.cuda.synchronize()
+    sums = sums.cpu().numpy()[0]
+    ref = approx.channel_sums_complex(x[0].astype(np.complex128), ops, opl)
+    assert sums.shape == ref.shape
+    np.testing.assert_allclose(sums[:, 0], ref[:, 0], rtol=1e-5)
+    ref_snr = 10 * np.log10(ref[:, 0].sum() / ref[:, 1].sum())
+    assert abs(snr[0].item() - ref_snr) < 0.05, (snr[0].item(), ref_snr)
+
+
+def test_nsgt_complex_roundtrip_and_oracle():
+    from paper_1210_0084_b200 import api
+    args = (44100.0, 50.0, 22050.0, 48, 2 ** 18, 64, 0)
+    plan = api.Plan(*args)
+    ref = cqplan.make_plan(*args)
+    n = 2 ** 18 - 5
+    x = (random_signal(41, 1, n) + 1j * random_signal(42, 1, n)).astype(np.complex64)
+    xt = torch.from_numpy(x).cuda()
+    c = plan.nsgt_forward_complex(xt)
+    y = plan.nsgt_inverse_complex(c, n)
+    torch.cuda.synchronize()
+    xp = np.zeros(2 ** 18, np.complex128)
+    xp[:n] = x[0]
+    cr = np.concatenate(onsgt.analysis(xp, ref.full, 2 ** 18))
+    cg = c.cpu().numpy()[0].astype(np.complex128)
+    assert np.linalg.norm(cg - cr) / np.linalg.norm(cr) <= 1e-5
+    assert np.linalg.norm(y.cpu().numpy()[0] - x[0]) / np.linalg.norm(x[0]) <= 1e-5

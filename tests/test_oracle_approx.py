@@ -119,3 +119,23 @@ def test_host_plan_options_rejected():
                dict(window="kaiser")):
         with pytest.raises(Exception):
             api.Plan(*args, host_only=True, **kw)
+
+
+def test_prop4_identity_complex_signal_all_channels():
+    """Set 1 is complex: the identity over all 2K+2 channels, mirrors included."""
+    from oracle.nsgt import analysis
+    from oracle.slicq import forward_complex, offsets_full
+    ps, pl = _pair("blackman_harris", 8)
+    r = np.random.default_rng(13)
+    f = r.standard_normal(pl.sl_len) + 1j * r.standard_normal(pl.sl_len)
+    L, N2 = pl.sl_len, ps.sl_len
+    c = [ck * approx.p4_scale(ch.M, L) for ck, ch in zip(analysis(f, pl.full, L), pl.full)]
+    s = approx._two_layer_sum(forward_complex(f[None], ps)[0], ps.full, offsets_full(ps), L, N2)
+    K = ps.layout.K
+    for k in (0, 2, K + 1, K + 2, 2 * K + 1):
+        sk = s[k] * approx.p4_scale(ps.full[k].M, N2)
+        R, bound = approx.residual_and_bound(f, ps, pl, k, full=True)
+        assert np.abs((sk - c[k]) - R).max() <= 1e-10 * np.abs(c[k]).max(), k
+        assert np.all(np.abs(R) <= bound * (1 + 1e-12)), k
+    sums = approx.channel_sums_complex(f, ps, pl)
+    assert sums.shape == (2 * K + 2, 2)
