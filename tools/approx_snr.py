@@ -1,9 +1,10 @@
 """Sec. V-A / Fig. CoeffQual on the GPU: SNR of the sliCQ's
 s^0 + s^1 against the full-length CQ-NSGT of the sampled system (Prop. 4), versus the
 minimal filter width, for slice lengths 4096 / 16384 / 65536 and transition areas of 1/4
-and 1/128 of the slice; Blackman-Harris filters.  Set-1-like inputs: seeded random REAL
-signals of 2^20 samples (the paper's Set 1 is complex, reading C23; Set 2, music, is not
-available).  Prints one JSON line per configuration and a table."""
+and 1/128 of the slice; Blackman-Harris filters.  Set-1-like inputs: seeded random signals
+of 2^20 samples, complex like the paper's Set 1 (all 2K+2 channels) or, with --real, real
+(stored channels); Set 2 (music) is not available.  Prints one JSON line per configuration
+and a table."""
 import json
 import os
 import sys
@@ -16,7 +17,9 @@ from synth.signals import random_signal
 
 L, BATCH = 2 ** 20, 8
 BASE = (44100.0, 50.0, 22050.0, 48)
-x = torch.from_numpy(random_signal(2024, BATCH, L)).cuda()
+REAL = "--real" in sys.argv
+xr = random_signal(2024, BATCH, L)
+x = torch.from_numpy(xr if REAL else (xr + 1j * random_signal(2025, BATCH, L)).astype("complex64")).cuda()
 rows = []
 for N2 in (4096, 16384, 65536):
     for frac in (4, 128):
@@ -25,7 +28,8 @@ for N2 in (4096, 16384, 65536):
             ps = api.Plan(*BASE, N2, tr, 0, window="blackman_harris", min_width=mw)
             pl = api.Plan(*BASE, L, tr, 0, window="blackman_harris", min_width=mw, sampled_from=N2)
             snr, _ = api.approximation_error(x, ps, pl)
-            r = dict(slice=N2, tr=f"1/{frac}", min_width=mw, snr_db_mean=round(snr.mean().item(), 2),
+            r = dict(input="real" if REAL else "complex", slice=N2, tr=f"1/{frac}", min_width=mw,
+                     snr_db_mean=round(snr.mean().item(), 2),
                      snr_db_std=round(snr.std().item(), 3))
             rows.append(r)
             print(json.dumps(r), flush=True)
