@@ -149,16 +149,35 @@ constexpr int kSmallMax = SLICQ_SMALL_MAX;  // channels with M <= this: one lane
 #ifndef SLICQ_LITE_MINB
 #define SLICQ_LITE_MINB 3
 #endif
+#ifndef SLICQ_MICRO_MAX
+#define SLICQ_MICRO_MAX 0  // 0: no micro variant (8: measured within +-0.5 %, cfg2 -7 %)
+#endif
+#ifndef SLICQ_MICRO_MINB
+#define SLICQ_MICRO_MINB 4
+#endif
 constexpr int kLiteMax = SLICQ_LITE_MAX, kLiteMinB = SLICQ_LITE_MINB, kFullMax = 32, kFullMinB = 2;
+constexpr int kMicroMax = SLICQ_MICRO_MAX, kMicroMinB = SLICQ_MICRO_MINB;
+constexpr int kVariants = 3;  // micro (DFT sizes <= kMicroMax), lite (<= kLiteMax), full
 using ChanFn = void (*)(const KArgs);
-// mask: inverse with a fused coefficient mask (0 none, 1 linear, 2 dB)
-static ChanFn chan_fn(bool fwd, bool lite, int mask = 0) {
-  if (fwd) return lite ? slicq_fwd_chan_kernel<kLiteMax, kLiteMinB> : slicq_fwd_chan_kernel<kFullMax, kFullMinB>;
-  switch (mask) {
-    case 1: return lite ? slicq_inv_chan_kernel<kLiteMax, kLiteMinB, 1> : slicq_inv_chan_kernel<kFullMax, kFullMinB, 1>;
-    case 2: return lite ? slicq_inv_chan_kernel<kLiteMax, kLiteMinB, 2> : slicq_inv_chan_kernel<kFullMax, kFullMinB, 2>;
+template <int MK>
+static ChanFn inv_fn(int variant) {
+  if (variant == 0) return slicq_inv_chan_kernel<(kMicroMax ? kMicroMax : 1), kMicroMinB, MK>;
+  return variant == 1 ? slicq_inv_chan_kernel<kLiteMax, kLiteMinB, MK>
+                      : slicq_inv_chan_kernel<kFullMax, kFullMinB, MK>;
+}
+// variant 0 micro, 1 lite, 2 full; mask: inverse with a fused coefficient mask (0 none,
+// 1 linear, 2 dB)
+static ChanFn chan_fn(bool fwd, int variant, int mask = 0) {
+  if (fwd) {
+    if (variant == 0) return slicq_fwd_chan_kernel<(kMicroMax ? kMicroMax : 1), kMicroMinB>;
+    return variant == 1 ? slicq_fwd_chan_kernel<kLiteMax, kLiteMinB>
+                        : slicq_fwd_chan_kernel<kFullMax, kFullMinB>;
   }
-  return lite ? slicq_inv_chan_kernel<kLiteMax, kLiteMinB> : slicq_inv_chan_kernel<kFullMax, kFullMinB>;
+  switch (mask) {
+    case 1: return inv_fn<1>(variant);
+    case 2: return inv_fn<2>(variant);
+  }
+  return inv_fn<0>(variant);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -358,19 +377,21 @@ int configure_kernels(slicq_plan *p) {
     pk.scr = nu * pk.d.ustride * (small ? M : 1);
     pks.push_back(std::move(pk));
   }
-  // shape-sorted (the warps of a channel-kernel CTA run the same code), longer first
-  // lite packets (every DFT size <= kLiteMax) first: they run in the channel-kernel variant
-  // with the smaller register budget (more resident warps), the rest in the full variant
-  auto lite = [](const Pk &x) {
-    const int m1 = x.d.m1m2 & 255, m2 = (x.d.m1m2 >> 8) & 255;
-    return std::max(m1, m2) <= kLiteMax;
+  // shape-sorted (the warps of a channel-kernel CTA run the same code), longer first, by
+  // channel-kernel variant: packets whose DFT sizes are all <= kMicroMax / kLiteMax run in
+  // the variants with the smaller register budgets (more resident warps), the rest in full
+  auto variant = [](const Pk &x) {
+    const int m1 = x.d.m1m2 & 255, m2 = (x.d.m1m2 >> 8) & 255, mx = std::max(m1, m2);
+    return mx <= kMicroMax ? 0 : mx <= kLiteMax ? 1 : 2;
   };
   std::stable_sort(pks.begin(), pks.end(), [&](const Pk &x, const Pk &y) {
-    const bool lx = lite(x), ly = lite(y);
-    return lx != ly ? lx : x.M > y.M;
+    const int vx = variant(x), vy = variant(y);
+    return vx != vy ? vx < vy : x.M > y.M;
   });
-  kc.nlite = 0;
-  for (const Pk &x : pks) kc.nlite += lite(x) ? 1 : 0;
+  for (int v = 0; v <= kVariants; ++v) kc.voff[v] = 0;
+  for (const Pk &x : pks) ++kc.voff[variant(x) + 1];
+  for (int v = 0; v < kVariants; ++v) kc.voff[v + 1] += kc.voff[v];
+  kc.nlite = kc.voff[2];
 
   // ---------------- inverse destinations (I3b gather without index tables): every channel
   // contribution Z_k[d] goes to half-spectrum bin b by the Hermitian rule of C15 (term at
@@ -693,8 +714,8 @@ int upload(slicq_plan *p) {
     case 16: rc = large_set_attrs<16>(); break;
     default: rc = long_set_attrs(p->kc.logN, p->kc.lcls); break;
   }
-  for (int v = 0; v < 12 && rc == 0 && !p->kc.longmode; ++v)  // bit 0: forward, bit 1: lite, v >> 2: mask mode
-    rc = (int)allow_max_dyn_smem((const void *)chan_fn(v & 1, v & 2, v >> 2));
+  for (int v = 0; v < 2 * kVariants * 3 && rc == 0 && !p->kc.longmode; ++v)  // fwd, variant, mask
+    rc = (int)allow_max_dyn_smem((const void *)chan_fn(v & 1, (v >> 1) % kVariants, v / (2 * kVariants)));
   if (rc != 0)
     return set_error(SLICQ_ECUDA, std::string("cudaFuncSetAttribute: ") +
                                       cudaGetErrorString((cudaError_t)rc));
@@ -782,7 +803,8 @@ int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t
   const WsLayout w = ws_layout(p, nslices, batch);
   const int64_t chunks = (nslices * batch + w.chunk - 1) / w.chunk;
   if (p->kc.longmode) return (int)(chunks * (direction == 0 ? 3 : 4));
-  const int nchan = (p->kc.nlite > 0) + (p->kc.npackets > p->kc.nlite);
+  int nchan = 0;
+  for (int v = 0; v < 3; ++v) nchan += p->kc.voff[v + 1] > p->kc.voff[v];
   const int nspec = !p->kc.large ? 1 : direction == 0 ? 2 : 4;
   return (int)(chunks * (nchan + nspec));
 }
@@ -844,15 +866,13 @@ static int64_t chan_capacity(const slicq_plan *p, ChanFn fn) {
   return (int64_t)per_sm * nsm;
 }
 
-// the channel kernels of one direction: lite packets [0, nlite), then the full variant
+// the channel kernels of one direction: one launch per non-empty variant (micro, lite, full)
 static cudaError_t launch_chan(bool fwd, const slicq_plan *p, KArgs a, cudaStream_t s) {
-  const int np = p->kc.npackets, nl = p->kc.nlite;
-  for (int v = 0; v < 2; ++v) {
-    const bool lite = v == 0;
-    a.packets = p->d.packets + (lite ? 0 : nl);
-    a.npackets = lite ? nl : np - nl;
+  for (int v = 0; v < kVariants; ++v) {
+    a.packets = p->d.packets + p->kc.voff[v];
+    a.npackets = p->kc.voff[v + 1] - p->kc.voff[v];
     if (a.npackets == 0) continue;
-    const ChanFn fn = chan_fn(fwd, lite, fwd || !a.mask ? 0 : (a.mask_db ? 2 : 1));
+    const ChanFn fn = chan_fn(fwd, v, fwd || !a.mask ? 0 : (a.mask_db ? 2 : 1));
     // small calls (e.g. the ranges of the streaming executor): shrink the tile until there
     // are >= 4 work items per resident CTA (load balance of the persistent grid)
     const int64_t cap = chan_capacity(p, fn);

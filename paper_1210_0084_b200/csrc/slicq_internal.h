@@ -73,7 +73,8 @@ struct KernelConfig {
   int scr = 0;           // channel kernels: per-warp scratch (float2 entries)
   size_t chan_smem = 0;
   int npackets = 0;
-  int nlite = 0;              // packets [0, nlite) run in the lite channel-kernel variant
+  int nlite = 0;              // packets [0, nlite) run in the micro / lite variants
+  int voff[4] = {0, 0, 0, 0}; // packets [voff[v], voff[v+1]) run in variant v (micro, lite, full)
   int64_t xs = 0, zs = 0;     // staging row strides (float2): X spectra, contributions
   int64_t zso = 0, nover = 0; // inverse staging: slot-1 offset, overflow entries
   bool large = false;         // 2N >= 65536: four-step FFT through the staging buffer

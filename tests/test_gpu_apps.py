@@ -22,14 +22,17 @@ def test_t7_runtime_linear_in_length():
         c = plan.forward(x)
         y = plan.inverse(c, n)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(5):
-            plan.forward(x, out=c)
-            plan.inverse(c, n, out=y)
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) / 5)
+        best = float("inf")
+        for _ in range(3):  # best of 3 (a fresh GPU ramps its clocks during the first calls)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                plan.forward(x, out=c)
+                plan.inverse(c, n, out=y)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 5)
+        ts.append(best)
         del x, c, y
     slope = np.polyfit(np.log(ns), np.log(ts), 1)[0]
     assert 0.85 <= slope <= 1.15, (slope, ts)
