@@ -38,7 +38,10 @@
  *   The hot-path calls are asynchronous and stream-ordered on `stream` (a
  *   cudaStream_t passed as void*; NULL = legacy default stream), perform no
  *   allocation and no host synchronisation.  A plan is immutable: concurrent
- *   calls on different streams are safe if they use distinct workspaces.
+ *   calls on different streams are safe if they use distinct workspaces.  Calls of
+ *   >= 8192 (row, slice) units run their chunks on two streams owned by the plan (forked
+ *   from and joined back into `stream`); such calls on one plan are serialised on those
+ *   streams -- use one plan per stream for concurrent large calls.
  *   Device faults surface at the caller's next synchronisation (CUDA semantics).
  *
  * Errors: every int-returning call returns SLICQ_OK (0) or a negative code and

@@ -778,9 +778,11 @@ struct Pipe {
   const slicq_plan *p;
   cudaStream_t s;
   bool on;
+  std::unique_lock<std::mutex> lk;  // held from the fork to the join (shared streams / events)
   Pipe(const slicq_plan *p_, cudaStream_t s_, const WsLayout &w)
       : p(p_), s(s_), on(w.pipe) {
     if (!on) return;
+    lk = std::unique_lock<std::mutex>(p->pipe_mu);
     cudaEventRecord(p->d.pev[0], s);
     cudaStreamWaitEvent(p->d.pipe[0], p->d.pev[0], 0);
     cudaStreamWaitEvent(p->d.pipe[1], p->d.pev[0], 0);

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector_types.h>
 #include <vector>
@@ -101,6 +102,9 @@ struct slicq_plan {
   double min_width = 4.0;      // C7 lower bound on the filter width (bins)
   int64_t sampled_from = 0;    // Prop. 4: 2N' whose filters this system samples (0: none)
   bool painless = true;        // M_k >= L_k for all k (false only with sampled_from)
+  // serialises the fork / launch / join sequence of pipelined calls (the plan's two
+  // streams and three events are shared by all calls on the plan)
+  mutable std::mutex pipe_mu;
   // Table 1 layout
   int K;
   double Q;
