@@ -726,6 +726,18 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
     const bool fast = vec && s0 + 2 * q_lo >= 0 && s0 + 2 * q_hi + 1 < a.x_len;
     const float2 *xp = reinterpret_cast<const float2 *>(xr + (fast ? s0 : 0));
     float2 v[PER][R];
+    if (fast) {  // unswitched: predicated pair loads, no divergent branches
+#pragma unroll
+      for (int qq = 0; qq < PER; ++qq) {
+        const int j = tid + qq * T;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int q = j + r * TASKS;
+          const bool in = (TASKS % T == 0 || j < TASKS) && (unsigned)(q - q_lo) <= (unsigned)(q_hi - q_lo);
+          v[qq][r] = in ? __ldcs(xp + q) : make_float2(0.f, 0.f);
+        }
+      }
+    } else {
 #pragma unroll
     for (int qq = 0; qq < PER; ++qq) {
       const int j = tid + qq * T;
@@ -734,11 +746,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
         const int q = j + r * TASKS;
         float x0 = 0.f, x1 = 0.f;
         if ((TASKS % T == 0 || j < TASKS) && q >= q_lo && q <= q_hi) {
-          if (fast) {
-            const float2 t2 = __ldcs(xp + q);
-            x0 = t2.x;
-            x1 = t2.y;
-          } else {
+          {
             int64_t xi = s0 + 2 * q;
             if (a.wrap && xi < 0) xi += a.L;
             if (vec && xi >= 0 && xi + 1 < a.x_len) {
@@ -753,6 +761,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
         }
         v[qq][r] = make_float2(x0, x1);
       }
+    }
     }
     __syncthreads();  // window table staged (and twiddles)
     const int qa = (N - A + 1) >> 1, qb = (N + A - 1) >> 1;  // pairs with |t| <= A for both
@@ -769,11 +778,13 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
           if constexpr (MODE == 1) continue;  // no window
           const int w0 = jw + r * TASKS, w1 = w0 + 31;
           if ((w0 >= qa && w1 <= qb) || w1 < q_lo || w0 > q_hi) continue;
-          if (q >= qa && q <= qb) continue;  // both samples on the flat top (h_0 = 1)
-          // |t| of the two samples (t = 2q - N and 2q + 1 - N); h_0 = 1 for |t| <= A
+          // |t| of the two samples (t = 2q - N and 2q + 1 - N); h_0 = 1 for |t| <= A, the
+          // staged transition for A < |t| < Bw, 0 beyond (selects, no divergent branches)
           const int t0 = abs(2 * q - N), t1 = abs(2 * q + 1 - N);
-          if (t0 > A) v[qq][r].x = t0 < Bw ? v[qq][r].x * htab[t0 - A - 1] : 0.f;
-          if (t1 > A) v[qq][r].y = t1 < Bw ? v[qq][r].y * htab[t1 - A - 1] : 0.f;
+          const float h0a = t0 <= A ? 1.f : (t0 < Bw ? htab[t0 - A - 1] : 0.f);
+          const float h0b = t1 <= A ? 1.f : (t1 < Bw ? htab[t1 - A - 1] : 0.f);
+          v[qq][r].x *= h0a;
+          v[qq][r].y *= h0b;
         }
         dft<R, -1>(v[qq]);
 #pragma unroll
