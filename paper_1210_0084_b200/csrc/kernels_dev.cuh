@@ -345,6 +345,15 @@ __device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes, int id
 #ifndef SLICQ_INV_STEP_INLINE
 #define SLICQ_INV_STEP_INLINE __noinline__
 #endif
+#ifndef SLICQ_INV1_INLINE_MAXS
+#define SLICQ_INV1_INLINE_MAXS 16
+#endif
+#ifndef SLICQ_INV2_INLINE
+#define SLICQ_INV2_INLINE SLICQ_INV_STEP_INLINE
+#endif
+#ifndef SLICQ_INVS_INLINE
+#define SLICQ_INVS_INLINE SLICQ_INV_STEP_INLINE
+#endif
 // ------------------------------------------------------------------ channel packets
 // A packet = channels of one length M.  Big packets (M > 32) are a four-step M1 x M2 DFT
 // with one task per lane and step; channel ci owns the region ci*M1*S2 (S2 = M2 | 1) of the
@@ -443,7 +452,7 @@ __device__ __forceinline__ float2 mask_coef(float2 c, const float *m) {
 
 // I2 step 1: task (ci, p2) loads c[M2 p1 + p2]; DFT_{M1} (sign -); twiddle.
 template <int M1, int V, int MK = 0>  // V: channel-kernel variant; MK: fused mask mode
-__device__ SLICQ_INV_STEP_INLINE void inv_step1(const float2 *twM, const float2 *in_row, float2 *reg,
+__device__ __forceinline__ void inv_step1_body(const float2 *twM, const float2 *in_row, float2 *reg,
                                           int m2, int nch, unsigned mag2, int off_lane,
                                           int twoff_lane, int lane, const float *mrow = nullptr) {
   const int nt = nch * m2;
@@ -466,10 +475,27 @@ __device__ SLICQ_INV_STEP_INLINE void inv_step1(const float2 *twM, const float2 
 #pragma unroll
   for (int n1 = 0; n1 < M1; ++n1) A[n1 * S2] = v[n1];
 }
+template <int M1, int V, int MK = 0>  // V: channel-kernel variant; MK: fused mask mode
+__device__ __noinline__ void inv_step1_ool(const float2 *twM, const float2 *in_row, float2 *reg,
+                                          int m2, int nch, unsigned mag2, int off_lane,
+                                          int twoff_lane, int lane, const float *mrow) {
+  inv_step1_body<M1, V, MK>(twM, in_row, reg, m2, nch, mag2, off_lane, twoff_lane, lane, mrow);
+}
+// inlined in the variants with DFT sizes <= SLICQ_INV1_INLINE_MAXS (the lite variant: -1.6 %
+// on cfg4), out of line in the full variant (instruction-cache footprint: cfg3 +1 % inlined)
+template <int M1, int V, int MK = 0>  // V: channel-kernel variant; MK: fused mask mode
+__device__ __forceinline__ void inv_step1(const float2 *twM, const float2 *in_row, float2 *reg,
+                                          int m2, int nch, unsigned mag2, int off_lane,
+                                          int twoff_lane, int lane, const float *mrow = nullptr) {
+  if constexpr (V <= SLICQ_INV1_INLINE_MAXS)
+    inv_step1_body<M1, V, MK>(twM, in_row, reg, m2, nch, mag2, off_lane, twoff_lane, lane, mrow);
+  else
+    inv_step1_ool<M1, V, MK>(twM, in_row, reg, m2, nch, mag2, off_lane, twoff_lane, lane, mrow);
+}
 
 // I2 step 2, in place: F[n1 + M1 n2] = (unnormalised FFT_M of c) overwrites the region.
 template <int M2, int V>  // V: channel-kernel variant (separate register budgets)
-__device__ SLICQ_INV_STEP_INLINE void inv_step2(float2 *reg, int m1, int nch, unsigned mag1, int lane) {
+__device__ SLICQ_INV2_INLINE void inv_step2(float2 *reg, int m1, int nch, unsigned mag1, int lane) {
   const int nt = nch * m1;
   constexpr int S2 = M2 | 1;
   const bool act = lane < nt;
@@ -490,7 +516,7 @@ __device__ SLICQ_INV_STEP_INLINE void inv_step2(float2 *reg, int m1, int nch, un
 
 // Small inverse packet: lane vc loads virtual channel vc, FFT_M, F[q] -> scratch q*nv + vc.
 template <int M, int V, int MK = 0>  // V: channel-kernel variant; MK: fused mask mode
-__device__ SLICQ_INV_STEP_INLINE void inv_small(const float2 *in_row, float2 *reg, int nvc, int nv,
+__device__ SLICQ_INVS_INLINE void inv_small(const float2 *in_row, float2 *reg, int nvc, int nv,
                                           int off_lane, int lane, const float *mrow = nullptr) {
   if (lane >= nvc) return;
   const float2 *src = in_row + off_lane;
