@@ -145,8 +145,9 @@ SLICQ_API int64_t slicq_halo(const slicq_plan *p);                          /* (
  * host-only plans).  One workspace serves both directions: it holds the inverse's overlap-add
  * pairing counters and boundary halves, and a staging area for the spectra / channel
  * contributions of one chunk of slices (by default at most 8 GB of staging: larger calls
- * run chunk by chunk with identical results).  Zero-fill it once before its first use and
- * then reuse it unmodified, one workspace per concurrently running call. */
+ * run chunk by chunk with identical results).  No initialisation is needed (each inverse
+ * call resets its boundary-pairing counters on its stream); a workspace may be reused by
+ * calls of any size, one workspace per concurrently running call. */
 SLICQ_API size_t slicq_workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
 /* Number of CUDA kernels one slicq_forward (direction 0) or slicq_inverse (direction 1) call
  * (or the _range variant) launches for nslices x batch slices -- for launch accounting.

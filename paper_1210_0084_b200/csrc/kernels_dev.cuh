@@ -342,6 +342,12 @@ __device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes, int id
 #ifndef SLICQ_FWD_STEP_INLINE
 #define SLICQ_FWD_STEP_INLINE __forceinline__
 #endif
+#ifndef SLICQ_FWDS_INLINE
+#define SLICQ_FWDS_INLINE SLICQ_FWD_STEP_INLINE
+#endif
+#ifndef SLICQ_FWD2_INLINE
+#define SLICQ_FWD2_INLINE SLICQ_FWD_STEP_INLINE
+#endif
 #ifndef SLICQ_INV_STEP_INLINE
 #define SLICQ_INV_STEP_INLINE __noinline__
 #endif
@@ -397,7 +403,7 @@ __device__ SLICQ_FWD_STEP_INLINE void fwd_step1f(const uint2 *ent, const float2 
 
 // F4 step 2 + F5: task (ci, n1): DFT_{M2} over p2 -> c[n1 + M1 n2] (coalesced over n1).
 template <int M2, int V>  // V: channel-kernel variant (separate register budgets)
-__device__ SLICQ_FWD_STEP_INLINE void fwd_step2(const float2 *reg, float2 *out_row, int m1, int nch,
+__device__ SLICQ_FWD2_INLINE void fwd_step2(const float2 *reg, float2 *out_row, int m1, int nch,
                                           unsigned mag1, int off_lane, int lane) {
   const int nt = nch * m1;
   constexpr int S2 = M2 | 1;
@@ -420,7 +426,7 @@ __device__ SLICQ_FWD_STEP_INLINE void fwd_step2(const float2 *reg, float2 *out_r
 // as its sign; weight 0 for
 // zero padding) -- ent and X arrive offset by c and u.
 template <int M, int V>  // V: channel-kernel variant (separate register budgets)
-__device__ SLICQ_FWD_STEP_INLINE void fwd_small(const uint2 *ent, const float2 *X, float2 *out_row,
+__device__ SLICQ_FWDS_INLINE void fwd_small(const uint2 *ent, const float2 *X, float2 *out_row,
                                           bool act, int off_lane) {
   if (!act) return;
   float2 v[M];

@@ -588,6 +588,7 @@ int configure_kernels(slicq_plan *p) {
   int64_t cu = env_int("SLICQ_CHUNK_UNITS", std::max<int64_t>(1, budget / per_unit));
   // chunk pipelining (Pipe below): calls of >= pipe_min units run as pipe_parts chunks
   kc.pipe = env_int("SLICQ_PIPE", 1) != 0;
+  kc.pdl = env_int("SLICQ_PDL", 1) != 0;  // programmatic dependent launch between kernels
   kc.pipe_min = env_int("SLICQ_PIPE_MIN_UNITS", 8192);
   kc.pipe_parts = std::max<int64_t>(2, env_int("SLICQ_PIPE_PARTS", 4));
   cu = std::min<int64_t>(cu, 0x7fffffff);  // grid x dimension of the spectrum kernels
@@ -891,7 +892,7 @@ static cudaError_t launch_chan(bool fwd, const slicq_plan *p, KArgs a, cudaStrea
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = p->kc.pdl ? 1 : 0;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
     if (e != cudaSuccess) return e;
   }
@@ -904,8 +905,8 @@ static cudaError_t launch_spec(bool fwd, const slicq_plan *p, const KArgs &a, di
   switch (p->kc.logN) {
 #define CASE_(L)                                                                           \
   case L:                                                                                  \
-    return fwd ? launch_fwd_spec<L>(a, grid, sm, s, true, mode)                            \
-               : launch_inv_spec<L>(a, grid, sm, s, true, mode);
+    return fwd ? launch_fwd_spec<L>(a, grid, sm, s, p->kc.pdl, mode)                       \
+               : launch_inv_spec<L>(a, grid, sm, s, p->kc.pdl, mode);
     CASE_(11)
     CASE_(12)
     CASE_(13)
@@ -998,6 +999,15 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
   a.nslices = (int)nslices;
   char *wb = static_cast<char *>(ws);
   a.cnt = reinterpret_cast<unsigned *>(wb + w.cnt);
+  // the boundary-pairing counters start every call at zero: the workspace layout depends on
+  // the call's unit count, so a workspace reused by calls of different sizes (the streaming
+  // executor's ranges) would otherwise read an earlier call's boundary halves as counters
+  {
+    const cudaError_t e = cudaMemsetAsync(a.cnt, 0, sizeof(unsigned) * (size_t)(nslices * batch),
+                                          static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess)
+      return set_error(SLICQ_ECUDA, std::string("counter reset: ") + cudaGetErrorString(e));
+  }
   a.bnd = reinterpret_cast<float *>(wb + w.bnd);
   a.stage = reinterpret_cast<float2 *>(wb + w.stage);
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -84,6 +84,7 @@ struct KernelConfig {
   int tile = 16;              // units per channel-kernel tile
   int chan_per_sm = 0;        // channel-kernel CTAs per SM cap (0: occupancy)
   bool pipe = false;          // chunks alternate between two streams, ping-pong staging
+  bool pdl = true;            // launch with programmatic stream serialization
   int64_t pipe_min = 8192;    // ... for calls of at least this many units
   int64_t pipe_parts = 4;     // ... split into this many chunks
   bool longmode = false;      // sl_len 2^18..2^22: full-length CQ-NSGT only (kernels_long.cuh)

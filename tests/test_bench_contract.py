@@ -46,4 +46,5 @@ def test_cuda_arm_line():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["recon_rel_l2"] <= 1e-5
+    assert e["recon_rel_l2"] <= 1e-5  # the host round trip reconstructs too
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]

@@ -284,7 +284,11 @@ def test_range_api_matches_full(api, G):
                              f"y={y[bad[0,0], bad[0,1]].item()} full={y_full[bad[0,0], bad[0,1]].item()}")
 
 
-@pytest.mark.parametrize("pieces,n,batch", [(1, 70000, 1), (3, 9 * 16384 + 5, 2), (8, 200001, 1)])
+@pytest.mark.parametrize("pieces,n,batch", [(1, 70000, 1), (3, 9 * 16384 + 5, 2), (8, 200001, 1),
+                                            # ranges of unequal lengths (ramp) with > 64
+                                            # slices: the range workspace's layout changes
+                                            # from call to call
+                                            (4, 300 * 8192 + 1, 1), (6, 700 * 8192 + 3, 2)])
 def test_process_host_matches_device_path(api, pieces, n, batch):
     """api.process_host (pipelined host round trip over slice ranges) equals
     slicq_forward + slicq_inverse bit for bit, and applies fn to every range's coefficients."""
