@@ -348,6 +348,9 @@ __device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes, int id
 #ifndef SLICQ_FWD2_INLINE
 #define SLICQ_FWD2_INLINE SLICQ_FWD_STEP_INLINE
 #endif
+#ifndef SLICQ_IB_PF_AHEAD
+#define SLICQ_IB_PF_AHEAD 1
+#endif
 #ifndef SLICQ_INV_STEP_INLINE
 #define SLICQ_INV_STEP_INLINE __noinline__
 #endif
@@ -676,10 +679,12 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
       const int nvc = nuu * r;
       const float2 *in_row = a.coef_in + (a.unit0 + g0) * a.C;
       const float *mrow = MK ? a.mask + (a.unit0 + g0) * a.C : nullptr;
-      if (t + NW < ntask) {
-        const int g1 = g0 + NW * nu, n1u = min(nu, u_hi - g1);
+      // L2 prefetch of the coefficient rows SLICQ_IB_PF_AHEAD tasks of this warp ahead
+      if (t + SLICQ_IB_PF_AHEAD * NW < ntask) {
+        const int g1 = g0 + SLICQ_IB_PF_AHEAD * NW * nu, n1u = min(nu, u_hi - g1);
         for (int u = 0; u < n1u; ++u)
-          prefetch_l2(in_row + (int64_t)(NW * nu + u) * a.C + cbase, (int64_t)clen * 8, lane);
+          prefetch_l2(in_row + (int64_t)(SLICQ_IB_PF_AHEAD * NW * nu + u) * a.C + cbase,
+                      (int64_t)clen * 8, lane);
       }
       if (small) {
         switch (m1) {
