@@ -243,6 +243,30 @@ SLICQ_API int slicq_nsgt_inverse_complex(const slicq_plan *p, const slicq_c32 *c
                                          int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes,
                                          void *stream);
 
+/* ------------------------------------------------------------------ coefficient processing
+ * Device kernels on the slice-major coefficient layout [rows][C] (rows = batch x S; paper
+ * §VI).  All enqueue on `stream` and return
+ * SLICQ_ESHAPE for NULL / misaligned buffers or bad counts.
+ *
+ * slicq_apply_mask: coeffs[r][i] *= a, a = m (mask_db = 0) or 10^(-5 (1 - m)) (mask_db = 1:
+ *   0 -> -100 dB, 1 -> 0 dB), m = mask[i] (mask_full = 0: one float32 per column,
+ *   [C]) or mask[r][i] (mask_full = 1: float32 [rows][C]).  In place.
+ * slicq_spectrogram: the sliCQ spectrogram |s^0 + s^1|^2 of coefficients
+ *   [batch][nslices][C] (nslices even): out float32 [batch][nslices C / 2], channel k at
+ *   nslices off_k / 2, entry p = m M_k/2 + n' = |c^m_k[n' + M_k/2] + c^{m+1}_k[n']|^2 (the
+ *   two-layer array of Alg. 3; slices circular), hop 2N / M_k samples.
+ * slicq_transpose_bins: out = coeffs with every CQ channel k taking channel k - shift's
+ *   coefficients (B bins = one octave), modulated by e^{2 pi i d n / M}
+ *   (d = round(centre_k - centre_{k-shift}) in bins: the library's coefficients carry
+ *   absolute phase, C6); vacated CQ channels are zero, the plateaus copied.  Needs equal
+ *   M_k over the CQ channels (SLICQ_RASTER_FULL) else SLICQ_EINVAL; out must not alias. */
+SLICQ_API int slicq_apply_mask(const slicq_plan *p, slicq_c32 *coeffs, const float *mask,
+                               int64_t rows, int mask_full, int mask_db, void *stream);
+SLICQ_API int slicq_spectrogram(const slicq_plan *p, const slicq_c32 *coeffs, int64_t nslices,
+                                int64_t batch, float *out, void *stream);
+SLICQ_API int slicq_transpose_bins(const slicq_plan *p, const slicq_c32 *coeffs, slicq_c32 *out,
+                                   int64_t rows, int shift, void *stream);
+
 /* ------------------------------------------------------------------ Prop. 4 / Sec. V-A
  * slicq_approx_error: the sliCQ's approximation of the full-length CQ-NSGT (Prop. 4,
  * P:377-391; the experiment of P:475-497).  Per row b and stored

@@ -28,6 +28,9 @@ SIGNATURES = {
     "slicq_nsgt_forward_complex": (_i32, [_p, _p, _i64, _i64, _p, _p, _sz, _p]),
     "slicq_nsgt_inverse_complex": (_i32, [_p, _p, _i64, _i64, _p, _p, _sz, _p]),
     "slicq_approx_error_complex": (_i32, [_p, _p, _p, _p, _i64, _p, _p]),
+    "slicq_apply_mask": (_i32, [_p, _p, _p, _i64, _i32, _i32, _p]),
+    "slicq_spectrogram": (_i32, [_p, _p, _i64, _i64, _p, _p]),
+    "slicq_transpose_bins": (_i32, [_p, _p, _p, _i64, _i32, _p]),
     "plan_destroy": (None, [_p]),
     "slicq_num_channels": (_i32, [_p]),
     "slicq_num_cq_channels": (_i32, [_p]),

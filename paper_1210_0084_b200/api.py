@@ -407,52 +407,69 @@ def approximation_error(x: torch.Tensor, ps: Plan, pl: Plan, stream=None):
     return 10.0 * torch.log10(tot[:, 0] / tot[:, 1]), out
 
 
-def apply_mask(c: torch.Tensor, mask, db: bool = True) -> torch.Tensor:
-    """Coefficient masking (paper §VI): c * a, with a = 10^(-5 (1 - mask)) for
-    dB-scaled masks ("0 in the mask corresponds to 10^-5 (-100 dB) and 1 corresponds to 1
-    (0 dB)"), else a = mask.  `mask` broadcasts against c [batch][S][C] (e.g. a per-column
-    [C] or full [batch][S][C] grid); real-valued, on c's device."""
-    m = torch.as_tensor(mask, device=c.device, dtype=torch.float64)
-    a = torch.pow(10.0, -5.0 * (1.0 - m)) if db else m
-    return c * a.to(torch.float32 if c.dtype == torch.complex64 else torch.float64)
+def _rows(plan: Plan, c: torch.Tensor) -> torch.Tensor:
+    if c.dim() == 2:
+        c = c[None]
+    _check_tensor(c, torch.complex64, "coeffs")
+    if c.shape[-1] != plan.coeffs_per_slice:
+        raise ValueError("coefficient rows must hold C = plan.coeffs_per_slice entries")
+    return c
 
 
-def spectrogram(plan: Plan, c: torch.Tensor):
-    """The paper's sliCQ spectrogram |s^0 + s^1|^2 per channel: a list of
-    [batch][S M_k / 2] real tensors, time-ordered with hop 2N/M_k samples per entry."""
-    return [(s[:, 0] + s[:, 1]).abs() ** 2 for s in two_layer(plan, c)]
+def apply_mask(plan: Plan, c: torch.Tensor, mask, db: bool = True, inplace: bool = False,
+               stream=None) -> torch.Tensor:
+    """Coefficient masking (paper §VI) on the device (slicq_apply_mask): c * a,
+    a = 10^(-5 (1 - mask)) for dB-scaled masks ("0 in the mask corresponds to 10^-5 (-100 dB)
+    and 1 corresponds to 1 (0 dB)"), else a = mask.  c: complex64 [batch][S][C]; mask: a
+    number, a per-column [C] or a full [batch][S][C] real grid.  The fused alternative is
+    Plan.inverse(c, n, mask=...)."""
+    c = _rows(plan, c)
+    m = torch.as_tensor(mask, dtype=torch.float32, device=c.device)
+    C = plan.coeffs_per_slice
+    if m.dim() == 0:
+        m = m.expand(C)
+    m = m.contiguous()
+    if tuple(m.shape) == (C,):
+        full = 0
+    elif tuple(m.shape) == tuple(c.shape):
+        full = 1
+    else:
+        raise ValueError("mask must be a number, [C] or the coefficients' shape")
+    out = c if inplace else c.clone()
+    check(lib().slicq_apply_mask(plan._h, out.data_ptr(), m.data_ptr(), out.numel() // C, full,
+                                 1 if db else 0, _stream_ptr(stream)), "slicq_apply_mask")
+    return out
 
 
-def transpose_bins(plan: Plan, c: torch.Tensor, shift: int) -> torch.Tensor:
+def spectrogram(plan: Plan, c: torch.Tensor, stream=None):
+    """The paper's sliCQ spectrogram |s^0 + s^1|^2 per channel (slicq_spectrogram):
+    a list of [batch][S M_k / 2] float32 views into one device buffer, time-ordered with hop
+    2N/M_k samples per entry."""
+    c = _rows(plan, c)
+    B, S, C = c.shape
+    out = torch.empty((B, S * C // 2), dtype=torch.float32, device=c.device)
+    check(lib().slicq_spectrogram(plan._h, c.data_ptr(), S, B, out.data_ptr(),
+                                  _stream_ptr(stream)), "slicq_spectrogram")
+    Ms, offs = plan.channel_lengths(), plan.channel_offsets()
+    return [out[:, S * int(o) // 2: S * (int(o) + int(M)) // 2] for M, o in zip(Ms, offs)]
+
+
+def transpose_bins(plan: Plan, c: torch.Tensor, shift: int, stream=None) -> torch.Tensor:
     """Pitch transposition by `shift` CQ bins (B bins = one octave, SURVEY
-    NEXT-4): CQ channel k takes channel (k - shift)'s coefficients, vacated channels are
-    zero, the DC / Nyquist plateaus are kept.  Needs one coefficient count M for all CQ
-    channels (a rasterised plan, C10; the paper's "rectangular representation").
+    NEXT-4) on the device (slicq_transpose_bins): CQ channel k takes channel (k - shift)'s
+    coefficients, vacated channels are zero, the DC / Nyquist plateaus are kept.  Needs one
+    coefficient count M for all CQ channels (a rasterised plan, C10; the paper's
+    "rectangular representation").
 
     The library's coefficients carry absolute phase (C6): channel k's content at bin j sits
     at folded frequency j mod M.  Moving it to channel k' is the demodulated ("verbatim")
     copy of the paper's toolbox, which in absolute phase is a modulation by the difference
     of the two channels' centre bins: c'_{k'}[n] = c_k[n] e^{2 pi i (w_k' - w_k) n / M}."""
-    if c.dim() == 2:
-        c = c[None]
-    ex = plan.export()
-    Ms, offs, lo, ln = ex["M"], ex["off"], ex["lo"], ex["len"]
-    K = len(Ms) - 2
-    if len(set(int(m) for m in Ms[1:K + 1])) != 1:
-        raise ValueError("transpose_bins needs equal M_k over the CQ channels (rasterize=2)")
-    M = int(Ms[1])
-    centre = lo.astype(np.float64) + (ln.astype(np.float64) - 1.0) / 2.0
-    out = c.clone()
-    out[:, :, int(offs[1]):int(offs[K + 1])] = 0
-    s = int(shift)
-    n = torch.arange(M, device=c.device, dtype=torch.float64)
-    for k in range(1, K + 1):
-        src = k - s
-        if not 1 <= src <= K:
-            continue
-        d = int(round(centre[k] - centre[src]))
-        ph = torch.polar(torch.ones_like(n), 2.0 * np.pi * d * n / M).to(c.dtype)
-        out[:, :, int(offs[k]):int(offs[k]) + M] = c[:, :, int(offs[src]):int(offs[src]) + M] * ph
+    c = _rows(plan, c)
+    out = torch.empty_like(c)
+    check(lib().slicq_transpose_bins(plan._h, c.data_ptr(), out.data_ptr(),
+                                     c.numel() // plan.coeffs_per_slice, int(shift),
+                                     _stream_ptr(stream)), "slicq_transpose_bins")
     return out
 
 

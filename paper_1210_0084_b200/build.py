@@ -20,7 +20,7 @@ OUT = os.path.join(PKG, "libslicq.so")
 OBJ = os.path.join(PKG, "_build")
 
 SOURCES = ["plan.cpp", "kernels_host.cu", "kernels_l11.cu", "kernels_l12.cu", "kernels_l13.cu",
-           "kernels_l14.cu", "kernels_large_l15.cu", "kernels_large_l16.cu", "kernels_long.cu", "kernels_complex.cu", "stream_exec.cpp"]
+           "kernels_l14.cu", "kernels_large_l15.cu", "kernels_large_l16.cu", "kernels_long.cu", "kernels_complex.cu", "kernels_coeff.cu", "stream_exec.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v"]

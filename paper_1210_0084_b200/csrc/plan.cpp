@@ -510,6 +510,41 @@ int slicq_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t 
   return slicq::launch_inverse_complex(p, coeffs, n, batch, y, ws, ws_bytes, stream);
 }
 
+int slicq_apply_mask(const slicq_plan *p, slicq_c32 *coeffs, const float *mask, int64_t rows,
+                     int mask_full, int mask_db, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (rows < 1) return set_error(SLICQ_ESHAPE, "rows must be >= 1");
+  if (!coeffs || !mask) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)coeffs % 8 || (uintptr_t)mask % 4) return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  return slicq::launch_mask(p, coeffs, mask, rows, mask_full ? 1 : 0, mask_db ? 1 : 0, stream);
+}
+
+int slicq_spectrogram(const slicq_plan *p, const slicq_c32 *coeffs, int64_t nslices,
+                      int64_t batch, float *out, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (nslices < 2 || nslices % 2 || batch < 1)
+    return set_error(SLICQ_ESHAPE, "need an even number of slices >= 2 and batch >= 1");
+  if (!coeffs || !out) return set_error(SLICQ_ESHAPE, "NULL buffer");
+  if ((uintptr_t)coeffs % 8 || (uintptr_t)out % 4) return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  return slicq::launch_spectrogram(p, coeffs, nslices, batch, out, stream);
+}
+
+int slicq_transpose_bins(const slicq_plan *p, const slicq_c32 *coeffs, slicq_c32 *out,
+                         int64_t rows, int shift, void *stream) {
+  int rc = check_dev_plan(p);
+  if (rc) return rc;
+  if (rows < 1) return set_error(SLICQ_ESHAPE, "rows must be >= 1");
+  if (!coeffs || !out || coeffs == out) return set_error(SLICQ_ESHAPE, "NULL or aliased buffer");
+  if ((uintptr_t)coeffs % 8 || (uintptr_t)out % 8) return set_error(SLICQ_ESHAPE, "misaligned buffer");
+  for (int k = 2; k <= p->K; ++k)
+    if (p->M[k] != p->M[1])
+      return set_error(SLICQ_EINVAL, "transposition needs equal M_k over the CQ channels "
+                                     "(rasterize = SLICQ_RASTER_FULL)");
+  return slicq::launch_transpose(p, coeffs, out, rows, shift, stream);
+}
+
 int slicq_nsgt_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n,
                                int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes,
                                void *stream) {

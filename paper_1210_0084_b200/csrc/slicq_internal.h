@@ -159,6 +159,13 @@ int launch_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n, i
 int launch_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t n,
                            int64_t batch, slicq_c32 *y, void *ws, size_t ws_bytes, void *stream,
                            int nsgt = 0);
+// coefficient processing (kernels_coeff.cu)
+int launch_mask(const slicq_plan *p, slicq_c32 *c, const float *mask, int64_t rows, int full,
+                int db, void *stream);
+int launch_spectrogram(const slicq_plan *p, const slicq_c32 *c, int64_t nslices, int64_t batch,
+                       float *out, void *stream);
+int launch_transpose(const slicq_plan *p, const slicq_c32 *c, slicq_c32 *out, int64_t rows,
+                     int shift, void *stream);
 int launch_approx(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s,
                   const slicq_c32 *c, int64_t batch, double *out, void *stream, int full = 0);
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);

@@ -82,12 +82,12 @@ def test_mask_decomposition_adds_up():
     c = plan.forward(x)
     g = torch.Generator().manual_seed(1)
     m = torch.rand(c.shape, generator=g, dtype=torch.float64).cuda()
-    y1 = plan.inverse(api.apply_mask(c, m, db=False), n)
-    y2 = plan.inverse(api.apply_mask(c, 1.0 - m, db=False), n)
+    y1 = plan.inverse(api.apply_mask(plan, c, m, db=False), n)
+    y2 = plan.inverse(api.apply_mask(plan, c, 1.0 - m, db=False), n)
     err = ((y1 + y2 - x).norm() / x.norm()).item()
     assert err <= 1e-5, err
     # -100 dB everywhere: the output is x scaled by 1e-5
-    y0 = plan.inverse(api.apply_mask(c, 0.0), n)
+    y0 = plan.inverse(api.apply_mask(plan, c, 0.0), n)
     assert ((y0 - 1e-5 * x).norm() / (1e-5 * x.norm())).item() <= 1e-5
 
 
@@ -106,7 +106,7 @@ def test_masked_inverse_fused_equals_separate_mask():
         m = torch.rand(c.shape, generator=g).cuda()
         for db in (True, False):
             y_f = plan.inverse(c, n, mask=m, mask_db=db)
-            y_s = plan.inverse(api.apply_mask(c, m, db=db), n)
+            y_s = plan.inverse(api.apply_mask(plan, c, m, db=db), n)
             err = ((y_f - y_s).norm() / y_s.norm()).item()
             assert err <= 1e-5, (cfg_id, db, err)
         ones = torch.ones(c.shape, device="cuda")

@@ -21,4 +21,4 @@ def t(fn, it=10):
     return e0.elapsed_time(e1) / it
 print(f"inverse {t(lambda: plan.inverse(c, n, out=y)):.3f} ms  "
       f"fused masked {t(lambda: plan.inverse(c, n, out=y, mask=m)):.3f} ms  "
-      f"separate mask + inverse {t(lambda: plan.inverse(api.apply_mask(c, m), n, out=y)):.3f} ms")
+      f"separate mask + inverse {t(lambda: plan.inverse(api.apply_mask(plan, c, m), n, out=y)):.3f} ms")
