@@ -11,6 +11,7 @@
 // (exact on real-consistent sets, C15) and interleaves y = y_u + i y_v.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 
@@ -38,48 +39,37 @@ __global__ void cx_join_rows(const float *r, int64_t n, float2 *y) {  // [2B][n]
     y[b * n + i] = make_float2(r[(2 * b) * n + i], r[(2 * b + 1) * n + i]);
 }
 
-// w_n = e^{2 pi i 2N n / M} from the plan's e^{2 pi i t / M} table
-__device__ __forceinline__ float2 mirror_phase(const float2 *tw, int64_t n2, int n, int M) {
-  return tw[(int)(((n2 % M) * (int64_t)n) % M)];
-}
-
-// one CTA per (coefficient row (b, m), stored channel k); T: [2B][S][C], out: [B][S][Cf]
-__global__ void cx_combine(const ChanDev *ch, const float2 *twM, const float2 *T, float2 *out,
-                           int64_t S, int64_t C, int64_t Cf, int K, int64_t n2) {
-  const int64_t row = blockIdx.x, b = row / S, m = row - b * S;
-  const int k = blockIdx.y;
-  const ChanDev c = ch[k];
-  const float2 *a = T + ((2 * b) * S + m) * C + c.off;
-  const float2 *bb = T + ((2 * b + 1) * S + m) * C + c.off;
+// out[b][m][j] over the full layout from the Re / Im rows T[2b][m], T[2b+1][m] ([C] each):
+// stored column: a + i b; mirror column: w (conj a + i conj b) = w (a.x + b.y, b.x - a.y)
+__global__ void cx_combine(const uint2 *cxf, const float2 *twM, const float2 *T, float2 *out,
+                           int64_t S, int64_t C, int64_t Cf, int64_t row0) {
+  const int64_t row = row0 + blockIdx.y, b = row / S, m = row - b * S;
+  const float2 *ta = T + ((2 * b) * S + m) * C, *tb = T + ((2 * b + 1) * S + m) * C;
   float2 *o = out + row * Cf;
-  const bool mirrored = k >= 1 && k <= K;
-  const int64_t moff = C + (ch[K + 1].off - (c.off + c.M));  // mirrors of K..1 after stored
-  for (int n = threadIdx.x; n < c.M; n += blockDim.x) {
-    const float2 av = a[n], bv = bb[n];
-    o[c.off + n] = make_float2(av.x - bv.y, av.y + bv.x);
-    if (mirrored)  // w (conj a + i conj b) = w (a.x + b.y, b.x - a.y)
-      o[moff + n] = cmul(mirror_phase(twM + c.twoff, n2, n, c.M),
-                         make_float2(av.x + bv.y, bv.x - av.y));
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < Cf;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 e = __ldg(cxf + j);
+    const float2 av = ta[e.x], bv = tb[e.x];
+    o[j] = (e.y & 1u) ? cmul(__ldg(twM + (e.y >> 1)), make_float2(av.x + bv.y, bv.x - av.y))
+                      : make_float2(av.x - bv.y, av.y + bv.x);
   }
 }
 
-// c: [B][S][Cf] -> U: [2B][S][C] (rows u_b, v_b)
-__global__ void cx_split(const ChanDev *ch, const float2 *twM, const float2 *cf, float2 *U,
-                         int64_t S, int64_t C, int64_t Cf, int K, int64_t n2) {
-  const int64_t row = blockIdx.x, b = row / S, m = row - b * S;
-  const int k = blockIdx.y;
-  const ChanDev c = ch[k];
-  const float2 *ck = cf + row * Cf + c.off;
-  const int64_t moff = (k >= 1 && k <= K) ? C + (ch[K + 1].off - (c.off + c.M)) : c.off;
-  const float2 *cm = cf + row * Cf + moff;
-  float2 *u = U + ((2 * b) * S + m) * C + c.off;
-  float2 *v = U + ((2 * b + 1) * S + m) * C + c.off;
-  for (int n = threadIdx.x; n < c.M; n += blockDim.x) {
-    const float2 w = k == 0 ? make_float2(1.f, 0.f) : mirror_phase(twM + c.twoff, n2, n, c.M);
-    const float2 z = cmul(w, cconj(cm[n]));
-    const float2 x = ck[n];
-    u[n] = make_float2(0.5f * (x.x + z.x), 0.5f * (x.y + z.y));
-    v[n] = make_float2(0.5f * (x.y - z.y), -0.5f * (x.x - z.x));  // (x - z) / (2i)
+// c: [B][S][Cf] -> U: [2B][S][C] (rows u_b, v_b): z = w conj(c_mirror) (DC: conj c),
+// u = (c + z) / 2, v = (c - z) / (2i)
+__global__ void cx_split(const uint2 *cxs, const float2 *twM, const float2 *cf, float2 *U,
+                         int64_t S, int64_t C, int64_t Cf, int64_t row0) {
+  const int64_t row = row0 + blockIdx.y, b = row / S, m = row - b * S;
+  const float2 *cr = cf + row * Cf;
+  float2 *u = U + ((2 * b) * S + m) * C, *v = U + ((2 * b + 1) * S + m) * C;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < C;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 e = __ldg(cxs + j);
+    const float2 w = (e.y & 1u) ? make_float2(1.f, 0.f) : __ldg(twM + (e.y >> 1));
+    const float2 z = cmul(w, cconj(cr[e.x]));
+    const float2 x = cr[j];
+    u[j] = make_float2(0.5f * (x.x + z.x), 0.5f * (x.y + z.y));
+    v[j] = make_float2(0.5f * (x.y - z.y), -0.5f * (x.x - z.x));  // (x - z) / (2i)
   }
 }
 
@@ -125,9 +115,14 @@ int launch_forward_complex(const slicq_plan *p, const slicq_c32 *x, int64_t n, i
             : launch_forward(p, R, n, n, 0, L, 1, 0, S, 2 * batch,
                              reinterpret_cast<slicq_c32 *>(T), ws, wr, stream);
   if (rc) return rc;
-  cx_combine<<<dim3((unsigned)(batch * S), (unsigned)(p->K + 2)), 128, 0, s>>>(
-      p->d.chan, reinterpret_cast<const float2 *>(p->d.twM), T,
-      reinterpret_cast<float2 *>(coeffs), S, p->C, coeffs_full(p), p->K, p->sl_len);
+  {
+    const int64_t Cf = coeffs_full(p), rows = batch * S;
+    const unsigned gx = (unsigned)std::min<int64_t>((Cf + 255) / 256, 64);
+    for (int64_t r0 = 0; r0 < rows; r0 += 65535)  // grid y <= 65535 rows per launch
+      cx_combine<<<dim3(gx, (unsigned)std::min<int64_t>(65535, rows - r0)), 256, 0, s>>>(
+          p->d.cxf, reinterpret_cast<const float2 *>(p->d.twM), T,
+          reinterpret_cast<float2 *>(coeffs), S, p->C, Cf, r0);
+  }
   return cuda_err(cudaGetLastError(), "complex combine");
 }
 
@@ -144,9 +139,14 @@ int launch_inverse_complex(const slicq_plan *p, const slicq_c32 *coeffs, int64_t
   float *Y = reinterpret_cast<float *>(w + wr);
   float2 *U = reinterpret_cast<float2 *>(w + wr + al(sizeof(float) * 2 * batch * n));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cx_split<<<dim3((unsigned)(batch * S), (unsigned)(p->K + 2)), 128, 0, s>>>(
-      p->d.chan, reinterpret_cast<const float2 *>(p->d.twM),
-      reinterpret_cast<const float2 *>(coeffs), U, S, p->C, coeffs_full(p), p->K, p->sl_len);
+  {
+    const int64_t rows = batch * S;
+    const unsigned gx = (unsigned)std::min<int64_t>((p->C + 255) / 256, 64);
+    for (int64_t r0 = 0; r0 < rows; r0 += 65535)
+      cx_split<<<dim3(gx, (unsigned)std::min<int64_t>(65535, rows - r0)), 256, 0, s>>>(
+          p->d.cxs, reinterpret_cast<const float2 *>(p->d.twM),
+          reinterpret_cast<const float2 *>(coeffs), U, S, p->C, coeffs_full(p), r0);
+  }
   int rc = cuda_err(cudaGetLastError(), "complex split");
   if (rc) return rc;
   rc = nsgt ? launch_inverse(p, reinterpret_cast<const slicq_c32 *>(U), 1, 1, 2, 2 * batch, 0, n,

@@ -651,6 +651,36 @@ int upload(slicq_plan *p) {
     tw.push_back((float)std::cos(a));
     tw.push_back((float)std::sin(a));
   }
+  // complex-input column maps (kernels_complex.cu): full layout (stored 0..K+1, then the
+  // mirrors of K..1) -> (source stored column, e^{2 pi i 2N n/M} table index << 1 | mirror);
+  // stored column -> (its mirror's full-layout column, table index << 1 | (DC ? no phase))
+  {
+    const int K2 = p->K + 2;
+    int64_t Cf = p->C;
+    for (int k = 1; k <= p->K; ++k) Cf += p->M[k];
+    p->cxf.assign(Cf, make_uint2(0u, 0u));
+    p->cxs.assign(p->C, make_uint2(0u, 0u));
+    for (int64_t j = 0; j < p->C; ++j) p->cxf[j] = make_uint2((uint32_t)j, 0u);
+    int64_t mo = p->C;
+    for (int k = p->K; k >= 1; --k) {  // mirror of k: full channel 2K+2-k, after the stored
+      const int M = p->M[k];
+      const int64_t n2m = (2 * N) % M;
+      for (int n = 0; n < M; ++n) {
+        const uint32_t t = (uint32_t)(twoff[M] + (int)((n2m * n) % M));
+        p->cxf[mo + n] = make_uint2((uint32_t)(p->off[k] + n), (t << 1) | 1u);
+        p->cxs[p->off[k] + n] = make_uint2((uint32_t)(mo + n), t << 1);
+      }
+      mo += M;
+    }
+    for (int k : {0, K2 - 1}) {  // self-mirrored plateaus
+      const int M = p->M[k];
+      const int64_t n2m = (2 * N) % M;
+      for (int n = 0; n < M; ++n) {
+        const uint32_t t = (uint32_t)(twoff[M] + (int)((n2m * n) % M));
+        p->cxs[p->off[k] + n] = make_uint2((uint32_t)(p->off[k] + n), k == 0 ? 1u : (t << 1));
+      }
+    }
+  }
   struct Part {
     const void *src;
     size_t bytes;
@@ -671,6 +701,8 @@ int upload(slicq_plan *p) {
       {p->lgdw.data(), sizeof(float) * p->lgdw.size(), 0},
       {p->lrow.data(), sizeof(uint32_t) * p->lrow.size(), 0},
       {p->lent.data(), sizeof(uint32_t) * p->lent.size(), 0},
+      {p->cxf.data(), sizeof(uint2) * p->cxf.size(), 0},
+      {p->cxs.data(), sizeof(uint2) * p->cxs.size(), 0},
   };
   size_t o = 0;
   for (Part &pt : parts) {
@@ -701,6 +733,8 @@ int upload(slicq_plan *p) {
   p->d.gdw = reinterpret_cast<float *>(b + parts[11].off);
   p->d.lrow = reinterpret_cast<uint32_t *>(b + parts[12].off);
   p->d.lent = reinterpret_cast<uint32_t *>(b + parts[13].off);
+  p->d.cxf = reinterpret_cast<uint2 *>(b + parts[14].off);
+  p->d.cxs = reinterpret_cast<uint2 *>(b + parts[15].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));

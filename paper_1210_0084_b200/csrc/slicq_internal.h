@@ -61,6 +61,8 @@ struct DeviceTables {
   float *gdw = nullptr;     // long mode: g~_k / sqrt(M_k) (x 1/2 on the plateaus)
   uint32_t *lrow = nullptr; // long mode: per-bin term list start [N + 2]
   uint32_t *lent = nullptr; // long mode: term index | conj << 31
+  uint2 *cxf = nullptr;     // complex input, per full-layout column: source column, twiddle
+  uint2 *cxs = nullptr;     // complex input, per stored column: mirror column, twiddle
   void *block = nullptr;    // single allocation holding all of the above
   cudaStream_t pipe[2] = {nullptr, nullptr};  // chunk pipelining (kc.pipe): two streams
   cudaEvent_t pev[3] = {nullptr, nullptr, nullptr};
@@ -129,6 +131,7 @@ struct slicq_plan {
   std::vector<float> lgw, lgdw;          // long mode filter weights
   std::vector<uint32_t> lrow, lent;      // long mode per-bin term lists
   std::vector<int32_t> lm1;              // long mode: four-step factor of M_k > 26000 (else 0)
+  std::vector<uint2> cxf, cxs;           // complex-input column maps (kernels_complex.cu)
   std::vector<int64_t> lsoff;            // long mode: staging scratch offset of those channels
 };
 
