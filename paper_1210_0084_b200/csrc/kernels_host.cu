@@ -155,14 +155,18 @@ constexpr int kSmallMax = SLICQ_SMALL_MAX;  // channels with M <= this: one lane
 #ifndef SLICQ_MICRO_MINB
 #define SLICQ_MICRO_MINB 4
 #endif
+#ifndef SLICQ_LITE_MINB_INV
+#define SLICQ_LITE_MINB_INV SLICQ_LITE_MINB
+#endif
 constexpr int kLiteMax = SLICQ_LITE_MAX, kLiteMinB = SLICQ_LITE_MINB, kFullMax = 32, kFullMinB = 2;
+constexpr int kLiteMinBInv = SLICQ_LITE_MINB_INV;  // the inverse lite variant's CTAs per SM
 constexpr int kMicroMax = SLICQ_MICRO_MAX, kMicroMinB = SLICQ_MICRO_MINB;
 constexpr int kVariants = 3;  // micro (DFT sizes <= kMicroMax), lite (<= kLiteMax), full
 using ChanFn = void (*)(const KArgs);
 template <int MK>
 static ChanFn inv_fn(int variant) {
   if (variant == 0) return slicq_inv_chan_kernel<(kMicroMax ? kMicroMax : 1), kMicroMinB, MK>;
-  return variant == 1 ? slicq_inv_chan_kernel<kLiteMax, kLiteMinB, MK>
+  return variant == 1 ? slicq_inv_chan_kernel<kLiteMax, kLiteMinBInv, MK>
                       : slicq_inv_chan_kernel<kFullMax, kFullMinB, MK>;
 }
 // variant 0 micro, 1 lite, 2 full; mask: inverse with a fused coefficient mask (0 none,
