@@ -357,9 +357,7 @@ __global__ void __launch_bounds__(LT) inv_large_row(const KArgs a) {
     }
     (void)A; (void)Bw; (void)left_paired; (void)right_paired; (void)bl; (void)br; (void)trp;
     (void)bnd_row; (void)S;
-    pdl_trigger();
-    return;
-  }
+  } else {
   // consecutive threads take consecutive n1 (16 rows) of one n2: 32 consecutive samples
   for (int idx = tid; idx < LB * N2; idx += LT) {
     const int s = idx % LB, n2 = idx / LB;
@@ -400,6 +398,7 @@ __global__ void __launch_bounds__(LT) inv_large_row(const KArgs a) {
   }
   if (!a.circular && mloc == 0 && blockIdx.y == 0)
     for (int u = tid; u < a.halo - (Bw - 1); u += LT) a.spill[row * a.halo + u] = 0.f;
+  }  // MODE 0
   pdl_trigger();
 }
 
