@@ -86,3 +86,23 @@ def test_nsgt_rejects_long_input():
     plan = api.Plan(44100.0, 50.0, 22050.0, 24, 4096, 64, 0)
     with pytest.raises(Exception):
         plan.nsgt_forward(torch.zeros(1, 4097, device="cuda"))
+
+
+def test_long_nsgt_chunked_is_bit_identical(monkeypatch):
+    """Long mode runs rows chunk by chunk when the staging budget is small (SLICQ_STAGE_MB,
+    read at plan creation): identical coefficients and reconstruction."""
+    from paper_1210_0084_b200 import api
+    args = (44100.0, 50.0, 22050.0, 48, 2 ** 18, 64, 0)
+    x = torch.from_numpy(random_signal(5, 5, 2 ** 18 - 3)).cuda()
+    plan = api.Plan(*args)
+    c = plan.nsgt_forward(x)
+    y = plan.nsgt_inverse(c, x.shape[1])
+    monkeypatch.setenv("SLICQ_STAGE_MB", "8")  # < 2 rows of staging per chunk
+    small = api.Plan(*args)
+    monkeypatch.delenv("SLICQ_STAGE_MB")
+    assert small.kernel_launches("forward", 1, 5) > plan.kernel_launches("forward", 1, 5)
+    c2 = small.nsgt_forward(x)
+    y2 = small.nsgt_inverse(c2, x.shape[1])
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
+    assert torch.equal(y, y2)
