@@ -969,6 +969,14 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
     // H at the thread's 32 bins jA + TASKS1 r (vA) and jB + TASKS1 r (vB): 4 r per batch,
     // all 16 slot loads and 8 overflow descriptors of a batch in flight together
     float2 vA[16], vB[16];
+    // bin N (thread 0's self-mirrored task 0 pairs bin 0 with it): loads issued first, in
+    // flight with the slot loads below (warp 0 must not wait on them alone)
+    float2 hN = make_float2(0.f, 0.f);
+    uint32_t dN = 0;
+    if (tid == 0) {
+      hN = cadd(__ldcg(Z0 + N), __ldcg(Z1 + N));
+      dN = __ldg(a.dpos + N);
+    }
     constexpr int IG = SLICQ_IA_GROUP;  // r values per load batch
 #pragma unroll
     for (int r0 = 0; r0 < 16; r0 += IG) {
@@ -996,27 +1004,42 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
         }
       }
     }
-    if (tid != 0) {
-      // N - (jA + TASKS1 r) = jB + TASKS1 (15 - r)
-#pragma unroll
-      for (int r = 0; r < 16; ++r) pack(vA[r], vB[15 - r], jA + TASKS1 * r);
-    } else {
-      // task 0: bins TASKS1 r pair as (r, 16 - r), r = 8 is N/2, r = 0 pairs with bin N;
-      // task TASKS1/2: bins TASKS1/2 + TASKS1 r pair as (r, 15 - r)
-      float2 hN = cadd(__ldcg(Z0 + N), __ldcg(Z1 + N));
-      {
-        const uint32_t dN = __ldg(a.dpos + N);
+    // Thread 0's tasks 0 and TASKS1/2 are their own mirrors (bins TASKS1 r pair as
+    // (r, 16 - r) with r = 0 pairing bin N, bins TASKS1/2 + TASKS1 r as (r, 15 - r)).  Rather
+    // than a divergent special path in warp 0, the warp packs those 32 bins cooperatively,
+    // one bin per lane, with the same formula: Z[k] = F(H[k], H[N-k], k) (the second output
+    // of a pair is F at N - k).  Every lane also runs the regular pairing (lane 0's result is
+    // replaced).
+    __shared__ float2 sv[33], sz[32];
+    if (tid < 32) {  // warp 0 (warp-uniform branch)
+      if (tid == 0) {
         for (int e = 0; e < (int)(dN >> 20); ++e) hN = cadd(hN, __ldcg(Zo + (dN & 0xfffff) + e));
-      }
-      pack(vA[0], hN, 0);
 #pragma unroll
-      for (int r = 1; r < 8; ++r) pack(vA[r], vA[16 - r], TASKS1 * r);
-      {
-        float2 m = vA[8];
-        pack(vA[8], m, N / 2);
+        for (int r = 0; r < 16; ++r) {
+          sv[r] = vA[r];
+          sv[16 + r] = vB[r];
+        }
+        sv[32] = hN;
       }
+      __syncwarp();
+      const int L = tid;
+      const int ia = L < 16 ? L : L;                                    // H[k]
+      const int ib = L == 0 ? 32 : (L < 16 ? 16 - L : 16 + 15 - (L - 16));  // H[N - k]
+      const int kk = L < 16 ? TASKS1 * L : TASKS1 / 2 + TASKS1 * (L - 16);
+      float2 hk = sv[ia], hn = sv[ib];
+      pack(hk, hn, kk);
+      sz[L] = hk;
+      __syncwarp();
+    }
+    // N - (jA + TASKS1 r) = jB + TASKS1 (15 - r)
 #pragma unroll
-      for (int r = 0; r < 8; ++r) pack(vB[r], vB[15 - r], TASKS1 / 2 + TASKS1 * r);
+    for (int r = 0; r < 16; ++r) pack(vA[r], vB[15 - r], jA + TASKS1 * r);
+    if (tid == 0) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        vA[r] = sz[r];
+        vB[r] = sz[16 + r];
+      }
     }
     dft<16, +1>(vA);
     dft<16, +1>(vB);
