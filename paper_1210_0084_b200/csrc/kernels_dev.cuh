@@ -869,17 +869,33 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
       SLICQ_XSTORE(Xo + k, cadd(E, wO));
       if (mirror) SLICQ_XSTORE(Xo + (N - k), csub(cconj(E), cconj(wO)));
     };
+    // thread 0's tasks 0 and TASKS3/2 are their own mirrors: warp 0 packs their 32 bins
+    // cooperatively, one bin per lane (X[k] = E + e^{-i pi k/N} O at each k; k = 0 also
+    // gives X[N]), instead of a divergent special path
+    __shared__ float2 svz[32];
+    if (tid < 32) {  // warp 0 (warp-uniform branch)
+      if (tid == 0) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          svz[r] = vA[r];
+          svz[16 + r] = vB[r];
+        }
+      }
+      __syncwarp();
+      const int L = tid;
+      const int ib = L == 0 ? 0 : (L < 16 ? 16 - L : 16 + 15 - (L - 16));  // Z[N - k]
+      const int kk = L < 16 ? TASKS3 * L : TASKS3 / 2 + TASKS3 * (L - 16);
+      const float2 zk = svz[L], zn = svz[ib];
+      if (L == 0) {  // X[0], X[N] from Z[0]
+        SLICQ_XSTORE(Xo, make_float2(zk.x + zk.y, 0.f));
+        SLICQ_XSTORE(Xo + N, make_float2(zk.x - zk.y, 0.f));
+      } else {
+        r2c(zk, zn, kk, false);
+      }
+    }
     if (tid != 0) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) r2c(vA[r], vB[15 - r], jA + TASKS3 * r, true);
-    } else {
-      SLICQ_XSTORE(Xo, make_float2(vA[0].x + vA[0].y, 0.f));  // X[0], X[N] from Z[0]
-      SLICQ_XSTORE(Xo + N, make_float2(vA[0].x - vA[0].y, 0.f));
-#pragma unroll
-      for (int r = 1; r < 8; ++r) r2c(vA[r], vA[16 - r], TASKS3 * r, true);
-      r2c(vA[8], vA[8], N / 2, false);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) r2c(vB[r], vB[15 - r], TASKS3 / 2 + TASKS3 * r, true);
     }
   } else {
     pass_smem<N, CF::F3, CF::F1 * CF::F2, -1, T>(spec, tw);
