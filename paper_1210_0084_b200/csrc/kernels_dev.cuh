@@ -8,7 +8,8 @@
 //       F1  first radix pass straight from HBM: Tukey-windowed frame pairs
 //       F2  r2c FFT_{2N}: complex N-point Stockham FFT in shared memory; the last pass, the
 //           packing step and the store of X[0..N] to the staging buffer fused in registers
-//           (mirror-paired tasks)
+//           (mirror-paired tasks; the two self-mirrored tasks of thread 0 are packed by
+//           warp 0 cooperatively, one bin per lane)
 //     slicq_fwd_chan_kernel<MAXS,MINB>  one warp task = (packet, nu units) of a tile:
 //       F3  fold: buf[p] = X(j) g_k[j]/sqrt(M_k), j = p mod M_k, from a plan-time element
 //           table (bin | scratch position, weight with the conjugation flag as its sign)
