@@ -975,6 +975,13 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       return cconj(cmul(__ldg(a.tw2n + 64 + (k >> 6)), __ldg(a.tw2n + (k & 63))));
     };
     // c2r packing of the pair (k, N - k): Z[k] = E + iO, Z[N-k] = conj(E) + i conj(D) conj(w)
+    auto pack_w = [&](float2 &hk, float2 &hn, float2 w) {
+      const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
+      const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+      const float2 O = cmul(D, w), O2 = cmul(cconj(D), cconj(w));
+      hk = make_float2(E.x - O.y, E.y + O.x);
+      hn = make_float2(E.x - O2.y, -E.y + O2.x);
+    };
     auto pack = [&](float2 &hk, float2 &hn, int k) {
       const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
       const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
@@ -994,6 +1001,10 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       hN = cadd(__ldcg(Z0 + N), __ldcg(Z1 + N));
       dN = __ldg(a.dpos + N);
     }
+    // warp 0's cooperative packing of the self-mirrored bins (below): lane L's bin and its
+    // twiddle, loaded now
+    const int ksp = tid < 16 ? TASKS1 * tid : TASKS1 / 2 + TASKS1 * (tid - 16);
+    const float2 wsp = tid < 32 ? wk(ksp) : make_float2(1.f, 0.f);
     constexpr int IG = SLICQ_IA_GROUP;  // r values per load batch
 #pragma unroll
     for (int r0 = 0; r0 < 16; r0 += IG) {
@@ -1042,9 +1053,8 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       const int L = tid;
       const int ia = L < 16 ? L : L;                                    // H[k]
       const int ib = L == 0 ? 32 : (L < 16 ? 16 - L : 16 + 15 - (L - 16));  // H[N - k]
-      const int kk = L < 16 ? TASKS1 * L : TASKS1 / 2 + TASKS1 * (L - 16);
       float2 hk = sv[ia], hn = sv[ib];
-      pack(hk, hn, kk);
+      pack_w(hk, hn, wsp);  // twiddle of bin ksp = TASKS1 L (L < 16), TASKS1/2 + TASKS1 (L-16)
       sz[L] = hk;
       __syncwarp();
     }
