@@ -93,7 +93,7 @@ __device__ __forceinline__ void st_plain(float2 *p, float2 v) { *p = v; }
 #define SLICQ_ZSTORE __stcs  // (measured: evict-first beats .cg by ~1 % on cfg4)
 #endif
 #ifndef SLICQ_IA_GROUP
-#define SLICQ_IA_GROUP 4
+#define SLICQ_IA_GROUP 8
 #endif
 #ifndef SLICQ_T13
 #define SLICQ_T13 256
