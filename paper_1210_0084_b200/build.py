@@ -2,9 +2,10 @@
 
     python -m paper_1210_0084_b200.build          # or __graft_entry__.build()
 
-The four kernel instantiations (2N = 4096 .. 32768) are separate translation units
-compiled in parallel; the host plan (plan.cpp) and the dispatch (kernels_host.cu)
-are linked with them into one shared library with a static CUDA runtime.
+The per-size kernel instantiations (kernels_spec.cu for 2N = 4096 .. 32768, kernels_large.cu
+for 2N = 65536, 131072) are one source compiled once per size (-DSLICQ_LOGN=...) in parallel;
+the host plan (plan.cpp) and the dispatch (kernels_host.cu, fused_host.cu) are linked with
+them into one shared library with a static CUDA runtime.
 """
 from __future__ import annotations
 
@@ -19,8 +20,13 @@ CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libslicq.so")
 OBJ = os.path.join(PKG, "_build")
 
-SOURCES = ["plan.cpp", "kernels_host.cu", "kernels_l11.cu", "kernels_l12.cu", "kernels_l13.cu",
-           "kernels_l14.cu", "kernels_large_l15.cu", "kernels_large_l16.cu", "kernels_long.cu", "kernels_complex.cu", "kernels_coeff.cu", "stream_exec.cpp"]
+# (source, object name, extra defines)
+SOURCES = [("plan.cpp", "plan", ()), ("kernels_host.cu", "kernels_host", ()),
+           ("fused_host.cu", "fused_host", ())]
+SOURCES += [("kernels_spec.cu", f"kernels_spec_l{n}", (f"SLICQ_LOGN={n}",)) for n in (11, 12, 13, 14)]
+SOURCES += [("kernels_large.cu", f"kernels_large_l{n}", (f"SLICQ_LOGN={n}",)) for n in (15, 16)]
+SOURCES += [("kernels_long.cu", "kernels_long", ()), ("kernels_complex.cu", "kernels_complex", ()),
+            ("kernels_coeff.cu", "kernels_coeff", ()), ("stream_exec.cpp", "stream_exec", ())]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v"]
@@ -33,12 +39,14 @@ def nvcc() -> str:
     return p
 
 
-def _compile(src: str, objdir: str = OBJ, extra=()) -> tuple[str, str]:
-    obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
-    cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(unit, objdir: str = OBJ, extra=()) -> tuple[str, str]:
+    src, name, defines = unit
+    obj = os.path.join(objdir, name + ".o")
+    cmd = [nvcc(), *ARCH, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-x", "cu", "-c",
+           os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        raise RuntimeError(f"nvcc failed for {name}:\n{r.stderr}")
     return obj, r.stderr
 
 

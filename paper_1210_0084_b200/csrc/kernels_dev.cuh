@@ -198,6 +198,16 @@ struct KArgs {
   // (x 1/2 on the plateaus, C15) at the filter offsets goff_k; per-bin term lists (CSR)
   const float *gw, *gdw;
   const uint32_t *lrow, *lent;
+  // fused kernels (kernels_fused.cuh)
+  const FChan *fch;     // channel descriptors in task order
+  const FTask *ftask;   // warp tasks (inverse: phase A first)
+  int nftask, nphase_a;
+  int fscr;             // per-warp scratch entries
+  const int2 *ovb;      // inverse: overflow bins (bin, first | count << 20)
+  int novb;
+  const int32_t *ovl;   // inverse: overflow slot lists
+  int nov;              // inverse: overflow slots per unit
+  int vec16;            // coefficient rows are 16-byte aligned (vector stores / loads)
 };
 
 
@@ -735,23 +745,23 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
 // MODE 0: sliCQ slice m (Tukey window, hop N, circular indices).  MODE 1: full-length
 // CQ-NSGT (Alg. 1): the frame is the whole signal x[0..2N) (zeros past
 // x_len), no window; one unit per row.
-template <int LOGN, int MODE = 0>
-__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_kernel(const KArgs a) {
+// F1 + F2 of unit u (row * nslices + local slice) into X[0..N].  TOSMEM = false: X goes to
+// Xo[0..N] in global memory (the staging row of the split design, or a ring slot);
+// TOSMEM = true: X stays in shared memory, spec[padi(k)] for k = 0..N.  htab: tr - 1 floats
+// of shared scratch.  LOADTW: stage the twiddle table (persistent callers do it once).
+template <int LOGN, int MODE, bool TOSMEM, bool LOADTW = true>
+__device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float2 *tw, float *htab,
+                                             int64_t u, float2 *Xo) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T;
-  extern __shared__ float4 smem4[];
-  float2 *spec = reinterpret_cast<float2 *>(smem4);
-  float2 *tw = spec + spec_entries<LOGN>();
-  float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());  // window transitions
   const int tid = threadIdx.x;
-  const int64_t ul = blockIdx.x;             // unit within the chunk
-  const int64_t u = a.unit0 + ul;
   const int64_t row = u / a.nslices;
   const int64_t mloc = u - row * a.nslices;
   const int64_t mg = a.slice0 + mloc;
 
   PHASE_INIT();
-  for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
+  if constexpr (LOADTW)
+    for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
   pdl_wait();  // the staging buffer may still be read by the previous chunk's kernel
 
   // ---- F1 + first radix pass straight from HBM: task j takes the frame pairs
@@ -862,13 +872,17 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
     pass_twiddle<N, 16, TASKS3, -1>(vB, jB, tw);
     dft<16, -1>(vA);
     dft<16, -1>(vB);
-    float2 *Xo = a.stage + ul * a.xs;
+    auto xst = [&](int k, float2 v) {
+      if constexpr (TOSMEM) spec[padi(k)] = v;
+      else SLICQ_XSTORE(Xo + k, v);
+    };
+    if constexpr (TOSMEM) __syncthreads();  // every pass-3 input read before X overwrites it
     auto r2c = [&](float2 zk, float2 zn, int k, bool mirror) {
       const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
       const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
       const float2 wO = cmul(tw_lookup(tw, k), O);  // e^{-i pi k/N} O
-      SLICQ_XSTORE(Xo + k, cadd(E, wO));
-      if (mirror) SLICQ_XSTORE(Xo + (N - k), csub(cconj(E), cconj(wO)));
+      xst(k, cadd(E, wO));
+      if (mirror) xst(N - k, csub(cconj(E), cconj(wO)));
     };
     // thread 0's tasks 0 and TASKS3/2 are their own mirrors: warp 0 packs their 32 bins
     // cooperatively, one bin per lane (X[k] = E + e^{-i pi k/N} O at each k; k = 0 also
@@ -888,8 +902,8 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
       const int kk = L < 16 ? TASKS3 * L : TASKS3 / 2 + TASKS3 * (L - 16);
       const float2 zk = svz[L], zn = svz[ib];
       if (L == 0) {  // X[0], X[N] from Z[0]
-        SLICQ_XSTORE(Xo, make_float2(zk.x + zk.y, 0.f));
-        SLICQ_XSTORE(Xo + N, make_float2(zk.x - zk.y, 0.f));
+        xst(0, make_float2(zk.x + zk.y, 0.f));
+        xst(N, make_float2(zk.x - zk.y, 0.f));
       } else {
         r2c(zk, zn, kk, false);
       }
@@ -923,12 +937,21 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
     PHASE_MARK(0, 3);
 
     // ---- X[0..N] -> staging (coalesced)
-    {
-      float2 *Xo = a.stage + ul * a.xs;
+    if constexpr (!TOSMEM) {
       for (int k = tid; k <= N; k += T) Xo[k] = spec[padi(k)];
     }
   }
   PHASE_MARK(0, 4);
+}
+
+template <int LOGN, int MODE = 0>
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_kernel(const KArgs a) {
+  extern __shared__ float4 smem4[];
+  float2 *spec = reinterpret_cast<float2 *>(smem4);
+  float2 *tw = spec + spec_entries<LOGN>();
+  float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());  // window transitions
+  fwd_spectrum<LOGN, MODE, false>(a, spec, tw, htab, a.unit0 + blockIdx.x,
+                                  a.stage + (int64_t)blockIdx.x * a.xs);
   pdl_trigger();
 }
 

@@ -13,6 +13,8 @@
 
 #define SLICQ_DEFINE_CHAN_KERNELS
 #include "kernels_dev.cuh"
+#include "kernels_fused.cuh"
+#include "kernels_ring.cuh"
 #include "kernels_large.cuh"
 #include "kernels_long_api.h"
 
@@ -598,7 +600,9 @@ int configure_kernels(slicq_plan *p) {
   cu = std::min<int64_t>(cu, 0x7fffffff);  // grid x dimension of the spectrum kernels
   cu = std::max<int64_t>(kc.tile, cu / kc.tile * kc.tile);
   kc.chunk_units = cu;
-  return SLICQ_OK;
+  int rc = configure_fused(p);
+  if (rc == SLICQ_OK) rc = configure_ring(p);
+  return rc;
 }
 
 int upload(slicq_plan *p) {
@@ -622,6 +626,8 @@ int upload(slicq_plan *p) {
       twM.push_back((float)std::sin(ang));
     }
   }
+  for (std::vector<FChan> *v : {&p->fchf, &p->fchi})  // fused: channel index -> twiddle table
+    for (FChan &f : *v) f.twoff = twoff[p->M[f.twoff]];
   std::vector<ChanDev> ch(K2);
   for (int k = 0; k < K2; ++k) {
     ChanDev &c = ch[k];
@@ -707,6 +713,17 @@ int upload(slicq_plan *p) {
       {p->lent.data(), sizeof(uint32_t) * p->lent.size(), 0},
       {p->cxf.data(), sizeof(uint2) * p->cxf.size(), 0},
       {p->cxs.data(), sizeof(uint2) * p->cxs.size(), 0},
+      {p->fchf.data(), sizeof(FChan) * p->fchf.size(), 0},
+      {p->fchi.data(), sizeof(FChan) * p->fchi.size(), 0},
+      {p->ftf.data(), sizeof(FTask) * p->ftf.size(), 0},
+      {p->fti.data(), sizeof(FTask) * p->fti.size(), 0},
+      {p->ovb.data(), sizeof(int2) * p->ovb.size(), 0},
+      {p->ovl.data(), sizeof(int32_t) * p->ovl.size(), 0},
+      {p->rband.data(), sizeof(RBand) * p->rband.size(), 0},
+      {p->rtask.data(), sizeof(RTask) * p->rtask.size(), 0},
+      {p->rfch.data(), sizeof(FChan) * p->rfch.size(), 0},
+      {p->rbtw.data(), sizeof(float) * p->rbtw.size(), 0},
+      {p->rround.data(), sizeof(int32_t) * p->rround.size(), 0},
   };
   size_t o = 0;
   for (Part &pt : parts) {
@@ -739,6 +756,17 @@ int upload(slicq_plan *p) {
   p->d.lent = reinterpret_cast<uint32_t *>(b + parts[13].off);
   p->d.cxf = reinterpret_cast<uint2 *>(b + parts[14].off);
   p->d.cxs = reinterpret_cast<uint2 *>(b + parts[15].off);
+  p->d.fchf = reinterpret_cast<FChan *>(b + parts[16].off);
+  p->d.fchi = reinterpret_cast<FChan *>(b + parts[17].off);
+  p->d.ftf = reinterpret_cast<FTask *>(b + parts[18].off);
+  p->d.fti = reinterpret_cast<FTask *>(b + parts[19].off);
+  p->d.ovb = reinterpret_cast<int2 *>(b + parts[20].off);
+  p->d.ovl = reinterpret_cast<int32_t *>(b + parts[21].off);
+  p->d.rband = reinterpret_cast<RBand *>(b + parts[22].off);
+  p->d.rtask = reinterpret_cast<RTask *>(b + parts[23].off);
+  p->d.rfch = reinterpret_cast<FChan *>(b + parts[24].off);
+  p->d.rbtw = reinterpret_cast<float2 *>(b + parts[25].off);
+  p->d.rround = reinterpret_cast<int32_t *>(b + parts[26].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
@@ -753,6 +781,7 @@ int upload(slicq_plan *p) {
     case 16: rc = large_set_attrs<16>(); break;
     default: rc = long_set_attrs(p->kc.logN, p->kc.lcls); break;
   }
+  if (rc == 0 && p->kc.fused) rc = fused_set_attrs(p);
   for (int v = 0; v < 2 * kVariants * 3 && rc == 0 && !p->kc.longmode; ++v)  // fwd, variant, mask
     rc = (int)allow_max_dyn_smem((const void *)chan_fn(v & 1, (v >> 1) % kVariants, v / (2 * kVariants)));
   if (rc != 0)
@@ -844,15 +873,25 @@ int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t
   const WsLayout w = ws_layout(p, nslices, batch);
   const int64_t chunks = (nslices * batch + w.chunk - 1) / w.chunk;
   if (p->kc.longmode) return (int)(chunks * (direction == 0 ? 3 : 4));
+  if ((p->kc.fused || p->kc.ring) && direction == 0)
+    return (int)((nslices * batch + 0x7ffffffe) / 0x7fffffff);
   int nchan = 0;
   for (int v = 0; v < 3; ++v) nchan += p->kc.voff[v + 1] > p->kc.voff[v];
   const int nspec = !p->kc.large ? 1 : direction == 0 ? 2 : 4;
   return (int)(chunks * (nchan + nspec));
 }
 
+// ring kernels: [ring slots][ready, done flags, error word][dev stats: 1024 CTAs x 4 u64]
+constexpr size_t kRingStatsBytes = 1024 * 4 * sizeof(unsigned long long);
+static size_t ring_ws_bytes(const slicq_plan *p) {
+  if (!p->kc.ring) return 0;
+  return align_up(sizeof(float2) * (size_t)p->kc.rR * p->kc.rslot) +
+         align_up(sizeof(unsigned) * (size_t)(2 * p->kc.rR + 4)) + kRingStatsBytes;
+}
+
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch) {
   if (!p->has_device) return 0;  // the layout depends on the device configuration
-  return ws_layout(p, nslices, batch).total;
+  return std::max(ws_layout(p, nslices, batch).total, ring_ws_bytes(p));
 }
 
 static KArgs base_args(const slicq_plan *p) {
@@ -954,6 +993,21 @@ static cudaError_t launch_spec(bool fwd, const slicq_plan *p, const KArgs &a, di
   return cudaErrorInvalidValue;
 }
 
+static cudaError_t launch_fused(bool fwd, const slicq_plan *p, const KArgs &a, dim3 grid,
+                                cudaStream_t s) {
+  switch (p->kc.logN) {
+#define CASE_(L)                                                                           \
+  case L:                                                                                  \
+    return fwd ? launch_fwd_fused<L>(a, grid, p->kc.fsmem_f, s, p->kc.pdl) : cudaErrorInvalidValue;
+    CASE_(11)
+    CASE_(12)
+    CASE_(13)
+    CASE_(14)
+#undef CASE_
+  }
+  return cudaErrorInvalidValue;
+}
+
 int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x_stride,
                    int64_t base_off, int64_t L, int wrap, int64_t slice0, int64_t nslices,
                    int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream,
@@ -962,7 +1016,8 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
   if (rc) return rc;
   if (nslices > 0x7fffffff) return set_error(SLICQ_ESHAPE, "too many slices");
   const WsLayout w = ws_layout(p, nslices, batch);
-  if (!ws || ws_bytes < w.total) return set_error(SLICQ_ESHAPE, "workspace too small");
+  if (!ws || ws_bytes < std::max(w.total, ring_ws_bytes(p)))
+    return set_error(SLICQ_ESHAPE, "workspace too small");
   if ((uintptr_t)ws % 16) return set_error(SLICQ_ESHAPE, "workspace must be 16-byte aligned");
   KArgs a = base_args(p);
   a.x = x;
@@ -986,6 +1041,66 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
       a.unit0 = u0;
       a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
       const cudaError_t e = long_forward(p->kc.logN, a, p->kc.lcls, s);
+      if (e != cudaSuccess)
+        return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
+    }
+    return SLICQ_OK;
+  }
+  if (p->kc.ring && mode == 0 && units <= 0x7fffffff) {  // ring kernel (kernels_ring.cuh)
+    a.vec16 = (reinterpret_cast<uintptr_t>(coeffs) % 16 == 0) ? 1 : 0;
+    a.unit0 = 0;
+    a.nunits = (int)units;
+    RArgs r{};
+    char *wb = static_cast<char *>(ws);
+    r.ring = reinterpret_cast<float2 *>(wb);
+    r.slot_entries = p->kc.rslot;
+    unsigned *flags = reinterpret_cast<unsigned *>(wb + align_up(sizeof(float2) * (size_t)p->kc.rR * p->kc.rslot));
+    r.ready = flags;
+    r.done = flags + p->kc.rR;
+    r.err = flags + 2 * p->kc.rR;
+    r.R = p->kc.rR;
+    r.nb = p->kc.rnb;
+    r.bt = p->kc.rbt;
+    r.band = p->d.rband;
+    r.task = p->d.rtask;
+    r.fch = p->d.rfch;
+    r.btw = p->d.rbtw;
+    r.round = p->d.rround;
+    r.xstride = p->kc.rxstride;
+    r.wmax = p->kc.rwmax;
+    r.twmax = p->kc.rtwmax;
+    r.iscr = p->kc.rfscr;
+    r.grp = p->kc.rgroup;
+    r.meta = p->kc.rmeta;
+    const size_t fl_bytes = align_up(sizeof(unsigned) * (size_t)(2 * p->kc.rR + 4));
+    r.qctr = reinterpret_cast<unsigned long long *>(flags + 2 * p->kc.rR + 2);
+    r.la = p->kc.rla;
+    r.ngrid = p->kc.rnspec;
+    r.stats = std::getenv("SLICQ_RING_STATS")
+                  ? reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(flags) + fl_bytes)
+                  : nullptr;
+    cudaError_t e = cudaMemsetAsync(flags, 0, fl_bytes + (r.stats ? kRingStatsBytes : 0), s);
+    if (e == cudaSuccess) {
+      switch (p->kc.logN) {
+        case 12: e = launch_fwd_ring<12>(a, r, p->kc.rsmem, s); break;
+        case 13: e = launch_fwd_ring<13>(a, r, p->kc.rsmem, s); break;
+        default: e = cudaErrorInvalidValue;
+      }
+    }
+    if (e != cudaSuccess)
+      return set_error(SLICQ_ECUDA, std::string("forward ring launch: ") + cudaGetErrorString(e));
+    return SLICQ_OK;
+  }
+  if (p->kc.fused && mode == 0) {  // one fused kernel: no staging (kernels_fused.cuh)
+    a.fch = p->d.fchf;
+    a.ftask = p->d.ftf;
+    a.nftask = p->kc.nftf;
+    a.fscr = p->kc.fscr;
+    a.vec16 = (reinterpret_cast<uintptr_t>(coeffs) % 16 == 0) ? 1 : 0;
+    for (int64_t u0 = 0; u0 < units; u0 += 0x7fffffff) {
+      a.unit0 = u0;
+      a.nunits = (int)std::min<int64_t>(0x7fffffff, units - u0);
+      const cudaError_t e = launch_fused(true, p, a, dim3((unsigned)a.nunits), s);
       if (e != cudaSuccess)
         return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
     }
@@ -1119,6 +1234,23 @@ int launch_overlap_add(float *y, int64_t y_stride, const float *spill, int64_t c
 }
 
 }  // namespace slicq
+
+// Debug only (not part of include/slicq.h): the ring kernels' configuration and the byte
+// offset of their dev statistics in the workspace (tools/ring_stats.py).
+extern "C" __attribute__((visibility("default"))) int slicq_debug_ring_info(const slicq_plan *p,
+                                                                           long long *out) {
+  if (!p || !p->kc.ring) return -1;
+  out[0] = p->kc.rR;
+  out[1] = p->kc.rslot;
+  out[2] = p->kc.rnb;
+  out[3] = p->kc.rq;
+  out[4] = p->kc.rbt;
+  out[5] = p->kc.rnspec;
+  out[6] = (long long)(slicq::align_up(sizeof(float2) * (size_t)p->kc.rR * p->kc.rslot) +
+                       slicq::align_up(sizeof(unsigned) * (size_t)(2 * p->kc.rR + 4)));
+  out[7] = (long long)p->kc.rsmem;
+  return 0;
+}
 
 // Debug only (not part of include/slicq.h): accumulated per-phase clock64 cycles of the
 // forward [0..15] and inverse [16..31] spectrum kernels, in a library built with

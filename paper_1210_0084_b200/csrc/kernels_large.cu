@@ -1,5 +1,8 @@
-#define SLICQ_LOGN 15
-// Large-slice kernels (2N = 2^(SLICQ_LOGN+1) >= 65536), see kernels_large.cuh.
+// Large-slice kernels (2N = 2^(SLICQ_LOGN+1) >= 65536), see kernels_large.cuh.  Compiled once
+// per size (build.py: -DSLICQ_LOGN=15, 16).
+#ifndef SLICQ_LOGN
+#error "compile with -DSLICQ_LOGN=<15|16>"
+#endif
 #include "kernels_large.cuh"
 
 namespace slicq {

@@ -1,7 +1,11 @@
-#define SLICQ_LOGN 12
-// Instantiation of the per-slice spectrum kernels for N = 2^SLICQ_LOGN (one translation
-// unit per size so that the sizes compile in parallel).
+// Instantiation of the per-slice spectrum kernels and the fused kernels for N = 2^SLICQ_LOGN.
+// Compiled once per size (build.py: -DSLICQ_LOGN=11..14, one object each, in parallel).
+#ifndef SLICQ_LOGN
+#error "compile with -DSLICQ_LOGN=<11..14>"
+#endif
 #include "kernels_dev.cuh"
+#include "kernels_fused.cuh"
+#include "kernels_ring.cuh"
 #include "kernels_long_api.h"
 
 namespace slicq {
@@ -54,6 +58,43 @@ cudaError_t launch_inv_spec<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, 
                       pdl);
   return launch_pdl(slicq_inv_spec_kernel<SLICQ_LOGN, 0>, a, grid, Big<SLICQ_LOGN>::T, smem, s, pdl);
 }
+
+template <>
+int fused_attrs<SLICQ_LOGN>() {
+  const void *fns[] = {(const void *)slicq_fwd_fused_kernel<SLICQ_LOGN>};
+  for (const void *f : fns) {
+    const cudaError_t e = allow_max_dyn_smem(f);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
+}
+
+template <>
+cudaError_t launch_fwd_fused<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s,
+                                         bool pdl) {
+  return launch_pdl(slicq_fwd_fused_kernel<SLICQ_LOGN>, a, grid, Big<SLICQ_LOGN>::T, smem, s, pdl);
+}
+
+#if SLICQ_LOGN == 12 || SLICQ_LOGN == 13
+template <>
+int ring_attrs<SLICQ_LOGN>() {
+  return (int)allow_max_dyn_smem((const void *)slicq_fwd_ring_kernel<SLICQ_LOGN>);
+}
+template <>
+cudaError_t launch_fwd_ring<SLICQ_LOGN>(const KArgs &a, const RArgs &r, size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)r.ngrid);
+  cfg.blockDim = dim3(RING_T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the roles wait on each other
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, slicq_fwd_ring_kernel<SLICQ_LOGN>, a, r);
+}
+#endif
 
 template <>
 int phase_times<SLICQ_LOGN>(unsigned long long *out32, int reset) {

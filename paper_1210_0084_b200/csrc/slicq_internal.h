@@ -46,6 +46,59 @@ struct PacketDev {
   int32_t ustride;  // scratch entries per unit (small: nch, big: nch * M1 * (M2 | 1))
 };
 
+// Fused kernels (kernels_fused.cuh): a channel as one warp task reads it (48 bytes, three
+// int4).  Coefficient n of channel k is sum_d y[d] w^{(d + lo) n}, y[d] = X(lo + d) g_k[d]
+// (d < L_k), w = e^{2 pi i / M_k}: the support is read contiguously and the rotation by lo
+// (the fold's j mod M_k, C5) becomes a shift of the four-step twiddle and of the second
+// step's input index.
+struct FChan {
+  int32_t lo;      // first bin of J_k (unwrapped, C5)
+  int32_t len;     // L_k
+  int32_t M;       // M_k
+  int32_t goff;    // offset of the channel's weights in gw / gdw
+  int32_t off;     // column offset in a coefficient row
+  int32_t twoff;   // offset of the e^{+2 pi i t / M_k} table
+  int32_t lo_mod;  // lo mod M_k in [0, M_k)
+  int32_t lom2;    // lo mod M2 (two-step tasks), else 0
+  int32_t d0, d1;  // synthesis: core terms d in [d0, d1) are added to the bin lo + d in place
+  int32_t ovoff;   // synthesis: overflow slot of the channel's first non-core term
+  int32_t flags;   // bit 0: support inside [0, N] (no mirrored bins)
+};
+// A warp task: nch channels of one length M = M1 * M2 (two-step) or M (small: one lane per
+// channel).  code = M1 | M2 << 8 | small << 16 | interior << 17.
+struct FTask {
+  int32_t code;
+  int32_t nch;
+  int32_t coff;    // first FChan of the task
+  uint32_t mags;   // ceil(2^16 / M2) | ceil(2^16 / M1) << 16: exact q / M for the task's q
+};
+
+// Ring kernels (kernels_ring.cuh).  A band: channels forming a contiguous run, the X bins
+// [blo, blo + bspan) they read, its tasks [task0, task0 + ntask), its weights (gw / gdw
+// [g0, g0 + ng)), twiddles (btw [tw0, tw0 + ntw)) and its two lists of 32-lane rounds
+// (phase 1: small tasks and two-step step 1; phase 2: two-step step 2).
+struct RBand {
+  int32_t blo, bspan;
+  int32_t task0, ntask;
+  int32_t g0, ng;
+  int32_t tw0, ntw;
+  int32_t r1off, nr1;   // rounds: [r1off, r1off + nr1) phase 1, [r2off, r2off + nr2) phase 2
+  int32_t r2off, nr2;   // (r1off, r2off multiples of 4; r2off = r1off + nr1 rounded up to 4)
+  int32_t f0, nf;       // the band's channel descriptors [f0, f0 + nf) of rfch
+  int32_t pad0, pad1;
+};
+// A task of a band: nch channels of one length, for all bt units of an item.
+// code = M1 | M2 << 8 | small << 16 | interior << 17 (small: M1 = M, M2 = 1); soff: the
+// task's offset (float2) in the item scratch.
+struct RTask {
+  int32_t code, nch, coff, soff;
+  // exact q / d = (q * mag) >> 16 for the task's q (mag = ceil(2^16 / d) <= 2^16):
+  uint32_t magPa;  // d = nch * M2 (small: nch)
+  uint32_t magM2;  // d = M2
+  uint32_t magPb;  // d = nch * M1
+  uint32_t magM1;  // d = M1
+};
+
 struct DeviceTables {
   ChanDev *chan = nullptr;
   PacketDev *packets = nullptr;
@@ -63,6 +116,15 @@ struct DeviceTables {
   uint32_t *lent = nullptr; // long mode: term index | conj << 31
   uint2 *cxf = nullptr;     // complex input, per full-layout column: source column, twiddle
   uint2 *cxs = nullptr;     // complex input, per stored column: mirror column, twiddle
+  FChan *fchf = nullptr, *fchi = nullptr;  // fused kernels: channels in forward / inverse task order
+  FTask *ftf = nullptr, *fti = nullptr;    // fused kernels: forward / inverse warp tasks
+  int2 *ovb = nullptr;      // fused inverse: bins with overflow terms (bin, first entry | count << 20)
+  int32_t *ovl = nullptr;   // fused inverse: overflow slots per such bin, plan order
+  RBand *rband = nullptr;   // ring kernels: bands
+  RTask *rtask = nullptr;   // ring kernels: band warp tasks
+  FChan *rfch = nullptr;    // ring kernels: channels (band-local weight / twiddle offsets)
+  float2 *rbtw = nullptr;   // ring kernels: per-band twiddle tables
+  int32_t *rround = nullptr; // ring kernels: per-band round lists (task << 16 | round)
   void *block = nullptr;    // single allocation holding all of the above
   cudaStream_t pipe[2] = {nullptr, nullptr};  // chunk pipelining (kc.pipe): two streams
   cudaEvent_t pev[3] = {nullptr, nullptr, nullptr};
@@ -91,6 +153,20 @@ struct KernelConfig {
   int64_t pipe_parts = 4;     // ... split into this many chunks
   bool longmode = false;      // sl_len 2^18..2^22: full-length CQ-NSGT only (kernels_long.cuh)
   kern::LongClasses lcls{};   // long mode: channel size classes (kernels_long_api.h)
+  // fused kernels (kernels_fused.cuh): one CTA per unit, no staging
+  bool fused = false;         // forward and inverse run the fused kernels
+  int nftf = 0, nfti = 0;     // forward / inverse warp tasks
+  int nphase_a = 0;           // inverse: tasks [0, nphase_a) are phase A (even channels)
+  int fscr = 0;               // per-warp scratch (float2 entries)
+  int nov = 0, novb = 0;      // inverse overflow slots per unit, bins with overflow terms
+  size_t fsmem_f = 0, fsmem_i = 0;  // dynamic shared memory of the fused kernels
+  // ring kernels (kernels_ring.cuh): one persistent cooperative launch per call
+  bool ring = false;
+  int rR = 0, rnspec = 0, rnchan = 0, rnb = 0, rq = 0, rbt = 0, rla = 0;
+  int rxstride = 0, rwmax = 0, rtwmax = 0, rfscr = 0;  // rfscr: item scratch (float2)
+  int rgroup = 1, rmeta = 0;  // batches per channel item; largest band metadata (bytes)
+  int64_t rslot = 0;          // float2 entries per ring slot
+  size_t rsmem = 0;           // dynamic shared memory of the ring kernel
 };
 
 }  // namespace slicq
@@ -132,6 +208,15 @@ struct slicq_plan {
   std::vector<uint32_t> lrow, lent;      // long mode per-bin term lists
   std::vector<int32_t> lm1;              // long mode: four-step factor of M_k > 26000 (else 0)
   std::vector<uint2> cxf, cxs;           // complex-input column maps (kernels_complex.cu)
+  std::vector<slicq::FChan> fchf, fchi;  // fused kernels: channel descriptors in task order
+  std::vector<slicq::FTask> ftf, fti;    // fused kernels: warp tasks
+  std::vector<int2> ovb;                 // fused inverse: overflow bins
+  std::vector<int32_t> ovl;              // fused inverse: overflow slot lists
+  std::vector<slicq::RBand> rband;       // ring kernels: bands
+  std::vector<slicq::RTask> rtask;       // ring kernels: band warp tasks
+  std::vector<slicq::FChan> rfch;        // ring kernels: channels in band task order
+  std::vector<float> rbtw;               // ring kernels: per-band twiddles (re, im)
+  std::vector<int32_t> rround;           // ring kernels: per-band round lists
   std::vector<int64_t> lsoff;            // long mode: staging scratch offset of those channels
 };
 
@@ -173,4 +258,8 @@ int launch_approx(const slicq_plan *ps, const slicq_plan *pl, const slicq_c32 *s
                   const slicq_c32 *c, int64_t batch, double *out, void *stream, int full = 0);
 size_t workspace_bytes(const slicq_plan *p, int64_t nslices, int64_t batch);
 int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t batch);
+// fused kernels (fused_host.cu)
+int configure_fused(slicq_plan *p);  // after configure_kernels: task tables, smem budgets
+int fused_set_attrs(const slicq_plan *p);
+int configure_ring(slicq_plan *p);   // after configure_fused: bands, tasks, ring sizing
 }  // namespace slicq
