@@ -11,14 +11,15 @@ pytestmark = pytest.mark.gpu
 
 def test_t7_runtime_linear_in_length():
     """the sliCQ costs O(L); log-log slope of forward + inverse time vs L in
-    [0.8, 1.15] once the GPU is filled (>= 2^25 samples = 4096 slices; smaller calls still
-    amortise launch and tail costs, and calls of >= 8192 slices are pipelined, so the
-    measured slope sits slightly below 1), and doubling the largest size at most
-    2.3 x the time."""
+    [0.85, 1.15].  The sizes (2^26 .. 2^28 samples, 8192 .. 32768
+    slices) all fill the GPU and all run the same chunk-pipelined launch sequence (calls of
+    >= 8192 slices, kernels_host.cu), so the fit measures the transform's own scaling rather
+    than the switch into pipelining that 2^25 -> 2^26 crosses; doubling the largest size at
+    most 2.3 x the time."""
     from paper_1210_0084_b200 import api
     from synth.configs import CONFIGS
     plan = api.plan_for_config(CONFIGS[4])
-    ns = [1 << 25, 1 << 26, 1 << 27]
+    ns = [1 << 26, 1 << 27, 1 << 28]
     ts = []
     for n in ns:
         x = torch.randn(1, n, device="cuda") * 0.1
@@ -38,7 +39,7 @@ def test_t7_runtime_linear_in_length():
         ts.append(best)
         del x, c, y
     slope = np.polyfit(np.log(ns), np.log(ts), 1)[0]
-    assert 0.8 <= slope <= 1.15, (slope, ts)
+    assert 0.85 <= slope <= 1.15, (slope, ts)
     assert 1.6 <= ts[-1] / ts[-2] <= 2.3, ts
 
 
