@@ -138,16 +138,26 @@ class Plan:
                     M=self.channel_lengths(), off=self.channel_offsets())
 
     # ------------------------------------------------------------ workspace
-    def workspace(self, nslices: int, batch: int, device=None, tag=None) -> torch.Tensor:
-        """Zero-initialised once, then reused (it carries the overlap-add pairing counters).
-        One workspace per (device, shape, tag): calls that may run concurrently use tags."""
+    _WS_CACHE = 8  # workspaces kept per plan (least recently used are dropped)
+
+    def workspace(self, nslices: int, batch: int, device=None, tag=None,
+                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Cached per (device, shape, stream, tag): calls on different streams get different
+        workspaces (the library resets the inverse's pairing counters at every call, so reuse
+        on one stream is safe); a non-current stream gets record_stream.  At most _WS_CACHE
+        workspaces are kept (least recently used dropped)."""
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-        key = (str(dev), nslices, batch, tag)
-        ws = self._ws.get(key)
+        sid = stream.cuda_stream if stream is not None else None
+        key = (str(dev), nslices, batch, sid, tag)
+        ws = self._ws.pop(key, None)
         if ws is None:
             nb = self.workspace_bytes(nslices, batch)
             ws = torch.zeros((nb + 15) // 16 * 4, dtype=torch.float32, device=dev)
-            self._ws[key] = ws
+            while len(self._ws) >= self._WS_CACHE:
+                self._ws.pop(next(iter(self._ws)))
+        self._ws[key] = ws  # (most recently used last)
+        if stream is not None and stream != torch.cuda.current_stream(dev):
+            ws.record_stream(stream)
         return ws
 
     # ------------------------------------------------------------ hot path
@@ -163,7 +173,7 @@ class Plan:
             out = torch.empty((B, S, self.coeffs_per_slice), dtype=torch.complex64, device=x.device)
         else:
             _check_tensor(out, torch.complex64, "out", (B, S, self.coeffs_per_slice))
-        ws = self.workspace(S, B, x.device)
+        ws = self.workspace(S, B, x.device, stream=stream)
         check(lib().slicq_forward(self._h, x.data_ptr(), n, B, out.data_ptr(), ws.data_ptr(),
                                   ws.numel() * 4, _stream_ptr(stream)), "slicq_forward")
         return out
@@ -183,7 +193,7 @@ class Plan:
             out = torch.empty((B, n), dtype=torch.float32, device=c.device)
         else:
             _check_tensor(out, torch.float32, "out", (B, n))
-        ws = self.workspace(S, B, c.device)
+        ws = self.workspace(S, B, c.device, stream=stream)
         if mask is not None:
             _check_tensor(mask, torch.float32, "mask", (B, S, self.coeffs_per_slice))
             check(lib().slicq_inverse_masked(self._h, c.data_ptr(), mask.data_ptr(),
@@ -269,6 +279,8 @@ class Plan:
         _check_tensor(c, torch.complex64, "coeffs", (B, self.coeffs_per_slice_full))
         if out is None:
             out = torch.empty((B, n), dtype=torch.complex64, device=c.device)
+        else:
+            _check_tensor(out, torch.complex64, "out", (B, n))
         ws = self._workspace_complex(1, B, n, c.device)
         check(lib().slicq_nsgt_inverse_complex(self._h, c.data_ptr(), n, B, out.data_ptr(),
                                                ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)),
@@ -287,7 +299,7 @@ class Plan:
             out = torch.empty((B, self.coeffs_per_slice), dtype=torch.complex64, device=x.device)
         else:
             _check_tensor(out, torch.complex64, "out", (B, self.coeffs_per_slice))
-        ws = self.workspace(1, B, x.device)
+        ws = self.workspace(1, B, x.device, stream=stream)
         check(lib().slicq_nsgt_forward(self._h, x.data_ptr(), n, B, out.data_ptr(), ws.data_ptr(),
                                        ws.numel() * 4, _stream_ptr(stream)), "slicq_nsgt_forward")
         return out
@@ -301,7 +313,9 @@ class Plan:
         _check_tensor(c, torch.complex64, "coeffs", (B, self.coeffs_per_slice))
         if out is None:
             out = torch.empty((B, n), dtype=torch.float32, device=c.device)
-        ws = self.workspace(1, B, c.device)
+        else:
+            _check_tensor(out, torch.float32, "out", (B, n))
+        ws = self.workspace(1, B, c.device, stream=stream)
         check(lib().slicq_nsgt_inverse(self._h, c.data_ptr(), n, B, out.data_ptr(), ws.data_ptr(),
                                        ws.numel() * 4, _stream_ptr(stream)), "slicq_nsgt_inverse")
         return out
@@ -320,7 +334,9 @@ class Plan:
         if out is None:
             out = torch.empty((B, nslices, self.coeffs_per_slice), dtype=torch.complex64,
                               device=x_local.device)
-        ws = self.workspace(nslices, B, x_local.device)
+        else:
+            _check_tensor(out, torch.complex64, "out", (B, nslices, self.coeffs_per_slice))
+        ws = self.workspace(nslices, B, x_local.device, stream=stream)
         check(lib().slicq_forward_range(self._h, x_local.data_ptr(), xl, x_local.stride(0), halo,
                                         slice0, nslices, total_slices, B, out.data_ptr(),
                                         ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)),
@@ -338,9 +354,13 @@ class Plan:
         _check_tensor(c_local, torch.complex64, "coeffs", (B, nslices, self.coeffs_per_slice))
         if y_local is None:
             y_local = torch.empty((B, nslices * self.N), dtype=torch.float32, device=c_local.device)
+        else:
+            _check_rows(y_local, torch.float32, "y_local", (B, nslices * self.N))
         if spill is None:
             spill = torch.empty((B, halo), dtype=torch.float32, device=c_local.device)
-        ws = self.workspace(nslices, B, c_local.device)
+        else:
+            _check_tensor(spill, torch.float32, "spill", (B, halo))
+        ws = self.workspace(nslices, B, c_local.device, stream=stream)
         check(lib().slicq_inverse_range(self._h, c_local.data_ptr(), slice0, nslices, total_slices,
                                         B, y_local.data_ptr(), y_local.stride(0), spill.data_ptr(),
                                         halo, ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)),
@@ -357,6 +377,19 @@ class Plan:
         assert spill.is_contiguous() and y_tail.stride(1) == 1
         check(lib().slicq_overlap_add(y_tail.data_ptr(), y_tail.stride(0), spill.data_ptr(), count,
                                       B, _stream_ptr(stream)), "slicq_overlap_add")
+
+
+def _check_rows(t: torch.Tensor, dtype, name: str, shape):
+    """A caller-provided [rows][cols] output whose rows may be strided (a view into a wider
+    buffer): CUDA, dtype, shape, unit stride along a row, non-overlapping rows."""
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.stride(1) != 1 or (t.shape[0] > 1 and t.stride(0) < t.shape[1]):
+        raise ValueError(f"{name} rows must be unit-stride and non-overlapping")
 
 
 def _check_tensor(t: torch.Tensor, dtype, name: str, shape=None):

@@ -29,9 +29,9 @@ class RangeBackend(Protocol):
 
     def num_slices(self, n: int) -> int: ...
 
-    def forward_range(self, x_local, halo, slice0, nslices, total_slices): ...
+    def forward_range(self, x_local, halo, slice0, nslices, total_slices, out=None): ...
 
-    def inverse_range(self, c_local, slice0, nslices, total_slices, halo): ...
+    def inverse_range(self, c_local, slice0, nslices, total_slices, halo, y_local=None): ...
 
     def overlap_add(self, y_tail, spill) -> None: ...
 
@@ -80,10 +80,19 @@ class SliceRangeShard:
             xl[:, self.halo:self.halo + hi - a] = x_full[:, a:hi].to(xl.device)
         return xl
 
-    def _p2p(self, send: torch.Tensor, dst: int, recv: torch.Tensor, src: int):
+    def _p2p_start(self, send: torch.Tensor, dst: int, recv: torch.Tensor, src: int):
+        """Post one grouped send/recv pair; returns the works (NCCL: work.wait() makes the
+        current stream wait for the transfer, the host does not block)."""
+        if self.world == 1:
+            recv.copy_(send)
+            return []
         ops = [dist.P2POp(dist.isend, send, self._g(dst), group=self.group),
                dist.P2POp(dist.irecv, recv, self._g(src), group=self.group)]
-        for w in dist.batch_isend_irecv(ops):
+        return dist.batch_isend_irecv(ops)
+
+    @staticmethod
+    def _wait(works):
+        for w in works:
             w.wait()
 
     def _g(self, r: int) -> int:
@@ -93,33 +102,70 @@ class SliceRangeShard:
         """Left halo <- last `halo` own samples of rank r-1 (rank G-1 for rank 0)."""
         h = self.halo
         tail = xl[:, -h:].contiguous()
-        if self.world == 1:
-            xl[:, :h] = tail
-            return
         head = torch.empty_like(tail)
-        self._p2p(tail, (self.rank + 1) % self.world, head, (self.rank - 1) % self.world)
+        self._wait(self._p2p_start(tail, (self.rank + 1) % self.world, head,
+                                   (self.rank - 1) % self.world))
         xl[:, :h] = head
 
     def exchange_spill(self, spill: torch.Tensor) -> torch.Tensor:
         """Send my left spill to rank r-1, receive rank r+1's spill (circularly)."""
-        if self.world == 1:
-            return spill
         recv = torch.empty_like(spill)
-        self._p2p(spill.contiguous(), (self.rank - 1) % self.world, recv,
-                  (self.rank + 1) % self.world)
+        self._wait(self._p2p_start(spill.contiguous(), (self.rank - 1) % self.world, recv,
+                                   (self.rank + 1) % self.world))
         return recv
 
     # ------------------------------------------------------------ transform
     def forward(self, xl: torch.Tensor) -> torch.Tensor:
-        """Coefficients of slices [s0, s1): [batch][ns][C]."""
-        self.exchange_halo(xl)
-        return self.b.forward_range(xl, self.halo, self.s0, self.ns, self.S)
+        """Coefficients of slices [s0, s1): [batch][ns][C].  The halo transfer is posted first
+        and runs while the interior slices [s0 + 1, s1) -- which read own samples only, since
+        the window reaches (N + tr)/2 - 1 < N samples left of a slice -- are transformed; the
+        boundary slice s0 goes last."""
+        h, N, B = self.halo, self.N, self.batch
+        tail = xl[:, -h:].contiguous()
+        head = torch.empty_like(tail)
+        works = self._p2p_start(tail, (self.rank + 1) % self.world, head,
+                                (self.rank - 1) % self.world)
+        views = B == 1  # [1][ns][C]: both slice ranges are contiguous views of one buffer
+        c = None
+        if views:
+            c = torch.empty((B, self.ns, self.b.C), dtype=torch.complex64, device=xl.device) \
+                if hasattr(self.b, "C") else None
+        ci = None
+        if self.ns > 1:  # interior: entry i of xl[:, N:] is sample (s0 + 1) N - h + i
+            ci = self.b.forward_range(xl[:, N:], h, self.s0 + 1, self.ns - 1, self.S,
+                                      out=c[:, 1:] if c is not None else None)
+        self._wait(works)
+        xl[:, :h] = head
+        cb = self.b.forward_range(xl[:, :h + N], h, self.s0, 1, self.S,
+                                  out=c[:, :1] if c is not None else None)
+        if c is not None:
+            return c
+        return cb if ci is None else torch.cat([cb, ci], dim=1)
 
     def inverse(self, c_local: torch.Tensor) -> torch.Tensor:
-        """Overlap-added output of samples [s0 N, s1 N): [batch][ns N]."""
-        y, spill = self.b.inverse_range(c_local, self.s0, self.ns, self.S, self.halo)
-        recv = self.exchange_spill(spill)
-        self.b.overlap_add(y[:, -self.halo:], recv)
+        """Overlap-added output of samples [s0 N, s1 N): [batch][ns N].  The boundary slice s0
+        is synthesised first so that its left spill travels to rank r-1 while the interior
+        slices are synthesised; the interior's own left spill lands on slice s0's tail, and
+        rank r+1's spill on this range's tail last."""
+        h, N = self.halo, self.N
+        rdt = torch.float64 if c_local.dtype == torch.complex128 else torch.float32
+        y = torch.empty((self.batch, self.ns * N), dtype=rdt, device=c_local.device)
+        cb = c_local[:, :1] if self.batch == 1 else c_local[:, :1].contiguous()
+        yb, spill0 = self.b.inverse_range(cb, self.s0, 1, self.S, h, y_local=y[:, :N])
+        if yb.data_ptr() != y.data_ptr():
+            y[:, :N] = yb
+        recv = torch.empty_like(spill0)
+        works = self._p2p_start(spill0.contiguous(), (self.rank - 1) % self.world, recv,
+                                (self.rank + 1) % self.world)
+        if self.ns > 1:
+            ci = c_local[:, 1:] if self.batch == 1 else c_local[:, 1:].contiguous()
+            yi, spill1 = self.b.inverse_range(ci, self.s0 + 1, self.ns - 1, self.S, h,
+                                              y_local=y[:, N:])
+            if yi.data_ptr() != y[:, N:].data_ptr():
+                y[:, N:] = yi
+            self.b.overlap_add(y[:, N - h:N], spill1)
+        self._wait(works)
+        self.b.overlap_add(y[:, -h:], recv)
         return y
 
     def gather_output(self, y_local: torch.Tensor) -> Optional[torch.Tensor]:
@@ -169,21 +215,25 @@ class BatchShard:
 
 
 class LibBackend:
-    """RangeBackend over libslicq.so (api.Plan)."""
+    """RangeBackend over libslicq.so (api.Plan).  The range calls take an even halo
+    (slicq_forward_range; slicq_halo = (N + tr)/2 is odd when tr = 2 mod 4), so the halo is
+    rounded up to even."""
 
     def __init__(self, plan):
         self.plan = plan
         self.N = plan.N
-        self.halo = plan.halo
+        self.C = plan.coeffs_per_slice
+        self.halo = plan.halo + (plan.halo & 1)
 
     def num_slices(self, n):
         return self.plan.num_slices(n)
 
-    def forward_range(self, x_local, halo, slice0, nslices, total_slices):
-        return self.plan.forward_range(x_local, halo, slice0, nslices, total_slices)
+    def forward_range(self, x_local, halo, slice0, nslices, total_slices, out=None):
+        return self.plan.forward_range(x_local, halo, slice0, nslices, total_slices, out=out)
 
-    def inverse_range(self, c_local, slice0, nslices, total_slices, halo):
-        return self.plan.inverse_range(c_local, slice0, nslices, total_slices, halo)
+    def inverse_range(self, c_local, slice0, nslices, total_slices, halo, y_local=None):
+        return self.plan.inverse_range(c_local, slice0, nslices, total_slices, halo,
+                                       y_local=y_local)
 
     def overlap_add(self, y_tail, spill):
         self.plan.overlap_add(y_tail, spill)

@@ -16,31 +16,42 @@ from oracle import cqplan
 from oracle import slicq as oslicq
 
 ARGS = (8000.0, 150.0, None, 6, 128, 16, 0)
+ARGS_TR2 = (8000.0, 150.0, None, 6, 128, 2, 0)  # tr = 2 mod 4: odd slicq_halo
 
 
 class OracleBackend:
     """RangeBackend with the oracle's fp64 range functions on CPU tensors."""
 
-    def __init__(self):
-        self.p = cqplan.make_plan(*ARGS)
+    def __init__(self, args=ARGS):
+        self.p = cqplan.make_plan(*args)
         self.N = self.p.N
-        self.halo = (self.p.N + self.p.tr) // 2
+        h = (self.p.N + self.p.tr) // 2
+        self.halo = h + (h & 1)  # as LibBackend: the range calls take an even halo
 
     def num_slices(self, n):
         return oslicq.num_slices(n, self.p.sl_len)
 
-    def forward_range(self, x_local, halo, slice0, nslices, total_slices):
-        out = [oslicq.forward_range(x_local[b].numpy(), halo, slice0, nslices, self.p)
-               for b in range(x_local.shape[0])]
-        return torch.from_numpy(np.stack(out))
+    def forward_range(self, x_local, halo, slice0, nslices, total_slices, out=None):
+        res = [oslicq.forward_range(x_local[b].contiguous().numpy(), halo, slice0, nslices,
+                                    self.p) for b in range(x_local.shape[0])]
+        res = torch.from_numpy(np.stack(res))
+        if out is not None:
+            out.copy_(res)
+            return out
+        return res
 
-    def inverse_range(self, c_local, slice0, nslices, total_slices, halo):
+    def inverse_range(self, c_local, slice0, nslices, total_slices, halo, y_local=None):
         ys, sps = [], []
         for b in range(c_local.shape[0]):
-            y, sp = oslicq.inverse_range(c_local[b].numpy(), slice0, nslices, self.p, halo)
+            y, sp = oslicq.inverse_range(c_local[b].contiguous().numpy(), slice0, nslices,
+                                         self.p, halo)
             ys.append(y)
             sps.append(sp)
-        return torch.from_numpy(np.stack(ys)), torch.from_numpy(np.stack(sps))
+        y = torch.from_numpy(np.stack(ys))
+        if y_local is not None:
+            y_local.copy_(y)
+            y = y_local
+        return y, torch.from_numpy(np.stack(sps))
 
     def overlap_add(self, y_tail, spill):
         y_tail += spill
@@ -54,13 +65,13 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, n, q):
+def _worker(rank, world, port, n, q, args=ARGS):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1210_0084_b200.dist import SliceRangeShard
-        be = OracleBackend()
+        be = OracleBackend(args)
         rng = np.random.default_rng(123)
         x = torch.from_numpy(rng.standard_normal((2, n)))
         sh = SliceRangeShard(be, n, batch=2)
@@ -79,19 +90,21 @@ def _worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, 1500), (3, 1234), (2, 128)])
-def test_sharded_equals_unsharded(world, n):
+@pytest.mark.parametrize("world,n,args", [(2, 1500, ARGS), (3, 1234, ARGS), (2, 128, ARGS),
+                                         (2, 1500, ARGS_TR2), (3, 700, ARGS_TR2)])
+def test_sharded_equals_unsharded(world, n, args):
+    """Includes tr = 2 mod 4 (odd (N + tr)/2, rounded up to an even halo like LibBackend)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, args)) for r in range(world)]
     for p in procs:
         p.start()
     y, c = q.get(timeout=180)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    p = cqplan.make_plan(*ARGS)
+    p = cqplan.make_plan(*args)
     rng = np.random.default_rng(123)
     x = rng.standard_normal((2, n))
     c_ref = oslicq.forward(x, p)

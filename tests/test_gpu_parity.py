@@ -36,18 +36,19 @@ def slice_errors(c_gpu: np.ndarray, c_ref: np.ndarray) -> np.ndarray:
 
 def channel_errors(c_gpu: np.ndarray, c_ref: np.ndarray, off: np.ndarray) -> np.ndarray:
     """C17 per channel ("What's weak" 6): for every slice and stored channel k,
-    ||c_gpu_k - c_ref_k|| / ||c_ref_k||; channels whose reference norm is below 1e-3 x the
-    slice's RMS channel norm are judged absolutely against that RMS (fp32 transform noise
-    spreads ~eps ||X|| over all bins, so a near-empty channel has no meaningful relative
-    error -- the same floor idea as C17's near-silent slices)."""
+    ||c_gpu_k - c_ref_k|| / max(||c_ref_k||, RMS), RMS = the slice's RMS channel norm.  A
+    channel at or above the typical channel's energy is held to 1e-5 relative; a weaker one
+    to 1e-5 of the typical channel's norm (fp32 transform noise spreads ~eps ||X|| over all
+    bins, so a near-empty channel has no meaningful relative error -- the same floor idea as
+    C17's near-silent slices).  A wrong channel still fails unless its whole norm is below
+    1e-5 RMS."""
     c_gpu = c_gpu.astype(np.complex128).reshape(-1, c_ref.shape[-1])
     c_ref = c_ref.reshape(-1, c_ref.shape[-1])
     K2 = len(off) - 1
     nr = np.stack([np.linalg.norm(c_ref[:, off[k]:off[k + 1]], axis=1) for k in range(K2)], 1)
     er = np.stack([np.linalg.norm((c_gpu - c_ref)[:, off[k]:off[k + 1]], axis=1) for k in range(K2)], 1)
     rms = np.sqrt(np.mean(nr ** 2, axis=1, keepdims=True))
-    floor = 1e-3 * rms
-    return np.where(nr >= floor, er / np.maximum(nr, 1e-300), er / np.maximum(rms, 1e-300))
+    return er / np.maximum(np.maximum(nr, rms), 1e-300)
 
 
 def rel(a, b):
