@@ -451,6 +451,23 @@ def run_gpu(args, cfg):
         dist.destroy_process_group()
 
 
+def torchrun_cmd(argv, ngpus: int, port: int):
+    """The command that re-launches this script with one process per GPU (torchrun, rendezvous
+    on 127.0.0.1), for `--gpus N > 1` started without a launcher (no WORLD_SIZE)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={ngpus}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__), *argv]
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -463,6 +480,13 @@ def main():
     ap.add_argument("--force-shard", action="store_true",
                     help="run the multi-GPU slice-range code path even at N=1 (testing)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (rank 0 prints the JSON line)
+        import subprocess
+        sys.exit(subprocess.call(torchrun_cmd(sys.argv[1:], args.gpus, _free_port())))
+    _, world, _ = _env_rank()
+    if args.gpus > 1 and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     args.warmup = max(args.warmup, 3) if args.impl == "cuda" else args.warmup
     from synth.configs import CONFIGS
     cfg = CONFIGS[args.config]

@@ -303,7 +303,9 @@ SLICQ_API int slicq_approx_error_complex(const slicq_plan *ps, const slicq_plan 
  *   floats) where x_local[i] is global sample slice0*N - halo + i; the caller places the
  *   left neighbour's samples (circularly wrapped for slice0 = 0) in the first
  *   `halo` entries and zeros for padding positions >= n.  halo must be even and
- *   >= slicq_halo(p) - 1; positions outside [0, x_len) read as 0.
+ *   >= slicq_halo(p) - 1; slicq_halo(p) = (N + tr)/2 is itself odd when tr = 2 mod 4, so
+ *   callers use slicq_halo(p) rounded up to even (paper_1210_0084_b200/dist.py LibBackend);
+ *   positions outside [0, x_len) read as 0.
  *   coeffs_local: [batch][nslices][C]; ws as for slicq_forward with S = nslices.
  * slicq_inverse_range: y_local [batch][nslices*N] (row stride y_stride) receives the
  *   overlap-added output of samples [slice0*N, (slice0+nslices)*N) from these slices
@@ -338,8 +340,9 @@ SLICQ_API int slicq_overlap_add(float *y, int64_t y_stride, const float *spill, 
  *     slice0 + nslices) and the stream its device work must be enqueued on (in-place
  *     coefficient processing, e.g. masking); a nonzero return aborts with SLICQ_EINVAL
  *   ws  device, >= slicq_process_host_workspace_bytes(p, n, batch, pieces) bytes,
- *       256-byte aligned, zero-filled before its first use (a ring of 4 range buffers;
- *       its size does not grow with n beyond one range)
+ *       256-byte aligned (a ring of 4 range buffers; its size does not grow with n beyond
+ *       one range).  No initialisation is needed: every inverse call resets its own
+ *       overlap-add pairing counters.
  * Asynchronous with respect to the host: synchronise `stream` before reading y_host.
  * One call per workspace at a time. */
 typedef int (*slicq_coeff_fn)(void *user, slicq_c32 *coeffs, int64_t slice0, int64_t nslices,

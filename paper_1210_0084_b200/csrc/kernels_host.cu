@@ -845,26 +845,35 @@ WsLayout ws_layout(const slicq_plan *p, int64_t nslices, int64_t batch) {
 struct Pipe {
   const slicq_plan *p;
   cudaStream_t s;
-  bool on;
+  bool on, joined = false;
+  cudaError_t err = cudaSuccess;    // first failure of the fork / join
   std::unique_lock<std::mutex> lk;  // held from the fork to the join (shared streams / events)
   Pipe(const slicq_plan *p_, cudaStream_t s_, const WsLayout &w)
       : p(p_), s(s_), on(w.pipe) {
     if (!on) return;
     lk = std::unique_lock<std::mutex>(p->pipe_mu);
-    cudaEventRecord(p->d.pev[0], s);
-    cudaStreamWaitEvent(p->d.pipe[0], p->d.pev[0], 0);
-    cudaStreamWaitEvent(p->d.pipe[1], p->d.pev[0], 0);
+    note(cudaEventRecord(p->d.pev[0], s));
+    note(cudaStreamWaitEvent(p->d.pipe[0], p->d.pev[0], 0));
+    note(cudaStreamWaitEvent(p->d.pipe[1], p->d.pev[0], 0));
+  }
+  // every exit path (including a launch failure part-way) joins the plan streams back into
+  // the caller's stream, so the caller never reuses buffers that queued chunks still use
+  ~Pipe() { join(); }
+  void note(cudaError_t e) {
+    if (err == cudaSuccess && e != cudaSuccess) err = e;
   }
   cudaStream_t stream(int64_t i) const { return on ? p->d.pipe[i & 1] : s; }
   float2 *stage(float2 *base, int64_t i, int64_t chunk, int64_t row) const {
     return on ? base + (i & 1) * chunk * row : base;
   }
-  void join() {
-    if (!on) return;
-    cudaEventRecord(p->d.pev[1], p->d.pipe[0]);
-    cudaEventRecord(p->d.pev[2], p->d.pipe[1]);
-    cudaStreamWaitEvent(s, p->d.pev[1], 0);
-    cudaStreamWaitEvent(s, p->d.pev[2], 0);
+  cudaError_t join() {
+    if (!on || joined) return err;
+    joined = true;
+    note(cudaEventRecord(p->d.pev[1], p->d.pipe[0]));
+    note(cudaEventRecord(p->d.pev[2], p->d.pipe[1]));
+    note(cudaStreamWaitEvent(s, p->d.pev[1], 0));
+    note(cudaStreamWaitEvent(s, p->d.pev[2], 0));
+    return err;
   }
 };
 }  // namespace
@@ -1107,6 +1116,8 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     return SLICQ_OK;
   }
   Pipe pp(p, s, w);
+  if (pp.err != cudaSuccess)
+    return set_error(SLICQ_ECUDA, std::string("stream fork: ") + cudaGetErrorString(pp.err));
   float2 *stage0 = a.stage;
   for (int64_t u0 = 0, i = 0; u0 < units; u0 += w.chunk, ++i) {
     a.unit0 = u0;
@@ -1120,7 +1131,8 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
   }
-  pp.join();
+  if (pp.join() != cudaSuccess)
+    return set_error(SLICQ_ECUDA, std::string("stream join: ") + cudaGetErrorString(pp.err));
   return SLICQ_OK;
 }
 
@@ -1182,6 +1194,8 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     return SLICQ_OK;
   }
   Pipe pp(p, s, w);
+  if (pp.err != cudaSuccess)
+    return set_error(SLICQ_ECUDA, std::string("stream fork: ") + cudaGetErrorString(pp.err));
   float2 *stage0 = a.stage;
   for (int64_t u0 = 0, i = 0; u0 < units; u0 += w.chunk, ++i) {
     a.unit0 = u0;
@@ -1196,7 +1210,8 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
   }
-  pp.join();
+  if (pp.join() != cudaSuccess)
+    return set_error(SLICQ_ECUDA, std::string("stream join: ") + cudaGetErrorString(pp.err));
   return SLICQ_OK;
 }
 

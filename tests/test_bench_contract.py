@@ -32,6 +32,26 @@ def test_reference_arm_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
 
 
+def test_gpus_flag_relaunches_one_process_per_gpu():
+    """`bench.py --gpus N` without a launcher re-executes itself under torchrun with N
+    processes on one node (rendezvous on 127.0.0.1), forwarding every argument."""
+    sys.path.insert(0, ROOT)
+    import bench
+    cmd = bench.torchrun_cmd(["--gpus", "8", "--steps", "3"], 8, 29511)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=8" in cmd and "--nnodes=1" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "8", "--steps", "3"] and cmd[-5].endswith("bench.py")
+
+
+def test_reference_arm_under_launcher_world_2():
+    """The reference arm launched with --gpus 2 (re-launched under torchrun): rank 0 alone runs
+    and prints one line with n_gpus = 2; the other rank exits 0 without work."""
+    d = _run(["--impl", "reference", "--config", "1", "--steps", "1", "--warmup", "0",
+              "--gpus", "2"], 900)
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
 @pytest.mark.gpu
 def test_cuda_arm_line():
     d = _run(["--config", "1", "--steps", "5", "--warmup", "3"], 1200)
