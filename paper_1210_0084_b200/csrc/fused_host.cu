@@ -131,8 +131,11 @@ RShape ring_shape(int M, int G, int bt, int scr_cap) {
 
 int configure_fused(slicq_plan *p) {
   KernelConfig &kc = p->kc;
-  kc.fused = false;
-  if (env_i("SLICQ_FUSED", 0) == 0) return SLICQ_OK;  // opt-in (measured slower)
+  kc.fused = kc.ftables = false;
+  // the fused per-slice forward (opt-in: measured slower), the ring kernel
+  // (opt-in) and the band-major channel kernel share these tables
+  const bool want = env_i("SLICQ_FUSED", 0) || env_i("SLICQ_RING", 0) || env_i("SLICQ_BAND", 0);
+  if (!want) return SLICQ_OK;
   if (kc.longmode || kc.large || kc.logN < 11 || kc.logN > 14 || !p->painless) return SLICQ_OK;
   const int K2 = p->K + 2;
   const int N = (int)p->N, N2 = 2 * N;
@@ -294,7 +297,8 @@ int configure_fused(slicq_plan *p) {
   }
   if (fs > 227 * 1024) return SLICQ_OK;
   kc.fsmem_f = fs;
-  kc.fused = true;
+  kc.ftables = true;
+  kc.fused = env_i("SLICQ_FUSED", 0) != 0;
   return SLICQ_OK;
 }
 
@@ -307,7 +311,8 @@ int configure_ring(slicq_plan *p) {
     if (dbg) std::fprintf(stderr, "ring off: %s\n", why);
     return SLICQ_OK;
   };
-  if (env_i("SLICQ_RING", 1) == 0 || !kc.fused) return off("disabled / not fused");
+  kc.band = false;
+  if (!kc.ftables) return off("no fused tables");
   if (kc.logN != 12 && kc.logN != 13) return off("2N");  // spectrum role: 256-thread CTAs
   const int K2 = p->K + 2;
   const int N = (int)p->N, N2 = 2 * N;
@@ -504,11 +509,13 @@ int configure_ring(slicq_plan *p) {
   if (dbg)
     std::fprintf(stderr, "ring smem: meta %d w+tw %zu xset %zu scr %zu chan %zu total %zu (xstride %d iscr %d)\n",
                  kc.rmeta, L.set[0] - L.w, L.set[1] - L.set[0], L.total - L.scr, L.total, kc.rsmem, kc.rxstride, kc.rfscr);
+  kc.rchsmem = L.total;
+  if (kc.rchsmem <= 112 * 1024) kc.band = env_i("SLICQ_BAND", 0) != 0;
   if (kc.rsmem > 112 * 1024) return off("shared memory");  // two CTAs per SM
   const int64_t ring_mb = env_i("SLICQ_RING_MB", 32);
   const int64_t need = (int64_t)(la + 2) * bt * grp + 2 * (int64_t)kc.rnspec;
   kc.rR = (int)std::max<int64_t>(need, (ring_mb << 20) / (kc.rslot * 8));
-  kc.ring = true;
+  kc.ring = env_i("SLICQ_RING", 0) != 0;
   if (env_i("SLICQ_DEBUG", 0))
     std::fprintf(stderr, "ring: nb=%d la=%d bt=%d grid=%d xstride=%d wmax=%d twmax=%d fscr=%d "
                          "smem=%zu R=%d tasks=%zu\n",
@@ -536,7 +543,7 @@ int fused_set_attrs(const slicq_plan *p) {
     case 13: rc = fused_attrs<13>(); break;
     case 14: rc = fused_attrs<14>(); break;
   }
-  if (rc == 0 && p->kc.ring) {
+  if (rc == 0 && (p->kc.ring || p->kc.band)) {
     if (p->kc.logN == 12) rc = ring_attrs<12>();
     if (p->kc.logN == 13) rc = ring_attrs<13>();
   }

@@ -168,6 +168,7 @@ struct KArgs {
   int64_t unit0;
   int nunits;
   int tile;       // units per channel-kernel tile
+  int stiles;     // channel kernels: tiles per super-tile (0: the whole chunk)
   // coefficients
   int64_t C;
   float2 *coef_out;
@@ -588,8 +589,15 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArg
   // code at the same time (instruction-cache locality) and the packet's tables stay hot
   const int ntiles = (a.nunits + a.tile - 1) / a.tile;
   const int nitems = a.npackets * ntiles;
+  const int sts = a.stiles > 0 ? a.stiles : ntiles;  // tiles per super-tile
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int pk = item / ntiles;
+    // packet-major inside super-tiles of sts tiles: a super-tile's staged spectra stay in L2
+    // while its packets pass over them (each packet's code still runs sts tiles in a row)
+    const int per_st = a.npackets * sts;
+    const int st = item / per_st, rem = item - st * per_st;
+    const int st_n = min(sts, ntiles - st * sts);  // tiles in this (possibly last) super-tile
+    const int pk = rem / st_n;
+    const int tile = st * sts + (rem - pk * st_n);
     float2 *scr = reinterpret_cast<float2 *>(smem4) + warp * a.scr;
     const PacketDev P = a.packets[pk];
     const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
@@ -603,7 +611,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArg
     const int c_twoff = __ldg(&a.chan[ck].twoff);
     const uint2 *ent = a.fent + P.fent_off;
     const int ne = small ? 0 : r * m1 * m2;
-    const int u_lo = (item % ntiles) * a.tile;
+    const int u_lo = tile * a.tile;
     const int u_hi = min(a.nunits, u_lo + a.tile);
     const int ntask = (u_hi - u_lo + nu - 1) / nu;
     for (int t = warp; t < ntask; t += NW) {
@@ -664,8 +672,15 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
   // code at the same time (instruction-cache locality) and the packet's tables stay hot
   const int ntiles = (a.nunits + a.tile - 1) / a.tile;
   const int nitems = a.npackets * ntiles;
+  const int sts = a.stiles > 0 ? a.stiles : ntiles;  // tiles per super-tile
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int pk = item / ntiles;
+    // packet-major inside super-tiles of sts tiles: a super-tile's staged spectra stay in L2
+    // while its packets pass over them (each packet's code still runs sts tiles in a row)
+    const int per_st = a.npackets * sts;
+    const int st = item / per_st, rem = item - st * per_st;
+    const int st_n = min(sts, ntiles - st * sts);  // tiles in this (possibly last) super-tile
+    const int pk = rem / st_n;
+    const int tile = st * sts + (rem - pk * st_n);
     float2 *scr = reinterpret_cast<float2 *>(smem4) + warp * a.scr;
     const PacketDev P = a.packets[pk];
     const int m1 = P.m1m2 & 255, m2 = (P.m1m2 >> 8) & 255;
@@ -679,7 +694,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
     const int c_twoff = __ldg(&a.chan[ck].twoff);
     const uint2 *ent = a.ient + P.ient_off;
     const int ne = P.nz;  // entries (channel term -> staging slot) of the packet
-    const int u_lo = (item % ntiles) * a.tile;
+    const int u_lo = tile * a.tile;
     const int u_hi = min(a.nunits, u_lo + a.tile);
     const int cbase = __shfl_sync(FULL, c_off0, 0);
     const int clen = __shfl_sync(FULL, c_off0, r - 1) - cbase + m1 * m2;

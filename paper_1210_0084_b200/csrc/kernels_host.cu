@@ -585,6 +585,7 @@ int configure_kernels(slicq_plan *p) {
     kc.zs += p->N;
   }
   kc.tile = (int)std::max<int64_t>(1, env_int("SLICQ_TILE", 128));
+  kc.stiles = (int)std::max<int64_t>(0, env_int("SLICQ_STILES", 0));
   kc.chan_per_sm = (int)env_int("SLICQ_CHAN_PER_SM", 0);  // dev override: 0 = occupancy
   // staging is sized for one chunk of units; calls with more units run chunk by chunk
   // (each chunk costs kernel tails, so the default budget keeps every BASELINE config in a
@@ -781,7 +782,7 @@ int upload(slicq_plan *p) {
     case 16: rc = large_set_attrs<16>(); break;
     default: rc = long_set_attrs(p->kc.logN, p->kc.lcls); break;
   }
-  if (rc == 0 && p->kc.fused) rc = fused_set_attrs(p);
+  if (rc == 0 && p->kc.ftables) rc = fused_set_attrs(p);
   for (int v = 0; v < 2 * kVariants * 3 && rc == 0 && !p->kc.longmode; ++v)  // fwd, variant, mask
     rc = (int)allow_max_dyn_smem((const void *)chan_fn(v & 1, (v >> 1) % kVariants, v / (2 * kVariants)));
   if (rc != 0)
@@ -884,6 +885,7 @@ int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t
   if (p->kc.longmode) return (int)(chunks * (direction == 0 ? 3 : 4));
   if ((p->kc.fused || p->kc.ring) && direction == 0)
     return (int)((nslices * batch + 0x7ffffffe) / 0x7fffffff);
+  if (p->kc.band && direction == 0 && !p->kc.large) return (int)(chunks * 2);
   int nchan = 0;
   for (int v = 0; v < 3; ++v) nchan += p->kc.voff[v + 1] > p->kc.voff[v];
   const int nspec = !p->kc.large ? 1 : direction == 0 ? 2 : 4;
@@ -923,6 +925,7 @@ static KArgs base_args(const slicq_plan *p) {
   a.xs = p->kc.xs;
   a.zs = p->kc.zs;
   a.tile = p->kc.tile;
+  a.stiles = p->kc.stiles;
   a.gw = p->d.gw;
   a.gdw = p->d.gdw;
   a.lrow = p->d.lrow;
@@ -1017,6 +1020,26 @@ static cudaError_t launch_fused(bool fwd, const slicq_plan *p, const KArgs &a, d
   return cudaErrorInvalidValue;
 }
 
+// the band / ring tables of RArgs (the ring buffers and flags are set by the ring launch)
+static RArgs band_args(const slicq_plan *p) {
+  RArgs r{};
+  r.nb = p->kc.rnb;
+  r.bt = p->kc.rbt;
+  r.la = p->kc.rla;
+  r.grp = p->kc.rgroup;
+  r.meta = p->kc.rmeta;
+  r.band = p->d.rband;
+  r.task = p->d.rtask;
+  r.fch = p->d.rfch;
+  r.btw = p->d.rbtw;
+  r.round = p->d.rround;
+  r.xstride = p->kc.rxstride;
+  r.wmax = p->kc.rwmax;
+  r.twmax = p->kc.rtwmax;
+  r.iscr = p->kc.rfscr;
+  return r;
+}
+
 int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x_stride,
                    int64_t base_off, int64_t L, int wrap, int64_t slice0, int64_t nslices,
                    int64_t batch, slicq_c32 *coeffs, void *ws, size_t ws_bytes, void *stream,
@@ -1059,7 +1082,7 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     a.vec16 = (reinterpret_cast<uintptr_t>(coeffs) % 16 == 0) ? 1 : 0;
     a.unit0 = 0;
     a.nunits = (int)units;
-    RArgs r{};
+    RArgs r = band_args(p);
     char *wb = static_cast<char *>(ws);
     r.ring = reinterpret_cast<float2 *>(wb);
     r.slot_entries = p->kc.rslot;
@@ -1068,19 +1091,8 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     r.done = flags + p->kc.rR;
     r.err = flags + 2 * p->kc.rR;
     r.R = p->kc.rR;
-    r.nb = p->kc.rnb;
-    r.bt = p->kc.rbt;
-    r.band = p->d.rband;
-    r.task = p->d.rtask;
-    r.fch = p->d.rfch;
-    r.btw = p->d.rbtw;
-    r.round = p->d.rround;
-    r.xstride = p->kc.rxstride;
-    r.wmax = p->kc.rwmax;
-    r.twmax = p->kc.rtwmax;
-    r.iscr = p->kc.rfscr;
-    r.grp = p->kc.rgroup;
-    r.meta = p->kc.rmeta;
+    r.qctr = reinterpret_cast<unsigned long long *>(flags + 2 * p->kc.rR + 2);
+    r.ngrid = p->kc.rnspec;
     const size_t fl_bytes = align_up(sizeof(unsigned) * (size_t)(2 * p->kc.rR + 4));
     r.qctr = reinterpret_cast<unsigned long long *>(flags + 2 * p->kc.rR + 2);
     r.la = p->kc.rla;
@@ -1127,7 +1139,28 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     cudaError_t e = !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), st, mode)
                     : p->kc.logN == 15 ? large_forward<15>(a, st, mode)
                                        : large_forward<16>(a, st, mode);
-    if (e == cudaSuccess) e = launch_chan(true, p, a, st);
+    if (e == cudaSuccess && p->kc.band && !p->kc.large) {
+      // band-major channel kernel (kernels_ring.cuh): claim counter per chunk in the
+      // (forward-unused) pairing-counter area of the workspace
+      RArgs r = band_args(p);
+      r.qctr = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + w.cnt) + i;
+      a.vec16 = (reinterpret_cast<uintptr_t>(coeffs) % 16 == 0) ? 1 : 0;
+      e = cudaMemsetAsync(r.qctr, 0, sizeof(unsigned long long), st);
+      if (e == cudaSuccess) {
+        static int nsm = 0;
+        if (!nsm) {
+          int dev = 0;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+          if (nsm <= 0) nsm = 148;
+        }
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * nsm, a.nunits));
+        e = p->kc.logN == 12 ? launch_fwd_band<12>(a, r, p->kc.rchsmem, grid, st, p->kc.pdl)
+            : launch_fwd_band<13>(a, r, p->kc.rchsmem, grid, st, p->kc.pdl);
+      }
+    } else if (e == cudaSuccess) {
+      e = launch_chan(true, p, a, st);
+    }
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
   }

@@ -386,6 +386,152 @@ __device__ __forceinline__ void x_load(const KArgs &a, const RArgs &r, const RBa
   }
 }
 
+// (warp 0) the band's X bins of batch t from the split design's staging (unit u of the chunk
+// at a.stage + u * a.xs; the spectrum kernel has completed: no flags)
+__device__ __forceinline__ void x_load_staged(const KArgs &a, const RArgs &r, const RBand &B, int t,
+                                              float2 *xb, uint64_t *bar, int lane) {
+  const int64_t u0 = (int64_t)t * r.bt;
+  const int nsb = (int)min((int64_t)r.bt, (int64_t)a.nunits - u0);
+  const unsigned xbytes = (unsigned)B.bspan * 8u;
+  if (lane == 0) mbar_arrive_tx(bar, xbytes * (unsigned)nsb);
+  __syncwarp();
+  for (int i = lane; i < nsb; i += 32)
+    bulk_g2s(xb + (int64_t)i * r.xstride, a.stage + (u0 + i) * a.xs + B.blo, xbytes, bar);
+}
+
+// One channel item: band p1 for batches [p0 grp, p0 grp + grp) of bt units (F3 - F5).  The
+// band's tables land once; the X bins of batch t + 1 land while batch t computes.  STAGED:
+// X comes from the split design's staging buffer, else from the ring (ready flags; the slots
+// are released once a batch has landed).
+template <int LOGN, bool STAGED>
+__device__ __forceinline__ void chan_item(const KArgs &a, const RArgs &r, int p0, int p1, char *uni,
+                                          const ChanSmem &L, uint64_t *bar, unsigned *uses,
+                                          int *s_round, uint64_t &t_wait) {
+  constexpr int N = Big<LOGN>::N;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int U = a.nunits;
+  const int NB = (U + r.bt - 1) / r.bt;
+  float2 *scr = reinterpret_cast<float2 *>(uni + L.scr);
+  const RBand B = r.band[p1];
+  const int tb0 = p0 * r.grp, tb1 = min(NB, tb0 + r.grp);
+  if (warp == 0) {
+    if (lane == 0) band_load(a, r, B, uni, L, &bar[2]);
+    if (STAGED) x_load_staged(a, r, B, tb0, reinterpret_cast<float2 *>(uni + L.set[0]), &bar[0], lane);
+    else x_load(a, r, B, tb0, reinterpret_cast<float2 *>(uni + L.set[0]), &bar[0], lane);
+  }
+  mbar_wait(&bar[2], uses[2] & 1, r.err, 6u);
+  ++uses[2];
+  const RTask *tks = reinterpret_cast<const RTask *>(uni + L.meta);
+  const FChan *fchs = reinterpret_cast<const FChan *>(uni + L.meta + sizeof(RTask) * B.ntask) - B.f0;
+  const int32_t *rnd = reinterpret_cast<const int32_t *>(uni + L.meta + sizeof(RTask) * B.ntask +
+                                                         sizeof(FChan) * B.nf);
+  const int32_t *rnd2 = rnd + (B.r2off - B.r1off);
+  const float *wb = reinterpret_cast<const float *>(uni + L.w) + (B.g0 & 3);
+  const float2 *twsm = reinterpret_cast<const float2 *>(uni + L.tw);
+  for (int t = tb0; t < tb1; ++t) {
+    const int set = (t - tb0) & 1;
+    const int64_t u0 = (int64_t)t * r.bt;
+    const int nsb = (int)min((int64_t)r.bt, (int64_t)U - u0);
+    const uint64_t tw0 = r.stats ? globaltimer_ns() : 0;
+    if (tid == 0) *s_round = 0;
+    mbar_wait(&bar[set], uses[set] & 1, r.err, 4u);
+    ++uses[set];
+    if (r.stats) t_wait += globaltimer_ns() - tw0;
+    __syncthreads();  // (s_round; every warp past the previous batch's phase 2)
+    if (warp == 0) {
+      if (!STAGED)  // this batch's slots are free for the spectrum items of units u + R
+        for (int i = lane; i < nsb; i += 32) red_release_add_u32(r.done + (int)((u0 + i) % r.R), 1u);
+      if (t + 1 < tb1) {
+        float2 *nx = reinterpret_cast<float2 *>(uni + L.set[set ^ 1]);
+        if (STAGED) x_load_staged(a, r, B, t + 1, nx, &bar[set ^ 1], lane);
+        else x_load(a, r, B, t + 1, nx, &bar[set ^ 1], lane);
+      }
+    }
+    const float2 *Xb = reinterpret_cast<const float2 *>(uni + L.set[set]);
+    const int64_t ub = a.unit0 + u0;
+    // phase 1: small tasks and two-step step 1, rounds claimed dynamically
+    for (;;) {
+      int ri = 0;
+      if (lane == 0) ri = atomicAdd(s_round, 1);
+      ri = __shfl_sync(0xffffffffu, ri, 0);
+      if (ri >= B.nr1) break;
+      const int e = rnd[ri];
+      const RTask tk = ld_rtask(tks + (e >> 16));
+      const int i = (e & 0xffff) * 32 + lane;
+      const int m1 = tk.code & 255;
+      const bool small = (tk.code >> 16) & 1, inter = (tk.code >> 17) & 1;
+      if (small) {
+        switch (m1) {
+#define X_(S) case S: if (inter) rf_small<S, N, true>(a, r, tk, i, nsb, ub, Xb, B.blo, wb, fchs); \
+                      else rf_small<S, N, false>(a, r, tk, i, nsb, ub, Xb, B.blo, wb, fchs); break;
+          SLICQ_FSMALL(X_)
+#undef X_
+        }
+      } else {
+        switch (m1) {
+#define X_(S) case S: if (inter) rf_s1<S, N, true>(r, tk, i, nsb, Xb, B.blo, wb, twsm, scr, fchs); \
+                      else rf_s1<S, N, false>(r, tk, i, nsb, Xb, B.blo, wb, twsm, scr, fchs); break;
+          SLICQ_FSIZES(X_)
+#undef X_
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) *s_round = 0;
+    __syncthreads();
+    // phase 2: two-step step 2
+    for (;;) {
+      int ri = 0;
+      if (lane == 0) ri = atomicAdd(s_round, 1);
+      ri = __shfl_sync(0xffffffffu, ri, 0);
+      if (ri >= B.nr2) break;
+      const int e = rnd2[ri];
+      const RTask tk = ld_rtask(tks + (e >> 16));
+      const int i = (e & 0xffff) * 32 + lane;
+      switch ((tk.code >> 8) & 255) {
+#define X_(S) case S: rf_s2<S>(a, r, tk, i, nsb, ub, scr, fchs); break;
+        SLICQ_FSIZES(X_)
+#undef X_
+      }
+    }
+    __syncthreads();  // (the scratch and this set are free)
+  }
+}
+
+// ------------------------------------------------------------------ band-major channel kernel
+// The split design's forward channel stage as band items: a persistent grid claims (group of
+// grp batches, band) items in group-major order from a counter (zeroed by the launcher) and
+// reads the staged spectra with TMA bulk copies.
+template <int LOGN>
+__global__ void __launch_bounds__(RING_T, 2) slicq_fwd_band_kernel(const KArgs a, const RArgs r) {
+  extern __shared__ float4 smem4[];
+  char *uni = reinterpret_cast<char *>(smem4);
+  __shared__ uint64_t bar[3];
+  __shared__ int s_item, s_round;
+  const int tid = threadIdx.x;
+  const ChanSmem L = chan_smem_layout(r.bt, r.xstride, r.wmax, r.twmax, r.iscr, r.meta);
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned uses[3] = {0u, 0u, 0u};
+  uint64_t t_wait = 0;
+  const int NBt = (a.nunits + r.bt - 1) / r.bt;
+  const int ngroups = (NBt + r.grp - 1) / r.grp;
+  const int nitems = ngroups * r.nb;
+  pdl_wait();  // the staged spectra come from the spectrum kernel
+  __syncthreads();
+  for (;;) {
+    if (tid == 0) s_item = (int)atomicAdd(r.qctr, 1ull);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= nitems) break;
+    const int g = item / r.nb, b = item - g * r.nb;
+    chan_item<LOGN, true>(a, r, g, b, uni, L, bar, uses, &s_round, t_wait);
+  }
+  pdl_trigger();
+}
+
 // ------------------------------------------------------------------ forward kernel
 // Every CTA runs both kinds of items.  Dynamic shared memory: [FFT twiddles (persistent)]
 // [union: FFT frame + window table | channel region (chan_smem_layout)].  A channel item is
@@ -405,10 +551,8 @@ __global__ void __launch_bounds__(RING_T, 2) slicq_fwd_ring_kernel(const KArgs a
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < tw_entries<LOGN>(); i += RING_T) tw[i] = a.tw2n[i];
   const ChanSmem L = chan_smem_layout(r.bt, r.xstride, r.wmax, r.twmax, r.iscr, r.meta);
-  float2 *scr = reinterpret_cast<float2 *>(uni + L.scr);
   const int U = a.nunits;
   const int UG = r.bt * r.grp;                   // units per channel item
-  const int NB = (U + r.bt - 1) / r.bt;          // batches
   const int64_t nitems = ring_items(U, UG, r.nb, r.la);
   if (tid == 0) {
     for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
@@ -443,88 +587,7 @@ __global__ void __launch_bounds__(RING_T, 2) slicq_fwd_ring_kernel(const KArgs a
       }
       if (r.stats) t_spec += globaltimer_ns() - t0;
     } else if (type == 1) {
-      // ---- channel item: band p1 for batches [p0 grp, p0 grp + grp) (F3 - F5)
-      const RBand B = r.band[p1];
-      const int tb0 = p0 * r.grp, tb1 = min(NB, tb0 + r.grp);
-      if (warp == 0) {
-        if (lane == 0) band_load(a, r, B, uni, L, &bar[2]);
-        x_load(a, r, B, tb0, reinterpret_cast<float2 *>(uni + L.set[0]), &bar[0], lane);
-      }
-      mbar_wait(&bar[2], uses[2] & 1, r.err, 6u);
-      ++uses[2];
-      const RTask *tks = reinterpret_cast<const RTask *>(uni + L.meta);
-      const FChan *fchs = reinterpret_cast<const FChan *>(uni + L.meta + sizeof(RTask) * B.ntask) - B.f0;
-      const int32_t *rnd = reinterpret_cast<const int32_t *>(uni + L.meta + sizeof(RTask) * B.ntask +
-                                                             sizeof(FChan) * B.nf);
-      const int32_t *rnd2 = rnd + (B.r2off - B.r1off);
-      const float *wb = reinterpret_cast<const float *>(uni + L.w) + (B.g0 & 3);
-      const float2 *twsm = reinterpret_cast<const float2 *>(uni + L.tw);
-      for (int t = tb0; t < tb1; ++t) {
-        const int set = (t - tb0) & 1;
-        const int64_t u0 = (int64_t)t * r.bt;
-        const int nsb = (int)min((int64_t)r.bt, (int64_t)U - u0);
-        const uint64_t tw0 = r.stats ? globaltimer_ns() : 0;
-        if (tid == 0) s_round = 0;
-        mbar_wait(&bar[set], uses[set] & 1, r.err, 4u);
-        ++uses[set];
-        if (r.stats) t_wait += globaltimer_ns() - tw0;
-        __syncthreads();  // (s_round; every warp past the previous batch's phase 2)
-        if (warp == 0) {
-          // this batch's slots are free for the spectrum items of units u + R; the next
-          // batch's bins land in the other set while this one computes
-          for (int i = lane; i < nsb; i += 32) red_release_add_u32(r.done + (int)((u0 + i) % r.R), 1u);
-          if (t + 1 < tb1)
-            x_load(a, r, B, t + 1, reinterpret_cast<float2 *>(uni + L.set[set ^ 1]), &bar[set ^ 1], lane);
-        }
-        const float2 *Xb = reinterpret_cast<const float2 *>(uni + L.set[set]);
-        const int64_t ub = a.unit0 + u0;
-        // phase 1: small tasks and two-step step 1, rounds claimed dynamically
-        for (;;) {
-          int ri = 0;
-          if (lane == 0) ri = atomicAdd(&s_round, 1);
-          ri = __shfl_sync(0xffffffffu, ri, 0);
-          if (ri >= B.nr1) break;
-          const int e = rnd[ri];
-          const RTask tk = ld_rtask(tks + (e >> 16));
-          const int i = (e & 0xffff) * 32 + lane;
-          const int m1 = tk.code & 255;
-          const bool small = (tk.code >> 16) & 1, inter = (tk.code >> 17) & 1;
-          if (small) {
-            switch (m1) {
-#define X_(S) case S: if (inter) rf_small<S, N, true>(a, r, tk, i, nsb, ub, Xb, B.blo, wb, fchs); \
-                      else rf_small<S, N, false>(a, r, tk, i, nsb, ub, Xb, B.blo, wb, fchs); break;
-              SLICQ_FSMALL(X_)
-#undef X_
-            }
-          } else {
-            switch (m1) {
-#define X_(S) case S: if (inter) rf_s1<S, N, true>(r, tk, i, nsb, Xb, B.blo, wb, twsm, scr, fchs); \
-                      else rf_s1<S, N, false>(r, tk, i, nsb, Xb, B.blo, wb, twsm, scr, fchs); break;
-              SLICQ_FSIZES(X_)
-#undef X_
-            }
-          }
-        }
-        __syncthreads();
-        if (tid == 0) s_round = 0;
-        __syncthreads();
-        // phase 2: two-step step 2
-        for (;;) {
-          int ri = 0;
-          if (lane == 0) ri = atomicAdd(&s_round, 1);
-          ri = __shfl_sync(0xffffffffu, ri, 0);
-          if (ri >= B.nr2) break;
-          const int e = rnd2[ri];
-          const RTask tk = ld_rtask(tks + (e >> 16));
-          const int i = (e & 0xffff) * 32 + lane;
-          switch ((tk.code >> 8) & 255) {
-#define X_(S) case S: rf_s2<S>(a, r, tk, i, nsb, ub, scr, fchs); break;
-            SLICQ_FSIZES(X_)
-#undef X_
-          }
-        }
-        __syncthreads();  // (the scratch and this set are free)
-      }
+      chan_item<LOGN, false>(a, r, p0, p1, uni, L, bar, uses, &s_round, t_wait);
       if (r.stats) t_chan += globaltimer_ns() - t0;
     }
     if (tid == 0) s_next = (long long)claim;
@@ -547,6 +610,9 @@ constexpr size_t ring_smem(int tr, size_t chan_bytes) {
 
 template <int LOGN>
 int ring_attrs();
+template <int LOGN>
+cudaError_t launch_fwd_band(const KArgs &a, const RArgs &r, size_t smem, int grid, cudaStream_t s,
+                            bool pdl);
 template <int LOGN>
 cudaError_t launch_fwd_ring(const KArgs &a, const RArgs &r, size_t smem, cudaStream_t s);
 

@@ -78,7 +78,24 @@ cudaError_t launch_fwd_fused<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem,
 #if SLICQ_LOGN == 12 || SLICQ_LOGN == 13
 template <>
 int ring_attrs<SLICQ_LOGN>() {
-  return (int)allow_max_dyn_smem((const void *)slicq_fwd_ring_kernel<SLICQ_LOGN>);
+  int rc = (int)allow_max_dyn_smem((const void *)slicq_fwd_ring_kernel<SLICQ_LOGN>);
+  if (rc == 0) rc = (int)allow_max_dyn_smem((const void *)slicq_fwd_band_kernel<SLICQ_LOGN>);
+  return rc;
+}
+template <>
+cudaError_t launch_fwd_band<SLICQ_LOGN>(const KArgs &a, const RArgs &r, size_t smem, int grid,
+                                        cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(RING_T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, slicq_fwd_band_kernel<SLICQ_LOGN>, a, r);
 }
 template <>
 cudaError_t launch_fwd_ring<SLICQ_LOGN>(const KArgs &a, const RArgs &r, size_t smem, cudaStream_t s) {

@@ -146,6 +146,7 @@ struct KernelConfig {
   int64_t toff_f = 0, toff_i = 0;  // offsets of the four-step intermediate in a unit
   int64_t chunk_units = 0;    // units per chunk (staging is sized for one chunk)
   int tile = 16;              // units per channel-kernel tile
+  int stiles = 0;             // channel kernels: tiles per super-tile (0: the whole chunk)
   int chan_per_sm = 0;        // channel-kernel CTAs per SM cap (0: occupancy)
   bool pipe = false;          // chunks alternate between two streams, ping-pong staging
   bool pdl = true;            // launch with programmatic stream serialization
@@ -154,7 +155,9 @@ struct KernelConfig {
   bool longmode = false;      // sl_len 2^18..2^22: full-length CQ-NSGT only (kernels_long.cuh)
   kern::LongClasses lcls{};   // long mode: channel size classes (kernels_long_api.h)
   // fused kernels (kernels_fused.cuh): one CTA per unit, no staging
-  bool fused = false;         // forward and inverse run the fused kernels
+  bool ftables = false;       // fused / ring tables built (fused_host.cu)
+  bool fused = false;         // forward runs the fused per-slice kernel (opt-in)
+  bool band = false;          // forward channel stage runs the band-major kernel (split design)
   int nftf = 0, nfti = 0;     // forward / inverse warp tasks
   int nphase_a = 0;           // inverse: tasks [0, nphase_a) are phase A (even channels)
   int fscr = 0;               // per-warp scratch (float2 entries)
@@ -167,6 +170,7 @@ struct KernelConfig {
   int rgroup = 1, rmeta = 0;  // batches per channel item; largest band metadata (bytes)
   int64_t rslot = 0;          // float2 entries per ring slot
   size_t rsmem = 0;           // dynamic shared memory of the ring kernel
+  size_t rchsmem = 0;         // dynamic shared memory of the band-major channel kernel
 };
 
 }  // namespace slicq

@@ -12,7 +12,7 @@ torch.manual_seed(0)
 x = torch.randn(batch, n, device="cuda") * 0.1
 ref = None
 for v in variants:
-    for kv in ("SLICQ_FUSED", "SLICQ_RING", "SLICQ_RING_NB", "SLICQ_RING_Q", "SLICQ_RING_BT", "SLICQ_RING_MB"):
+    for kv in [k for k in os.environ if k.startswith("SLICQ_")]:
         os.environ.pop(kv, None)
     for kv in filter(None, v.split(",")):
         k, val = kv.split("=")
