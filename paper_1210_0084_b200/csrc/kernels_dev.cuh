@@ -973,29 +973,25 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
 // ------------------------------------------------------------------ inverse spectrum kernel
 // MODE 0: sliCQ (dual window, overlap-add, paired boundaries).  MODE 1: full-length CQ-NSGT
 // synthesis (Alg. 2): y[row][i] = the frame sample i for i < y_len, nothing else.
-template <int LOGN, int MODE = 0>
-__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_kernel(const KArgs a) {
+// I3b + I4 + I5 of unit ul of the chunk: the slot sum, c2r FFT, dual window and overlap-add.
+// The caller has staged tw and htab (and waited for the channel kernel).  ll / rl: the left /
+// right overlap with the neighbouring slice of the same row is resolved locally (persistent
+// kernel: the neighbour is this CTA's previous / next unit), through carry[0 .. tr-1) in
+// shared memory instead of the cross-CTA pairing through the workspace; the sums are the
+// same (a + b, each half rounded as stored), so both kernels give bit-identical output.
+template <int LOGN, int MODE>
+__device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *tw, float *htab,
+                                         float *carry, int64_t ul, bool ll, bool rl) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T;
-  extern __shared__ float4 smem4[];
-  float2 *spec = reinterpret_cast<float2 *>(smem4);
-  float2 *tw = spec + spec_entries<LOGN>();
-  float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());
   const int tid = threadIdx.x;
-  const int64_t ul = blockIdx.x;
   const int64_t u = a.unit0 + ul;
   const int64_t row = u / a.nslices;
   const int mloc = (int)(u - row * a.nslices);
   const int64_t mg = a.slice0 + mloc;
 
   PHASE_INIT();
-  for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
-  if constexpr (MODE == 0)
-    for (int u2 = tid; u2 < a.tr - 1; u2 += T)
-      htab[u2] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u2);
   constexpr bool hsm = true;
-  pdl_wait();  // contributions of this chunk come from the channel kernel
-  prefetch_l2(a.stage + ul * a.zs, a.zs * 8, tid, T);
 
   constexpr int R1 = CF::I1, TASKS1 = N / R1;
   if constexpr (R1 == 16 && TASKS1 == 2 * T) {
@@ -1187,8 +1183,9 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
     const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
     const float invN = 1.0f / (float)N;
     const int S = a.nslices;
-    const bool left_paired = a.circular || mloc > 0;
-    const bool right_paired = a.circular || mloc + 1 < S;
+    // ll / rl: resolved locally (carry); otherwise paired across CTAs through the workspace
+    const bool left_paired = (a.circular || mloc > 0) && !ll;
+    const bool right_paired = (a.circular || mloc + 1 < S) && !rl;
     const int bl = mloc > 0 ? mloc - 1 : S - 1;  // boundary ids (local)
     const int br = mloc;
     const int trp = a.tr;
@@ -1227,7 +1224,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       const int cnt = (int)min((int64_t)(2 * N), a.y_len);
       for (int i = tid; i < cnt; i += T) yrow[i] = fr(i);
       (void)A; (void)Bw; (void)left_paired; (void)right_paired; (void)bl; (void)br; (void)bnd_row;
-      pdl_trigger();
+      (void)carry;
       return;
     }
     const int64_t sbase = (mg - 1) * N;  // global sample of frame index 0
@@ -1256,13 +1253,20 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
     // transitions, u = 0 .. tr-2 (|t| = A + 1 + u on the right, Bw - 1 - u on the left)
     for (int u = tid; u < a.tr - 1; u += T) {
       const int il = N - Bw + 1 + u;  // left: t = u - Bw + 1
-      const float vl = fr(il) * htab[Bw - 2 - u - A];
       const int64_t sl = sbase + il;
-      if (left_paired) bnd_row[((int64_t)bl * 2 + 1) * trp + u] = vl;
-      else a.spill[row * a.halo + (sl - a.y_base + a.halo)] = vl;
+      if (ll) {  // previous slice's right half (same samples: index u) + this left half
+        const float v = carry[u] + __fmul_rn(fr(il), htab[Bw - 2 - u - A]);
+        if (!a.circular) yrow[sl - a.y_base] = v;
+        else if (sl < a.y_len) yrow[sl] = v;  // (sl in [0, L) since mloc > 0; padding dropped)
+      } else {
+        const float vl = fr(il) * htab[Bw - 2 - u - A];
+        if (left_paired) bnd_row[((int64_t)bl * 2 + 1) * trp + u] = vl;
+        else a.spill[row * a.halo + (sl - a.y_base + a.halo)] = vl;
+      }
       const int ir = N + A + 1 + u;   // right: t = A + 1 + u
       const float vr = fr(ir) * htab[u];
-      if (right_paired) bnd_row[((int64_t)br * 2 + 0) * trp + u] = vr;
+      if (rl) carry[u] = vr;
+      else if (right_paired) bnd_row[((int64_t)br * 2 + 0) * trp + u] = vr;
       else yrow[sbase + ir - a.y_base] = vr;
     }
     (void)hsm;
@@ -1275,6 +1279,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       for (int u = tid; u < a.halo - (Bw - 1); u += T) a.spill[row * a.halo + u] = 0.f;
     }
     PHASE_MARK(1, 4);
+    if (!left_paired && !right_paired) return;  // (both sides local or unpaired)
     // ---- pairing: the second CTA to finish a boundary adds both halves (side0 + side1).
     // Release: barrier, then one thread fences (cumulative, gpu scope) and counts; acquire:
     // that thread fences after the count, then the barrier (the cooperative-groups pattern).
@@ -1316,6 +1321,57 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
     }
   }
   PHASE_MARK(1, 5);
+}
+
+template <int LOGN, int MODE = 0>
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_kernel(const KArgs a) {
+  using CF = Big<LOGN>;
+  constexpr int N = CF::N, T = CF::T;
+  extern __shared__ float4 smem4[];
+  float2 *spec = reinterpret_cast<float2 *>(smem4);
+  float2 *tw = spec + spec_entries<LOGN>();
+  float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());
+  const int tid = threadIdx.x;
+  for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
+  if constexpr (MODE == 0)
+    for (int u2 = tid; u2 < a.tr - 1; u2 += T)
+      htab[u2] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u2);
+  pdl_wait();  // contributions of this chunk come from the channel kernel
+  prefetch_l2(a.stage + (int64_t)blockIdx.x * a.zs, a.zs * 8, tid, T);
+  inv_unit<LOGN, MODE>(a, spec, tw, htab, nullptr, blockIdx.x, false, false);
+  pdl_trigger();
+}
+
+// Persistent variant (MODE 0): CTA c handles the contiguous units [c U / G, (c+1) U / G) of the
+// chunk; tw and htab are staged once, the next unit's slots are prefetched to L2 while this one
+// is synthesised, and the overlap of consecutive slices of one row handled by the same CTA is
+// added on chip (carry) instead of through the workspace pairing.
+template <int LOGN>
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_persist_kernel(const KArgs a) {
+  using CF = Big<LOGN>;
+  constexpr int N = CF::N, T = CF::T;
+  extern __shared__ float4 smem4[];
+  float2 *spec = reinterpret_cast<float2 *>(smem4);
+  float2 *tw = spec + spec_entries<LOGN>();
+  float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());
+  float *carry = htab + ((a.tr + 3) & ~3);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
+  for (int u2 = tid; u2 < a.tr - 1; u2 += T) htab[u2] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u2);
+  pdl_wait();  // contributions of this chunk come from the channel kernel
+  const int64_t G = gridDim.x;
+  const int64_t ub = blockIdx.x * (int64_t)a.nunits / G, ue = (blockIdx.x + 1) * (int64_t)a.nunits / G;
+  if (ub < ue) prefetch_l2(a.stage + ub * a.zs, a.zs * 8, tid, T);
+  __syncthreads();
+  for (int64_t ul = ub; ul < ue; ++ul) {
+    const int64_t u = a.unit0 + ul;
+    const int mloc = (int)(u % a.nslices);
+    const bool ll = ul > ub && mloc > 0;                    // unit ul - 1 is slice mloc - 1
+    const bool rl = ul + 1 < ue && mloc + 1 < a.nslices;  // unit ul + 1 is slice mloc + 1
+    if (ul + 1 < ue) prefetch_l2(a.stage + (ul + 1) * a.zs, a.zs * 8, tid, T);
+    inv_unit<LOGN, 0>(a, spec, tw, htab, carry, ul, ll, rl);
+    __syncthreads();  // (spec and carry reused by the next unit)
+  }
   pdl_trigger();
 }
 
@@ -1323,6 +1379,11 @@ template <int LOGN>
 constexpr size_t spec_smem_bytes(int tr) {
   return sizeof(float2) * (size_t)(spec_entries<LOGN>() + tw_entries<LOGN>()) +
          sizeof(float) * (size_t)((tr + 3) & ~3);
+}
+// the persistent inverse spectrum kernel adds the overlap carry (tr floats)
+template <int LOGN>
+constexpr size_t spec_persist_smem_bytes(int tr) {
+  return spec_smem_bytes<LOGN>(tr) + sizeof(float) * (size_t)((tr + 3) & ~3);
 }
 
 // Per-size entry points (defined in kernels_l<LOGN>.cu)
@@ -1336,6 +1397,9 @@ cudaError_t launch_fwd_spec(const KArgs &a, dim3 grid, size_t smem, cudaStream_t
 template <int LOGN>
 cudaError_t launch_inv_spec(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s, bool pdl,
                             int mode = 0);
+template <int LOGN>
+cudaError_t launch_inv_spec_persist(const KArgs &a, size_t smem, cudaStream_t s, bool pdl,
+                                    int *grid_out);
 
 }  // namespace kern
 }  // namespace slicq

@@ -336,6 +336,15 @@ int configure_kernels(slicq_plan *p) {
                           : spec_smem_for(logN, (int)p->tr);
   if (kc.spec_smem > kSmemCap)
     return set_error(SLICQ_EUNSUPPORTED, "spectrum kernel shared memory exceeds 227 KB");
+  if (!kc.large) {
+    switch (logN) {
+      case 11: kc.spec_smem_p = spec_persist_smem_bytes<11>((int)p->tr); break;
+      case 12: kc.spec_smem_p = spec_persist_smem_bytes<12>((int)p->tr); break;
+      case 13: kc.spec_smem_p = spec_persist_smem_bytes<13>((int)p->tr); break;
+      case 14: kc.spec_smem_p = spec_persist_smem_bytes<14>((int)p->tr); break;
+    }
+    kc.inv_persist = env_int("SLICQ_INV_PERSIST", 1) != 0 && kc.spec_smem_p <= kSmemCap;
+  }
   const int K2 = p->K + 2;
   const int N = (int)p->N, N2 = 2 * N;
   std::map<int, std::pair<int, int>> fac;
@@ -1169,6 +1178,20 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
   return SLICQ_OK;
 }
 
+static cudaError_t launch_inv_persist(const slicq_plan *p, const KArgs &a, cudaStream_t s) {
+  const size_t sm = p->kc.spec_smem_p;
+  switch (p->kc.logN) {
+#define CASE_(L) \
+  case L: return launch_inv_spec_persist<L>(a, sm, s, p->kc.pdl, nullptr);
+    CASE_(11)
+    CASE_(12)
+    CASE_(13)
+    CASE_(14)
+#undef CASE_
+  }
+  return cudaErrorInvalidValue;
+}
+
 int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0, int64_t nslices,
                    int64_t total_slices, int64_t batch, int circular, int64_t n_valid, int64_t L,
                    float *y, int64_t y_stride, int64_t y_base, float *left_spill, int64_t halo,
@@ -1236,7 +1259,9 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     a.stage = pp.stage(stage0, i, w.chunk, std::max(p->kc.xs, p->kc.zs));
     const cudaStream_t st = pp.stream(i);
     cudaError_t e = launch_chan(false, p, a, st);
-    if (e == cudaSuccess)
+    if (e == cudaSuccess && !p->kc.large && mode == 0 && p->kc.inv_persist)
+      e = launch_inv_persist(p, a, st);
+    else if (e == cudaSuccess)
       e = !p->kc.large ? launch_spec(false, p, a, dim3((unsigned)a.nunits), st, mode)
           : p->kc.logN == 15 ? large_inverse_spec<15>(a, st, mode)
                              : large_inverse_spec<16>(a, st, mode);

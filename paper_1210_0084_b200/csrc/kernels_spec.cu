@@ -3,6 +3,8 @@
 #ifndef SLICQ_LOGN
 #error "compile with -DSLICQ_LOGN=<11..14>"
 #endif
+#include <algorithm>
+
 #include "kernels_dev.cuh"
 #include "kernels_fused.cuh"
 #include "kernels_ring.cuh"
@@ -15,6 +17,7 @@ template <>
 int set_attrs<SLICQ_LOGN>(size_t smem) {
   const void *fns[] = {(const void *)slicq_fwd_spec_kernel<SLICQ_LOGN, 0>,
                        (const void *)slicq_inv_spec_kernel<SLICQ_LOGN, 0>,
+                       (const void *)slicq_inv_spec_persist_kernel<SLICQ_LOGN>,
                        (const void *)slicq_fwd_spec_kernel<SLICQ_LOGN, 1>,
                        (const void *)slicq_inv_spec_kernel<SLICQ_LOGN, 1>};
   for (const void *f : fns) {
@@ -112,6 +115,26 @@ cudaError_t launch_fwd_ring<SLICQ_LOGN>(const KArgs &a, const RArgs &r, size_t s
   return cudaLaunchKernelEx(&cfg, slicq_fwd_ring_kernel<SLICQ_LOGN>, a, r);
 }
 #endif
+
+template <>
+cudaError_t launch_inv_spec_persist<SLICQ_LOGN>(const KArgs &a, size_t smem, cudaStream_t s,
+                                                bool pdl, int *grid_out) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ, slicq_inv_spec_persist_kernel<SLICQ_LOGN>, Big<SLICQ_LOGN>::T, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(occ, 1) * nsm, a.nunits));
+  if (grid_out) *grid_out = grid;
+  return launch_pdl(slicq_inv_spec_persist_kernel<SLICQ_LOGN>, a, dim3((unsigned)grid),
+                    Big<SLICQ_LOGN>::T, smem, s, pdl);
+}
 
 template <>
 int phase_times<SLICQ_LOGN>(unsigned long long *out32, int reset) {

@@ -135,6 +135,8 @@ struct KernelConfig {
   int logN = 0;          // N = 2^logN complex points in the r2c FFT of a 2N slice
   int threads = 0;       // spectrum-kernel CTA size
   size_t spec_smem = 0;  // spectrum kernels: dynamic shared memory bytes
+  size_t spec_smem_p = 0;  // persistent inverse spectrum kernel (+ overlap carry)
+  bool inv_persist = false;  // inverse spectrum stage runs persistent (on-chip overlap carry)
   int scr = 0;           // channel kernels: per-warp scratch (float2 entries)
   size_t chan_smem = 0;
   int npackets = 0;
