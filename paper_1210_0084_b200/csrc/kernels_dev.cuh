@@ -970,6 +970,34 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
   pdl_trigger();
 }
 
+// Persistent variant (MODE 0): CTA c transforms the contiguous units [c U / G, (c+1) U / G) of
+// the chunk; the twiddle table is staged once and the next unit's frame is prefetched to L2
+// while this one is transformed (consecutive frames of a row also share tr - 1 samples).
+template <int LOGN>
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_persist_kernel(const KArgs a) {
+  using CF = Big<LOGN>;
+  constexpr int N = CF::N, T = CF::T;
+  extern __shared__ float4 smem4[];
+  float2 *spec = reinterpret_cast<float2 *>(smem4);
+  float2 *tw = spec + spec_entries<LOGN>();
+  float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());
+  const int tid = threadIdx.x;
+  for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
+  const int64_t G = gridDim.x;
+  const int64_t ub = blockIdx.x * (int64_t)a.nunits / G, ue = (blockIdx.x + 1) * (int64_t)a.nunits / G;
+  for (int64_t ul = ub; ul < ue; ++ul) {
+    if (ul + 1 < ue) {  // the next frame's window support -> L2
+      const int64_t u = a.unit0 + ul + 1, row = u / a.nslices;
+      const int64_t s0 = (a.slice0 + (u - row * a.nslices) - 1) * N - a.base_off + (N - a.tr) / 2;
+      if (s0 >= 0 && s0 + N + a.tr <= a.x_len)
+        prefetch_l2(a.x + row * a.x_stride + s0, (int64_t)(N + a.tr) * 4, tid, T);
+    }
+    fwd_spectrum<LOGN, 0, false, false>(a, spec, tw, htab, a.unit0 + ul, a.stage + ul * a.xs);
+    __syncthreads();  // (spec and htab reused by the next unit)
+  }
+  pdl_trigger();
+}
+
 // ------------------------------------------------------------------ inverse spectrum kernel
 // MODE 0: sliCQ (dual window, overlap-add, paired boundaries).  MODE 1: full-length CQ-NSGT
 // synthesis (Alg. 2): y[row][i] = the frame sample i for i < y_len, nothing else.
@@ -1400,6 +1428,8 @@ cudaError_t launch_inv_spec(const KArgs &a, dim3 grid, size_t smem, cudaStream_t
 template <int LOGN>
 cudaError_t launch_inv_spec_persist(const KArgs &a, size_t smem, cudaStream_t s, bool pdl,
                                     int *grid_out);
+template <int LOGN>
+cudaError_t launch_fwd_spec_persist(const KArgs &a, size_t smem, cudaStream_t s, bool pdl);
 
 }  // namespace kern
 }  // namespace slicq

@@ -344,6 +344,7 @@ int configure_kernels(slicq_plan *p) {
       case 14: kc.spec_smem_p = spec_persist_smem_bytes<14>((int)p->tr); break;
     }
     kc.inv_persist = env_int("SLICQ_INV_PERSIST", 1) != 0 && kc.spec_smem_p <= kSmemCap;
+    kc.fwd_persist = env_int("SLICQ_FWD_PERSIST", 0) != 0;
   }
   const int K2 = p->K + 2;
   const int N = (int)p->N, N2 = 2 * N;
@@ -1029,6 +1030,20 @@ static cudaError_t launch_fused(bool fwd, const slicq_plan *p, const KArgs &a, d
   return cudaErrorInvalidValue;
 }
 
+static cudaError_t launch_fwd_persist(const slicq_plan *p, const KArgs &a, cudaStream_t s) {
+  const size_t sm = p->kc.spec_smem;
+  switch (p->kc.logN) {
+#define CASE_(L) \
+  case L: return launch_fwd_spec_persist<L>(a, sm, s, p->kc.pdl);
+    CASE_(11)
+    CASE_(12)
+    CASE_(13)
+    CASE_(14)
+#undef CASE_
+  }
+  return cudaErrorInvalidValue;
+}
+
 // the band / ring tables of RArgs (the ring buffers and flags are set by the ring launch)
 static RArgs band_args(const slicq_plan *p) {
   RArgs r{};
@@ -1145,7 +1160,9 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
     a.stage = pp.stage(stage0, i, w.chunk, std::max(p->kc.xs, p->kc.zs));
     const cudaStream_t st = pp.stream(i);
-    cudaError_t e = !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), st, mode)
+    cudaError_t e = !p->kc.large && mode == 0 && p->kc.fwd_persist
+                        ? launch_fwd_persist(p, a, st)
+                    : !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), st, mode)
                     : p->kc.logN == 15 ? large_forward<15>(a, st, mode)
                                        : large_forward<16>(a, st, mode);
     if (e == cudaSuccess && p->kc.band && !p->kc.large) {

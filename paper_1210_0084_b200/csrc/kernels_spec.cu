@@ -18,6 +18,7 @@ int set_attrs<SLICQ_LOGN>(size_t smem) {
   const void *fns[] = {(const void *)slicq_fwd_spec_kernel<SLICQ_LOGN, 0>,
                        (const void *)slicq_inv_spec_kernel<SLICQ_LOGN, 0>,
                        (const void *)slicq_inv_spec_persist_kernel<SLICQ_LOGN>,
+                       (const void *)slicq_fwd_spec_persist_kernel<SLICQ_LOGN>,
                        (const void *)slicq_fwd_spec_kernel<SLICQ_LOGN, 1>,
                        (const void *)slicq_inv_spec_kernel<SLICQ_LOGN, 1>};
   for (const void *f : fns) {
@@ -133,6 +134,25 @@ cudaError_t launch_inv_spec_persist<SLICQ_LOGN>(const KArgs &a, size_t smem, cud
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(occ, 1) * nsm, a.nunits));
   if (grid_out) *grid_out = grid;
   return launch_pdl(slicq_inv_spec_persist_kernel<SLICQ_LOGN>, a, dim3((unsigned)grid),
+                    Big<SLICQ_LOGN>::T, smem, s, pdl);
+}
+
+template <>
+cudaError_t launch_fwd_spec_persist<SLICQ_LOGN>(const KArgs &a, size_t smem, cudaStream_t s,
+                                                bool pdl) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ, slicq_fwd_spec_persist_kernel<SLICQ_LOGN>, Big<SLICQ_LOGN>::T, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(occ, 1) * nsm, a.nunits));
+  return launch_pdl(slicq_fwd_spec_persist_kernel<SLICQ_LOGN>, a, dim3((unsigned)grid),
                     Big<SLICQ_LOGN>::T, smem, s, pdl);
 }
 

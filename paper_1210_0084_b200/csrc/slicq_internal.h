@@ -137,6 +137,7 @@ struct KernelConfig {
   size_t spec_smem = 0;  // spectrum kernels: dynamic shared memory bytes
   size_t spec_smem_p = 0;  // persistent inverse spectrum kernel (+ overlap carry)
   bool inv_persist = false;  // inverse spectrum stage runs persistent (on-chip overlap carry)
+  bool fwd_persist = false;  // forward spectrum stage runs persistent
   int scr = 0;           // channel kernels: per-warp scratch (float2 entries)
   size_t chan_smem = 0;
   int npackets = 0;
