@@ -134,7 +134,8 @@ int configure_fused(slicq_plan *p) {
   kc.fused = kc.ftables = false;
   // the fused per-slice forward (opt-in: measured slower), the ring kernel
   // (opt-in) and the band-major channel kernel share these tables
-  const bool want = env_i("SLICQ_FUSED", 0) || env_i("SLICQ_RING", 0) || env_i("SLICQ_BAND", 0);
+  const bool want = env_i("SLICQ_FUSED", 0) || env_i("SLICQ_RING", 0) || env_i("SLICQ_BAND", 0) ||
+                    env_i("SLICQ_FWD2", 0);
   if (!want) return SLICQ_OK;
   if (kc.longmode || kc.large || kc.logN < 11 || kc.logN > 14 || !p->painless) return SLICQ_OK;
   const int K2 = p->K + 2;
@@ -532,6 +533,136 @@ int configure_ring(slicq_plan *p) {
                      T.nch, T.soff, p->rfch[T.coff].lo);
       }
     }
+  return SLICQ_OK;
+}
+
+// ---- forward channel kernel v2 (kernels_chan2.cuh): packets of equal-length channels with
+// multi-round warp tasks (shapes chosen to fill the lanes), table-free contiguous folds
+int configure_fwd2(slicq_plan *p) {
+  KernelConfig &kc = p->kc;
+  kc.fwd2 = false;
+  if (!kc.ftables || kc.large || env_i("SLICQ_FWD2", 0) == 0) return SLICQ_OK;
+  const int K2 = p->K + 2;
+  const int N = (int)p->N;
+  const int tile = kc.tile;
+  const int SCR = (int)env_i("SLICQ_FWD2_SCR", 1024), RMAX = 4;
+  auto interior = [&](int k) { return p->lo[k] >= 0 && p->lo[k] + p->len[k] - 1 <= N; };
+  struct Pk {
+    P2Dev d;
+    std::vector<int> ks;
+    int var;
+  };
+  std::vector<Pk> pks;
+  std::vector<int> Ms;
+  for (int k = 0; k < K2; ++k)
+    if (std::find(Ms.begin(), Ms.end(), p->M[k]) == Ms.end()) Ms.push_back(p->M[k]);
+  int scr = 2;
+  for (int M : Ms) {
+    std::vector<int> grp;
+    for (int k = 0; k < K2; ++k)
+      if (p->M[k] == M) grp.push_back(k);
+    const int G = (int)grp.size();
+    // best (small | m1, m2, nch, nu) by issue cost per channel-unit
+    struct Best {
+      double cost = 1e300;
+      bool small = false;
+      int m1 = 0, m2 = 0, nch = 1, nu = 1;
+    } best;
+    auto consider = [&](bool small, int m1, int m2, int nch, int nu) {
+      const int nvc = nch * nu;
+      if (nu > tile) return;
+      double c;
+      if (small) {
+        if (nvc > 32 || !mag_exact(nch, nvc)) return;
+        c = (cost_small(M) + 20.0) / nvc;
+      } else {
+        const int i1 = nvc * m2, i2 = nvc * m1;
+        if ((i1 + 31) / 32 > RMAX || (i2 + 31) / 32 > RMAX) return;
+        if (nvc * m1 * (m2 | 1) > SCR) return;
+        if (!mag_exact(m2, i1) || !mag_exact(m1, i2) || !mag_exact(nch, nvc)) return;
+        c = (((i1 + 31) / 32) * cost_s1(m1) + ((i2 + 31) / 32) * cost_s2(m2) + 40.0) / nvc;
+      }
+      // coalescing: lanes of one unit read neighbouring bins and write neighbouring columns;
+      // lanes spread over units do neither (each touches another row)
+      c *= 1.0 + 0.5 * (1.0 - (double)nch / nvc);
+      if (c < best.cost - 1e-9) best = Best{c, small, m1, m2, nch, nu};
+    };
+    for (int nch = 1; nch <= std::min(G, 32); ++nch)
+      for (int nu = 1; nu <= 32; ++nu) {
+        if (fsmall(M)) consider(true, M, 1, nch, nu);
+        for (int m1 : kFSizes) {
+          if (M % m1 || !fsize(M / m1)) continue;
+          consider(false, m1, M / m1, nch, nu);
+        }
+      }
+    if (best.cost >= 1e299) return SLICQ_OK;
+    for (int i = 0; i < G; i += best.nch) {
+      Pk pk;
+      for (int q = i; q < std::min(G, i + best.nch); ++q) pk.ks.push_back(grp[q]);
+      const int r = (int)pk.ks.size();
+      // units per task for this packet's channel count (the last packet may be shorter)
+      int nu = std::max(1, best.nu * best.nch / r);
+      while (nu > 1) {
+        const int nvc = r * nu;
+        const bool ok = best.small ? (nvc <= 32 && mag_exact(r, nvc))
+                                   : ((nvc * best.m2 + 31) / 32 <= RMAX && (nvc * best.m1 + 31) / 32 <= RMAX &&
+                                      nvc * best.m1 * (best.m2 | 1) <= SCR && mag_exact(best.m2, nvc * best.m2) &&
+                                      mag_exact(best.m1, nvc * best.m1) && mag_exact(r, nvc));
+        if (ok) break;
+        --nu;
+      }
+      if (!mag_exact(r, r * nu)) return SLICQ_OK;
+      bool in = true;
+      for (int k : pk.ks) in = in && interior(k);
+      pk.d = P2Dev{};
+      pk.d.code = best.m1 | (best.m2 << 8) | ((best.small ? 1 : 0) << 16) | ((in ? 1 : 0) << 17);
+      pk.d.nch = r;
+      pk.d.nu = nu;
+      pk.d.magA = mag16(best.m2);
+      pk.d.magB = mag16(best.m1);
+      pk.d.magC = mag16(r);
+      pk.var = std::max(best.m1, best.m2) <= 16 ? 0 : 1;
+      if (!best.small) scr = std::max(scr, r * nu * best.m1 * (best.m2 | 1));
+      pks.push_back(std::move(pk));
+    }
+  }
+  std::stable_sort(pks.begin(), pks.end(), [](const Pk &x, const Pk &y) {
+    if (x.var != y.var) return x.var < y.var;
+    return (x.d.code & 0x1ffff) > (y.d.code & 0x1ffff);
+  });
+  p->f2pk.clear();
+  p->f2ch.clear();
+  kc.f2voff[0] = kc.f2voff[1] = kc.f2voff[2] = 0;
+  for (Pk &pk : pks) {
+    pk.d.coff = (int)p->f2ch.size();
+    const int m2 = (pk.d.code >> 16) & 1 ? 1 : (pk.d.code >> 8) & 255;
+    for (int k : pk.ks) {
+      FChan c{};
+      const int M = p->M[k];
+      c.lo = p->lo[k];
+      c.len = p->len[k];
+      c.M = M;
+      c.goff = (int)p->goff[k];
+      c.off = (int)p->off[k];
+      c.twoff = k;  // channel index: upload() replaces it with the twiddle-table offset
+      c.lo_mod = ((c.lo % M) + M) % M;
+      c.lom2 = ((c.lo % m2) + m2) % m2;
+      c.flags = interior(k) ? 1 : 0;
+      p->f2ch.push_back(c);
+    }
+    ++kc.f2voff[pk.var + 1];
+    p->f2pk.push_back(pk.d);
+  }
+  kc.f2voff[2] += kc.f2voff[1];
+  kc.f2scr = (scr + 1) & ~1;
+  kc.fwd2 = true;
+  if (env_i("SLICQ_DEBUG", 0))
+    std::fprintf(stderr, "fwd2: %zu packets (lite %d, full %d), scratch %d\n", p->f2pk.size(),
+                 kc.f2voff[1], kc.f2voff[2] - kc.f2voff[1], kc.f2scr);
+  if (env_i("SLICQ_DEBUG", 0) > 1)
+    for (const P2Dev &d : p->f2pk)
+      std::fprintf(stderr, "  pk m1=%d m2=%d small=%d inter=%d nch=%d nu=%d\n", d.code & 255,
+                   (d.code >> 8) & 255, (d.code >> 16) & 1, (d.code >> 17) & 1, d.nch, d.nu);
   return SLICQ_OK;
 }
 

@@ -169,6 +169,7 @@ struct KArgs {
   int nunits;
   int tile;       // units per channel-kernel tile
   int stiles;     // channel kernels: tiles per super-tile (0: the whole chunk)
+  int Nh;         // N (half the slice length)
   // coefficients
   int64_t C;
   float2 *coef_out;

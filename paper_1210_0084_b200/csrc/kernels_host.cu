@@ -15,6 +15,7 @@
 #include "kernels_dev.cuh"
 #include "kernels_fused.cuh"
 #include "kernels_ring.cuh"
+#include "kernels_chan2.cuh"
 #include "kernels_large.cuh"
 #include "kernels_long_api.h"
 
@@ -613,6 +614,7 @@ int configure_kernels(slicq_plan *p) {
   kc.chunk_units = cu;
   int rc = configure_fused(p);
   if (rc == SLICQ_OK) rc = configure_ring(p);
+  if (rc == SLICQ_OK) rc = configure_fwd2(p);
   return rc;
 }
 
@@ -637,7 +639,7 @@ int upload(slicq_plan *p) {
       twM.push_back((float)std::sin(ang));
     }
   }
-  for (std::vector<FChan> *v : {&p->fchf, &p->fchi})  // fused: channel index -> twiddle table
+  for (std::vector<FChan> *v : {&p->fchf, &p->fchi, &p->f2ch})  // channel index -> twiddle table
     for (FChan &f : *v) f.twoff = twoff[p->M[f.twoff]];
   std::vector<ChanDev> ch(K2);
   for (int k = 0; k < K2; ++k) {
@@ -735,6 +737,8 @@ int upload(slicq_plan *p) {
       {p->rfch.data(), sizeof(FChan) * p->rfch.size(), 0},
       {p->rbtw.data(), sizeof(float) * p->rbtw.size(), 0},
       {p->rround.data(), sizeof(int32_t) * p->rround.size(), 0},
+      {p->f2pk.data(), sizeof(P2Dev) * p->f2pk.size(), 0},
+      {p->f2ch.data(), sizeof(FChan) * p->f2ch.size(), 0},
   };
   size_t o = 0;
   for (Part &pt : parts) {
@@ -778,6 +782,8 @@ int upload(slicq_plan *p) {
   p->d.rfch = reinterpret_cast<FChan *>(b + parts[24].off);
   p->d.rbtw = reinterpret_cast<float2 *>(b + parts[25].off);
   p->d.rround = reinterpret_cast<int32_t *>(b + parts[26].off);
+  p->d.f2pk = reinterpret_cast<P2Dev *>(b + parts[27].off);
+  p->d.f2ch = reinterpret_cast<FChan *>(b + parts[28].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
@@ -793,6 +799,10 @@ int upload(slicq_plan *p) {
     default: rc = long_set_attrs(p->kc.logN, p->kc.lcls); break;
   }
   if (rc == 0 && p->kc.ftables) rc = fused_set_attrs(p);
+  if (rc == 0 && p->kc.fwd2) {
+    rc = (int)allow_max_dyn_smem((const void *)slicq_fwd_chan2_kernel<kLiteMax, kLiteMinB>);
+    if (rc == 0) rc = (int)allow_max_dyn_smem((const void *)slicq_fwd_chan2_kernel<kFullMax, kFullMinB>);
+  }
   for (int v = 0; v < 2 * kVariants * 3 && rc == 0 && !p->kc.longmode; ++v)  // fwd, variant, mask
     rc = (int)allow_max_dyn_smem((const void *)chan_fn(v & 1, (v >> 1) % kVariants, v / (2 * kVariants)));
   if (rc != 0)
@@ -936,6 +946,7 @@ static KArgs base_args(const slicq_plan *p) {
   a.zs = p->kc.zs;
   a.tile = p->kc.tile;
   a.stiles = p->kc.stiles;
+  a.Nh = (int)p->N;
   a.gw = p->d.gw;
   a.gdw = p->d.gdw;
   a.lrow = p->d.lrow;
@@ -948,6 +959,21 @@ static int check_device(const slicq_plan *p) {
   if (cudaGetDevice(&dev) != cudaSuccess || dev != p->device)
     return set_error(SLICQ_EINVAL, "current CUDA device differs from the plan's device");
   return SLICQ_OK;
+}
+
+// resident CTAs (occupancy x SMs) of a persistent kernel with `smem` dynamic shared memory
+static int64_t chan_capacity_smem(ChanFn fn, size_t smem) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, CHAN_T, smem) != cudaSuccess || occ <= 0)
+    occ = 2;
+  return (int64_t)occ * nsm;
 }
 
 // persistent channel-kernel grid: resident CTAs (occupancy x SMs), capped by the work items
@@ -993,6 +1019,40 @@ static cudaError_t launch_chan(bool fwd, const slicq_plan *p, KArgs a, cudaStrea
     cfg.attrs = at;
     cfg.numAttrs = p->kc.pdl ? 1 : 0;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// the forward channel kernel v2 (kernels_chan2.cuh): one launch per non-empty variant
+static cudaError_t launch_chan2(const slicq_plan *p, KArgs a, cudaStream_t s) {
+  for (int v = 0; v < 2; ++v) {
+    C2Args c2{};
+    c2.pk = p->d.f2pk + p->kc.f2voff[v];
+    c2.npk = p->kc.f2voff[v + 1] - p->kc.f2voff[v];
+    c2.fch = p->d.f2ch;
+    if (c2.npk == 0) continue;
+    const ChanFn fn0 = reinterpret_cast<ChanFn>(v == 0 ? slicq_fwd_chan2_kernel<kLiteMax, kLiteMinB>
+                                                       : slicq_fwd_chan2_kernel<kFullMax, kFullMinB>);
+    a.scr = p->kc.f2scr;
+    const size_t smem = sizeof(float2) * (size_t)p->kc.f2scr * (CHAN_T / 32);
+    const int64_t cap = chan_capacity_smem(fn0, smem);
+    a.tile = p->kc.tile;
+    while (a.tile > 8 && (int64_t)c2.npk * ((a.nunits + a.tile - 1) / a.tile) < 4 * cap) a.tile /= 2;
+    const int64_t items = (int64_t)c2.npk * ((a.nunits + a.tile - 1) / a.tile);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(items, cap)));
+    cfg.blockDim = dim3(CHAN_T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = p->kc.pdl ? 1 : 0;
+    const cudaError_t e =
+        v == 0 ? cudaLaunchKernelEx(&cfg, slicq_fwd_chan2_kernel<kLiteMax, kLiteMinB>, a, c2)
+               : cudaLaunchKernelEx(&cfg, slicq_fwd_chan2_kernel<kFullMax, kFullMinB>, a, c2);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -1184,6 +1244,9 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
         e = p->kc.logN == 12 ? launch_fwd_band<12>(a, r, p->kc.rchsmem, grid, st, p->kc.pdl)
             : launch_fwd_band<13>(a, r, p->kc.rchsmem, grid, st, p->kc.pdl);
       }
+    } else if (e == cudaSuccess && p->kc.fwd2 && !p->kc.large) {
+      a.vec16 = (reinterpret_cast<uintptr_t>(coeffs) % 16 == 0) ? 1 : 0;
+      e = launch_chan2(p, a, st);
     } else if (e == cudaSuccess) {
       e = launch_chan(true, p, a, st);
     }

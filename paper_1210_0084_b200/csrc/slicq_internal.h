@@ -99,6 +99,17 @@ struct RTask {
   uint32_t magM1;  // d = M1
 };
 
+// Forward channel kernel v2 (kernels_chan2.cuh): a packet of nch channels of one length
+// (two-step M1 x M2, or small: M1 = M, a whole DFT per lane), nu units per warp task;
+// code = M1 | M2 << 8 | small << 16 | interior << 17.  Exact q / d = (q * mag) >> 16.
+struct P2Dev {
+  int32_t code, nch, coff, nu;
+  uint32_t magA;  // d = M2: step-1 item -> virtual channel
+  uint32_t magB;  // d = M1: step-2 item -> virtual channel
+  uint32_t magC;  // d = nch: virtual channel -> unit
+  int32_t pad;
+};
+
 struct DeviceTables {
   ChanDev *chan = nullptr;
   PacketDev *packets = nullptr;
@@ -125,6 +136,8 @@ struct DeviceTables {
   FChan *rfch = nullptr;    // ring kernels: channels (band-local weight / twiddle offsets)
   float2 *rbtw = nullptr;   // ring kernels: per-band twiddle tables
   int32_t *rround = nullptr; // ring kernels: per-band round lists (task << 16 | round)
+  P2Dev *f2pk = nullptr;     // forward channel kernel v2: packets
+  FChan *f2ch = nullptr;     // forward channel kernel v2: channels in packet order
   void *block = nullptr;    // single allocation holding all of the above
   cudaStream_t pipe[2] = {nullptr, nullptr};  // chunk pipelining (kc.pipe): two streams
   cudaEvent_t pev[3] = {nullptr, nullptr, nullptr};
@@ -171,6 +184,10 @@ struct KernelConfig {
   int rR = 0, rnspec = 0, rnchan = 0, rnb = 0, rq = 0, rbt = 0, rla = 0;
   int rxstride = 0, rwmax = 0, rtwmax = 0, rfscr = 0;  // rfscr: item scratch (float2)
   int rgroup = 1, rmeta = 0;  // batches per channel item; largest band metadata (bytes)
+  // forward channel kernel v2 (kernels_chan2.cuh)
+  bool fwd2 = false;
+  int f2voff[3] = {0, 0, 0};  // packets [f2voff[v], f2voff[v+1]) run in variant v (lite, full)
+  int f2scr = 0;              // per-warp scratch (float2)
   int64_t rslot = 0;          // float2 entries per ring slot
   size_t rsmem = 0;           // dynamic shared memory of the ring kernel
   size_t rchsmem = 0;         // dynamic shared memory of the band-major channel kernel
@@ -224,6 +241,8 @@ struct slicq_plan {
   std::vector<slicq::FChan> rfch;        // ring kernels: channels in band task order
   std::vector<float> rbtw;               // ring kernels: per-band twiddles (re, im)
   std::vector<int32_t> rround;           // ring kernels: per-band round lists
+  std::vector<slicq::P2Dev> f2pk;        // forward channel kernel v2: packets
+  std::vector<slicq::FChan> f2ch;        // forward channel kernel v2: channels
   std::vector<int64_t> lsoff;            // long mode: staging scratch offset of those channels
 };
 
@@ -269,4 +288,5 @@ int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t
 int configure_fused(slicq_plan *p);  // after configure_kernels: task tables, smem budgets
 int fused_set_attrs(const slicq_plan *p);
 int configure_ring(slicq_plan *p);   // after configure_fused: bands, tasks, ring sizing
+int configure_fwd2(slicq_plan *p);   // after configure_fused: forward channel kernel v2
 }  // namespace slicq
