@@ -96,9 +96,12 @@ enum { SLICQ_WINDOW_HANN = 0, SLICQ_WINDOW_BLACKMAN_HARRIS = 1 };
  *   bins_per_octave  B >= 1
  *   sl_len           2N: divisible by 4 and 2/3/5-smooth.  The CUDA path implements
  *                    2N = 2^12 .. 2^17 (4096 .. 131072; 2N >= 65536 use a four-step FFT
- *                    through the workspace) for every entry point, and 2N = 2^18 .. 2^22
- *                    for the full-length CQ-NSGT (slicq_nsgt_*) only; other valid values
- *                    give SLICQ_EUNSUPPORTED unless SLICQ_PLAN_HOST_ONLY is set.
+ *                    through the workspace) and every other 2/3/5-smooth 2N from 128 to
+ *                    53248 (a mixed-radix in-place FFT in one CTA's shared memory,
+ *                    kernels_generic.cu; e.g. the paper's 12288, 24000, 50000) for
+ *                    every entry point, and 2N = 2^18 .. 2^22 for the full-length CQ-NSGT
+ *                    (slicq_nsgt_*) only; other valid values give SLICQ_EUNSUPPORTED unless
+ *                    SLICQ_PLAN_HOST_ONLY is set.
  *   tr_area          Tukey transition length (the paper's M): even, 2 <= tr < N
  *   rasterize        SLICQ_RASTER_*
  *   out              receives the plan (NULL on failure)

@@ -25,6 +25,7 @@ SOURCES = [("plan.cpp", "plan", ()), ("kernels_host.cu", "kernels_host", ()),
            ("fused_host.cu", "fused_host", ())]
 SOURCES += [("kernels_spec.cu", f"kernels_spec_l{n}", (f"SLICQ_LOGN={n}",)) for n in (11, 12, 13, 14)]
 SOURCES += [("kernels_large.cu", f"kernels_large_l{n}", (f"SLICQ_LOGN={n}",)) for n in (15, 16)]
+SOURCES += [("kernels_generic.cu", "kernels_generic", ())]
 SOURCES += [("kernels_long.cu", "kernels_long", ()), ("kernels_complex.cu", "kernels_complex", ()),
             ("kernels_coeff.cu", "kernels_coeff", ()), ("stream_exec.cpp", "stream_exec", ())]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -318,26 +318,84 @@ int configure_long(slicq_plan *p, int logN) {
 }
 }  // namespace
 
+// generic-length spectrum kernels: the in-place mixed-radix DIT plan of N (radices 16, 8, 4,
+// 2, 3, 5; r_1 the outermost factor), its digit-reversal map and twiddle table
+static int configure_generic(slicq_plan *p) {
+  const int N = (int)p->N;
+  std::vector<int> R;
+  int m = N;
+  for (int r : {16, 8, 4, 2, 3, 5})
+    while (m % r == 0 && (r != 16 || m >= 256)) {
+      R.push_back(r);
+      m /= r;
+    }
+  for (int r : {4, 2})
+    while (m % r == 0) {
+      R.push_back(r);
+      m /= r;
+    }
+  if (m != 1 || (int)R.size() > kGenericMaxPasses)
+    return set_error(SLICQ_EUNSUPPORTED, "slice length is not 2/3/5-smooth");
+  KernelConfig &kc = p->kc;
+  kc.gargs = GArgs{};
+  kc.gargs.N = N;
+  kc.gargs.np = (int)R.size();
+  int S = 1;
+  for (int i = (int)R.size() - 1, q = 0; i >= 0; --i, ++q) {  // innermost factor first
+    kc.gargs.pass[q] = GPass{R[i], S};
+    S *= R[i];
+  }
+  p->gperm.assign(N, 0);
+  for (int n = 0; n < N; ++n) {
+    int rem = n, prod = 1, pos = 0;
+    for (int r : R) {
+      const int j = rem % r;
+      rem /= r;
+      prod *= r;
+      pos += j * (N / prod);
+    }
+    p->gperm[n] = pos;
+  }
+  p->gtw.resize(2 * (size_t)N);
+  for (int t = 0; t < N; ++t) {
+    const double a = -2.0 * 3.14159265358979323846 * (double)t / (double)N;
+    p->gtw[2 * t] = (float)std::cos(a);
+    p->gtw[2 * t + 1] = (float)std::sin(a);
+  }
+  return SLICQ_OK;
+}
+
 int configure_kernels(slicq_plan *p) {
   int logN = 0;
   while ((int64_t(1) << logN) < p->N) ++logN;
-  if ((int64_t(1) << logN) != p->N || !device_supports(logN))
+  const bool pow2 = (int64_t(1) << logN) == p->N;
+  const bool generic = (!pow2 || env_int("SLICQ_GENERIC", 0) != 0) && p->N <= kGenericMaxN &&
+                       p->N >= 64 && p->sampled_from == 0;
+  if (!generic && (!pow2 || !device_supports(logN)))
     return set_error(SLICQ_EUNSUPPORTED,
-                     "CUDA path implements sl_len = 2^12 .. 2^17 (sliCQ) and up to 2^22 "
+                     "CUDA path implements sl_len = 2^12 .. 2^17 and any 2/3/5-smooth sl_len "
+                     "<= " + std::to_string(2 * kGenericMaxN) + " (sliCQ), up to 2^22 "
                      "(full-length CQ-NSGT)");
-  if (logN >= 17) return configure_long(p, logN);
+  if (!generic && logN >= 17) return configure_long(p, logN);
   if (!p->painless)  // the element tables hold one term per fold position
     return set_error(SLICQ_EUNSUPPORTED, "a system with M_k < L_k (sampled_from) needs "
                                          "sl_len >= 2^18 on the device");
   KernelConfig &kc = p->kc;
+  kc.generic = generic;
+  if (generic) {
+    const int rc = configure_generic(p);
+    if (rc != SLICQ_OK) return rc;
+    logN = 0;
+  }
   kc.logN = logN;
-  kc.large = logN >= 15;
-  kc.threads = kc.large ? LT : threads_for(logN);
-  kc.spec_smem = kc.large ? (logN == 15 ? large_smem_bytes<15>() : large_smem_bytes<16>())
-                          : spec_smem_for(logN, (int)p->tr);
+  kc.large = !generic && logN >= 15;
+  kc.threads = generic ? 512 : kc.large ? LT : threads_for(logN);
+  kc.spec_smem = generic ? generic_smem_bytes((int)p->N)
+                 : kc.large ? (logN == 15 ? large_smem_bytes<15>() : large_smem_bytes<16>())
+                            : spec_smem_for(logN, (int)p->tr);
   if (kc.spec_smem > kSmemCap)
     return set_error(SLICQ_EUNSUPPORTED, "spectrum kernel shared memory exceeds 227 KB");
-  if (!kc.large) {
+  if (!kc.large && !kc.generic) {
     switch (logN) {
       case 11: kc.spec_smem_p = spec_persist_smem_bytes<11>((int)p->tr); break;
       case 12: kc.spec_smem_p = spec_persist_smem_bytes<12>((int)p->tr); break;
@@ -739,6 +797,8 @@ int upload(slicq_plan *p) {
       {p->rround.data(), sizeof(int32_t) * p->rround.size(), 0},
       {p->f2pk.data(), sizeof(P2Dev) * p->f2pk.size(), 0},
       {p->f2ch.data(), sizeof(FChan) * p->f2ch.size(), 0},
+      {p->gtw.data(), sizeof(float) * p->gtw.size(), 0},
+      {p->gperm.data(), sizeof(int32_t) * p->gperm.size(), 0},
   };
   size_t o = 0;
   for (Part &pt : parts) {
@@ -784,12 +844,15 @@ int upload(slicq_plan *p) {
   p->d.rround = reinterpret_cast<int32_t *>(b + parts[26].off);
   p->d.f2pk = reinterpret_cast<P2Dev *>(b + parts[27].off);
   p->d.f2ch = reinterpret_cast<FChan *>(b + parts[28].off);
+  p->kc.gargs.twN = reinterpret_cast<const float2 *>(b + parts[29].off);
+  p->kc.gargs.perm = reinterpret_cast<const int *>(b + parts[30].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
   // (the dynamic shared-memory limit: the device cap, allow_max_dyn_smem)
   int rc = 0;
-  switch (p->kc.logN) {
+  if (p->kc.generic) rc = generic_set_attrs();
+  else switch (p->kc.logN) {
     case 11: rc = set_attrs<11>(kSmemCap); break;
     case 12: rc = set_attrs<12>(kSmemCap); break;
     case 13: rc = set_attrs<13>(kSmemCap); break;
@@ -1220,7 +1283,8 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     a.nunits = (int)std::min<int64_t>(w.chunk, units - u0);
     a.stage = pp.stage(stage0, i, w.chunk, std::max(p->kc.xs, p->kc.zs));
     const cudaStream_t st = pp.stream(i);
-    cudaError_t e = !p->kc.large && mode == 0 && p->kc.fwd_persist
+    cudaError_t e = p->kc.generic ? launch_generic(true, a, p->kc.gargs, a.nunits, st, p->kc.pdl, mode)
+                    : !p->kc.large && mode == 0 && p->kc.fwd_persist
                         ? launch_fwd_persist(p, a, st)
                     : !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), st, mode)
                     : p->kc.logN == 15 ? large_forward<15>(a, st, mode)
@@ -1339,7 +1403,9 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     a.stage = pp.stage(stage0, i, w.chunk, std::max(p->kc.xs, p->kc.zs));
     const cudaStream_t st = pp.stream(i);
     cudaError_t e = launch_chan(false, p, a, st);
-    if (e == cudaSuccess && !p->kc.large && mode == 0 && p->kc.inv_persist)
+    if (e == cudaSuccess && p->kc.generic)
+      e = launch_generic(false, a, p->kc.gargs, a.nunits, st, p->kc.pdl, mode);
+    else if (e == cudaSuccess && !p->kc.large && mode == 0 && p->kc.inv_persist)
       e = launch_inv_persist(p, a, st);
     else if (e == cudaSuccess)
       e = !p->kc.large ? launch_spec(false, p, a, dim3((unsigned)a.nunits), st, mode)

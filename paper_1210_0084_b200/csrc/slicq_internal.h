@@ -10,6 +10,7 @@
 
 #include "../../include/slicq.h"
 #include "kernels_long_api.h"
+#include "kernels_generic.h"
 
 namespace slicq {
 
@@ -184,6 +185,9 @@ struct KernelConfig {
   int rR = 0, rnspec = 0, rnchan = 0, rnb = 0, rq = 0, rbt = 0, rla = 0;
   int rxstride = 0, rwmax = 0, rtwmax = 0, rfscr = 0;  // rfscr: item scratch (float2)
   int rgroup = 1, rmeta = 0;  // batches per channel item; largest band metadata (bytes)
+  // generic-length spectrum kernels (kernels_generic.cu): any 2/3/5-smooth N that fits
+  bool generic = false;
+  kern::GArgs gargs{};        // radix plan; device pointers set by upload()
   // forward channel kernel v2 (kernels_chan2.cuh)
   bool fwd2 = false;
   int f2voff[3] = {0, 0, 0};  // packets [f2voff[v], f2voff[v+1]) run in variant v (lite, full)
@@ -241,6 +245,8 @@ struct slicq_plan {
   std::vector<slicq::FChan> rfch;        // ring kernels: channels in band task order
   std::vector<float> rbtw;               // ring kernels: per-band twiddles (re, im)
   std::vector<int32_t> rround;           // ring kernels: per-band round lists
+  std::vector<float> gtw;                // generic kernels: e^{-2 pi i t / N} (re, im), t < N
+  std::vector<int32_t> gperm;            // generic kernels: mixed-radix digit reversal
   std::vector<slicq::P2Dev> f2pk;        // forward channel kernel v2: packets
   std::vector<slicq::FChan> f2ch;        // forward channel kernel v2: channels
   std::vector<int64_t> lsoff;            // long mode: staging scratch offset of those channels

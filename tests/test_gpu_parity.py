@@ -191,6 +191,52 @@ def test_other_slice_lengths(api, args):
         assert rel(y[b], x[b].astype(np.float64)) <= TOL
 
 
+@pytest.mark.parametrize("args", [
+    (44100.0, 60.0, 22050.0, 24, 12288, 1024, 0),     # N = 6144 = 2^11 3
+    (48000.0, 50.0, 24000.0, 48, 24000, 2400, 0),     # N = 12000 = 2^5 3 5^3
+    (44100.0, 40.0, 22050.0, 48, 50000, 4000, 0),     # N = 25000 = 2^3 5^5 (P:597's length)
+    (44100.0, 100.0, 20000.0, 24, 6000, 600, 2),      # N = 3000, fully rasterised
+])
+def test_mixed_radix_slice_lengths(api, args):
+    """2/3/5-smooth slice lengths that are not powers of two (the paper's own slice lengths,
+    P:597): the generic-length spectrum kernels (mixed-radix in-place
+    DIT) with the same channel kernels, every slice and every channel against the oracle,
+    reconstruction, and the range API bit-identical to the full transform."""
+    plan = api.Plan(*args)
+    ref = cqplan.make_plan(*args)
+    n = 5 * args[4] // 2 + 77
+    x = random_signal(int(args[4]) + 7, 2, n)
+    c, _ = check_forward(plan, ref, x)
+    y = plan.inverse(c, n)
+    yn = y.cpu().numpy()
+    for b in range(2):
+        assert rel(yn[b], x[b].astype(np.float64)) <= TOL
+    # inverse of oracle coefficients against the oracle's inverse
+    cr = oslicq.forward(x, ref)
+    yg = plan.inverse(torch.from_numpy(cr.astype(np.complex64)).cuda(), n).cpu().numpy()
+    yr = oslicq.inverse(cr, ref, n)
+    for b in range(2):
+        assert rel(yg[b], yr[b]) <= TOL
+
+
+def test_generic_kernels_match_power_of_two_kernels(api, monkeypatch):
+    """The generic-length kernels forced onto a power-of-two slice (SLICQ_GENERIC=1) agree with
+    the specialised radix-16/32 kernels to fp32 rounding and with the oracle."""
+    args = (44100.0, 65.4, 22050.0, 12, 16384, 2048, 0)
+    n = 70001
+    x = random_signal(4711, 1, n)
+    p0 = api.Plan(*args)
+    monkeypatch.setenv("SLICQ_GENERIC", "1")
+    p1 = api.Plan(*args)
+    monkeypatch.delenv("SLICQ_GENERIC")
+    xt = torch.from_numpy(x).cuda()
+    c0, c1 = p0.forward(xt), p1.forward(xt)
+    assert (torch.linalg.vector_norm(c1 - c0) / torch.linalg.vector_norm(c0)).item() <= 1e-6
+    check_forward(p1, cqplan.make_plan(*args), x)
+    y1 = p1.inverse(c1, n).cpu().numpy()
+    assert rel(y1[0], x[0].astype(np.float64)) <= TOL
+
+
 # ------------------------------------------------------------------ configs 2-4
 def test_cfg2_full(api):
     cfg = CONFIGS[2]
