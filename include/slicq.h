@@ -101,7 +101,9 @@ enum { SLICQ_WINDOW_HANN = 0, SLICQ_WINDOW_BLACKMAN_HARRIS = 1 };
  *                    kernels_generic.cu; e.g. the paper's 12288, 24000, 50000) for
  *                    every entry point, and 2N = 2^18 .. 2^22 for the full-length CQ-NSGT
  *                    (slicq_nsgt_*) only; other valid values give SLICQ_EUNSUPPORTED unless
- *                    SLICQ_PLAN_HOST_ONLY is set.
+ *                    SLICQ_PLAN_HOST_ONLY is set.  Channel lengths: M_k <= 1024 run in the
+ *                    register-DFT channel kernels, 1024 < M_k <= 26000 in one CTA per
+ *                    (channel, unit) with a shared-memory mixed-radix DFT.
  *   tr_area          Tukey transition length (the paper's M): even, 2 <= tr < N
  *   rasterize        SLICQ_RASTER_*
  *   out              receives the plan (NULL on failure)

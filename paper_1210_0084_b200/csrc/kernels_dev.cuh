@@ -170,6 +170,7 @@ struct KArgs {
   int tile;       // units per channel-kernel tile
   int stiles;     // channel kernels: tiles per super-tile (0: the whole chunk)
   int Nh;         // N (half the slice length)
+  const uint2 *bent;  // sliCQ channels with M_k > 1024: inverse term destinations (kernels_long.cuh)
   // coefficients
   int64_t C;
   float2 *coef_out;

@@ -416,10 +416,54 @@ int configure_kernels(slicq_plan *p) {
       fac[M] = {M, 1};
       continue;
     }
-    if (M > 1024 || !factor_m(M, m1, m2))
-      return set_error(SLICQ_EUNSUPPORTED, "channel length M_k = " + std::to_string(M) +
-                                               " is not a product of two DFT sizes <= 32");
+    if (M > 1024 || !factor_m(M, m1, m2)) {
+      // too long for the register-DFT packets: one CTA per (channel, unit) with a
+      // shared-memory mixed-radix DFT (the long-mode channel kernels, kernels_long.cuh)
+      if (M > long_class_maxm(kLongClasses - 2))
+        return set_error(SLICQ_EUNSUPPORTED, "channel length M_k = " + std::to_string(M) +
+                                                 " exceeds the sliCQ channel kernels (26000)");
+      fac[M] = {0, 0};
+      continue;
+    }
     fac[M] = {m1, m2};
+  }
+  // big channels (fac = {0, 0}) by size class; their fp32 weights
+  p->pbig.clear();
+  kc.nbig = 0;
+  {
+    int maxm[kLongClasses] = {};
+    for (int c = 0; c < kLongClasses - 1; ++c) {
+      kc.bcls.off[c] = (int)p->pbig.size();
+      for (int k = 0; k < K2; ++k) {
+        const int M = p->M[k];
+        if (fac[M].first != 0) continue;
+        int cls = 0;
+        while (cls + 1 < kLongClasses - 1 && M > long_class_maxm(cls)) ++cls;
+        if (cls != c) continue;
+        p->pbig.push_back(k);
+        maxm[c] = std::max(maxm[c], M);
+      }
+      kc.bcls.smem[c] = maxm[c] ? sizeof(float2) * (size_t)(padi(maxm[c]) + 1 +
+                                                            long_twiddle_entries(maxm[c]) +
+                                                            kDifPlanEntries)
+                                : 0;
+    }
+    kc.bcls.off[kLongClasses - 1] = kc.bcls.off[kLongClasses] = (int)p->pbig.size();
+    kc.bcls.smem[kLongClasses - 1] = 0;
+    kc.nbig = (int)p->pbig.size();
+    if (kc.nbig && p->lgw.size() != p->g.size()) {
+      p->lgw.assign(p->g.size(), 0.f);
+      p->lgdw.assign(p->g.size(), 0.f);
+      for (int k = 0; k < K2; ++k) {
+        const double sc = 1.0 / std::sqrt((double)p->M[k]);
+        const double half = (k == 0 || k == K2 - 1) ? 0.5 : 1.0;
+        for (int d = 0; d < p->len[k]; ++d) {
+          const int64_t e = p->goff[k] + d;
+          p->lgw[e] = (float)(p->g[e] * sc);
+          p->lgdw[e] = (float)(p->gdual[e] * sc * half);
+        }
+      }
+    }
   }
 
   // ---------------- packets: runs of consecutive channels of one length
@@ -431,6 +475,10 @@ int configure_kernels(slicq_plan *p) {
   std::vector<Pk> pks;
   for (int k = 0; k < K2;) {
     const int M = p->M[k];
+    if (fac[M].first == 0) {  // big channel (above)
+      ++k;
+      continue;
+    }
     const bool small = M <= kSmallMax && in_small(M);
     const int m1 = fac[M].first, m2 = fac[M].second;
     const int nch = small ? std::min(32, kSmallCap / M) : std::max(1, 32 / std::max(m1, m2));
@@ -532,6 +580,19 @@ int configure_kernels(slicq_plan *p) {
     kc.nover = start;
     if (2 * zso + start >= (int64_t(1) << 18))
       return set_error(SLICQ_EUNSUPPORTED, "slice too long for the inverse element tables");
+  }
+
+  // ---------------- big channels: their terms' destinations (kernels_long.cuh
+  // long_chan_inv_slots): (dst | conj << 31, d | zero << 31)
+  p->bent.clear();
+  p->bentoff.assign(K2, 0);
+  p->bentn.assign(K2, 0);
+  for (int k : p->pbig) {
+    p->bentoff[k] = (int)p->bent.size();
+    for (const Dst &ds : dsts[k])
+      p->bent.push_back(make_uint2(ds.dst | ((uint32_t)ds.conj << 31),
+                                   (uint32_t)ds.d | ((ds.zero ? 1u : 0u) << 31)));
+    p->bentn[k] = (int)p->bent.size() - p->bentoff[k];
   }
 
   // ---------------- element tables
@@ -713,6 +774,9 @@ int upload(slicq_plan *p) {
     if (p->kc.longmode) {
       c.m1 = p->lm1[k];
       c.soff = (int32_t)p->lsoff[k];
+    } else if (!p->bentn.empty() && p->bentn[k]) {  // big sliCQ channel: its term destinations
+      c.m1 = p->bentn[k];
+      c.soff = p->bentoff[k];
     }
   }
   std::vector<float> h0(N2), h0d(N2);
@@ -799,6 +863,8 @@ int upload(slicq_plan *p) {
       {p->f2ch.data(), sizeof(FChan) * p->f2ch.size(), 0},
       {p->gtw.data(), sizeof(float) * p->gtw.size(), 0},
       {p->gperm.data(), sizeof(int32_t) * p->gperm.size(), 0},
+      {p->pbig.data(), sizeof(int32_t) * p->pbig.size(), 0},
+      {p->bent.data(), sizeof(uint2) * p->bent.size(), 0},
   };
   size_t o = 0;
   for (Part &pt : parts) {
@@ -846,12 +912,15 @@ int upload(slicq_plan *p) {
   p->d.f2ch = reinterpret_cast<FChan *>(b + parts[28].off);
   p->kc.gargs.twN = reinterpret_cast<const float2 *>(b + parts[29].off);
   p->kc.gargs.perm = reinterpret_cast<const int *>(b + parts[30].off);
+  p->d.pbig = reinterpret_cast<int32_t *>(b + parts[31].off);
+  p->d.bent = reinterpret_cast<uint2 *>(b + parts[32].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
   // (the dynamic shared-memory limit: the device cap, allow_max_dyn_smem)
   int rc = 0;
-  if (p->kc.generic) rc = generic_set_attrs();
+  if (rc == 0 && p->kc.nbig) rc = slice_big_attrs();
+  if (p->kc.generic) rc = rc ? rc : generic_set_attrs();
   else switch (p->kc.logN) {
     case 11: rc = set_attrs<11>(kSmemCap); break;
     case 12: rc = set_attrs<12>(kSmemCap); break;
@@ -971,6 +1040,7 @@ int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t
   if (p->kc.band && direction == 0 && !p->kc.large) return (int)(chunks * 2);
   int nchan = 0;
   for (int v = 0; v < 3; ++v) nchan += p->kc.voff[v + 1] > p->kc.voff[v];
+  for (int c = 0; c + 1 < kLongClasses; ++c) nchan += p->kc.bcls.off[c + 1] > p->kc.bcls.off[c];
   const int nspec = !p->kc.large ? 1 : direction == 0 ? 2 : 4;
   return (int)(chunks * (nchan + nspec));
 }
@@ -1010,6 +1080,7 @@ static KArgs base_args(const slicq_plan *p) {
   a.tile = p->kc.tile;
   a.stiles = p->kc.stiles;
   a.Nh = (int)p->N;
+  a.bent = p->d.bent;
   a.gw = p->d.gw;
   a.gdw = p->d.gdw;
   a.lrow = p->d.lrow;
@@ -1314,6 +1385,7 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
     } else if (e == cudaSuccess) {
       e = launch_chan(true, p, a, st);
     }
+    if (e == cudaSuccess && p->kc.nbig) e = slice_big_launch(true, a, p->d.pbig, p->kc.bcls, st);
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));
   }
@@ -1403,6 +1475,7 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     a.stage = pp.stage(stage0, i, w.chunk, std::max(p->kc.xs, p->kc.zs));
     const cudaStream_t st = pp.stream(i);
     cudaError_t e = launch_chan(false, p, a, st);
+    if (e == cudaSuccess && p->kc.nbig) e = slice_big_launch(false, a, p->d.pbig, p->kc.bcls, st);
     if (e == cudaSuccess && p->kc.generic)
       e = launch_generic(false, a, p->kc.gargs, a.nunits, st, p->kc.pdl, mode);
     else if (e == cudaSuccess && !p->kc.large && mode == 0 && p->kc.inv_persist)

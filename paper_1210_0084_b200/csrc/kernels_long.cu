@@ -104,6 +104,36 @@ static cudaError_t inv_logn(const KArgs &a, const LongClasses &cls, cudaStream_t
   return e;
 }
 
+static void (*big_kernel(bool fwd, int c))(const KArgs) {
+  switch (c) {
+    case 0: return fwd ? long_chan_fwd<long_class_threads(0)> : long_chan_inv_slots<long_class_threads(0)>;
+    case 1: return fwd ? long_chan_fwd<long_class_threads(1)> : long_chan_inv_slots<long_class_threads(1)>;
+  }
+  return fwd ? long_chan_fwd<512> : long_chan_inv_slots<512>;
+}
+
+int slice_big_attrs() {
+  cudaError_t e = cudaSuccess;
+  for (int c = 0; c < kLongClasses - 1 && e == cudaSuccess; ++c)
+    for (int f = 0; f < 2 && e == cudaSuccess; ++f)
+      e = allow_max_dyn_smem((const void *)big_kernel(f == 0, c));
+  return (int)e;
+}
+
+cudaError_t slice_big_launch(bool fwd, KArgs a, const int32_t *list, const LongClasses &cls,
+                             cudaStream_t s) {
+  a.L = 2 * (int64_t)a.Nh;  // long_chan_fwd reads 2N from L
+  for (int c = 0; c < kLongClasses - 1; ++c) {
+    const int n = cls.off[c + 1] - cls.off[c];
+    if (!n) continue;
+    a.pchans = list + cls.off[c];
+    const cudaError_t e = pdl_launch(big_kernel(fwd, c), a, dim3((unsigned)n, (unsigned)a.nunits),
+                                     long_class_threads(c), cls.smem[c], s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t long_forward(int logN, const KArgs &a, const LongClasses &cls, cudaStream_t s) {
   switch (logN) {
     case 17: return fwd_logn<17>(a, cls, s);

@@ -390,6 +390,40 @@ __global__ void __launch_bounds__(T, 65536 / (64 * T)) long_chan_inv(const KArgs
   pdl_trigger();
 }
 
+// sliCQ channels too long for the register-DFT packets (M_k > 1024; split design): Alg. 2 per
+// channel as long_chan_inv, the terms going to their slots of the unit's half-spectrum staging
+// (slot arrays / overflow, the destinations the plan assigned to every (channel, d) term with the
+// Hermitian rule C15) -- entries a.bent[ch.soff .. + ch.m1): (dst | conj << 31, d | zero << 31)
+template <int T>
+__global__ void __launch_bounds__(T, 65536 / (64 * T)) long_chan_inv_slots(const KArgs a) {
+  extern __shared__ float4 smem4[];
+  float2 *buf = reinterpret_cast<float2 *>(smem4);
+  const ChanDev ch = a.chan[a.pchans[blockIdx.x]];
+  const int64_t ul = blockIdx.y, row = a.unit0 + ul;
+  const int M = ch.M;
+  pdl_wait();
+  const float2 *in = a.coef_in + row * a.C + ch.off;
+  float2 *tws = long_tw_ptr(buf, M);
+  DifPlan &pl = *long_plan_ptr(buf, M);
+  if (threadIdx.x == 0) build_dif_plan(pl, M);
+  load_twiddles<T>(tws, a.twM + ch.twoff, M);
+  for (int m = threadIdx.x; m < M; m += T) buf[padi(m)] = __ldcs(in + m);
+  __syncthreads();
+  dif_fft<-1, T>(buf, M, tws, pl);
+  float2 *Z = a.stage + ul * a.zs;
+  for (int e = threadIdx.x; e < ch.m1; e += T) {
+    const uint2 en = __ldg(a.bent + ch.soff + e);
+    const int dd = (int)(en.y & 0x7fffffffu);
+    int q = ch.lo_mod + dd;
+    if (q >= M) q -= M;
+    const float2 F = buf[padi(dif_pos(q, pl))];
+    const float w = (en.y >> 31) ? 0.f : __ldg(a.gdw + ch.goff + dd);
+    const bool cj = en.x >> 31;
+    __stcs(Z + (en.x & 0x7fffffffu), make_float2(F.x * w, cj ? -F.y * w : F.y * w));
+  }
+  pdl_trigger();
+}
+
 // ------------------------------------------------------------------ M_k > 26000
 // Four-step M = M1 M2 (M2 <= 26000): q = M2 n1 + n2, k = k1 + M1 k2,
 //   Y[k1 + M1 k2] = sum_n2 w_M2^{n2 k2} w_M^{n2 k1} sum_n1 y[M2 n1 + n2] w_M1^{n1 k1}

@@ -52,5 +52,10 @@ struct LongClasses {
 int long_set_attrs(int logN, const LongClasses &cls);
 cudaError_t long_forward(int logN, const KArgs &a, const LongClasses &cls, cudaStream_t s);
 cudaError_t long_inverse(int logN, const KArgs &a, const LongClasses &cls, cudaStream_t s);
+// sliCQ channels with M_k > 1024 (split design): one CTA per (channel, unit), size classes 0..3
+// (M_k <= 26000); forward reads the staged X, inverse writes the slot staging (a.bent)
+int slice_big_attrs();
+cudaError_t slice_big_launch(bool fwd, KArgs a, const int32_t *list, const LongClasses &cls,
+                             cudaStream_t s);
 }  // namespace kern
 }  // namespace slicq

@@ -137,6 +137,8 @@ struct DeviceTables {
   FChan *rfch = nullptr;    // ring kernels: channels (band-local weight / twiddle offsets)
   float2 *rbtw = nullptr;   // ring kernels: per-band twiddle tables
   int32_t *rround = nullptr; // ring kernels: per-band round lists (task << 16 | round)
+  int32_t *pbig = nullptr;   // sliCQ channels with M_k > 1024, by size class
+  uint2 *bent = nullptr;     // their inverse term destinations
   P2Dev *f2pk = nullptr;     // forward channel kernel v2: packets
   FChan *f2ch = nullptr;     // forward channel kernel v2: channels in packet order
   void *block = nullptr;    // single allocation holding all of the above
@@ -185,6 +187,9 @@ struct KernelConfig {
   int rR = 0, rnspec = 0, rnchan = 0, rnb = 0, rq = 0, rbt = 0, rla = 0;
   int rxstride = 0, rwmax = 0, rtwmax = 0, rfscr = 0;  // rfscr: item scratch (float2)
   int rgroup = 1, rmeta = 0;  // batches per channel item; largest band metadata (bytes)
+  // sliCQ channels with M_k > 1024 (kernels_long.cuh, one CTA per channel and unit)
+  int nbig = 0;
+  kern::LongClasses bcls{};
   // generic-length spectrum kernels (kernels_generic.cu): any 2/3/5-smooth N that fits
   bool generic = false;
   kern::GArgs gargs{};        // radix plan; device pointers set by upload()
@@ -245,6 +250,9 @@ struct slicq_plan {
   std::vector<slicq::FChan> rfch;        // ring kernels: channels in band task order
   std::vector<float> rbtw;               // ring kernels: per-band twiddles (re, im)
   std::vector<int32_t> rround;           // ring kernels: per-band round lists
+  std::vector<int32_t> pbig;             // sliCQ channels with M_k > 1024 (by size class)
+  std::vector<uint2> bent;               // their term destinations
+  std::vector<int> bentoff, bentn;       // per channel: first entry, count
   std::vector<float> gtw;                // generic kernels: e^{-2 pi i t / N} (re, im), t < N
   std::vector<int32_t> gperm;            // generic kernels: mixed-radix digit reversal
   std::vector<slicq::P2Dev> f2pk;        // forward channel kernel v2: packets
