@@ -169,6 +169,7 @@ struct KArgs {
   int nunits;
   int tile;       // units per channel-kernel tile
   int stiles;     // channel kernels: tiles per super-tile (0: the whole chunk)
+  int pf;         // persistent inverse spectrum kernel: L2 prefetch of the next unit (0 off)
   int Nh;         // N (half the slice length)
   const uint2 *bent;  // sliCQ channels with M_k > 1024: inverse term destinations (kernels_long.cuh)
   // coefficients
@@ -1391,14 +1392,14 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
   pdl_wait();  // contributions of this chunk come from the channel kernel
   const int64_t G = gridDim.x;
   const int64_t ub = blockIdx.x * (int64_t)a.nunits / G, ue = (blockIdx.x + 1) * (int64_t)a.nunits / G;
-  if (ub < ue) prefetch_l2(a.stage + ub * a.zs, a.zs * 8, tid, T);
+  if (a.pf && ub < ue) prefetch_l2(a.stage + ub * a.zs, a.zs * 8, tid, T);
   __syncthreads();
   for (int64_t ul = ub; ul < ue; ++ul) {
     const int64_t u = a.unit0 + ul;
     const int mloc = (int)(u % a.nslices);
     const bool ll = ul > ub && mloc > 0;                    // unit ul - 1 is slice mloc - 1
     const bool rl = ul + 1 < ue && mloc + 1 < a.nslices;  // unit ul + 1 is slice mloc + 1
-    if (ul + 1 < ue) prefetch_l2(a.stage + (ul + 1) * a.zs, a.zs * 8, tid, T);
+    if (a.pf && ul + 1 < ue) prefetch_l2(a.stage + (ul + 1) * a.zs, a.zs * 8, tid, T);
     inv_unit<LOGN, 0>(a, spec, tw, htab, carry, ul, ll, rl);
     __syncthreads();  // (spec and carry reused by the next unit)
   }

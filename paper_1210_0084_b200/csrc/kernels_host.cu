@@ -716,6 +716,7 @@ int configure_kernels(slicq_plan *p) {
   }
   kc.tile = (int)std::max<int64_t>(1, env_int("SLICQ_TILE", 128));
   kc.stiles = (int)std::max<int64_t>(0, env_int("SLICQ_STILES", 0));
+  kc.pf = (int)env_int("SLICQ_INV_PF", 0);
   kc.chan_per_sm = (int)env_int("SLICQ_CHAN_PER_SM", 0);  // dev override: 0 = occupancy
   // staging is sized for one chunk of units; calls with more units run chunk by chunk
   // (each chunk costs kernel tails, so the default budget keeps every BASELINE config in a
@@ -1079,6 +1080,7 @@ static KArgs base_args(const slicq_plan *p) {
   a.zs = p->kc.zs;
   a.tile = p->kc.tile;
   a.stiles = p->kc.stiles;
+  a.pf = p->kc.pf;
   a.Nh = (int)p->N;
   a.bent = p->d.bent;
   a.gw = p->d.gw;

@@ -166,6 +166,9 @@ struct KernelConfig {
   int64_t chunk_units = 0;    // units per chunk (staging is sized for one chunk)
   int tile = 16;              // units per channel-kernel tile
   int stiles = 0;             // channel kernels: tiles per super-tile (0: the whole chunk)
+  int pf = 0;                 // persistent inverse spectrum kernel: L2 prefetch of the next unit
+                              // (SLICQ_INV_PF; measured: off is 2 % faster on cfg4, the prefetched
+                              // slots were evicted before use -- 1.6 GB of re-reads per call)
   int chan_per_sm = 0;        // channel-kernel CTAs per SM cap (0: occupancy)
   bool pipe = false;          // chunks alternate between two streams, ping-pong staging
   bool pdl = true;            // launch with programmatic stream serialization
