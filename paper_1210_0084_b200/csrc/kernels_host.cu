@@ -931,6 +931,12 @@ int upload(slicq_plan *p) {
     case 16: rc = large_set_attrs<16>(); break;
     default: rc = long_set_attrs(p->kc.logN, p->kc.lcls); break;
   }
+  // 2N = 131072: the four-step slice FFT on a 16-CTA cluster (DSMEM transpose) when the
+  // device can co-schedule it; SLICQ_LCLUSTER bit 0 forward, bit 1 inverse (0: the split
+  // column / row kernels through the staging buffer)
+  p->kc.lcluster = 0;
+  if (rc == 0 && !p->kc.generic && p->kc.logN == 16 && large_cluster_ok<16>())
+    p->kc.lcluster = (int)(env_int("SLICQ_LCLUSTER", 3) & 3);
   if (rc == 0 && p->kc.ftables) rc = fused_set_attrs(p);
   if (rc == 0 && p->kc.fwd2) {
     rc = (int)allow_max_dyn_smem((const void *)slicq_fwd_chan2_kernel<kLiteMax, kLiteMinB>);
@@ -1042,7 +1048,9 @@ int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t
   int nchan = 0;
   for (int v = 0; v < 3; ++v) nchan += p->kc.voff[v + 1] > p->kc.voff[v];
   for (int c = 0; c + 1 < kLongClasses; ++c) nchan += p->kc.bcls.off[c + 1] > p->kc.bcls.off[c];
-  const int nspec = !p->kc.large ? 1 : direction == 0 ? 2 : 4;
+  const int nspec = !p->kc.large ? 1
+                    : direction == 0 ? ((p->kc.lcluster & 1) ? 1 : 2)
+                                     : ((p->kc.lcluster & 2) ? 2 : 4);
   return (int)(chunks * (nchan + nspec));
 }
 
@@ -1361,7 +1369,7 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
                         ? launch_fwd_persist(p, a, st)
                     : !p->kc.large ? launch_spec(true, p, a, dim3((unsigned)a.nunits), st, mode)
                     : p->kc.logN == 15 ? large_forward<15>(a, st, mode)
-                                       : large_forward<16>(a, st, mode);
+                                       : large_forward<16>(a, st, mode, p->kc.lcluster & 1);
     if (e == cudaSuccess && p->kc.band && !p->kc.large) {
       // band-major channel kernel (kernels_ring.cuh): claim counter per chunk in the
       // (forward-unused) pairing-counter area of the workspace
@@ -1485,7 +1493,7 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
     else if (e == cudaSuccess)
       e = !p->kc.large ? launch_spec(false, p, a, dim3((unsigned)a.nunits), st, mode)
           : p->kc.logN == 15 ? large_inverse_spec<15>(a, st, mode)
-                             : large_inverse_spec<16>(a, st, mode);
+                             : large_inverse_spec<16>(a, st, mode, (p->kc.lcluster & 2) != 0);
     if (e != cudaSuccess)
       return set_error(SLICQ_ECUDA, std::string("inverse launch: ") + cudaGetErrorString(e));
   }

@@ -439,9 +439,11 @@ constexpr size_t large_smem_bytes() {
 template <int LOGN>
 int large_set_attrs();
 template <int LOGN>
-cudaError_t large_forward(const KArgs &a, cudaStream_t s, int mode = 0);
+cudaError_t large_forward(const KArgs &a, cudaStream_t s, int mode = 0, bool cluster = false);
 template <int LOGN>
-cudaError_t large_inverse_spec(const KArgs &a, cudaStream_t s, int mode = 0);
+cudaError_t large_inverse_spec(const KArgs &a, cudaStream_t s, int mode = 0, bool cluster = false);
+template <int LOGN>
+bool large_cluster_ok();  // the 16-CTA cluster kernels can be resident (2N = 131072)
 
 }  // namespace kern
 }  // namespace slicq

@@ -166,6 +166,7 @@ struct KernelConfig {
   int64_t chunk_units = 0;    // units per chunk (staging is sized for one chunk)
   int tile = 16;              // units per channel-kernel tile
   int stiles = 0;             // channel kernels: tiles per super-tile (0: the whole chunk)
+  int lcluster = 0;           // 2N = 131072 slice FFT on 16-CTA clusters: bit 0 fwd, 1 inv
   int pf = 0;                 // persistent inverse spectrum kernel: L2 prefetch of the next unit
                               // (SLICQ_INV_PF; measured: off is 2 % faster on cfg4, the prefetched
                               // slots were evicted before use -- 1.6 GB of re-reads per call)

@@ -345,6 +345,36 @@ def test_cfg5_sampled(api):
     assert rel(y[0, a0:b0], yr) <= TOL
 
 
+@pytest.mark.gpu
+def test_cfg5_cluster_fft_bit_identical_to_split(api, monkeypatch):
+    """2N = 131072: the 16-CTA cluster slice FFT (kernels_large_cluster.cuh, DSMEM transpose)
+    computes exactly what the split column / row kernels compute (same arithmetic, same
+    order): bit-identical coefficients and outputs, full and slice-range calls."""
+    cfg = CONFIGS[5]
+    n = 7 * 65536 + 1234
+    x = torch.from_numpy(random_signal(55, 3, n)).cuda()
+    out = {}
+    for flag in ("0", "3"):
+        monkeypatch.setenv("SLICQ_LCLUSTER", flag)
+        plan = api.plan_for_config(cfg)
+        c = plan.forward(x)
+        y = plan.inverse(c, n)
+        N, S = plan.N, c.shape[1]
+        halo = plan.halo + (plan.halo & 1)
+        xl = torch.zeros((3, halo + 4 * N), dtype=torch.float32, device=x.device)
+        xl[:, halo:] = x[:, N:5 * N]
+        xl[:, :halo] = x[:, N - halo:N]
+        cr = plan.forward_range(xl, halo, 1, 4, S)
+        yr, sp = plan.inverse_range(cr, 1, 4, S, halo)
+        torch.cuda.synchronize()
+        out[flag] = (c, y, cr, yr, sp, plan.kernel_launches("forward", S, 3),
+                     plan.kernel_launches("inverse", S, 3))
+    a, b = out["0"], out["3"]
+    assert b[5] < a[5] and b[6] < a[6], "cluster path not selected"
+    for i in range(5):
+        assert torch.equal(a[i], b[i]), i
+
+
 # ------------------------------------------------------------------ slice-range API
 @pytest.mark.parametrize("G", [2, 3])
 def test_range_api_matches_full(api, G):
