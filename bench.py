@@ -336,9 +336,18 @@ def run_gpu(args, cfg):
     # the dominant direction; each C-ABI call is one spectrum kernel + the channel kernel
     # variants its packets need (lite <16,3> and full <32,2>)
     dom = "slicq_inverse" if ms_i >= ms_f else "slicq_forward"
-    kernels = ("slicq_inv_chan_kernel (lite + full variants) + slicq_inv_spec_kernel"
+    # (the spectrum kernel by slice length: persistent single-CTA for 2N = 2^12..2^15, the
+    # mixed-radix generic kernel, four-step for 2^16, 16-CTA cluster for 2^17)
+    spec = {"slicq_inverse": ("slicq_inv_spec_persist_kernel", "slicq_inv_spec_generic",
+                              "inv_large_pack/col/row + inv_large_bnd",
+                              "inv_large_cluster + inv_large_bnd"),
+            "slicq_forward": ("slicq_fwd_spec_kernel", "slicq_fwd_spec_generic",
+                              "fwd_large_col/row", "fwd_large_cluster")}[dom]
+    sl = plan.sl_len
+    si = 3 if sl == 131072 else 2 if sl == 65536 else 0 if sl & (sl - 1) == 0 else 1
+    kernels = (f"slicq_inv_chan_kernel (lite + full variants) + {spec[si]}"
                if dom == "slicq_inverse"
-               else "slicq_fwd_spec_kernel + slicq_fwd_chan_kernel (lite + full variants)")
+               else f"{spec[si]} + slicq_fwd_chan_kernel (lite + full variants)")
     ms_dom = max(ms_i, ms_f)
     achieved = (bytes_inv if dom == "slicq_inverse" else bytes_fwd) / (ms_dom / 1e3) / 1e9
     traffic = None

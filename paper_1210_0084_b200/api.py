@@ -328,9 +328,13 @@ class Plan:
         slice0*N - halo + i  ->  complex64 [batch][nslices][C]."""
         if x_local.dim() == 1:
             x_local = x_local[None]
-        _check_tensor(x_local, torch.float32, "x_local")
+        # rows may be strided (a view into a wider buffer: the shard's boundary slice)
+        _check_rows(x_local, torch.float32, "x_local", tuple(x_local.shape))
         B, xl = x_local.shape
-        xl = xl if x_len is None else x_len
+        if x_len is not None:
+            if not 0 < x_len <= xl:
+                raise ValueError(f"x_len {x_len} outside (0, {xl}]")
+            xl = x_len
         if out is None:
             out = torch.empty((B, nslices, self.coeffs_per_slice), dtype=torch.complex64,
                               device=x_local.device)

@@ -40,6 +40,14 @@ def slice_bounds(S: int, world: int):
     return [r * S // world for r in range(world + 1)]
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 class SliceRangeShard:
     """This rank's share of a sliCQ forward/inverse over one long stream."""
 
@@ -116,53 +124,82 @@ class SliceRangeShard:
 
     # ------------------------------------------------------------ transform
     def forward(self, xl: torch.Tensor) -> torch.Tensor:
-        """Coefficients of slices [s0, s1): [batch][ns][C].  The halo transfer is posted first
-        and runs while the interior slices [s0 + 1, s1) -- which read own samples only, since
-        the window reaches (N + tr)/2 - 1 < N samples left of a slice -- are transformed; the
-        boundary slice s0 goes last."""
+        """Coefficients of slices [s0, s1): [batch][ns][C].  The halo transfer is posted first;
+        the interior slices [s0 + 1, s1) -- which read own samples only, since the window
+        reaches (N + tr)/2 - 1 < N samples left of a slice -- are transformed while it is in
+        flight.  On the GPU the boundary slice s0 runs on a side stream gated
+        on the halo's arrival, so its kernels overlap the interior's instead of following
+        them; on CPU tensors (gloo tests) it simply goes last."""
         h, N, B = self.halo, self.N, self.batch
         tail = xl[:, -h:].contiguous()
         head = torch.empty_like(tail)
-        works = self._p2p_start(tail, (self.rank + 1) % self.world, head,
-                                (self.rank - 1) % self.world)
-        views = B == 1  # [1][ns][C]: both slice ranges are contiguous views of one buffer
         c = None
-        if views:
-            c = torch.empty((B, self.ns, self.b.C), dtype=torch.complex64, device=xl.device) \
-                if hasattr(self.b, "C") else None
+        if B == 1 and hasattr(self.b, "C"):  # both slice ranges are views of one buffer
+            c = torch.empty((B, self.ns, self.b.C), dtype=torch.complex64, device=xl.device)
+        side = torch.cuda.Stream(device=xl.device) if xl.is_cuda else None
+        if side is not None:
+            side.wait_stream(torch.cuda.current_stream(xl.device))
+            with torch.cuda.stream(side):  # halo exchange + boundary slice
+                works = self._p2p_start(tail, (self.rank + 1) % self.world, head,
+                                        (self.rank - 1) % self.world)
+                self._wait(works)
+                xl[:, :h] = head
+                cb = self.b.forward_range(xl[:, :h + N], h, self.s0, 1, self.S,
+                                          out=c[:, :1] if c is not None else None)
+        else:
+            works = self._p2p_start(tail, (self.rank + 1) % self.world, head,
+                                    (self.rank - 1) % self.world)
         ci = None
         if self.ns > 1:  # interior: entry i of xl[:, N:] is sample (s0 + 1) N - h + i
             ci = self.b.forward_range(xl[:, N:], h, self.s0 + 1, self.ns - 1, self.S,
                                       out=c[:, 1:] if c is not None else None)
-        self._wait(works)
-        xl[:, :h] = head
-        cb = self.b.forward_range(xl[:, :h + N], h, self.s0, 1, self.S,
-                                  out=c[:, :1] if c is not None else None)
+        if side is not None:
+            torch.cuda.current_stream(xl.device).wait_stream(side)
+            for t in (xl, head, tail, cb):
+                t.record_stream(side)
+        else:
+            self._wait(works)
+            xl[:, :h] = head
+            cb = self.b.forward_range(xl[:, :h + N], h, self.s0, 1, self.S,
+                                      out=c[:, :1] if c is not None else None)
         if c is not None:
             return c
         return cb if ci is None else torch.cat([cb, ci], dim=1)
 
     def inverse(self, c_local: torch.Tensor) -> torch.Tensor:
         """Overlap-added output of samples [s0 N, s1 N): [batch][ns N].  The boundary slice s0
-        is synthesised first so that its left spill travels to rank r-1 while the interior
-        slices are synthesised; the interior's own left spill lands on slice s0's tail, and
-        rank r+1's spill on this range's tail last."""
+        is synthesised first (on the GPU: on a side stream, concurrently with the interior)
+        so that its left spill travels to rank r-1 while the interior slices are
+        synthesised; the interior's own left spill lands on slice s0's tail, and rank r+1's
+        spill on this range's tail last."""
         h, N = self.halo, self.N
         rdt = torch.float64 if c_local.dtype == torch.complex128 else torch.float32
         y = torch.empty((self.batch, self.ns * N), dtype=rdt, device=c_local.device)
-        cb = c_local[:, :1] if self.batch == 1 else c_local[:, :1].contiguous()
-        yb, spill0 = self.b.inverse_range(cb, self.s0, 1, self.S, h, y_local=y[:, :N])
-        if yb.data_ptr() != y.data_ptr():
-            y[:, :N] = yb
-        recv = torch.empty_like(spill0)
-        works = self._p2p_start(spill0.contiguous(), (self.rank - 1) % self.world, recv,
-                                (self.rank + 1) % self.world)
+        side = torch.cuda.Stream(device=c_local.device) if c_local.is_cuda else None
+        cur = torch.cuda.current_stream(c_local.device) if side is not None else None
+        if side is not None:
+            side.wait_stream(cur)
+        ctx = torch.cuda.stream(side) if side is not None else _nullctx()
+        with ctx:  # boundary slice, then its spill to rank r-1
+            cb = c_local[:, :1] if self.batch == 1 else c_local[:, :1].contiguous()
+            yb, spill0 = self.b.inverse_range(cb, self.s0, 1, self.S, h, y_local=y[:, :N])
+            if yb.data_ptr() != y.data_ptr():
+                y[:, :N] = yb
+            recv = torch.empty_like(spill0)
+            works = self._p2p_start(spill0.contiguous(), (self.rank - 1) % self.world, recv,
+                                    (self.rank + 1) % self.world)
+        spill1 = None
         if self.ns > 1:
             ci = c_local[:, 1:] if self.batch == 1 else c_local[:, 1:].contiguous()
             yi, spill1 = self.b.inverse_range(ci, self.s0 + 1, self.ns - 1, self.S, h,
                                               y_local=y[:, N:])
             if yi.data_ptr() != y[:, N:].data_ptr():
                 y[:, N:] = yi
+        if side is not None:
+            cur.wait_stream(side)  # (slice s0's samples complete before the spill lands)
+            for t in (y, recv, spill0, c_local):
+                t.record_stream(side)
+        if spill1 is not None:
             self.b.overlap_add(y[:, N - h:N], spill1)
         self._wait(works)
         self.b.overlap_add(y[:, -h:], recv)
