@@ -212,6 +212,7 @@ struct KArgs {
   const int32_t *ovl;   // inverse: overflow slot lists
   int nov;              // inverse: overflow slots per unit
   int vec16;            // coefficient rows are 16-byte aligned (vector stores / loads)
+  int tbe;              // TMA-staged channel kernels: per-warp buffer entries (kernels_tb.cuh)
 };
 
 
@@ -538,7 +539,8 @@ __device__ SLICQ_INV2_INLINE void inv_step2(float2 *reg, int m1, int nch, unsign
   }
 }
 
-// Small inverse packet: lane vc loads virtual channel vc, FFT_M, F[q] -> scratch q*nv + vc.
+// Small inverse packet: lane vc loads virtual channel vc, FFT_M, F[q] -> scratch q*nv + vc
+// (nv odd: the term scatter's reads of consecutive q are bank-conflict free).
 template <int M, int V, int MK = 0>  // V: channel-kernel variant; MK: fused mask mode
 __device__ SLICQ_INVS_INLINE void inv_small(const float2 *in_row, float2 *reg, int nvc, int nv,
                                           int off_lane, int lane, const float *mrow = nullptr) {
@@ -718,7 +720,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
       if (small) {
         switch (m1) {
 #define X_(S) \
-  case S: if constexpr (S <= MAXS) inv_small<S, MAXS, MK>(in_row, scr, nvc, nu * r, c_off, lane, mrow); break;
+  case S: if constexpr (S <= MAXS) inv_small<S, MAXS, MK>(in_row, scr, nvc, (nu * r) | 1, c_off, lane, mrow); break;
           SLICQ_SMALL(X_)
 #undef X_
         }

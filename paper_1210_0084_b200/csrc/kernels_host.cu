@@ -16,6 +16,7 @@
 #include "kernels_fused.cuh"
 #include "kernels_ring.cuh"
 #include "kernels_chan2.cuh"
+#include "kernels_tb.cuh"
 #include "kernels_large.cuh"
 #include "kernels_long_api.h"
 
@@ -185,6 +186,14 @@ static ChanFn chan_fn(bool fwd, int variant, int mask = 0) {
     case 2: return inv_fn<2>(variant);
   }
   return inv_fn<0>(variant);
+}
+// TMA-staged channel kernels (kernels_tb.cuh); variant 0 (micro) runs as lite
+static ChanFn tb_fn(bool fwd, int variant) {
+  if (fwd)
+    return variant <= 1 ? slicq_fwd_chan_tb_kernel<kLiteMax, kLiteMinB>
+                        : slicq_fwd_chan_tb_kernel<kFullMax, kFullMinB>;
+  return variant <= 1 ? slicq_inv_chan_tb_kernel<kLiteMax, kLiteMinBInv>
+                      : slicq_inv_chan_tb_kernel<kFullMax, kFullMinB>;
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -466,6 +475,20 @@ int configure_kernels(slicq_plan *p) {
     }
   }
 
+  // X(j) = X[b] or conj(X[b]) for real input
+  auto bin_of = [&](int j, int &conj) {
+    int jj = j % N2;
+    if (jj < 0) jj += N2;
+    conj = jj > N;
+    return jj > N ? N2 - jj : jj;
+  };
+  // TMA-staged channel kernels (kernels_tb.cuh): a warp task's operand block (forward: the
+  // packet's bins for nu units; inverse: its coefficient columns for nu units) must fit the
+  // per-warp buffer; nu is capped so that it does (SLICQ_TB_CAP entries)
+  kc.tb = env_int("SLICQ_TB", 0) != 0;  // opt-in: measured slower
+  const int tb_cap = (int)env_int("SLICQ_TB_CAP", 600);
+  kc.tbe_f = kc.tbe_i = 0;
+
   // ---------------- packets: runs of consecutive channels of one length
   struct Pk {
     PacketDev d;
@@ -492,12 +515,29 @@ int configure_kernels(slicq_plan *p) {
     const int r = (int)pk.ks.size();
     pk.d.nch = r;
     // units per warp task: fill the lanes (short runs of one M would leave them idle)
-    const int nu = small ? std::max(1, std::min(32 / r, kSmallCap / (r * M)))
-                         : std::max(1, 32 / (r * std::max(m1, m2)));
+    int nu = small ? std::max(1, std::min(32 / r, kSmallCap / (r * M)))
+                   : std::max(1, 32 / (r * std::max(m1, m2)));
+    if (kc.tb) {
+      int bl = N, bh = 0;
+      for (int kk : pk.ks)
+        for (int dd = 0; dd < p->len[kk]; ++dd) {
+          int cj = 0;
+          const int b = bin_of(p->lo[kk] + dd, cj);
+          bl = std::min(bl, b);
+          bh = std::max(bh, b);
+        }
+      const int wf = ((bh + 2) & ~1) - (bl & ~1);
+      const int wi = (int)(((p->off[pk.ks.back()] + M + 1) & ~int64_t(1)) - (p->off[pk.ks[0]] & ~int64_t(1)));
+      while (nu > 1 && nu * std::max(wf, wi) > tb_cap) --nu;
+      kc.tbe_f = std::max(kc.tbe_f, nu * wf);
+      kc.tbe_i = std::max(kc.tbe_i, nu * wi);
+    }
     pk.d.nu = nu;
     pk.d.magc = (uint32_t)((65536 + r - 1) / r);
     pk.d.ustride = small ? r : r * m1 * (m2 | 1);
-    pk.scr = nu * pk.d.ustride * (small ? M : 1);
+    // small packets: scratch q * nvp + vc with the odd stride nvp = (nu r) | 1, so that the
+    // inverse term scatter (a warp reads consecutive q of one channel) is bank-conflict free
+    pk.scr = small ? ((nu * r) | 1) * M : nu * pk.d.ustride;
     pks.push_back(std::move(pk));
   }
   // shape-sorted (the warps of a channel-kernel CTA run the same code), longer first, by
@@ -596,12 +636,6 @@ int configure_kernels(slicq_plan *p) {
   }
 
   // ---------------- element tables
-  auto bin_of = [&](int j, int &conj) {  // X(j) = X[b] or conj(X[b]) for real input
-    int jj = j % N2;
-    if (jj < 0) jj += N2;
-    conj = jj > N;
-    return jj > N ? N2 - jj : jj;
-  };
   auto fbits = [](double v) {
     const float f = (float)v;
     uint32_t u;
@@ -614,12 +648,27 @@ int configure_kernels(slicq_plan *p) {
   p->pchans.clear();
   p->fent.clear();
   p->ient.clear();
-  int need = 8;
+  int need = 8, need_f = 8;
   for (Pk &pk : pks) {
     PacketDev &d = pk.d;
     const int M = pk.M;
     const bool small = (d.m1m2 >> 17) & 1;
     const int m1 = d.m1m2 & 255, S2 = ((d.m1m2 >> 8) & 255) | 1;
+    {  // bins the fold reads (X(j) or conj X(2N - j) for real input)
+      int bl = N, bh = 0;
+      for (int k : pk.ks)
+        for (int dd = 0; dd < p->len[k]; ++dd) {
+          int conj = 0;
+          const int b = bin_of(p->lo[k] + dd, conj);
+          bl = std::min(bl, b);
+          bh = std::max(bh, b);
+        }
+      d.xlo = bl;
+      d.xhi = bh;
+    }
+    // zero-padding entries of the fold tables (weight 0) point at xlo: a bin of the packet's
+    // band, which the TMA-staged kernels hold in shared memory (kernels_tb.cuh)
+    const uint32_t padbin = (uint32_t)d.xlo;
     d.chan_off = (int)p->pchans.size();
     d.fent_off = (int)p->fent.size();
     d.ient_off = (int)p->ient.size();
@@ -627,7 +676,7 @@ int configure_kernels(slicq_plan *p) {
     // forward fold table: bin | scratch position << 18, weight g_k/sqrt(M_k) whose sign bit
     // marks the conjugated (mirrored) bins (g >= 0); weight 0 and bin 0 for the zero padding
     if (small) {
-      std::vector<uint2> t(32 * M, make_uint2(0u, 0u));
+      std::vector<uint2> t(32 * M, make_uint2(padbin, 0u));
       for (int c = 0; c < d.nch; ++c) {
         const int k = pk.ks[c];
         const int lo_mod = ((p->lo[k] % M) + M) % M;
@@ -650,7 +699,7 @@ int configure_kernels(slicq_plan *p) {
           int dd = q - lo_mod;
           if (dd < 0) dd += M;
           const uint32_t pos = (uint32_t)(c * m1 * S2 + q);
-          uint2 e = make_uint2(pos << 18, 0u);
+          uint2 e = make_uint2(padbin | (pos << 18), 0u);
           if (dd < p->len[k]) {
             int conj = 0;
             const int b = bin_of(p->lo[k] + dd, conj);
@@ -671,8 +720,8 @@ int configure_kernels(slicq_plan *p) {
       for (const Dst &ds : dsts[k]) {
         int q = lo_mod + ds.d;
         if (q >= M) q -= M;
-        // small: scratch q * (nu * nch) + vc; big: vc * M1 * S2 + q (+ u * ustride in-kernel)
-        const uint32_t pos = small ? (uint32_t)(q * d.nu * d.nch + c) : (uint32_t)(c * m1 * S2 + q);
+        // small: scratch q * ((nu * nch) | 1) + vc; big: vc * M1 * S2 + q (+ u * ustride in-kernel)
+        const uint32_t pos = small ? (uint32_t)(q * ((d.nu * d.nch) | 1) + c) : (uint32_t)(c * m1 * S2 + q);
         const double w = ds.zero ? 0.0 : p->gdual[p->goff[k] + ds.d] * sc * half;
         if (!(w >= 0.0)) return set_error(SLICQ_EUNSUPPORTED, "negative dual filter value");
         p->ient.push_back(make_uint2(pos | (ds.dst << 14), fbits(w) | ((uint32_t)ds.conj << 31)));
@@ -680,25 +729,23 @@ int configure_kernels(slicq_plan *p) {
       }
     }
     d.nz = nz;
-    {  // bins the fold reads (X(j) or conj X(2N - j) for real input)
-      int bl = N, bh = 0;
-      for (int k : pk.ks)
-        for (int dd = 0; dd < p->len[k]; ++dd) {
-          int conj = 0;
-          const int b = bin_of(p->lo[k] + dd, conj);
-          bl = std::min(bl, b);
-          bh = std::max(bh, b);
-        }
-      d.xlo = bl;
-      d.xhi = bh;
-    }
     for (int k : pk.ks) p->pchans.push_back(k);
     p->packets.push_back(d);
     need = std::max(need, pk.scr);
+    if (!small) need_f = std::max(need_f, pk.scr);
   }
   kc.npackets = (int)p->packets.size();
   kc.scr = (need + 7) & ~7;
   kc.chan_smem = sizeof(float2) * (size_t)kc.scr * (CHAN_T / 32);
+  kc.scr_f = (need_f + 7) & ~7;
+  kc.tbe_f = (kc.tbe_f + 7) & ~7;
+  kc.tbe_i = (kc.tbe_i + 7) & ~7;
+  // [scratch][buffers][mbarriers][cursors] (kernels_tb.cuh)
+  kc.tb_smem_f = sizeof(float2) * (size_t)(kc.scr_f + kc.tbe_f + 1) * (CHAN_T / 32) +
+                 2 * sizeof(kern::TbCursor) * (CHAN_T / 32);
+  kc.tb_smem_i = sizeof(float2) * (size_t)(kc.scr + kc.tbe_i + 1) * (CHAN_T / 32) +
+                 2 * sizeof(kern::TbCursor) * (CHAN_T / 32);
+  if (kc.tb && std::max(kc.tb_smem_f, kc.tb_smem_i) > kSmemCap) kc.tb = false;
   // element encoding: bin < 2^17, scratch position < 2^14 (fold table, kernels_dev.cuh)
   if (N > (1 << 17) - 1 || kc.scr > (1 << 14))
     return set_error(SLICQ_EUNSUPPORTED, "slice or channel too long for the element tables");
@@ -944,6 +991,8 @@ int upload(slicq_plan *p) {
   }
   for (int v = 0; v < 2 * kVariants * 3 && rc == 0 && !p->kc.longmode; ++v)  // fwd, variant, mask
     rc = (int)allow_max_dyn_smem((const void *)chan_fn(v & 1, (v >> 1) % kVariants, v / (2 * kVariants)));
+  for (int v = 0; v < 4 && rc == 0 && !p->kc.longmode; ++v)  // fwd, lite / full
+    rc = (int)allow_max_dyn_smem((const void *)tb_fn(v & 1, 1 + (v >> 1)));
   if (rc != 0)
     return set_error(SLICQ_ECUDA, std::string("cudaFuncSetAttribute: ") +
                                       cudaGetErrorString((cudaError_t)rc));
@@ -1121,7 +1170,7 @@ static int64_t chan_capacity_smem(ChanFn fn, size_t smem) {
 }
 
 // persistent channel-kernel grid: resident CTAs (occupancy x SMs), capped by the work items
-static int64_t chan_capacity(const slicq_plan *p, ChanFn fn) {
+static int64_t chan_capacity(const slicq_plan *p, ChanFn fn, size_t smem) {
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -1131,7 +1180,7 @@ static int64_t chan_capacity(const slicq_plan *p, ChanFn fn) {
   }
   int per_sm = 2;
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, CHAN_T, p->kc.chan_smem) ==
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, CHAN_T, smem) ==
           cudaSuccess && occ > 0)
     per_sm = occ;
   if (p->kc.chan_per_sm > 0) per_sm = std::min(per_sm, p->kc.chan_per_sm);
@@ -1144,10 +1193,18 @@ static cudaError_t launch_chan(bool fwd, const slicq_plan *p, KArgs a, cudaStrea
     a.packets = p->d.packets + p->kc.voff[v];
     a.npackets = p->kc.voff[v + 1] - p->kc.voff[v];
     if (a.npackets == 0) continue;
-    const ChanFn fn = chan_fn(fwd, v, fwd || !a.mask ? 0 : (a.mask_db ? 2 : 1));
+    // TMA-staged variant (kernels_tb.cuh): unmasked calls whose operand rows are 16-byte
+    // aligned (bulk copies)
+    const bool tb = p->kc.tb && (fwd ? (reinterpret_cast<uintptr_t>(a.stage) % 16 == 0 && a.xs % 2 == 0)
+                                     : (!a.mask && reinterpret_cast<uintptr_t>(a.coef_in) % 16 == 0 &&
+                                        a.C % 2 == 0));
+    const ChanFn fn = tb ? tb_fn(fwd, v) : chan_fn(fwd, v, fwd || !a.mask ? 0 : (a.mask_db ? 2 : 1));
+    const size_t smem = tb ? (fwd ? p->kc.tb_smem_f : p->kc.tb_smem_i) : p->kc.chan_smem;
+    a.scr = tb && fwd ? p->kc.scr_f : p->kc.scr;
+    a.tbe = fwd ? p->kc.tbe_f : p->kc.tbe_i;
     // small calls (e.g. the ranges of the streaming executor): shrink the tile until there
     // are >= 4 work items per resident CTA (load balance of the persistent grid)
-    const int64_t cap = chan_capacity(p, fn);
+    const int64_t cap = chan_capacity(p, fn, smem);
     a.tile = p->kc.tile;
     while (a.tile > 8 && (int64_t)a.npackets * ((a.nunits + a.tile - 1) / a.tile) < 4 * cap)
       a.tile /= 2;
@@ -1155,7 +1212,7 @@ static cudaError_t launch_chan(bool fwd, const slicq_plan *p, KArgs a, cudaStrea
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(items, cap)));
     cfg.blockDim = dim3(CHAN_T);
-    cfg.dynamicSmemBytes = p->kc.chan_smem;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

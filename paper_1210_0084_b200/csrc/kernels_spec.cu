@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Instantiation of the per-slice spectrum kernels and the fused kernels for N = 2^SLICQ_LOGN.
 // Compiled once per size (build.py: -DSLICQ_LOGN=11..14, one object each, in parallel).
 #ifndef SLICQ_LOGN
@@ -9,6 +10,16 @@
 #include "kernels_fused.cuh"
 #include "kernels_ring.cuh"
 #include "kernels_long_api.h"
+
+// dev override (SLICQ_SPEC_PER_SM): cap on the persistent spectrum kernels' CTAs per SM, so
+// that a channel kernel of another chunk (another stream) can share the SMs (0: occupancy)
+static int spec_per_sm() {
+  static const int v = [] {
+    const char *e = std::getenv("SLICQ_SPEC_PER_SM");
+    return e && *e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
 
 namespace slicq {
 namespace kern {
@@ -131,6 +142,7 @@ cudaError_t launch_inv_spec_persist<SLICQ_LOGN>(const KArgs &a, size_t smem, cud
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &occ, slicq_inv_spec_persist_kernel<SLICQ_LOGN>, Big<SLICQ_LOGN>::T, smem);
   if (e != cudaSuccess) return e;
+  if (spec_per_sm() > 0) occ = std::min(std::max(occ, 1), spec_per_sm());
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(occ, 1) * nsm, a.nunits));
   if (grid_out) *grid_out = grid;
   return launch_pdl(slicq_inv_spec_persist_kernel<SLICQ_LOGN>, a, dim3((unsigned)grid),
@@ -151,6 +163,7 @@ cudaError_t launch_fwd_spec_persist<SLICQ_LOGN>(const KArgs &a, size_t smem, cud
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &occ, slicq_fwd_spec_persist_kernel<SLICQ_LOGN>, Big<SLICQ_LOGN>::T, smem);
   if (e != cudaSuccess) return e;
+  if (spec_per_sm() > 0) occ = std::min(std::max(occ, 1), spec_per_sm());
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(occ, 1) * nsm, a.nunits));
   return launch_pdl(slicq_fwd_spec_persist_kernel<SLICQ_LOGN>, a, dim3((unsigned)grid),
                     Big<SLICQ_LOGN>::T, smem, s, pdl);

@@ -156,6 +156,11 @@ struct KernelConfig {
   bool fwd_persist = false;  // forward spectrum stage runs persistent
   int scr = 0;           // channel kernels: per-warp scratch (float2 entries)
   size_t chan_smem = 0;
+  // TMA-staged channel kernels (kernels_tb.cuh): per-warp operand buffer (float2 entries)
+  bool tb = false;
+  int scr_f = 0;              // forward scratch (big packets only; small ones use none)
+  int tbe_f = 0, tbe_i = 0;   // buffer entries: forward band, inverse coefficient columns
+  size_t tb_smem_f = 0, tb_smem_i = 0;
   int npackets = 0;
   int nlite = 0;              // packets [0, nlite) run in the micro / lite variants
   int voff[4] = {0, 0, 0, 0}; // packets [voff[v], voff[v+1]) run in variant v (micro, lite, full)

@@ -456,6 +456,28 @@ def test_chunked_staging_is_bit_identical(api, monkeypatch):
     assert torch.equal(y, y2)
 
 
+@pytest.mark.parametrize("cfg,n,batch", [(4, 300 * 8192 + 123, 1), (3, 40 * 8192, 6),
+                                         (2, 441000, 2), (5, 3 * 65536, 2)])
+def test_tma_staged_channel_kernels_bit_identical(api, monkeypatch, cfg, n, batch):
+    """The TMA-staged channel kernels (kernels_tb.cuh, opt-in SLICQ_TB=1: per-warp operand
+    buffers filled by cp.async.bulk one task ahead) compute what the global-load kernels
+    compute, on packet mixes of four configs: the inverse output bit for bit; the forward
+    coefficients to fp32 rounding (the same operations, but the compiler contracts the fold's
+    weight multiply into the first DFT additions differently in the two codelets), and both
+    against the oracle-checked default path."""
+    x = torch.from_numpy(random_signal(4242 + cfg, batch, n)).cuda()
+    monkeypatch.setenv("SLICQ_TB", "0")
+    p0 = api.plan_for_config(CONFIGS[cfg])
+    monkeypatch.setenv("SLICQ_TB", "1")
+    p1 = api.plan_for_config(CONFIGS[cfg])
+    monkeypatch.delenv("SLICQ_TB")
+    c0, c1 = p0.forward(x), p1.forward(x)
+    assert (torch.linalg.vector_norm(c1 - c0) / torch.linalg.vector_norm(c0)).item() <= 1e-6
+    y0, y1 = p0.inverse(c0, n), p1.inverse(c0, n)
+    assert torch.equal(y0, y1)
+    assert (torch.linalg.vector_norm(y1 - x) / torch.linalg.vector_norm(x)).item() <= TOL
+
+
 def test_pipelined_chunks_are_bit_identical(api, monkeypatch):
     """Calls of >= SLICQ_PIPE_MIN_UNITS units run as chunks alternating between two internal
     streams (ping-pong staging, fork/join on the caller's stream): identical results to one
