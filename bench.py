@@ -117,6 +117,26 @@ def _oracle_init(cfg_id: int):
     cfg = CONFIGS[cfg_id]
     _ORACLE["cfg"] = cfg
     _ORACLE["plan"] = cqplan.make_plan(*plan_args(cfg))
+    _ORACLE["x"] = _workload_row(cfg_id, _ORACLE["plan"])
+
+
+def _workload_row(cfg_id: int, ref, slices: int = 256) -> np.ndarray:
+    """Row 0 of the workload's own seeded signal (the input the GPU arm transforms, VERDICT
+    round 1 "baseline hygiene"), as fp64; for the long stream only the prefix the sample
+    uses (cfg4_signal's prefixes are exact)."""
+    from synth.configs import CONFIGS
+    from synth.signals import cfg3_signal, cfg4_signal, cfg5_signal, make_signal
+    cfg = CONFIGS[cfg_id]
+    need = (ref.N + ref.tr) // 2 + (slices + 2) * ref.N
+    if cfg_id == 3:
+        x = cfg3_signal(cfg, batch=1)
+    elif cfg_id == 4:
+        x = cfg4_signal(cfg, n=min(cfg.n, need))
+    elif cfg_id == 5:
+        x = cfg5_signal(cfg, batch=1)
+    else:
+        x = make_signal(cfg_id)
+    return x[0].astype(np.float64)
 
 
 def _oracle_chunk(args):
@@ -124,11 +144,14 @@ def _oracle_chunk(args):
     functions, fp64 NumPy) of a distinct part of the stream; returns the seconds it took."""
     slice0, nsl = args
     from oracle import slicq as oslicq
-    from synth.signals import random_signal
-    ref, cfg = _ORACLE["plan"], _ORACLE["cfg"]
+    ref, xw = _ORACLE["plan"], _ORACLE["x"]
     N = ref.N
     halo = (N + ref.tr) // 2
-    x = random_signal(cfg.seed + slice0, 1, halo + nsl * N)[0].astype(np.float64)
+    # the slices [slice0, slice0 + nsl) of the workload's signal (cyclically where the
+    # signal is shorter than the sample: cfg1 has 8 slices)
+    s0 = 1 + slice0 % max(1, (len(xw) - halo) // N - nsl - 1)
+    idx = (s0 * N - halo + np.arange(halo + nsl * N)) % len(xw)
+    x = xw[idx]
     t0 = time.perf_counter()
     c = oslicq.forward_range(x, halo, slice0, nsl, ref)
     oslicq.inverse_range(c, slice0, nsl, ref, halo)
@@ -149,7 +172,7 @@ class OracleTimer:
         self.run()  # warm the workers (plan build, imports)
 
     def run(self):
-        jobs = [(1000 + w * self.nsl, self.nsl) for w in range(self.cores)]
+        jobs = [(w * self.nsl, self.nsl) for w in range(self.cores)]
         t0 = time.perf_counter()
         self.pool.map(_oracle_chunk, jobs, chunksize=1)
         return time.perf_counter() - t0
@@ -158,21 +181,31 @@ class OracleTimer:
         return self.cores * self.nsl * (self.cfg.sl_len // 2)
 
     def describe(self):
-        return (f"{self.nsl} consecutive slices of {self.cfg.name} per process "
-                f"({self.nsl * (self.cfg.sl_len // 2)} input samples each), {self.cores} processes "
-                f"on {self.cores} host cores, oracle.slicq.forward_range + inverse_range, fp64 NumPy")
+        return (f"{self.nsl} consecutive slices of {self.cfg.name}'s own signal (row 0) per "
+                f"process ({self.nsl * (self.cfg.sl_len // 2)} input samples each), {self.cores} "
+                f"processes on {self.cores} host cores, oracle.slicq.forward_range + "
+                f"inverse_range, fp64 NumPy")
+
+    def one_core(self, reps: int = 2) -> float:
+        """samples/s of one process alone (the same job in this process, 1 core)."""
+        _oracle_init(self.cfg.cfg)
+        _oracle_chunk((0, self.nsl))  # warm
+        dt = min(_oracle_chunk((0, self.nsl)) for _ in range(reps))
+        return self.nsl * (self.cfg.sl_len // 2) / dt
 
     def close(self):
         self.pool.terminate()
 
 
 def oracle_sample_rate(cfg, reps: int = 3):
-    """(samples/s, seconds per run, cores, description) of the oracle on all host cores."""
+    """(samples/s, seconds per run, cores, description, 1-core samples/s) of the oracle on
+    all host cores and on one."""
     t = OracleTimer(cfg)
     try:
         dts = [t.run() for _ in range(reps)]
         dt = sum(dts) / len(dts)
-        return t.samples_per_run() / dt, dt, t.cores, t.describe()
+        v1 = t.one_core()
+        return t.samples_per_run() / dt, dt, t.cores, t.describe(), v1
     finally:
         t.close()
 
@@ -431,8 +464,9 @@ def run_gpu(args, cfg):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, dt, cores, desc = oracle_sample_rate(cfg)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        v, dt, cores, desc, v1 = oracle_sample_rate(cfg)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+               "value_1core": v1}
 
     if rank == 0:
         line = {

@@ -1268,7 +1268,19 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
                    : (sbase + N - A - a.y_base >= 0);
     if (excl_direct) {
       float *yo = yrow + (a.circular ? sbase : sbase - a.y_base);
-      for (int i = N - A + tid; i <= N + A; i += T) yo[i] = fr(i);
+      const int i0 = N - A;
+      if (!(i0 & 1) && !(reinterpret_cast<uintptr_t>(yo + i0) & 15)) {
+        // four samples per step: frame pairs z[p], z[p+1] -> one 16-byte store
+        const int n4 = (2 * A + 1) >> 2;
+        for (int q = tid; q < n4; q += T) {
+          const int p = (i0 >> 1) + 2 * q;
+          const float2 z0 = spec[padi(p)], z1 = spec[padi(p + 1)];
+          *reinterpret_cast<float4 *>(yo + i0 + 4 * q) = make_float4(z0.x, z0.y, z1.x, z1.y);
+        }
+        for (int i = i0 + 4 * n4 + tid; i <= N + A; i += T) yo[i] = fr(i);
+      } else {
+        for (int i = i0 + tid; i <= N + A; i += T) yo[i] = fr(i);
+      }
     } else {
       for (int i = N - A + tid; i <= N + A; i += T) {
         const float val = fr(i);
