@@ -328,6 +328,40 @@ __global__ void __launch_bounds__(LT, SLICQ_LCL_MINB) inv_large_cluster(const KA
   const int trp = a.tr;
   float *yrow = a.y + row * a.y_stride;
   float *bnd_row = a.bnd + row * (int64_t)S * 2 * trp;
+  const int64_t sbase = (mg - 1) * N;  // global sample of frame index 0
+  // interior slice (both boundaries paired, the frame inside the row: no wrap, no trim, no
+  // spill): 32-bit frame indices, exclusive sample pairs as one 8-byte store; the same
+  // products as the general path below (h~_0 = 1 on the exclusive part), so bit-identical
+  const bool fast = left_paired && right_paired &&
+                    (a.circular ? (sbase >= 0 && sbase + 2 * N <= a.L && sbase + 2 * N <= a.y_len)
+                                : (sbase + N - A - a.y_base >= 0)) &&
+                    !(reinterpret_cast<uintptr_t>(yrow + (a.circular ? sbase : sbase - a.y_base)) & 7);
+  if (fast) {
+    float *yb = yrow + (a.circular ? sbase : sbase - a.y_base);  // frame index i -> yb[i]
+    float *lh = bnd_row + (bl * 2 + 1) * trp + (Bw - 1 - N);      // left half: t + Bw - 1
+    float *rh = bnd_row + (br * 2 + 0) * trp + (-A - 1 - N);      // right half: t - A - 1
+    for (int idx = tid; idx < LB * N2; idx += LT) {
+      const int s = idx % LB, n2 = idx / LB;
+      const float2 z = rbuf[s * CS2 + padi(n2)];
+      const int i0 = 2 * (n1_0 + s + N1 * n2), t0 = i0 - N;
+      if (t0 >= -A && t0 < A) {  // both samples exclusive
+        *reinterpret_cast<float2 *>(yb + i0) = make_float2(z.x * invN, z.y * invN);
+        continue;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = i0 + h, t = i - N, at = t < 0 ? -t : t;
+        if (at >= Bw) continue;
+        const float hd = at <= A ? 1.f : __ldg(a.h0dual + i);
+        const float val = (h ? z.y : z.x) * invN * hd;
+        if (at <= A) yb[i] = val;
+        else if (t < 0) lh[i] = val;
+        else rh[i] = val;
+      }
+    }
+    pdl_trigger();
+    return;
+  }
   for (int idx = tid; idx < LB * N2; idx += LT) {
     const int s = idx % LB, n2 = idx / LB;
     const float2 z = rbuf[s * CS2 + padi(n2)];
