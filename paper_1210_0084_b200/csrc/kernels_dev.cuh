@@ -352,6 +352,17 @@ __device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes, int id
   for (int l = idx; l < nl; l += nthr)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a0 + ((uintptr_t)l << 7)));
 }
+// the same with one TMA bulk prefetch (cp.async.bulk.prefetch.L2, one instruction for the
+// whole 16-byte-aligned envelope of the range; the caller issues it from one lane)
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, int64_t bytes) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0))
+               : "memory");
+}
+#ifndef SLICQ_BULK_PF
+#define SLICQ_BULK_PF 1
+#endif
 // channel-kernel step codelets, per direction: inlined into the size switch (measured: the
 // forward gains 6 % -- no call/return, no spills around the calls, uniform addressing) or
 // out of line (one copy per DFT size: smaller instruction-cache footprint)
@@ -710,12 +721,20 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
       const int nvc = nuu * r;
       const float2 *in_row = a.coef_in + (a.unit0 + g0) * a.C;
       const float *mrow = MK ? a.mask + (a.unit0 + g0) * a.C : nullptr;
-      // L2 prefetch of the coefficient rows SLICQ_IB_PF_AHEAD tasks of this warp ahead
+      // L2 prefetch of the coefficient rows SLICQ_IB_PF_AHEAD tasks of this warp ahead: one
+      // TMA bulk prefetch per unit (lane u issues unit u's run), not one prefetch per line
       if (t + SLICQ_IB_PF_AHEAD * NW < ntask) {
         const int g1 = g0 + SLICQ_IB_PF_AHEAD * NW * nu, n1u = min(nu, u_hi - g1);
-        for (int u = 0; u < n1u; ++u)
-          prefetch_l2(in_row + (int64_t)(SLICQ_IB_PF_AHEAD * NW * nu + u) * a.C + cbase,
-                      (int64_t)clen * 8, lane);
+        // (16-byte aligned rows: the envelope stays inside the coefficient row)
+        if (SLICQ_BULK_PF && a.vec16) {
+          if (lane < n1u)
+            prefetch_l2_bulk(in_row + (int64_t)(SLICQ_IB_PF_AHEAD * NW * nu + lane) * a.C + cbase,
+                             (int64_t)clen * 8);
+        } else {
+          for (int u = 0; u < n1u; ++u)
+            prefetch_l2(in_row + (int64_t)(SLICQ_IB_PF_AHEAD * NW * nu + u) * a.C + cbase,
+                        (int64_t)clen * 8, lane);
+        }
       }
       if (small) {
         switch (m1) {

@@ -1489,6 +1489,7 @@ int launch_inverse(const slicq_plan *p, const slicq_c32 *coeffs, int64_t slice0,
   if ((uintptr_t)ws % 16) return set_error(SLICQ_ESHAPE, "workspace must be 16-byte aligned");
   KArgs a = base_args(p);
   a.coef_in = reinterpret_cast<const float2 *>(coeffs);
+  a.vec16 = (reinterpret_cast<uintptr_t>(coeffs) % 16 == 0 && p->C % 2 == 0) ? 1 : 0;
   a.mask = mask;
   a.mask_db = mask_db;
   a.y = y;
