@@ -636,12 +636,19 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArg
       const int nvc = nuu * r;
       const float2 *X = a.stage + (int64_t)g0 * a.xs;
       float2 *out_row = a.coef_out + (a.unit0 + g0) * a.C;
-#if SLICQ_FB_PREFETCH  // (measured: no gain on cfg4; the fold's loads are L2-latency bound)
+#if SLICQ_FB_PREFETCH == 1  // (measured: no gain on cfg4; the fold's loads are L2-latency bound)
       if (t + NW < ntask) {  // this warp's next task: its spectrum bins -> L2 (staging in DRAM)
         const int g1 = g0 + NW * nu, n1u = min(nu, u_hi - g1);
         for (int u = 0; u < n1u; ++u)
           prefetch_l2(X + (int64_t)(NW * nu + u) * a.xs + P.xlo, (int64_t)(P.xhi - P.xlo + 1) * 8,
                       lane);
+      }
+#elif SLICQ_FB_PREFETCH == 2  // one TMA bulk prefetch per unit (lane u: unit u's band)
+      if (t + NW < ntask) {
+        const int g1 = g0 + NW * nu, n1u = min(nu, u_hi - g1);
+        if (lane < n1u)
+          prefetch_l2_bulk(X + (int64_t)(NW * nu + lane) * a.xs + P.xlo,
+                           (int64_t)(P.xhi - P.xlo + 1) * 8);
       }
 #endif
       if (small) {
@@ -1432,7 +1439,13 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
     const int mloc = (int)(u % a.nslices);
     const bool ll = ul > ub && mloc > 0;                    // unit ul - 1 is slice mloc - 1
     const bool rl = ul + 1 < ue && mloc + 1 < a.nslices;  // unit ul + 1 is slice mloc + 1
-    if (a.pf && ul + 1 < ue) prefetch_l2(a.stage + (ul + 1) * a.zs, a.zs * 8, tid, T);
+    if (a.pf && ul + 1 < ue) {  // 1: per-line prefetches by all threads; 2: one bulk prefetch
+      if (a.pf == 2) {
+        if (tid == 0) prefetch_l2_bulk(a.stage + (ul + 1) * a.zs, a.zs * 8);
+      } else {
+        prefetch_l2(a.stage + (ul + 1) * a.zs, a.zs * 8, tid, T);
+      }
+    }
     inv_unit<LOGN, 0>(a, spec, tw, htab, carry, ul, ll, rl);
     __syncthreads();  // (spec and carry reused by the next unit)
   }
