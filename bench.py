@@ -197,6 +197,17 @@ class OracleTimer:
         self.pool.terminate()
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def oracle_sample_rate(cfg, reps: int = 3):
     """(samples/s, seconds per run, cores, description, 1-core samples/s) of the oracle on
     all host cores and on one."""
@@ -228,7 +239,7 @@ def run_reference(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(cfg, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": t.cores, "kind": "oracle",
-                             "sample": t.describe()},
+                             "sample": t.describe(), "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -333,8 +344,15 @@ def run_gpu(args, cfg):
         dist.barrier()
     torch.cuda.synchronize()
     ms_total = t_start.elapsed_time(t_end)
-    ms_f = sum(e_f0[k].elapsed_time(e_f1[k]) for k in range(args.steps)) / args.steps
-    ms_i = sum(e_f1[k].elapsed_time(e_i1[k]) for k in range(args.steps)) / args.steps
+    per_f = [e_f0[k].elapsed_time(e_f1[k]) for k in range(args.steps)]
+    per_i = [e_f1[k].elapsed_time(e_i1[k]) for k in range(args.steps)]
+    ms_f = sum(per_f) / args.steps
+    ms_i = sum(per_i) / args.steps
+    # SURVEY 8(d) (as the paper): spread of the per-step times besides the mean
+    step_stats = {"forward_ms_median": statistics.median(per_f),
+                  "forward_ms_std": statistics.pstdev(per_f),
+                  "inverse_ms_median": statistics.median(per_i),
+                  "inverse_ms_std": statistics.pstdev(per_i)}
     t = torch.tensor([ms_total, ms_f, ms_i], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -466,7 +484,7 @@ def run_gpu(args, cfg):
     if rank == 0 and world == 1 and not args.no_cpu:
         v, dt, cores, desc, v1 = oracle_sample_rate(cfg)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
-               "value_1core": v1}
+               "value_1core": v1, "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {
@@ -476,7 +494,7 @@ def run_gpu(args, cfg):
             "dtype": "f32", "data": "synthetic", "config": config_dict(cfg, world),
             "forward_samples_per_s": samples / (ms_f / 1e3),
             "inverse_samples_per_s": samples / (ms_i / 1e3),
-            "ms_forward": ms_f, "ms_inverse": ms_i,
+            "ms_forward": ms_f, "ms_inverse": ms_i, "step_stats": step_stats,
             "recon_rel_l2": rec,
             "roofline": {"bound": "hbm", "kernel": f"{dom} ({kernels})", "achieved": achieved,
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s",
