@@ -74,6 +74,12 @@ static __device__ unsigned long long g_phase_cycles[2][16];
 // bank-conflict free for 8-byte accesses
 __host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
 
+// unit u = row * S + local slice: 32-bit division when u fits (the 64-bit one is a
+// software routine of ~70 instructions, executed by every thread of a spectrum CTA)
+__device__ __forceinline__ int64_t unit_row(int64_t u, int S) {
+  return (u >> 32) == 0 ? (int64_t)((uint32_t)u / (uint32_t)S) : u / S;
+}
+
 // Big-FFT plans: N = 2^LOGN complex points, T threads, radix sequences per direction.
 template <int LOGN>
 struct Big;
@@ -801,7 +807,7 @@ __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T;
   const int tid = threadIdx.x;
-  const int64_t row = u / a.nslices;
+  const int64_t row = unit_row(u, a.nslices);
   const int64_t mloc = u - row * a.nslices;
   const int64_t mg = a.slice0 + mloc;
 
@@ -1018,7 +1024,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
   const int64_t ub = blockIdx.x * (int64_t)a.nunits / G, ue = (blockIdx.x + 1) * (int64_t)a.nunits / G;
   for (int64_t ul = ub; ul < ue; ++ul) {
     if (ul + 1 < ue) {  // the next frame's window support -> L2
-      const int64_t u = a.unit0 + ul + 1, row = u / a.nslices;
+      const int64_t u = a.unit0 + ul + 1, row = unit_row(u, a.nslices);
       const int64_t s0 = (a.slice0 + (u - row * a.nslices) - 1) * N - a.base_off + (N - a.tr) / 2;
       if (s0 >= 0 && s0 + N + a.tr <= a.x_len)
         prefetch_l2(a.x + row * a.x_stride + s0, (int64_t)(N + a.tr) * 4, tid, T);
@@ -1045,7 +1051,7 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
   constexpr int N = CF::N, T = CF::T;
   const int tid = threadIdx.x;
   const int64_t u = a.unit0 + ul;
-  const int64_t row = u / a.nslices;
+  const int64_t row = unit_row(u, a.nslices);
   const int mloc = (int)(u - row * a.nslices);
   const int64_t mg = a.slice0 + mloc;
 
@@ -1436,7 +1442,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
   __syncthreads();
   for (int64_t ul = ub; ul < ue; ++ul) {
     const int64_t u = a.unit0 + ul;
-    const int mloc = (int)(u % a.nslices);
+    const int mloc = (int)(u - unit_row(u, a.nslices) * a.nslices);
     const bool ll = ul > ub && mloc > 0;                    // unit ul - 1 is slice mloc - 1
     const bool rl = ul + 1 < ue && mloc + 1 < a.nslices;  // unit ul + 1 is slice mloc + 1
     if (a.pf && ul + 1 < ue) {  // 1: per-line prefetches by all threads; 2: one bulk prefetch

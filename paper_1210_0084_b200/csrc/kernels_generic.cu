@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(GT, 1) slicq_fwd_spec_generic(const KArgs a, c
   float2 *z = reinterpret_cast<float2 *>(smem4);
   const int N = g.N, tid = threadIdx.x;
   const int64_t ul = blockIdx.x, u = a.unit0 + ul;
-  const int64_t row = u / a.nslices, mloc = u - row * a.nslices;
+  const int64_t row = unit_row(u, a.nslices), mloc = u - row * a.nslices;
   const int64_t mg = a.slice0 + mloc;
   const float *xr = a.x + row * a.x_stride;
   const int64_t s0 = MODE ? -a.base_off : (mg - 1) * N - a.base_off;  // frame sample 0
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(GT, 1) slicq_inv_spec_generic(const KArgs a, c
   float2 *z = reinterpret_cast<float2 *>(smem4);
   const int N = g.N, tid = threadIdx.x;
   const int64_t ul = blockIdx.x, u = a.unit0 + ul;
-  const int64_t row = u / a.nslices;
+  const int64_t row = unit_row(u, a.nslices);
   const int mloc = (int)(u - row * a.nslices);
   const int64_t mg = a.slice0 + mloc;
   pdl_wait();

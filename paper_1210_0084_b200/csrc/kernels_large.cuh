@@ -83,7 +83,7 @@ __device__ __forceinline__ float2 tw_any(TW tw, int64_t e) {
 __device__ __forceinline__ void unit_coords(const KArgs &a, int64_t ul, int64_t &row,
                                             int64_t &mloc, int64_t &mg) {
   const int64_t u = a.unit0 + ul;
-  row = u / a.nslices;
+  row = unit_row(u, a.nslices);
   mloc = u - row * a.nslices;
   mg = a.slice0 + mloc;
 }
