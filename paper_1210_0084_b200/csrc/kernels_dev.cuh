@@ -98,6 +98,9 @@ __device__ __forceinline__ void st_plain(float2 *p, float2 v) { *p = v; }
 #ifndef SLICQ_ZSTORE
 #define SLICQ_ZSTORE __stcs  // (measured: evict-first beats .cg by ~1 % on cfg4)
 #endif
+#ifndef SLICQ_OVP
+#define SLICQ_OVP 1  // persistent inverse spectrum kernel: overflow-bin sums in a CTA-wide pre-pass
+#endif
 #ifndef SLICQ_IA_GROUP
 #define SLICQ_IA_GROUP 8
 #endif
@@ -197,6 +200,9 @@ struct KArgs {
   const uint2 *fent;        // forward element table (enc, weight bits)
   const uint2 *ient;        // inverse element table (scratch pos, weight bits)
   const uint32_t *dpos;     // inverse overflow run per bin: start | count << 20 (0: none)
+  const uint2 *ovbins;      // inverse: bins with an overflow run (bin, start | count << 20)
+  const uint32_t *dord;     // inverse: per bin 1 + its index in ovbins (0: none)
+  int novbins;
   int64_t zso;              // inverse staging: slot 1 at zso, overflow at 2 zso
   const float *h0;
   const float *h0dual;
@@ -1044,9 +1050,15 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
 // kernel: the neighbour is this CTA's previous / next unit), through carry[0 .. tr-1) in
 // shared memory instead of the cross-CTA pairing through the workspace; the sums are the
 // same (a + b, each half rounded as stored), so both kernels give bit-identical output.
-template <int LOGN, int MODE>
+// OVP (persistent kernel): the deep-overlap bins' sums slot0 + slot1 + overflow run (plan
+// order) are formed in a pre-pass spread over all threads of the CTA into `ovs` (shared),
+// instead of by the thread that owns the bin: the overflow bins crowd the low bins, i.e.
+// the first warps, whose serial overflow loops the other warps waited for at the next
+// barrier.  Same additions in the same order: bit-identical.
+template <int LOGN, int MODE, bool OVP = false>
 __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *tw, float *htab,
-                                         float *carry, int64_t ul, bool ll, bool rl) {
+                                         float *carry, int64_t ul, bool ll, bool rl,
+                                         float2 *ovs = nullptr) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T;
   const int tid = threadIdx.x;
@@ -1098,7 +1110,7 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
     uint32_t dN = 0;
     if (tid == 0) {
       hN = cadd(__ldcg(Z0 + N), __ldcg(Z1 + N));
-      dN = __ldg(a.dpos + N);
+      dN = OVP ? __ldg(a.dord + N) : __ldg(a.dpos + N);
     }
     // warp 0's cooperative packing of the self-mirrored bins (below): lane L's bin and its
     // twiddle, loaded now
@@ -1116,18 +1128,35 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
         a1[q] = SLICQ_ZLOAD(Z1 + ka);
         b0[q] = SLICQ_ZLOAD(Z0 + kb);
         b1[q] = SLICQ_ZLOAD(Z1 + kb);
-        da[q] = __ldg(a.dpos + ka);
-        db[q] = __ldg(a.dpos + kb);
+        da[q] = OVP ? __ldg(a.dord + ka) : __ldg(a.dpos + ka);
+        db[q] = OVP ? __ldg(a.dord + kb) : __ldg(a.dpos + kb);
       }
+      if constexpr (OVP) {
+        if (r0 == 0) {  // pre-pass, in flight with the first batch's loads
+          for (int i = tid; i < a.novbins; i += T) {
+            const uint2 e = __ldg(a.ovbins + i);
+            float2 h = cadd(__ldcg(Z0 + e.x), __ldcg(Z1 + e.x));
+            for (int k = 0; k < (int)(e.y >> 20); ++k) h = cadd(h, __ldcg(Zo + (e.y & 0xfffff) + k));
+            ovs[i] = h;
+          }
+          __syncthreads();
+        }
 #pragma unroll
-      for (int q = 0; q < IG; ++q) {
-        vA[r0 + q] = cadd(a0[q], a1[q]);
-        vB[r0 + q] = cadd(b0[q], b1[q]);
-        if (da[q] | db[q]) {  // deep-overlap bins: overflow terms in order
-          for (int e = 0; e < (int)(da[q] >> 20); ++e)
-            vA[r0 + q] = cadd(vA[r0 + q], __ldcg(Zo + (da[q] & 0xfffff) + e));
-          for (int e = 0; e < (int)(db[q] >> 20); ++e)
-            vB[r0 + q] = cadd(vB[r0 + q], __ldcg(Zo + (db[q] & 0xfffff) + e));
+        for (int q = 0; q < IG; ++q) {
+          vA[r0 + q] = da[q] ? ovs[da[q] - 1] : cadd(a0[q], a1[q]);
+          vB[r0 + q] = db[q] ? ovs[db[q] - 1] : cadd(b0[q], b1[q]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < IG; ++q) {
+          vA[r0 + q] = cadd(a0[q], a1[q]);
+          vB[r0 + q] = cadd(b0[q], b1[q]);
+          if (da[q] | db[q]) {  // deep-overlap bins: overflow terms in order
+            for (int e = 0; e < (int)(da[q] >> 20); ++e)
+              vA[r0 + q] = cadd(vA[r0 + q], __ldcg(Zo + (da[q] & 0xfffff) + e));
+            for (int e = 0; e < (int)(db[q] >> 20); ++e)
+              vB[r0 + q] = cadd(vB[r0 + q], __ldcg(Zo + (db[q] & 0xfffff) + e));
+          }
         }
       }
     }
@@ -1140,7 +1169,11 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
     __shared__ float2 sv[33], sz[32];
     if (tid < 32) {  // warp 0 (warp-uniform branch)
       if (tid == 0) {
-        for (int e = 0; e < (int)(dN >> 20); ++e) hN = cadd(hN, __ldcg(Zo + (dN & 0xfffff) + e));
+        if constexpr (OVP) {
+          if (dN) hN = ovs[dN - 1];
+        } else {
+          for (int e = 0; e < (int)(dN >> 20); ++e) hN = cadd(hN, __ldcg(Zo + (dN & 0xfffff) + e));
+        }
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
           sv[r] = vA[r];
@@ -1432,6 +1465,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
   float2 *tw = spec + spec_entries<LOGN>();
   float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());
   float *carry = htab + ((a.tr + 3) & ~3);
+  float2 *ovs = reinterpret_cast<float2 *>(carry + ((a.tr + 3) & ~3));  // overflow-bin sums
   const int tid = threadIdx.x;
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
   for (int u2 = tid; u2 < a.tr - 1; u2 += T) htab[u2] = __ldg(a.h0dual + N + (N - a.tr) / 2 + 1 + u2);
@@ -1452,8 +1486,9 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
         prefetch_l2(a.stage + (ul + 1) * a.zs, a.zs * 8, tid, T);
       }
     }
-    inv_unit<LOGN, 0>(a, spec, tw, htab, carry, ul, ll, rl);
-    __syncthreads();  // (spec and carry reused by the next unit)
+    constexpr bool fused1 = CF::I1 == 16 && N / 16 == 2 * T;  // (the pre-pass needs it)
+    inv_unit<LOGN, 0, fused1 && SLICQ_OVP>(a, spec, tw, htab, carry, ul, ll, rl, ovs);
+    __syncthreads();  // (spec, carry and ovs reused by the next unit)
   }
   pdl_trigger();
 }

@@ -618,6 +618,18 @@ int configure_kernels(slicq_plan *p) {
     }
     kc.zso = zso;
     kc.nover = start;
+    // the overflow bins as a list (the persistent inverse spectrum kernel sums them in a
+    // pre-pass spread over all threads of the CTA, kernels_dev.cuh inv_unit)
+    p->ovbins.clear();
+    p->dord.assign(N + 2, 0u);
+    for (int b = 0; b <= N; ++b)
+      if (p->dpos[b]) {
+        p->ovbins.push_back(make_uint2((uint32_t)b, p->dpos[b]));
+        p->dord[b] = (uint32_t)p->ovbins.size();
+      }
+    // the persistent inverse spectrum kernel keeps their sums in shared memory
+    kc.spec_smem_p += sizeof(float2) * p->ovbins.size();
+    if (kc.spec_smem_p > kSmemCap) kc.inv_persist = false;
     if (2 * zso + start >= (int64_t(1) << 18))
       return set_error(SLICQ_EUNSUPPORTED, "slice too long for the inverse element tables");
   }
@@ -913,6 +925,8 @@ int upload(slicq_plan *p) {
       {p->gperm.data(), sizeof(int32_t) * p->gperm.size(), 0},
       {p->pbig.data(), sizeof(int32_t) * p->pbig.size(), 0},
       {p->bent.data(), sizeof(uint2) * p->bent.size(), 0},
+      {p->ovbins.data(), sizeof(uint2) * p->ovbins.size(), 0},
+      {p->dord.data(), sizeof(uint32_t) * p->dord.size(), 0},
   };
   size_t o = 0;
   for (Part &pt : parts) {
@@ -962,6 +976,8 @@ int upload(slicq_plan *p) {
   p->kc.gargs.perm = reinterpret_cast<const int *>(b + parts[30].off);
   p->d.pbig = reinterpret_cast<int32_t *>(b + parts[31].off);
   p->d.bent = reinterpret_cast<uint2 *>(b + parts[32].off);
+  p->d.ovbins = reinterpret_cast<uint2 *>(b + parts[33].off);
+  p->d.dord = reinterpret_cast<uint32_t *>(b + parts[34].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
@@ -1128,6 +1144,9 @@ static KArgs base_args(const slicq_plan *p) {
   a.fent = p->d.fent;
   a.ient = p->d.ient;
   a.dpos = p->d.dpos;
+  a.ovbins = p->d.ovbins;
+  a.dord = p->d.dord;
+  a.novbins = (int)p->ovbins.size();
   a.zso = p->kc.zso;
   a.h0 = p->d.h0;
   a.h0dual = p->d.h0dual;

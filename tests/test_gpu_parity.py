@@ -478,6 +478,24 @@ def test_tma_staged_channel_kernels_bit_identical(api, monkeypatch, cfg, n, batc
     assert (torch.linalg.vector_norm(y1 - x) / torch.linalg.vector_norm(x)).item() <= TOL
 
 
+@pytest.mark.parametrize("cfg,n,batch", [(4, 300 * 8192 + 123, 1), (1, 65536, 3), (3, 40 * 8192, 6)])
+def test_persistent_inverse_spectrum_bit_identical(api, monkeypatch, cfg, n, batch):
+    """The persistent inverse spectrum kernel (contiguous unit ranges per CTA, on-chip overlap
+    carry, the deep-overlap bins summed in a CTA-wide pre-pass) gives exactly the output of
+    the one-CTA-per-unit kernel (per-thread overflow sums, pairing through the workspace):
+    the same additions in the same order."""
+    x = torch.from_numpy(random_signal(5151 + cfg, batch, n)).cuda()
+    monkeypatch.setenv("SLICQ_INV_PERSIST", "0")
+    p0 = api.plan_for_config(CONFIGS[cfg])
+    monkeypatch.setenv("SLICQ_INV_PERSIST", "1")
+    p1 = api.plan_for_config(CONFIGS[cfg])
+    monkeypatch.delenv("SLICQ_INV_PERSIST")
+    c = p1.forward(x)
+    y0, y1 = p0.inverse(c, n), p1.inverse(c, n)
+    assert torch.equal(y0, y1)
+    assert (torch.linalg.vector_norm(y1 - x) / torch.linalg.vector_norm(x)).item() <= TOL
+
+
 def test_pipelined_chunks_are_bit_identical(api, monkeypatch):
     """Calls of >= SLICQ_PIPE_MIN_UNITS units run as chunks alternating between two internal
     streams (ping-pong staging, fork/join on the caller's stream): identical results to one
