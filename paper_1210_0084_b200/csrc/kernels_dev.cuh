@@ -200,9 +200,11 @@ struct KArgs {
   const uint2 *fent;        // forward element table (enc, weight bits)
   const uint2 *ient;        // inverse element table (scratch pos, weight bits)
   const uint32_t *dpos;     // inverse overflow run per bin: start | count << 20 (0: none)
-  const uint2 *ovbins;      // inverse: bins with an overflow run (bin, start | count << 20)
+  const uint2 *ovbins;      // inverse: per overflow bin (first term, term count) in ovterm
   const uint32_t *dord;     // inverse: per bin 1 + its index in ovbins (0: none)
   int novbins;
+  const uint32_t *ovterm;   // inverse: the overflow bins' terms, staging-row offsets, in
+  int novterm;              //   summation order (slot 0, slot 1, overflow run)
   int64_t zso;              // inverse staging: slot 1 at zso, overflow at 2 zso
   const float *h0;
   const float *h0dual;
@@ -1133,10 +1135,15 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
       }
       if constexpr (OVP) {
         if (r0 == 0) {  // pre-pass, in flight with the first batch's loads
+          // (a) every term of every overflow bin -> shared memory, all loads in flight at once
+          float2 *ovt = ovs + a.novbins;
+          for (int i = tid; i < a.novterm; i += T) ovt[i] = __ldcg(Z0 + __ldg(a.ovterm + i));
+          __syncthreads();
+          // (b) each bin's sum in plan order, from shared memory
           for (int i = tid; i < a.novbins; i += T) {
             const uint2 e = __ldg(a.ovbins + i);
-            float2 h = cadd(__ldcg(Z0 + e.x), __ldcg(Z1 + e.x));
-            for (int k = 0; k < (int)(e.y >> 20); ++k) h = cadd(h, __ldcg(Zo + (e.y & 0xfffff) + k));
+            float2 h = cadd(ovt[e.x], ovt[e.x + 1]);
+            for (int k = 2; k < (int)e.y; ++k) h = cadd(h, ovt[e.x + k]);
             ovs[i] = h;
           }
           __syncthreads();

@@ -620,15 +620,24 @@ int configure_kernels(slicq_plan *p) {
     kc.nover = start;
     // the overflow bins as a list (the persistent inverse spectrum kernel sums them in a
     // pre-pass spread over all threads of the CTA, kernels_dev.cuh inv_unit)
+    // ovbins[i] = (first term, term count) of the i-th overflow bin in the flat term list
+    // ovterm (offsets into a unit's staging row: slot 0, slot 1, then the overflow run, the
+    // order of the sum)
     p->ovbins.clear();
+    p->ovterm.clear();
     p->dord.assign(N + 2, 0u);
     for (int b = 0; b <= N; ++b)
       if (p->dpos[b]) {
-        p->ovbins.push_back(make_uint2((uint32_t)b, p->dpos[b]));
+        const uint32_t st = p->dpos[b] & 0xfffffu, cnt = p->dpos[b] >> 20;
+        p->ovbins.push_back(make_uint2((uint32_t)p->ovterm.size(), 2u + cnt));
+        p->ovterm.push_back((uint32_t)b);
+        p->ovterm.push_back((uint32_t)(zso + b));
+        for (uint32_t k = 0; k < cnt; ++k) p->ovterm.push_back((uint32_t)(2 * zso + st + k));
         p->dord[b] = (uint32_t)p->ovbins.size();
       }
-    // the persistent inverse spectrum kernel keeps their sums in shared memory
-    kc.spec_smem_p += sizeof(float2) * p->ovbins.size();
+    // the persistent inverse spectrum kernel stages the terms and keeps the sums in shared
+    // memory
+    kc.spec_smem_p += sizeof(float2) * (p->ovbins.size() + p->ovterm.size());
     if (kc.spec_smem_p > kSmemCap) kc.inv_persist = false;
     if (2 * zso + start >= (int64_t(1) << 18))
       return set_error(SLICQ_EUNSUPPORTED, "slice too long for the inverse element tables");
@@ -927,6 +936,7 @@ int upload(slicq_plan *p) {
       {p->bent.data(), sizeof(uint2) * p->bent.size(), 0},
       {p->ovbins.data(), sizeof(uint2) * p->ovbins.size(), 0},
       {p->dord.data(), sizeof(uint32_t) * p->dord.size(), 0},
+      {p->ovterm.data(), sizeof(uint32_t) * p->ovterm.size(), 0},
   };
   size_t o = 0;
   for (Part &pt : parts) {
@@ -978,6 +988,7 @@ int upload(slicq_plan *p) {
   p->d.bent = reinterpret_cast<uint2 *>(b + parts[32].off);
   p->d.ovbins = reinterpret_cast<uint2 *>(b + parts[33].off);
   p->d.dord = reinterpret_cast<uint32_t *>(b + parts[34].off);
+  p->d.ovterm = reinterpret_cast<uint32_t *>(b + parts[35].off);
   e = cudaMemcpy(blk, host.data(), o, cudaMemcpyHostToDevice);
   if (e != cudaSuccess)
     return set_error(SLICQ_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
@@ -1147,6 +1158,8 @@ static KArgs base_args(const slicq_plan *p) {
   a.ovbins = p->d.ovbins;
   a.dord = p->d.dord;
   a.novbins = (int)p->ovbins.size();
+  a.ovterm = p->d.ovterm;
+  a.novterm = (int)p->ovterm.size();
   a.zso = p->kc.zso;
   a.h0 = p->d.h0;
   a.h0dual = p->d.h0dual;

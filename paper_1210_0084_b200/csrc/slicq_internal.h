@@ -118,8 +118,9 @@ struct DeviceTables {
   uint2 *fent = nullptr;     // forward element table
   uint2 *ient = nullptr;     // inverse element table
   uint32_t *dpos = nullptr;  // inverse overflow run per bin: start | count << 20 (0: none)
-  uint2 *ovbins = nullptr;   // inverse: the bins with an overflow run (bin, start | count << 20)
+  uint2 *ovbins = nullptr;   // inverse: per overflow bin (first term, term count) in ovterm
   uint32_t *dord = nullptr;  // inverse: per bin, 1 + its index in ovbins (0: none)
+  uint32_t *ovterm = nullptr;  // inverse: the overflow bins' terms (staging-row offsets)
   float *h0 = nullptr;      // fp32 h_0[t+N], t in [-N, N)
   float *h0dual = nullptr;  // fp32 h~_0[t+N]
   float *tw2n = nullptr;    // float2: [64] e^{-i pi t/N} for t < 64, then [2N/64] for t = 64 h
@@ -248,8 +249,9 @@ struct slicq_plan {
   std::vector<int32_t> pchans;
   std::vector<uint2> fent, ient;
   std::vector<uint32_t> dpos;
-  std::vector<uint2> ovbins;   // bins with overflow terms (bin, dpos[bin])
+  std::vector<uint2> ovbins;   // bins with overflow terms: (first term, count) in ovterm
   std::vector<uint32_t> dord;  // 1 + index into ovbins per bin (0: none)
+  std::vector<uint32_t> ovterm;  // their terms in summation order (staging-row offsets)
   std::vector<float> lgw, lgdw;          // long mode filter weights
   std::vector<uint32_t> lrow, lent;      // long mode per-bin term lists
   std::vector<int32_t> lm1;              // long mode: four-step factor of M_k > 26000 (else 0)
