@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
 // Xo[0..N] in global memory (the staging row of the split design, or a ring slot);
 // TOSMEM = true: X stays in shared memory, spec[padi(k)] for k = 0..N.  htab: tr - 1 floats
 // of shared scratch.  LOADTW: stage the twiddle table (persistent callers do it once).
-template <int LOGN, int MODE, bool TOSMEM, bool LOADTW = true>
+template <int LOGN, int MODE, bool TOSMEM, bool LOADTW = true, bool LOADH = true>
 __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float2 *tw, float *htab,
                                              int64_t u, float2 *Xo) {
   using CF = Big<LOGN>;
@@ -835,7 +835,7 @@ __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float
     const int64_t s0 = (mg - 1) * N - a.base_off;  // local x index of frame sample 0
     const bool vec = ((reinterpret_cast<uintptr_t>(xr + s0) & 7) == 0);  // 8-byte pairs
     const int A = MODE ? N : (N - a.tr) / 2, Bw = MODE ? N + 1 : (N + a.tr) / 2;
-    if constexpr (MODE == 0)
+    if constexpr (MODE == 0 && LOADH)
       for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0 + N + A + 1 + u);
     // window support: pairs q_lo..q_hi hold at least one nonzero-window sample
     const int q_lo = MODE ? 0 : (N - Bw + 1) >> 1, q_hi = MODE ? N - 1 : (N + Bw - 1) >> 1;
@@ -1028,17 +1028,23 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
   float *htab = reinterpret_cast<float *>(tw + tw_entries<LOGN>());
   const int tid = threadIdx.x;
   for (int i = tid; i < tw_entries<LOGN>(); i += T) tw[i] = a.tw2n[i];
+  {  // the window's transition table, once per CTA
+    const int A = (N - a.tr) / 2;
+    for (int u = tid; u < a.tr - 1; u += T) htab[u] = __ldg(a.h0 + N + A + 1 + u);
+  }
   const int64_t G = gridDim.x;
   const int64_t ub = blockIdx.x * (int64_t)a.nunits / G, ue = (blockIdx.x + 1) * (int64_t)a.nunits / G;
   for (int64_t ul = ub; ul < ue; ++ul) {
-    if (ul + 1 < ue) {  // the next frame's window support -> L2
+    if (ul + 1 < ue && tid == 0) {  // the next frame's window support -> L2 (one bulk prefetch)
       const int64_t u = a.unit0 + ul + 1, row = unit_row(u, a.nslices);
       const int64_t s0 = (a.slice0 + (u - row * a.nslices) - 1) * N - a.base_off + (N - a.tr) / 2;
-      if (s0 >= 0 && s0 + N + a.tr <= a.x_len)
-        prefetch_l2(a.x + row * a.x_stride + s0, (int64_t)(N + a.tr) * 4, tid, T);
+      const float *p0 = a.x + row * a.x_stride + s0;
+      // (inside the row and 16-byte aligned at the row start: the envelope stays in x)
+      if (s0 >= 4 && s0 + N + a.tr + 4 <= a.x_len)
+        prefetch_l2_bulk(p0, (int64_t)(N + a.tr) * 4);
     }
-    fwd_spectrum<LOGN, 0, false, false>(a, spec, tw, htab, a.unit0 + ul, a.stage + ul * a.xs);
-    __syncthreads();  // (spec and htab reused by the next unit)
+    fwd_spectrum<LOGN, 0, false, false, false>(a, spec, tw, htab, a.unit0 + ul, a.stage + ul * a.xs);
+    __syncthreads();  // (spec reused by the next unit)
   }
   pdl_trigger();
 }
