@@ -1,2 +1,8 @@
-for i in 1 2; do timeout 120 python tools/quick_time.py 5 2>&1 | grep "fwd:\|inv:"; done
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "cfg5 or range or large or 131072 or other_slice" > gpurun_out/g11_tests.txt 2>&1; tail -3 gpurun_out/g11_tests.txt
+run() { echo "== $*"; env "$@" timeout 120 python tools/quick_time.py 4 2>&1 | grep "fwd:\|inv:" ; }
+run X=0
+run SLICQ_PIPE_PARTS=3
+run SLICQ_PIPE_PARTS=6
+run SLICQ_PIPE_PARTS=8
+run SLICQ_PIPE=0
+run SLICQ_TILE=64
+run SLICQ_TILE=256
