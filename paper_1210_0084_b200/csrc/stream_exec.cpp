@@ -21,7 +21,13 @@
 #include "slicq_internal.h"
 
 namespace {
-constexpr int kSlots = 4;
+#ifndef SLICQ_EXEC_SLOTS
+#define SLICQ_EXEC_SLOTS 4
+#endif
+constexpr int kSlots = SLICQ_EXEC_SLOTS;
+#ifndef SLICQ_EXEC_SPLIT
+#define SLICQ_EXEC_SPLIT 1
+#endif
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Range boundaries over S slices: the first and last kRamp ranges are shorter (weights
@@ -170,14 +176,26 @@ int slicq_process_host(const slicq_plan *p, const float *x_host, float *y_host, 
       o += seg;
     }
   };
-  auto copy_out = [&](int r) {  // range r's samples -> y_host
-    const int64_t a = bounds[r] * N, hi = std::min(bounds[r + 1] * N, n);
-    if (hi > a)
-      cu(cudaMemcpy2DAsync(y_host + a, sizeof(float) * n, slot_y(r), sizeof(float) * e.yw,
-                           sizeof(float) * (hi - a), B, cudaMemcpyDeviceToHost, st[2]),
+  // range r's samples -> y_host, [lo, hi) of the range's global samples (clipped to n)
+  auto copy_seg = [&](int r, int64_t lo, int64_t hi) {
+    const int64_t a = bounds[r] * N;
+    hi = std::min(hi, n);
+    if (hi > lo)
+      cu(cudaMemcpy2DAsync(y_host + lo, sizeof(float) * n, slot_y(r) + (lo - a), sizeof(float) * e.yw,
+                           sizeof(float) * (hi - lo), B, cudaMemcpyDeviceToHost, st[2]),
          "cudaMemcpy2DAsync (out)");
+  };
+  // all but the last halo samples of a range are final once its own inverse ran (only the
+  // next range's spill adds to the tail): they go out right away (SLICQ_EXEC_SPLIT)
+  auto copy_out_head = [&](int r) {
+    copy_seg(r, bounds[r] * N, bounds[r + 1] * N - halo);
+  };
+  auto copy_out = [&](int r, bool head_done) {
+    const int64_t a = bounds[r] * N, b = bounds[r + 1] * N;
+    copy_seg(r, head_done ? std::max(a, b - halo) : a, b);
     cu(cudaEventRecord(ev_free[r], st[2]), "cudaEventRecord");
   };
+  const bool split = SLICQ_EXEC_SPLIT != 0;
 
   // host enqueue order per range: in(r), k(r) (completes range r-1), out(r-1); a slot is
   // refilled only after the copy-out of the range that used it kSlots ranges earlier
@@ -200,13 +218,18 @@ int slicq_process_host(const slicq_plan *p, const float *x_host, float *y_host, 
     if (!lib(slicq_inverse_range(p, slot_c(r), s0, ns, S, B, slot_y(r), e.yw, spill(r), halo,
                                  rws, e.ws_bytes, st[1])))
       break;
+    if (split) {  // the head of range r is final now
+      cu(cudaEventRecord(ev_in[r], st[1]), "cudaEventRecord");  // (ev_in[r] reused: k(r) done)
+      cu(cudaStreamWaitEvent(st[2], ev_in[r], 0), "cudaStreamWaitEvent");
+      copy_out_head(r);
+    }
     if (r > 0) {  // range r's spill completes range r-1's tail
       if (!lib(slicq_overlap_add(slot_y(r - 1) + (bounds[r] - bounds[r - 1]) * N - halo, e.yw,
                                  spill(r), halo, B, st[1])))
         break;
       cu(cudaEventRecord(ev_ready[r - 1], st[1]), "cudaEventRecord");
       cu(cudaStreamWaitEvent(st[2], ev_ready[r - 1], 0), "cudaStreamWaitEvent");
-      copy_out(r - 1);
+      copy_out(r - 1, split);
     }
   }
   if (rc == SLICQ_OK) {  // circular wrap: range 0's spill completes the last range's tail
@@ -215,7 +238,7 @@ int slicq_process_host(const slicq_plan *p, const float *x_host, float *y_host, 
                               halo, B, st[1]))) {
       cu(cudaEventRecord(ev_ready[r], st[1]), "cudaEventRecord");
       cu(cudaStreamWaitEvent(st[2], ev_ready[r], 0), "cudaStreamWaitEvent");
-      copy_out(r);
+      copy_out(r, split);
     }
   }
   // join: the caller's stream waits for all three (also on error, for what was enqueued)

@@ -1,8 +1,4 @@
-run() { echo "== $*"; env "$@" timeout 120 python tools/quick_time.py 4 2>&1 | grep "fwd:\|inv:" ; }
-run X=0
-run SLICQ_PIPE_PARTS=3
-run SLICQ_PIPE_PARTS=6
-run SLICQ_PIPE_PARTS=8
-run SLICQ_PIPE=0
-run SLICQ_TILE=64
-run SLICQ_TILE=256
+L=$PWD/paper_1210_0084_b200
+for v in "" nosplit slots8 "" nosplit; do if [ -n "$v" ]; then export SLICQ_LIB=$L/libslicq_$v.so; else unset SLICQ_LIB; fi; echo "== $v"; timeout 300 python tools/e2e_probe.py 32,64 2>&1 | tail -2; done
+unset SLICQ_LIB
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "process_host" 2>&1 | tail -2
