@@ -98,6 +98,9 @@ __device__ __forceinline__ void st_plain(float2 *p, float2 v) { *p = v; }
 #ifndef SLICQ_ZSTORE
 #define SLICQ_ZSTORE __stcs  // (measured: evict-first beats .cg by ~1 % on cfg4)
 #endif
+#ifndef SLICQ_INV_PF2
+#define SLICQ_INV_PF2 1  // inverse spectrum: bulk L2 prefetch of the second load batch's bins
+#endif
 #ifndef SLICQ_OVP
 #define SLICQ_OVP 1  // persistent inverse spectrum kernel: overflow-bin sums in a CTA-wide pre-pass
 #endif
@@ -1089,6 +1092,15 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
     const float2 *Z0 = a.stage + ul * a.zs;
     const float2 *Z1 = Z0 + a.zso, *Zo = Z0 + 2 * a.zso;
     const int jA = tid, jB = tid == 0 ? TASKS1 / 2 : TASKS1 - tid;
+#if SLICQ_INV_PF2
+    // the second load batch's bins (r >= IG: k >= TASKS1 IG) of both slots -> L2 now, two bulk
+    // prefetches, so that batch's loads hit L2 when they are issued after the first batch
+    if (tid == 0) {
+      constexpr int K2 = TASKS1 * SLICQ_IA_GROUP;
+      prefetch_l2_bulk(Z0 + K2, (int64_t)(N + 1 - K2) * 8);
+      prefetch_l2_bulk(Z1 + K2, (int64_t)(N + 1 - K2) * 8);
+    }
+#endif
     // e^{+i pi k / N} from the global two-level table (no wait for the shared copy)
     auto wk = [&](int k) {
       return cconj(cmul(__ldg(a.tw2n + 64 + (k >> 6)), __ldg(a.tw2n + (k & 63))));
