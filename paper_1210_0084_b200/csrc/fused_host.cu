@@ -132,9 +132,10 @@ RShape ring_shape(int M, int G, int bt, int scr_cap) {
 int configure_fused(slicq_plan *p) {
   KernelConfig &kc = p->kc;
   kc.fused = kc.ftables = false;
+  kc.cluster = 0;
   // the fused per-slice forward (opt-in: measured slower), the ring kernel
   // (opt-in) and the band-major channel kernel share these tables
-  const bool want = env_i("SLICQ_FUSED", 0) || env_i("SLICQ_RING", 0) || env_i("SLICQ_BAND", 0) ||
+  const bool want = env_i("SLICQ_FUSED", 0) || env_i("SLICQ_CLUSTER", 0) || env_i("SLICQ_RING", 0) || env_i("SLICQ_BAND", 0) ||
                     env_i("SLICQ_FWD2", 0);
   if (!want) return SLICQ_OK;
   if (kc.longmode || kc.large || kc.logN < 11 || kc.logN > 14 || !p->painless) return SLICQ_OK;
@@ -300,6 +301,10 @@ int configure_fused(slicq_plan *p) {
   kc.fsmem_f = fs;
   kc.ftables = true;
   kc.fused = env_i("SLICQ_FUSED", 0) != 0;
+  {
+    const int64_t G = env_i("SLICQ_CLUSTER", 0);
+    if (!kc.fused && G >= 2 && G <= 16) kc.cluster = (int)G;
+  }
   return SLICQ_OK;
 }
 

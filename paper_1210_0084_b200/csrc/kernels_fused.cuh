@@ -137,39 +137,45 @@ __device__ __forceinline__ void ff_s2(const KArgs &a, const FTask &tk, int m1, c
 #define SLICQ_FSIZES(X) \
   X(2) X(3) X(4) X(5) X(6) X(8) X(9) X(10) X(12) X(15) X(16) X(18) X(20) X(24) X(25) X(27) X(30) X(32)
 
+// F3 - F5 of forward task t for the unit whose spectrum X[0..N] (padded) is at X -- in this
+// CTA's shared memory, or (cluster kernel) another CTA's, through a generic DSMEM address
+template <int N>
+__device__ __forceinline__ void fwd_task(const KArgs &a, int t, const float2 *X, float2 *scr,
+                                         float2 *out_row, int lane) {
+  const int4 tv = __ldg(reinterpret_cast<const int4 *>(a.ftask + t));
+  FTask tk;
+  tk.code = tv.x; tk.nch = tv.y; tk.coff = tv.z; tk.mags = (uint32_t)tv.w;
+  const int m1 = tk.code & 255, m2 = (tk.code >> 8) & 255;
+  const bool small = (tk.code >> 16) & 1, inter = (tk.code >> 17) & 1;
+  if (small) {
+    switch (m1) {
+#define X_(S) case S: ff_small<S, N>(a, tk, X, out_row, lane, inter); break;
+      SLICQ_FSMALL(X_)
+#undef X_
+    }
+    return;
+  }
+  switch (m1) {
+#define X_(S) case S: ff_s1<S, N>(a, tk, m2, X, scr, lane, inter); break;
+    SLICQ_FSIZES(X_)
+#undef X_
+  }
+  __syncwarp();
+  switch (m2) {
+#define X_(S) case S: ff_s2<S>(a, tk, m1, scr, out_row, lane); break;
+    SLICQ_FSIZES(X_)
+#undef X_
+  }
+  __syncwarp();
+}
+
 // F3 - F5 for one unit: the warps of the CTA take the plan's forward tasks round robin
 template <int N, int T>
 __device__ __forceinline__ void fwd_channel_stage(const KArgs &a, const float2 *X, float2 *scr_all,
                                                   float2 *out_row) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float2 *scr = scr_all + warp * a.fscr;
-  for (int t = warp; t < a.nftask; t += T / 32) {
-    const int4 tv = __ldg(reinterpret_cast<const int4 *>(a.ftask + t));
-    FTask tk;
-    tk.code = tv.x; tk.nch = tv.y; tk.coff = tv.z; tk.mags = (uint32_t)tv.w;
-    const int m1 = tk.code & 255, m2 = (tk.code >> 8) & 255;
-    const bool small = (tk.code >> 16) & 1, inter = (tk.code >> 17) & 1;
-    if (small) {
-      switch (m1) {
-#define X_(S) case S: ff_small<S, N>(a, tk, X, out_row, lane, inter); break;
-        SLICQ_FSMALL(X_)
-#undef X_
-      }
-      continue;
-    }
-    switch (m1) {
-#define X_(S) case S: ff_s1<S, N>(a, tk, m2, X, scr, lane, inter); break;
-      SLICQ_FSIZES(X_)
-#undef X_
-    }
-    __syncwarp();
-    switch (m2) {
-#define X_(S) case S: ff_s2<S>(a, tk, m1, scr, out_row, lane); break;
-      SLICQ_FSIZES(X_)
-#undef X_
-    }
-    __syncwarp();
-  }
+  for (int t = warp; t < a.nftask; t += T / 32) fwd_task<N>(a, t, X, scr, out_row, lane);
 }
 
 // shared memory of the fused forward kernel: X (padded) | FFT twiddles | max(window
@@ -197,11 +203,81 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_fused
   pdl_trigger();
 }
 
+// ---- cluster-fused forward: a thread-block cluster of G CTAs
+// owns G consecutive units.  CTA r transforms unit r (F1 + F2) into its own shared memory;
+// after one cluster barrier the cluster's warps claim (task, unit) items in task-major order
+// from one counter in CTA 0's shared memory (atom.shared::cluster) and read each unit's
+// spectrum through DSMEM (mapa: the generic address of the same buffer in CTA g).  No
+// staging: the only HBM traffic is the frame read and the coefficient write.  Claiming in
+// task order keeps the cluster's warps on one or two code shapes at a time, and each CTA
+// walks the task list once per G slices instead of once per slice (the fused per-slice
+// kernel's instruction-cache starvation); the dynamic claim balances the CTAs.
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");  // (.release)
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");    // (.acquire)
+}
+template <class P>
+__device__ __forceinline__ const P *cl_map(const P *p, unsigned rank) {  // generic -> CTA rank's copy
+  uint64_t r;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<const P *>(r);
+}
+__device__ __forceinline__ unsigned cl_claim(unsigned *ctr_local, unsigned rank) {
+  uint32_t sa = (uint32_t)__cvta_generic_to_shared(ctr_local), ra, old;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(sa), "r"(rank));
+  asm volatile("atom.shared::cluster.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(ra) : "memory");
+  return old;
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_cluster_kernel(const KArgs a) {
+  using CF = Big<LOGN>;
+  extern __shared__ float4 smem4[];
+  __shared__ unsigned s_next;  // CTA 0's copy: the cluster's item counter
+  float2 *spec = reinterpret_cast<float2 *>(smem4);
+  float2 *tw = spec + spec_entries<LOGN>();
+  float2 *region = tw + tw_entries<LOGN>();
+  const unsigned rank = cl_rank(), G = cl_size();
+  const int64_t cu0 = (int64_t)blockIdx.x - rank;  // the cluster's first unit (chunk-local)
+  const int64_t rem_u = a.nunits - cu0;
+  const int nu = rem_u < (int64_t)G ? (int)rem_u : (int)G;
+  if (threadIdx.x == 0) s_next = 0;
+  if ((int)rank < nu)
+    fwd_spectrum<LOGN, 0, true>(a, spec, tw, reinterpret_cast<float *>(region), a.unit0 + cu0 + rank,
+                                nullptr);
+  cl_sync();  // every spectrum of the cluster complete and visible; the counter is 0
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float2 *scr = region + warp * a.fscr;
+  const int nitems = a.nftask * nu;
+  for (;;) {
+    unsigned i = 0;
+    if (lane == 0) i = cl_claim(&s_next, 0);
+    i = __shfl_sync(FULL, i, 0);
+    if ((int)i >= nitems) break;
+    const int t = (int)i / nu, g = (int)i - t * nu;
+    fwd_task<CF::N>(a, t, cl_map(spec, (unsigned)g), scr, a.coef_out + (a.unit0 + cu0 + g) * a.C, lane);
+  }
+  cl_sync();  // no CTA leaves while another still reads its spectrum
+  pdl_trigger();
+}
+
 // Per-size entry points (kernels_spec.cu, one object per LOGN)
 template <int LOGN>
 int fused_attrs();
 template <int LOGN>
 cudaError_t launch_fwd_fused(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s, bool pdl);
+template <int LOGN>
+cudaError_t launch_fwd_cluster(const KArgs &a, int G, size_t smem, cudaStream_t s, bool pdl);
 
 }  // namespace kern
 }  // namespace slicq

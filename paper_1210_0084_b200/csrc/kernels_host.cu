@@ -1118,8 +1118,8 @@ int kernel_launches(const slicq_plan *p, int direction, int64_t nslices, int64_t
   const WsLayout w = ws_layout(p, nslices, batch);
   const int64_t chunks = (nslices * batch + w.chunk - 1) / w.chunk;
   if (p->kc.longmode) return (int)(chunks * (direction == 0 ? 3 : 4));
-  if ((p->kc.fused || p->kc.ring) && direction == 0)
-    return (int)((nslices * batch + 0x7ffffffe) / 0x7fffffff);
+  if ((p->kc.fused || p->kc.cluster || p->kc.ring) && direction == 0)
+    return (int)((nslices * batch + 0x7fffffef) / 0x7ffffff0);
   if (p->kc.band && direction == 0 && !p->kc.large) return (int)(chunks * 2);
   int nchan = 0;
   for (int v = 0; v < 3; ++v) nchan += p->kc.voff[v + 1] > p->kc.voff[v];
@@ -1313,7 +1313,9 @@ static cudaError_t launch_fused(bool fwd, const slicq_plan *p, const KArgs &a, d
   switch (p->kc.logN) {
 #define CASE_(L)                                                                           \
   case L:                                                                                  \
-    return fwd ? launch_fwd_fused<L>(a, grid, p->kc.fsmem_f, s, p->kc.pdl) : cudaErrorInvalidValue;
+    return !fwd ? cudaErrorInvalidValue                                                   \
+           : p->kc.cluster ? launch_fwd_cluster<L>(a, p->kc.cluster, p->kc.fsmem_f, s, p->kc.pdl) \
+                           : launch_fwd_fused<L>(a, grid, p->kc.fsmem_f, s, p->kc.pdl);
     CASE_(11)
     CASE_(12)
     CASE_(13)
@@ -1429,15 +1431,15 @@ int launch_forward(const slicq_plan *p, const float *x, int64_t x_len, int64_t x
       return set_error(SLICQ_ECUDA, std::string("forward ring launch: ") + cudaGetErrorString(e));
     return SLICQ_OK;
   }
-  if (p->kc.fused && mode == 0) {  // one fused kernel: no staging (kernels_fused.cuh)
+  if ((p->kc.fused || p->kc.cluster) && mode == 0) {  // one fused kernel: no staging (kernels_fused.cuh)
     a.fch = p->d.fchf;
     a.ftask = p->d.ftf;
     a.nftask = p->kc.nftf;
     a.fscr = p->kc.fscr;
     a.vec16 = (reinterpret_cast<uintptr_t>(coeffs) % 16 == 0) ? 1 : 0;
-    for (int64_t u0 = 0; u0 < units; u0 += 0x7fffffff) {
+    for (int64_t u0 = 0; u0 < units; u0 += 0x7ffffff0) {  // (grid rounded up to the cluster)
       a.unit0 = u0;
-      a.nunits = (int)std::min<int64_t>(0x7fffffff, units - u0);
+      a.nunits = (int)std::min<int64_t>(0x7ffffff0, units - u0);
       const cudaError_t e = launch_fused(true, p, a, dim3((unsigned)a.nunits), s);
       if (e != cudaSuccess)
         return set_error(SLICQ_ECUDA, std::string("forward launch: ") + cudaGetErrorString(e));

@@ -76,7 +76,8 @@ cudaError_t launch_inv_spec<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, 
 
 template <>
 int fused_attrs<SLICQ_LOGN>() {
-  const void *fns[] = {(const void *)slicq_fwd_fused_kernel<SLICQ_LOGN>};
+  const void *fns[] = {(const void *)slicq_fwd_fused_kernel<SLICQ_LOGN>,
+                       (const void *)slicq_fwd_cluster_kernel<SLICQ_LOGN>};
   for (const void *f : fns) {
     const cudaError_t e = allow_max_dyn_smem(f);
     if (e != cudaSuccess) return (int)e;
@@ -88,6 +89,32 @@ template <>
 cudaError_t launch_fwd_fused<SLICQ_LOGN>(const KArgs &a, dim3 grid, size_t smem, cudaStream_t s,
                                          bool pdl) {
   return launch_pdl(slicq_fwd_fused_kernel<SLICQ_LOGN>, a, grid, Big<SLICQ_LOGN>::T, smem, s, pdl);
+}
+
+// cluster-fused forward: grid = the units rounded up to G, clusters of G consecutive CTAs
+template <>
+cudaError_t launch_fwd_cluster<SLICQ_LOGN>(const KArgs &a, int G, size_t smem, cudaStream_t s,
+                                           bool pdl) {
+  if (G > 8) {
+    const cudaError_t e = cudaFuncSetAttribute(slicq_fwd_cluster_kernel<SLICQ_LOGN>,
+                                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(((int64_t)a.nunits + G - 1) / G * G));
+  cfg.blockDim = dim3(Big<SLICQ_LOGN>::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, slicq_fwd_cluster_kernel<SLICQ_LOGN>, a);
 }
 
 #if SLICQ_LOGN == 12 || SLICQ_LOGN == 13

@@ -188,6 +188,7 @@ struct KernelConfig {
   // fused kernels (kernels_fused.cuh): one CTA per unit, no staging
   bool ftables = false;       // fused / ring tables built (fused_host.cu)
   bool fused = false;         // forward runs the fused per-slice kernel (opt-in)
+  int cluster = 0;            // forward runs the cluster-fused kernel with clusters of this many CTAs (0: off)
   bool band = false;          // forward channel stage runs the band-major kernel (split design)
   int nftf = 0, nfti = 0;     // forward / inverse warp tasks
   int nphase_a = 0;           // inverse: tasks [0, nphase_a) are phase A (even channels)

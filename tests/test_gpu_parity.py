@@ -478,6 +478,34 @@ def test_tma_staged_channel_kernels_bit_identical(api, monkeypatch, cfg, n, batc
     assert (torch.linalg.vector_norm(y1 - x) / torch.linalg.vector_norm(x)).item() <= TOL
 
 
+@pytest.mark.parametrize("G", [8, 16, 3])
+def test_cluster_fused_forward_matches_oracle(api, monkeypatch, G):
+    """Cluster-fused forward (kernels_fused.cuh slicq_fwd_cluster_kernel, SLICQ_CLUSTER=G: a
+    cluster of G CTAs transforms G consecutive slices into shared memory and runs every
+    channel task of the G slices over DSMEM; Alg. 1 per slice) against the oracle
+    on every slice of cfg1 with a ragged slice count (9 slices: not a multiple of G), and
+    against the default split path on a cfg4 range and a cfg3 batch (same arithmetic up to
+    fp32 rounding order: the fold reads X(lo + d) contiguously instead of through the table)."""
+    monkeypatch.setenv("SLICQ_CLUSTER", str(G))
+    cfg = CONFIGS[1]
+    p1 = api.plan_for_config(cfg)
+    ref = cqplan.make_plan(*plan_args(cfg))
+    x = random_signal(777 + G, 2, 9 * 8192 - 5)
+    check_forward(p1, ref, x)
+    y = p1.inverse(p1.forward(torch.from_numpy(x).cuda()), x.shape[1]).cpu().numpy()
+    assert rel(y, x) <= TOL
+    for cid, n, batch in ((4, 300 * 8192 + 123, 1), (3, 40 * 8192, 3)):
+        xg = torch.from_numpy(random_signal(4343 + cid, batch, n)).cuda()
+        monkeypatch.setenv("SLICQ_CLUSTER", str(G))
+        pc = api.plan_for_config(CONFIGS[cid])
+        monkeypatch.delenv("SLICQ_CLUSTER")
+        p0 = api.plan_for_config(CONFIGS[cid])
+        c0, c1 = p0.forward(xg), pc.forward(xg)
+        d = torch.linalg.vector_norm((c1 - c0).reshape(-1, c0.shape[-1]), dim=1)
+        r = torch.linalg.vector_norm(c0.reshape(-1, c0.shape[-1]), dim=1)
+        assert (d / r.clamp_min(1e-30)).max().item() <= 1e-6
+
+
 @pytest.mark.parametrize("cfg,n,batch", [(4, 300 * 8192 + 123, 1), (1, 65536, 3), (3, 40 * 8192, 6)])
 def test_persistent_inverse_spectrum_bit_identical(api, monkeypatch, cfg, n, batch):
     """The persistent inverse spectrum kernel (contiguous unit ranges per CTA, on-chip overlap
