@@ -357,6 +357,20 @@ __device__ __forceinline__ P *opaque(P *p) {
   asm("" : "+l"(p));
   return p;
 }
+#ifndef SLICQ_FWD_OPAQUE
+#define SLICQ_FWD_OPAQUE 1  // forward fold: per-lane spectrum base opaque (32-bit bin indexing);
+#endif                      // bit 0: four-step packets (full variant), bit 1: small packets
+                            // (measured neutral on cfg4: off)
+#if SLICQ_FWD_OPAQUE & 1
+#define SLICQ_FWD_OPQ1(p) opaque(p)
+#else
+#define SLICQ_FWD_OPQ1(p) (p)
+#endif
+#if SLICQ_FWD_OPAQUE & 2
+#define SLICQ_FWD_OPQ2(p) opaque(p)
+#else
+#define SLICQ_FWD_OPQ2(p) (p)
+#endif
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
@@ -431,7 +445,10 @@ __device__ SLICQ_FWD_STEP_INLINE void fwd_step1f(const uint2 *ent, const float2 
   const int u = (ci * (int)magc) >> 16, c = ci - u * r;
   const int M = M1 * m2;
   const uint2 *e0 = ent + c * M + p2;
-  const float2 *Xu = X + u * xs;
+  // full variant: the per-lane base made opaque (32-bit bin index, one IMAD.WIDE per load:
+  // cfg3 forward -1.6 %); the lite variant keeps the compiler's 64-bit index arithmetic
+  // (opaque there: +2.5 % on cfg4 -- more spills at 80 registers)
+  const float2 *Xu = V > 16 ? SLICQ_FWD_OPQ1(X + u * xs) : X + u * xs;
   float2 v[M1];
 #pragma unroll
   for (int p1 = 0; p1 < M1; ++p1) {
@@ -480,7 +497,11 @@ __device__ SLICQ_FWDS_INLINE void fwd_small(const uint2 *ent, const float2 *X, f
 #pragma unroll
   for (int p = 0; p < M; ++p) {
     const uint2 e = __ldg(ent + p * 32);
+#if SLICQ_FWD_OPAQUE & 2
+    const float2 xv = ld_global(X + e.x);  // (X opaque: global load, 32-bit index)
+#else
     const float2 xv = X[e.x];
+#endif
     const float gv = __uint_as_float(e.y);  // sign bit: conjugate X (g >= 0)
     v[p] = make_float2(xv.x * fabsf(gv), xv.y * gv);
   }
@@ -671,7 +692,7 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_fwd_chan_kernel(const KArg
       if (small) {
         switch (m1) {
 #define X_(S) \
-  case S: if constexpr (S <= MAXS) fwd_small<S, MAXS>(ent + c_l, X + (int64_t)u_l * a.xs, out_row, lane < nvc, c_off); break;
+  case S: if constexpr (S <= MAXS) fwd_small<S, MAXS>(ent + c_l, SLICQ_FWD_OPQ2(X + (int64_t)u_l * a.xs), out_row, lane < nvc, c_off); break;
           SLICQ_SMALL(X_)
 #undef X_
         }
