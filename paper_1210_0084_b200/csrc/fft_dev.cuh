@@ -51,13 +51,38 @@ constexpr double cos2pi(long t, long R) {
 constexpr double sin2pi(long t, long R) { return cos2pi(4 * t - R, 4 * R); }
 
 // ---------------------------------------------------------------- complex helpers
+// SLICQ_F32X2 = 1 (default): complex arithmetic on sm_100a's packed FP32 pair instructions
+// (FADD2 / FMUL2 / FFMA2: one issue slot for the real and the imaginary lane; the swap of
+// the two lanes, a per-lane sign and a scalar or immediate broadcast are operand modifiers
+// in SASS, so a complex add is one instruction, a complex multiply two, and a rotation by
+// +-i folds into its consumer).  The kernels are bound by instruction issue, not by the FP32
+// pipe, so halving the FP issue slots is what counts.  = 0 keeps the
+// scalar FADD/FMUL/FFMA forms (same values up to the order of the roundings in cmul).
+#ifndef SLICQ_F32X2
+#define SLICQ_F32X2 1
+#endif
+#if SLICQ_F32X2
+__device__ __forceinline__ float2 bcast2(float s) { return make_float2(s, s); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return __ffma2_rn(make_float2(-a.y, a.x), bcast2(b.y), __fmul2_rn(a, bcast2(b.x)));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, bcast2(s)); }
+// a * s + b with a real scalar s
+__device__ __forceinline__ float2 cfma_s(float2 a, float s, float2 b) { return __ffma2_rn(a, bcast2(s), b); }
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
-__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cfma_s(float2 a, float s, float2 b) {
+  return make_float2(fmaf(a.x, s, b.x), fmaf(a.y, s, b.y));
+}
+#endif
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 // multiply by SIGN * i
 template <int SIGN>
 __device__ __forceinline__ float2 mul_si(float2 a) {
@@ -87,7 +112,11 @@ __device__ __forceinline__ float2 twiddle_c(float2 v) {
   } else {
     constexpr float c = (float)cos2pi(t, R);
     constexpr float s = (float)(SIGN * sin2pi(t, R));
+#if SLICQ_F32X2
+    return cmul(v, make_float2(c, s));
+#else
     return make_float2(fmaf(v.x, c, -v.y * s), fmaf(v.x, s, v.y * c));
+#endif
   }
 }
 
@@ -116,7 +145,7 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
     float2 t1 = cadd(v[1], v[2]);
     float2 t2 = csub(v[1], v[2]);
     float2 y0 = cadd(v[0], t1);
-    float2 a = make_float2(fmaf(-0.5f, t1.x, v[0].x), fmaf(-0.5f, t1.y, v[0].y));
+    float2 a = cfma_s(t1, -0.5f, v[0]);
     float2 b = mul_si<SIGN>(cscale(t2, h));
     v[0] = y0;
     v[1] = cadd(a, b);
@@ -136,10 +165,17 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
     float2 t1 = cadd(v[1], v[4]), t2 = cadd(v[2], v[3]);
     float2 t3 = csub(v[1], v[4]), t4 = csub(v[2], v[3]);
     float2 y0 = cadd(v[0], cadd(t1, t2));
+#if SLICQ_F32X2
+    float2 a1 = cfma_s(t2, c2, cfma_s(t1, c1, v[0]));
+    float2 a2 = cfma_s(t2, c1, cfma_s(t1, c2, v[0]));
+    float2 b1 = cfma_s(t4, s2, cscale(t3, s1));
+    float2 b2 = cfma_s(t4, -s1, cscale(t3, s2));
+#else
     float2 a1 = make_float2(v[0].x + c1 * t1.x + c2 * t2.x, v[0].y + c1 * t1.y + c2 * t2.y);
     float2 a2 = make_float2(v[0].x + c2 * t1.x + c1 * t2.x, v[0].y + c2 * t1.y + c1 * t2.y);
     float2 b1 = make_float2(s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y);
     float2 b2 = make_float2(s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y);
+#endif
     b1 = mul_si<SIGN>(b1);
     b2 = mul_si<SIGN>(b2);
     v[0] = y0;
