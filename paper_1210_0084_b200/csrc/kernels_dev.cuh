@@ -962,8 +962,8 @@ __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float
     };
     if constexpr (TOSMEM) __syncthreads();  // every pass-3 input read before X overwrites it
     auto r2c = [&](float2 zk, float2 zn, int k, bool mirror) {
-      const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
-      const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
+      const float2 E = cscale(cadd(zk, cconj(zn)), 0.5f);
+      const float2 O = cscale(mul_si<-1>(csub(zk, cconj(zn))), 0.5f);
       const float2 wO = cmul(tw_lookup(tw, k), O);  // e^{-i pi k/N} O
       xst(k, cadd(E, wO));
       if (mirror) xst(N - k, csub(cconj(E), cconj(wO)));
@@ -1009,8 +1009,8 @@ __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float
         spec[padi(N)] = make_float2(zk.x - zk.y, 0.f);
       } else {
         // E = (Zk + conj Zn)/2, O = (Zk - conj Zn)/(2i)
-        const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
-        const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
+        const float2 E = cscale(cadd(zk, cconj(zn)), 0.5f);
+        const float2 O = cscale(mul_si<-1>(csub(zk, cconj(zn))), 0.5f);
         const float2 wO = cmul(tw_lookup(tw, k), O);  // e^{-i pi k/N} O
         spec[padi(k)] = cadd(E, wO);
         // X[N-k] = conj(E) + e^{-i pi (N-k)/N} conj(O) = conj(E) - conj(wO)
@@ -1128,19 +1128,19 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
     };
     // c2r packing of the pair (k, N - k): Z[k] = E + iO, Z[N-k] = conj(E) + i conj(D) conj(w)
     auto pack_w = [&](float2 &hk, float2 &hn, float2 w) {
-      const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
-      const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
-      const float2 O = cmul(D, w), O2 = cmul(cconj(D), cconj(w));
-      hk = make_float2(E.x - O.y, E.y + O.x);
-      hn = make_float2(E.x - O2.y, -E.y + O2.x);
+      const float2 E = cscale(cadd(hk, cconj(hn)), 0.5f);
+      const float2 D = cscale(csub(hk, cconj(hn)), 0.5f);
+      const float2 O = cmul(D, w);  // (conj D)(conj w) = conj O, exactly
+      hk = cadd(E, mul_si<+1>(O));                       // E + iO
+      hn = cadd(cconj(E), make_float2(O.y, O.x));        // conj(E) + i conj(O)
     };
     auto pack = [&](float2 &hk, float2 &hn, int k) {
-      const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
-      const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+      const float2 E = cscale(cadd(hk, cconj(hn)), 0.5f);
+      const float2 D = cscale(csub(hk, cconj(hn)), 0.5f);
       const float2 w = wk(k);
-      const float2 O = cmul(D, w), O2 = cmul(cconj(D), cconj(w));
-      hk = make_float2(E.x - O.y, E.y + O.x);
-      hn = make_float2(E.x - O2.y, -E.y + O2.x);
+      const float2 O = cmul(D, w);  // (conj D)(conj w) = conj O, exactly
+      hk = cadd(E, mul_si<+1>(O));                       // E + iO
+      hn = cadd(cconj(E), make_float2(O.y, O.x));        // conj(E) + i conj(O)
     };
     // H at the thread's 32 bins jA + TASKS1 r (vA) and jB + TASKS1 r (vB): 4 r per batch,
     // all 16 slot loads and 8 overflow descriptors of a batch in flight together
@@ -1298,15 +1298,14 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
     for (int k = tid; k <= N / 2; k += T) {
       const float2 hk = spec[padi(k)];
       const float2 hn = spec[padi(N - k)];
-      const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
-      const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+      const float2 E = cscale(cadd(hk, cconj(hn)), 0.5f);
+      const float2 D = cscale(csub(hk, cconj(hn)), 0.5f);
       const float2 w = cconj(tw_lookup(tw, k));  // e^{+i pi k/N}
       const float2 O = cmul(D, w);
-      spec[padi(k)] = make_float2(E.x - O.y, E.y + O.x);  // E + iO
+      spec[padi(k)] = cadd(E, mul_si<+1>(O));  // E + iO
       if (k != 0 && k != N / 2) {
-        // pair N-k: E' = conj(E), O' = conj(D) e^{-i pi k/N}
-        const float2 O2 = cmul(cconj(D), cconj(w));
-        spec[padi(N - k)] = make_float2(E.x - O2.y, -E.y + O2.x);  // conj(E) + i O'
+        // pair N-k: E' = conj(E), O' = conj(D) e^{-i pi k/N} = conj(O), exactly
+        spec[padi(N - k)] = cadd(cconj(E), make_float2(O.y, O.x));  // conj(E) + i O'
       }
     }
     __syncthreads();

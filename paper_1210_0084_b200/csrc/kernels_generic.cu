@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(GT, 1) slicq_fwd_spec_generic(const KArgs a, c
       z[0] = make_float2(zk.x + zk.y, 0.f);
       // X[N] goes straight to the staging row below (z has N entries)
     } else {
-      const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
-      const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
+      const float2 E = cscale(cadd(zk, cconj(zn)), 0.5f);
+      const float2 O = cscale(mul_si<-1>(csub(zk, cconj(zn))), 0.5f);
       const float2 wO = cmul(tw2(a.tw2n, k), O);
       z[k] = cadd(E, wO);
       if (k != N - k) z[N - k] = csub(cconj(E), cconj(wO));
@@ -140,14 +140,13 @@ __global__ void __launch_bounds__(GT, 1) slicq_inv_spec_generic(const KArgs a, c
   // written to the digit-reversed positions of the in-place DIT
   for (int k = tid; k <= N / 2; k += GT) {
     const float2 hk = H(k), hn = H(N - k);
-    const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
-    const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+    const float2 E = cscale(cadd(hk, cconj(hn)), 0.5f);
+    const float2 D = cscale(csub(hk, cconj(hn)), 0.5f);
     const float2 w = cconj(tw2(a.tw2n, k));
     const float2 O = cmul(D, w);
-    z[__ldg(g.perm + k)] = make_float2(E.x - O.y, E.y + O.x);
+    z[__ldg(g.perm + k)] = cadd(E, mul_si<+1>(O));
     if (k != 0 && k != N - k) {
-      const float2 O2 = cmul(cconj(D), cconj(w));
-      z[__ldg(g.perm + (N - k))] = make_float2(E.x - O2.y, -E.y + O2.x);
+      z[__ldg(g.perm + (N - k))] = cadd(cconj(E), make_float2(O.y, O.x));  // (conj D)(conj w) = conj O
     }
   }
   __syncthreads();

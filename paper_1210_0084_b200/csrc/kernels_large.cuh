@@ -215,8 +215,8 @@ __global__ void __launch_bounds__(LT) fwd_large_row(const KArgs a) {
       Xo[N] = make_float2(zk.x - zk.y, 0.f);
       continue;
     }
-    const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
-    const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
+    const float2 E = cscale(cadd(zk, cconj(zn)), 0.5f);
+    const float2 O = cscale(mul_si<-1>(csub(zk, cconj(zn))), 0.5f);
     const float2 wO = cmul(tw_lookup(tw, k), O);
     Xo[k] = cadd(E, wO);
     if (k != N / 2) Xo[N - k] = csub(cconj(E), cconj(wO));
@@ -253,14 +253,13 @@ __global__ void __launch_bounds__(LT) inv_large_pack(const KArgs a) {
   if (k <= N / 2) {
     const float2 hk = gather_bin<N>(a, Z, k);
     const float2 hn = gather_bin<N>(a, Z, N - k);
-    const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
-    const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+    const float2 E = cscale(cadd(hk, cconj(hn)), 0.5f);
+    const float2 D = cscale(csub(hk, cconj(hn)), 0.5f);
     const float2 w = cconj(tw_lookup(tw, k));  // e^{+i pi k/N}
     const float2 O = cmul(D, w);
-    W[k] = make_float2(E.x - O.y, E.y + O.x);
+    W[k] = cadd(E, mul_si<+1>(O));
     if (k != 0 && k != N / 2) {
-      const float2 O2 = cmul(cconj(D), cconj(w));
-      W[N - k] = make_float2(E.x - O2.y, -E.y + O2.x);
+      W[N - k] = cadd(cconj(E), make_float2(O.y, O.x));  // (conj D)(conj w) = conj O
     }
   }
   pdl_trigger();

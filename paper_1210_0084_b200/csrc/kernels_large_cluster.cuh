@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(LT, SLICQ_LCL_MINB) fwd_large_cluster(const KA
       Xo[N] = make_float2(zk.x - zk.y, 0.f);
       return;
     }
-    const float2 E = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
-    const float2 O = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
+    const float2 E = cscale(cadd(zk, cconj(zn)), 0.5f);
+    const float2 O = cscale(mul_si<-1>(csub(zk, cconj(zn))), 0.5f);
     const float2 wO = cmul(tw_lookup(tw, k), O);
     Xo[k] = cadd(E, wO);
     if (k != N / 2) Xo[N - k] = csub(cconj(E), cconj(wO));
@@ -263,14 +263,13 @@ __global__ void __launch_bounds__(LT, SLICQ_LCL_MINB) inv_large_cluster(const KA
   auto pack = [&](int k, int sa, int ia, int sb, int ib) {
     const float2 hk = buf[sa * CS1 + padi(ia)];
     const float2 hn = sb >= 0 ? buf[sb * CS1 + padi(ib)] : (k == 0 ? *hN : hk);
-    const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
-    const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+    const float2 E = cscale(cadd(hk, cconj(hn)), 0.5f);
+    const float2 D = cscale(csub(hk, cconj(hn)), 0.5f);
     const float2 w = cconj(tw_lookup(tw, k));  // e^{+i pi k/N}
     const float2 O = cmul(D, w);
-    buf[sa * CS1 + padi(ia)] = make_float2(E.x - O.y, E.y + O.x);
+    buf[sa * CS1 + padi(ia)] = cadd(E, mul_si<+1>(O));
     if (sb >= 0) {
-      const float2 O2 = cmul(cconj(D), cconj(w));
-      buf[sb * CS1 + padi(ib)] = make_float2(E.x - O2.y, -E.y + O2.x);
+      buf[sb * CS1 + padi(ib)] = cadd(cconj(E), make_float2(O.y, O.x));  // (conj D)(conj w) = conj O
     }
   };
   for (int idx = tid; idx < HC * N1; idx += LT) {

@@ -550,14 +550,13 @@ __global__ void __launch_bounds__(LT) long_inv_pack(const KArgs a) {
   if (k <= N / 2) {
     const float2 hk = long_gather(a, Tm, k);
     const float2 hn = long_gather(a, Tm, N - k);
-    const float2 E = make_float2(0.5f * (hk.x + hn.x), 0.5f * (hk.y - hn.y));
-    const float2 D = make_float2(0.5f * (hk.x - hn.x), 0.5f * (hk.y + hn.y));
+    const float2 E = cscale(cadd(hk, cconj(hn)), 0.5f);
+    const float2 D = cscale(csub(hk, cconj(hn)), 0.5f);
     const float2 w = cconj(tw_lookup(tw, k));  // e^{+i pi k/N}
     const float2 O = cmul(D, w);
-    W[k] = make_float2(E.x - O.y, E.y + O.x);
+    W[k] = cadd(E, mul_si<+1>(O));
     if (k != 0 && k != N / 2) {
-      const float2 O2 = cmul(cconj(D), cconj(w));
-      W[N - k] = make_float2(E.x - O2.y, -E.y + O2.x);
+      W[N - k] = cadd(cconj(E), make_float2(O.y, O.x));  // (conj D)(conj w) = conj O
     }
   }
   pdl_trigger();
