@@ -62,7 +62,7 @@ def _stale(out: str = OUT) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, debug_timing: bool = False,
-          variant: str = "", defines=()) -> str:
+          variant: str = "", defines=(), only=()) -> str:
     """Build libslicq.so (or, with debug_timing, libslicq_dbg.so with per-phase clock64
     instrumentation for tools/phase_timing.py; or, with variant, libslicq_<variant>.so with
     extra -D defines for tuning experiments, selected via SLICQ_LIB; never used by the
@@ -74,8 +74,13 @@ def build(force: bool = False, verbose: bool = False, debug_timing: bool = False
     objdir = OBJ if not tag else OBJ + "_" + tag
     os.makedirs(objdir, exist_ok=True)
     extra = (["-DSLICQ_PHASE_TIMING"] if debug_timing else []) + [f"-D{d}" for d in defines]
+    # only: object names a tuning variant recompiles; the rest is linked from the main build
+    def one(s):
+        if only and s[1] not in only:
+            return os.path.join(OBJ, s[1] + ".o"), ""
+        return _compile(s, objdir, extra)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        results = list(ex.map(lambda s: _compile(s, objdir, extra), SOURCES))
+        results = list(ex.map(one, SOURCES))
     log = "\n".join(r[1] for r in results)
     with open(os.path.join(objdir, "ptxas.log"), "w") as f:
         f.write(log)

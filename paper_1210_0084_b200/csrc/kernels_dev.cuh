@@ -113,17 +113,20 @@ __device__ __forceinline__ void st_plain(float2 *p, float2 v) { *p = v; }
 #ifndef SLICQ_MINB13
 #define SLICQ_MINB13 2
 #endif
+#ifndef SLICQ_MINB13F
+#define SLICQ_MINB13F SLICQ_MINB13  // forward spectrum kernels' CTAs per SM (register cap)
+#endif
 // MINB = CTAs per SM the shared-memory budget is sized for (two slices in flight per SM
 // overlap one CTA's HBM loads / barriers with the other's arithmetic).
 template <>
 struct Big<11> {
-  static constexpr int N = 2048, T = 128, MINB = 2;
+  static constexpr int N = 2048, T = 128, MINB = 2, MINBF = 2;
   static constexpr int F1 = 16, F2 = 16, F3 = 8;   // forward pass radices
   static constexpr int I1 = 16, I2 = 8, I3 = 16;   // inverse pass radices
 };
 template <>
 struct Big<12> {
-  static constexpr int N = 4096, T = 256, MINB = 2;
+  static constexpr int N = 4096, T = 256, MINB = 2, MINBF = 2;
   static constexpr int F1 = 16, F2 = 16, F3 = 16;
   static constexpr int I1 = 16, I2 = 16, I3 = 16;
 };
@@ -140,13 +143,13 @@ struct Big<12> {
 #endif
 template <>
 struct Big<13> {
-  static constexpr int N = 8192, T = SLICQ_T13, MINB = SLICQ_MINB13;
+  static constexpr int N = 8192, T = SLICQ_T13, MINB = SLICQ_MINB13, MINBF = SLICQ_MINB13F;
   static constexpr int F1 = SLICQ_F13A, F2 = SLICQ_F13B, F3 = SLICQ_F13C;
   static constexpr int I1 = SLICQ_I13A, I2 = SLICQ_I13B, I3 = SLICQ_I13C;
 };
 template <>
 struct Big<14> {
-  static constexpr int N = 16384, T = 512, MINB = 1;
+  static constexpr int N = 16384, T = 512, MINB = 1, MINBF = 1;
   static constexpr int F1 = 32, F2 = 32, F3 = 16;
   static constexpr int I1 = 16, I2 = 32, I3 = 32;
 };
@@ -1029,7 +1032,7 @@ __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float
 }
 
 template <int LOGN, int MODE = 0>
-__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_kernel(const KArgs a) {
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINBF) slicq_fwd_spec_kernel(const KArgs a) {
   extern __shared__ float4 smem4[];
   float2 *spec = reinterpret_cast<float2 *>(smem4);
   float2 *tw = spec + spec_entries<LOGN>();
@@ -1043,7 +1046,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_
 // the chunk; the twiddle table is staged once and the next unit's frame is prefetched to L2
 // while this one is transformed (consecutive frames of a row also share tr - 1 samples).
 template <int LOGN>
-__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_fwd_spec_persist_kernel(const KArgs a) {
+__global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINBF) slicq_fwd_spec_persist_kernel(const KArgs a) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T;
   extern __shared__ float4 smem4[];

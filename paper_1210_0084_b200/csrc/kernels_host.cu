@@ -412,7 +412,7 @@ int configure_kernels(slicq_plan *p) {
       case 14: kc.spec_smem_p = spec_persist_smem_bytes<14>((int)p->tr); break;
     }
     kc.inv_persist = env_int("SLICQ_INV_PERSIST", 1) != 0 && kc.spec_smem_p <= kSmemCap;
-    kc.fwd_persist = env_int("SLICQ_FWD_PERSIST", 0) != 0;
+    kc.fwd_persist = env_int("SLICQ_FWD_PERSIST", 1) != 0;
   }
   const int K2 = p->K + 2;
   const int N = (int)p->N, N2 = 2 * N;

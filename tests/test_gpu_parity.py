@@ -524,6 +524,21 @@ def test_persistent_inverse_spectrum_bit_identical(api, monkeypatch, cfg, n, bat
     assert (torch.linalg.vector_norm(y1 - x) / torch.linalg.vector_norm(x)).item() <= TOL
 
 
+@pytest.mark.parametrize("cfg,n,batch", [(4, 300 * 8192 + 123, 1), (1, 65536, 3), (3, 40 * 8192, 6),
+                                         (2, 441000, 2)])
+def test_persistent_forward_spectrum_bit_identical(api, monkeypatch, cfg, n, batch):
+    """The persistent forward spectrum kernel (default: contiguous unit ranges per CTA, the
+    twiddle and window tables staged once, the next frame prefetched to L2) gives exactly the
+    coefficients of the one-CTA-per-unit kernel: the same arithmetic per unit."""
+    x = torch.from_numpy(random_signal(6161 + cfg, batch, n)).cuda()
+    monkeypatch.setenv("SLICQ_FWD_PERSIST", "0")
+    p0 = api.plan_for_config(CONFIGS[cfg])
+    monkeypatch.setenv("SLICQ_FWD_PERSIST", "1")
+    p1 = api.plan_for_config(CONFIGS[cfg])
+    monkeypatch.delenv("SLICQ_FWD_PERSIST")
+    assert torch.equal(p0.forward(x), p1.forward(x))
+
+
 def test_pipelined_chunks_are_bit_identical(api, monkeypatch):
     """Calls of >= SLICQ_PIPE_MIN_UNITS units run as chunks alternating between two internal
     streams (ping-pong staging, fork/join on the caller's stream): identical results to one
