@@ -104,6 +104,9 @@ __device__ __forceinline__ void st_plain(float2 *p, float2 v) { *p = v; }
 #ifndef SLICQ_OVP
 #define SLICQ_OVP 1  // persistent inverse spectrum kernel: overflow-bin sums in a CTA-wide pre-pass
 #endif
+#ifndef SLICQ_OV_ASYNC
+#define SLICQ_OV_ASYNC 0  // (opt-in) the next unit's overflow terms fetched by cp.async one unit ahead: measured slower (cfg4 inverse 2.61 vs 2.575 ms)
+#endif
 #ifndef SLICQ_IA_GROUP
 #define SLICQ_IA_GROUP 8
 #endif
@@ -964,12 +967,15 @@ __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float
       else SLICQ_XSTORE(Xo + k, v);
     };
     if constexpr (TOSMEM) __syncthreads();  // every pass-3 input read before X overwrites it
-    auto r2c = [&](float2 zk, float2 zn, int k, bool mirror) {
+    auto r2c_w = [&](float2 zk, float2 zn, float2 w, int k, bool mirror) {
       const float2 E = cscale(cadd(zk, cconj(zn)), 0.5f);
       const float2 O = cscale(mul_si<-1>(csub(zk, cconj(zn))), 0.5f);
-      const float2 wO = cmul(tw_lookup(tw, k), O);  // e^{-i pi k/N} O
+      const float2 wO = cmul(w, O);  // e^{-i pi k/N} O
       xst(k, cadd(E, wO));
       if (mirror) xst(N - k, csub(cconj(E), cconj(wO)));
+    };
+    auto r2c = [&](float2 zk, float2 zn, int k, bool mirror) {
+      r2c_w(zk, zn, tw_lookup(tw, k), k, mirror);
     };
     // thread 0's tasks 0 and TASKS3/2 are their own mirrors: warp 0 packs their 32 bins
     // cooperatively, one bin per lane (X[k] = E + e^{-i pi k/N} O at each k; k = 0 also
@@ -996,8 +1002,13 @@ __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float
       }
     }
     if (tid != 0) {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) r2c(vA[r], vB[15 - r], jA + TASKS3 * r, true);
+      // e^{-i pi (jA + TASKS3 r)/N} = e^{-i pi jA/N} e^{-2 pi i r/32}: one table lookup per
+      // thread, the 16 rotations are compile-time twiddles (FMUL2/FFMA2 immediates)
+      const float2 wb = tw_lookup(tw, jA);
+      static_for<0, 16>([&](auto Rc) {
+        constexpr int r = decltype(Rc)::value;
+        r2c_w(vA[r], vB[15 - r], twiddle_c<r, 32, -1>(wb), jA + TASKS3 * r, true);
+      });
     }
   } else {
     pass_smem<N, CF::F3, CF::F1 * CF::F2, -1, T>(spec, tw);
@@ -1093,7 +1104,8 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINBF) slicq_fwd_spec
 template <int LOGN, int MODE, bool OVP = false>
 __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *tw, float *htab,
                                          float *carry, int64_t ul, bool ll, bool rl,
-                                         float2 *ovs = nullptr) {
+                                         float2 *ovs = nullptr, bool ovpre = false,
+                                         bool ovnext = false) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T;
   const int tid = threadIdx.x;
@@ -1137,14 +1149,6 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
       hk = cadd(E, mul_si<+1>(O));                       // E + iO
       hn = cadd(cconj(E), make_float2(O.y, O.x));        // conj(E) + i conj(O)
     };
-    auto pack = [&](float2 &hk, float2 &hn, int k) {
-      const float2 E = cscale(cadd(hk, cconj(hn)), 0.5f);
-      const float2 D = cscale(csub(hk, cconj(hn)), 0.5f);
-      const float2 w = wk(k);
-      const float2 O = cmul(D, w);  // (conj D)(conj w) = conj O, exactly
-      hk = cadd(E, mul_si<+1>(O));                       // E + iO
-      hn = cadd(cconj(E), make_float2(O.y, O.x));        // conj(E) + i conj(O)
-    };
     // H at the thread's 32 bins jA + TASKS1 r (vA) and jB + TASKS1 r (vB): 4 r per batch,
     // all 16 slot loads and 8 overflow descriptors of a batch in flight together
     float2 vA[16], vB[16];
@@ -1160,6 +1164,9 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
     // twiddle, loaded now
     const int ksp = tid < 16 ? TASKS1 * tid : TASKS1 / 2 + TASKS1 * (tid - 16);
     const float2 wsp = tid < 32 ? wk(ksp) : make_float2(1.f, 0.f);
+    // e^{+i pi (jA + TASKS1 r)/N} = e^{+i pi jA/N} e^{+2 pi i r/32}: one table lookup per
+    // thread (issued here, ahead of the slot loads), the 16 rotations are compile-time twiddles
+    const float2 wb = wk(jA);
     constexpr int IG = SLICQ_IA_GROUP;  // r values per load batch
 #pragma unroll
     for (int r0 = 0; r0 < 16; r0 += IG) {
@@ -1178,8 +1185,14 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
       if constexpr (OVP) {
         if (r0 == 0) {  // pre-pass, in flight with the first batch's loads
           // (a) every term of every overflow bin -> shared memory, all loads in flight at once
+          // (persistent kernel: the previous unit issued them as cp.async copies -- ovpre --
+          // so only the first unit of a CTA waits a full gather here)
           float2 *ovt = ovs + a.novbins;
-          for (int i = tid; i < a.novterm; i += T) ovt[i] = __ldcg(Z0 + __ldg(a.ovterm + i));
+          if (ovpre) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+          } else {
+            for (int i = tid; i < a.novterm; i += T) ovt[i] = __ldcg(Z0 + __ldg(a.ovterm + i));
+          }
           __syncthreads();
           // (b) each bin's sum in plan order, from shared memory
           for (int i = tid; i < a.novbins; i += T) {
@@ -1189,6 +1202,16 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
             ovs[i] = h;
           }
           __syncthreads();
+          if (ovnext) {  // the next unit's overflow terms -> ovt, asynchronously (ovt is free now)
+            const float2 *Zn = Z0 + a.zs;
+            for (int i = tid; i < a.novterm; i += T) {
+              const unsigned dst = (unsigned)__cvta_generic_to_shared(ovt + i);
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst),
+                           "l"(Zn + __ldg(a.ovterm + i))
+                           : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+          }
         }
 #pragma unroll
         for (int q = 0; q < IG; ++q) {
@@ -1240,8 +1263,10 @@ __device__ __forceinline__ void inv_unit(const KArgs &a, float2 *spec, float2 *t
       __syncwarp();
     }
     // N - (jA + TASKS1 r) = jB + TASKS1 (15 - r)
-#pragma unroll
-    for (int r = 0; r < 16; ++r) pack(vA[r], vB[15 - r], jA + TASKS1 * r);
+    static_for<0, 16>([&](auto Rc) {
+      constexpr int r = decltype(Rc)::value;
+      pack_w(vA[r], vB[15 - r], twiddle_c<r, 32, +1>(wb));
+    });
     if (tid == 0) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
@@ -1535,7 +1560,8 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINB) slicq_inv_spec_
       }
     }
     constexpr bool fused1 = CF::I1 == 16 && N / 16 == 2 * T;  // (the pre-pass needs it)
-    inv_unit<LOGN, 0, fused1 && SLICQ_OVP>(a, spec, tw, htab, carry, ul, ll, rl, ovs);
+    inv_unit<LOGN, 0, fused1 && SLICQ_OVP>(a, spec, tw, htab, carry, ul, ll, rl, ovs,
+                                           SLICQ_OV_ASYNC && ul > ub, SLICQ_OV_ASYNC && ul + 1 < ue);
     __syncthreads();  // (spec, carry and ovs reused by the next unit)
   }
   pdl_trigger();
