@@ -839,9 +839,36 @@ __global__ void __launch_bounds__(CHAN_T, MINB) slicq_inv_chan_kernel(const KArg
 // Xo[0..N] in global memory (the staging row of the split design, or a ring slot);
 // TOSMEM = true: X stays in shared memory, spec[padi(k)] for k = 0..N.  htab: tr - 1 floats
 // of shared scratch.  LOADTW: stage the twiddle table (persistent callers do it once).
+// Bit qq * R + r of the result: this warp's 32 frame pairs q = j + r TASKS (first pass, task
+// slot qq) touch a window transition, i.e. need the multiply by h_0 -- not all on the flat top
+// (h_0 = 1) and not all outside the window support (zeros, not loaded).  Depends on (N, tr)
+// and the warp only: the persistent kernel computes it once per CTA.
+template <int LOGN, int MODE>
+__device__ __forceinline__ uint32_t fwd_window_mask(const KArgs &a) {
+  using CF = Big<LOGN>;
+  constexpr int N = CF::N, T = CF::T, R = CF::F1, TASKS = N / R, PER = (TASKS + T - 1) / T;
+  static_assert(PER * R <= 32, "window mask bits");
+  if constexpr (MODE == 1) return 0u;  // no window
+  const int A = (N - a.tr) / 2, Bw = (N + a.tr) / 2;
+  const int q_lo = (N - Bw + 1) >> 1, q_hi = (N + Bw - 1) >> 1;
+  const int qa = (N - A + 1) >> 1, qb = (N + A - 1) >> 1;  // pairs with |t| <= A for both
+  uint32_t m = 0;
+#pragma unroll
+  for (int qq = 0; qq < PER; ++qq) {
+    const int jw = ((int)threadIdx.x & ~31) + qq * T;  // this warp's first task
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int w0 = jw + r * TASKS, w1 = w0 + 31;
+      if (!((w0 >= qa && w1 <= qb) || w1 < q_lo || w0 > q_hi)) m |= 1u << (qq * R + r);
+    }
+  }
+  return m;
+}
+
 template <int LOGN, int MODE, bool TOSMEM, bool LOADTW = true, bool LOADH = true>
 __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float2 *tw, float *htab,
-                                             int64_t u, float2 *Xo) {
+                                             int64_t u, float2 *Xo, uint32_t wmask = 0,
+                                             bool have_wmask = false) {
   using CF = Big<LOGN>;
   constexpr int N = CF::N, T = CF::T;
   const int tid = threadIdx.x;
@@ -911,20 +938,19 @@ __device__ __forceinline__ void fwd_spectrum(const KArgs &a, float2 *spec, float
     }
     }
     __syncthreads();  // window table staged (and twiddles)
-    const int qa = (N - A + 1) >> 1, qb = (N + A - 1) >> 1;  // pairs with |t| <= A for both
+    // warp-uniform skip mask (see fwd_window_mask; the persistent kernel passes it in)
+    const uint32_t wm = have_wmask ? wmask : fwd_window_mask<LOGN, MODE>(a);
 #pragma unroll
     for (int qq = 0; qq < PER; ++qq) {
       const int j = tid + qq * T;
       if (TASKS % T == 0 || j < TASKS) {
-        const int jw = (tid & ~31) + qq * T;  // this warp's first task
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int q = j + r * TASKS;
           // warp-uniform skip: the warp's 32 pairs all on the flat top (h_0 = 1), or all
           // outside the window support (not loaded: zeros)
           if constexpr (MODE == 1) continue;  // no window
-          const int w0 = jw + r * TASKS, w1 = w0 + 31;
-          if ((w0 >= qa && w1 <= qb) || w1 < q_lo || w0 > q_hi) continue;
+          if (!((wm >> (qq * R + r)) & 1u)) continue;
           // |t| of the two samples (t = 2q - N and 2q + 1 - N); h_0 = 1 for |t| <= A, the
           // staged transition for A < |t| < Bw, 0 beyond (selects, no divergent branches)
           const int t0 = abs(2 * q - N), t1 = abs(2 * q + 1 - N);
@@ -1072,6 +1098,7 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINBF) slicq_fwd_spec
   }
   const int64_t G = gridDim.x;
   const int64_t ub = blockIdx.x * (int64_t)a.nunits / G, ue = (blockIdx.x + 1) * (int64_t)a.nunits / G;
+  const uint32_t wmask = fwd_window_mask<LOGN, 0>(a);  // once per CTA
   for (int64_t ul = ub; ul < ue; ++ul) {
     if (ul + 1 < ue && tid == 0) {  // the next frame's window support -> L2 (one bulk prefetch)
       const int64_t u = a.unit0 + ul + 1, row = unit_row(u, a.nslices);
@@ -1081,7 +1108,8 @@ __global__ void __launch_bounds__(Big<LOGN>::T, Big<LOGN>::MINBF) slicq_fwd_spec
       if (s0 >= 4 && s0 + N + a.tr + 4 <= a.x_len)
         prefetch_l2_bulk(p0, (int64_t)(N + a.tr) * 4);
     }
-    fwd_spectrum<LOGN, 0, false, false, false>(a, spec, tw, htab, a.unit0 + ul, a.stage + ul * a.xs);
+    fwd_spectrum<LOGN, 0, false, false, false>(a, spec, tw, htab, a.unit0 + ul, a.stage + ul * a.xs,
+                                               wmask, true);
     __syncthreads();  // (spec reused by the next unit)
   }
   pdl_trigger();
