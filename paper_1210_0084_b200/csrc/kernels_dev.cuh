@@ -108,8 +108,8 @@ __device__ __forceinline__ void st_plain(float2 *p, float2 v) { *p = v; }
 #define SLICQ_OV_ASYNC 0  // (opt-in) the next unit's overflow terms fetched by cp.async one unit ahead: measured slower (cfg4 inverse 2.61 vs 2.575 ms)
 #endif
 #ifndef SLICQ_IA_GROUP
-#define SLICQ_IA_GROUP 8
-#endif
+#define SLICQ_IA_GROUP 4  // inverse spectrum: r-values of slot loads per batch (packed code: 4
+#endif                    // beats 8, cfg4 inverse 2.575 -> 2.52 ms; the scalar code preferred 8)
 #ifndef SLICQ_T13
 #define SLICQ_T13 256
 #endif
